@@ -1,0 +1,205 @@
+/* pbkd_b200.h -- C ABI of the B200-native blockwise-distillation path.
+ *
+ * This is the drop-in boundary for the reference's hot path:
+ * extern "C", plain pointers and sizes, no C++ or torch types.  The C++ host
+ * API in paper_2012_03096_b200/include/pbkd/*.hpp (same signatures as the
+ * reference's include/pbkd/*.hpp) is implemented on top of these calls; other
+ * languages bind them directly (INTEGRATION.md shows the ctypes binding).
+ *
+ * Reference interfaces replaced (file:line in /root/reference/proj):
+ *   pbkd_run / pbkd_run_parallel  <- pbkd::train_block   (include/pbkd/distill.hpp:72-73)
+ *                                    pbkd::run_parallel  (include/pbkd/runtime.hpp:41-43)
+ *   pbkd_eval_with_student        <- pbkd::evaluate_with_student_block (distill.hpp:77-79)
+ *   pbkd_prefix_infer             <- pbkd::prefix_infer (model.hpp:184-186)
+ *   pbkd_candidate_infer          <- pbkd::block_infer on a candidate (model.hpp:154-155)
+ *   pbkd_build_candidate          <- pbkd::build_candidate (replacement.hpp:39)
+ *   pbkd_round_robin / pbkd_wfd_bin_pack / pbkd_makespan
+ *                                 <- scheduler.hpp:29-38
+ *   pbkd_stratified_split, pbkd_epoch_order, pbkd_mix_seed
+ *                                 <- dataset.hpp:45, distill.cpp:198-200, tensor.hpp:94-99
+ *   pbkd_k_* (device pointers)    <- ops.hpp kernels (depthwise :114-178,
+ *                                    pointwise :184-239, sgd :545-558)
+ *
+ * Layout conventions: host tensors are fp32 NCHW exactly like pbkd::Tensor4
+ * (tensor.hpp:16-22); block weight vectors are flat in for_each_block_array
+ * order (model.cpp:448-478), moving statistics included.  Kernel-level
+ * entry points (pbkd_k_*) take DEVICE pointers in the engine's layout:
+ * activations NHWC, depthwise weights [9][C] (tap-major), pointwise [Cout][Cin].
+ *
+ * Errors: every int-returning call returns 0 on success; otherwise
+ * pbkd_last_error() (thread-local) holds the message and
+ * pbkd_last_error_kind() the class, which the C++ layer maps back to the
+ * reference's exception types (SpecError, ShapeError, out_of_range, ...).
+ */
+#ifndef PBKD_B200_H
+#define PBKD_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBKD_ERR_SPEC 1    /* pbkd::SpecError / std::invalid_argument */
+#define PBKD_ERR_SHAPE 2   /* pbkd::ShapeError */
+#define PBKD_ERR_RANGE 3   /* std::out_of_range */
+#define PBKD_ERR_LOGIC 4   /* std::logic_error */
+#define PBKD_ERR_CUDA 5    /* CUDA runtime failure */
+#define PBKD_ERR_OTHER 6
+
+#define PBKD_RUN_STEP_ONLY 1 /* skip epoch-0 baseline and evaluations */
+#define PBKD_RUN_NO_GRAPH 2  /* launch eagerly instead of CUDA graphs */
+
+typedef struct pbkd_ctx pbkd_ctx;
+typedef struct pbkd_results pbkd_results;
+
+/* Mirrors pbkd::DistillTask (distill.hpp:24-37). kind: CandidateKind ordinal
+ * (0 two_layer, 1 three_layer, 2 two_layer_skip, 3 three_layer_skip);
+ * loss_mode: 0 local_only, 1 combined. */
+typedef struct {
+    int block_index;
+    int kind;
+    int epochs;
+    int eval_every;
+    uint64_t seed;
+    double threshold;
+    int loss_mode;
+    float lambda_local;
+    float lr;
+    float momentum;
+    int batch_size;
+    long long max_steps;
+} pbkd_task;
+
+typedef struct {
+    int block_index;
+    int failed;
+    char kind[32];
+    char failure[256];
+    int n_loss;
+    int n_eval;
+    long long n_steps;
+    size_t n_block_floats;
+    int has_best;
+    double final_local_loss;
+    double best_eval;
+    double wall_time_s;
+} pbkd_result_info;
+
+typedef struct {
+    double timestamp_s;
+    int worker_id;
+    int task_id;
+    int kind; /* 0 dispatch, 1 task_start, 2 task_end, 3 steal, 4 gather */
+} pbkd_trace_event;
+
+const char* pbkd_last_error(void);
+int pbkd_last_error_kind(void);
+const char* pbkd_version(void);
+
+/* ---- context (one GPU) ------------------------------------------------- */
+int pbkd_ctx_create(int device, pbkd_ctx** out);
+void pbkd_ctx_destroy(pbkd_ctx* ctx);
+int pbkd_device_count(int* n);
+
+/* ---- teacher: model spec JSON (reference schema, model.cpp:225-344) ---- */
+int pbkd_spec_num_floats(const char* spec_json, size_t* n);
+int pbkd_spec_num_blocks(const char* spec_json, int* n);
+int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec_json, const float* weights, size_t n);
+int pbkd_teacher_init(pbkd_ctx* ctx, const char* spec_json, uint64_t seed); /* init_weights */
+int pbkd_teacher_weights(pbkd_ctx* ctx, float* out, size_t cap);
+
+/* ---- dataset: images fp32 NCHW in [0,1], labels int -------------------- */
+int pbkd_dataset_load(pbkd_ctx* ctx, const float* images, const int* labels, int count, int c,
+                      int h, int w, int classes);
+int pbkd_dataset_load_device(pbkd_ctx* ctx, const float* d_images, const int* labels, int count,
+                             int c, int h, int w, int classes);
+
+/* ---- distillation ------------------------------------------------------ */
+/* All tasks train on this context's GPU with train_block semantics. */
+int pbkd_run(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* train_idx,
+             int n_train, const int* eval_idx, int n_eval, int flags, pbkd_results** out);
+/* run_parallel semantics (runtime.cpp:124-243): plan validation (SpecError),
+ * per-task failure isolation, results gathered in task-id order, trace.
+ * plan_ids holds the concatenated per-worker lists, plan_counts their
+ * lengths.  policy: 0 round_robin, 1 wfd, 2 work_stealing. */
+int pbkd_run_parallel(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* train_idx,
+                      int n_train, const int* eval_idx, int n_eval, int worker_count, int policy,
+                      const int* plan_ids, const int* plan_counts, int flags, pbkd_results** out);
+int pbkd_run_count(const pbkd_results* r);
+int pbkd_run_info(const pbkd_results* r, int i, pbkd_result_info* info);
+int pbkd_run_loss_history(const pbkd_results* r, int i, double* out, int cap);
+int pbkd_run_eval_history(const pbkd_results* r, int i, int* epochs, double* acc, int cap);
+/* which: 0 best-eval snapshot (TrainedBlockResult::block), 1 final weights */
+int pbkd_run_block(const pbkd_results* r, int i, int which, float* out, size_t cap);
+int pbkd_run_step_losses(const pbkd_results* r, int i, float* out, long long cap);
+int pbkd_run_trace(const pbkd_results* r, pbkd_trace_event* out, int cap, int* n);
+double pbkd_run_wall_time(const pbkd_results* r);
+double pbkd_run_epoch_ms(const pbkd_results* r); /* device time of the training epochs */
+void pbkd_run_free(pbkd_results* r);
+/* Same as pbkd_run; device events bracket epochs >= timed_from_epoch (host
+ * gaps between epochs included), read back with pbkd_run_timing. */
+int pbkd_run_timed(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* train_idx,
+                   int n_train, const int* eval_idx, int n_eval, int flags, int timed_from_epoch,
+                   pbkd_results** out);
+int pbkd_run_timing(const pbkd_results* r, double* timed_ms, int* timed_epochs,
+                    long long* launches, double* epoch_ms, int cap, int* n_epochs);
+/* Times one launch of a hot kernel in isolation (roofline evidence):
+ * which 0 teacher conv implicit GEMM, 1 pointwise GEMM, 2 depthwise fwd,
+ * 3 depthwise bwd (fused), 4 loss + BN-backward sums; shapes from the loaded
+ * teacher's largest block at `batch` samples.  Outputs ms per launch and the
+ * algorithmic bytes / flops of that launch. */
+int pbkd_bench_kernel(pbkd_ctx* ctx, int which, int batch, int iters, double* ms, double* bytes,
+                      double* flops);
+
+/* ---- inference ----------------------------------------------------------- */
+int pbkd_prefix_infer(pbkd_ctx* ctx, const float* x, int n, int k, int inclusive, float* out,
+                      size_t cap, int* out_shape);
+int pbkd_candidate_infer(pbkd_ctx* ctx, int kind, int c_in, int c_out, int stride,
+                         const float* block_w, const float* x, int n, int h, int w, float* out,
+                         size_t cap);
+int pbkd_eval_with_student(pbkd_ctx* ctx, int block_index, int kind, const float* student_w,
+                           const int* eval_idx, int n_eval, int batch_size, double* acc);
+
+/* ---- host-side, bit-exact indexing and scheduling ------------------------ */
+uint64_t pbkd_mix_seed(uint64_t a, uint64_t b);
+int pbkd_stratified_split(const int* labels, int n, double eval_fraction, uint64_t seed,
+                          int* train_out, int* n_train, int* eval_out, int* n_eval);
+int pbkd_epoch_order(const int* train_idx, int n, uint64_t task_seed, int epoch, int* out);
+int pbkd_build_candidate(int kind, int c_in, int c_out, int stride, uint64_t seed, float* out,
+                         size_t cap, size_t* n);
+int pbkd_round_robin(const int* ids, int n, int workers, int* out_ids, int* out_counts);
+int pbkd_wfd_bin_pack(const int* ids, const double* weights, int n, int workers, int* out_ids,
+                      int* out_counts, double* predicted_makespan);
+int pbkd_makespan(const int* plan_ids, const int* plan_counts, int workers, const int* ids,
+                  const double* weights, int n, double* out);
+int pbkd_mac_proxy_weights(const char* spec_json, const int* blocks, int n, double* out);
+
+/* ---- kernel level (device pointers, NHWC, ctx stream; synchronous) ------ */
+int pbkd_k_dw_fwd(pbkd_ctx* ctx, const float* x, const float* w9c, float* y, int n, int h, int w,
+                  int c, int stride, int pad);
+/* Fused stride-1 depthwise backward of a unit whose input is
+ * relu(gamma*((p-mean)*inv)+beta): writes gy_prev = dX * [bn(p) > 0],
+ * the depthwise weight gradient gk[9][c] and the batch-norm sums
+ * sum_g[c], sum_gx[c] of gy_prev (ops.hpp:149-178, 333-342, 387-393). */
+int pbkd_k_dw_bwd(pbkd_ctx* ctx, const float* gy, const float* p, const float* w9c,
+                  const float* mean, const float* inv, const float* gamma, const float* beta,
+                  float* gy_prev, float* gk, float* sum_g, float* sum_gx, int n, int h, int w,
+                  int c);
+int pbkd_k_dw_gk(pbkd_ctx* ctx, const float* gy, const float* x, float* gk, int n, int h, int w,
+                 int c, int stride, int pad);
+/* y[m][o] = sum_j x[m][j] w[o][j]; optional per-channel sum / sum of squares */
+int pbkd_k_pw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int rows, int cin,
+                  int cout, float* col_sum, float* col_sq);
+/* gx[m][j] = sum_o gy[m][o] w[o][j];  gw[o][j] = sum_m gy[m][o] x[m][j] */
+int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy, float* gx,
+                  float* gw, int rows, int cin, int cout);
+int pbkd_k_sgd(pbkd_ctx* ctx, float* w, const float* g, float* v, size_t n, float lr,
+               float momentum);
+/* host-buffer SGD through the device kernel (pbkd::SgdState::step) */
+int pbkd_sgd_host(float* w, const float* g, float* v, size_t n, float lr, float momentum);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

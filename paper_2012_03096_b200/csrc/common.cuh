@@ -1,0 +1,57 @@
+// common.cuh -- shared helpers for the pbkd B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace pbkd_gpu {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define PBKD_CUDA(expr)                                                                     \
+    do {                                                                                    \
+        cudaError_t e__ = (expr);                                                           \
+        if (e__ != cudaSuccess)                                                             \
+            throw ::pbkd_gpu::CudaError(std::string("CUDA error ") + cudaGetErrorString(e__) + \
+                                        " at " __FILE__ ":" + std::to_string(__LINE__));   \
+    } while (0)
+
+#define PBKD_LAUNCH_CHECK() PBKD_CUDA(cudaGetLastError())
+
+constexpr int kThreads = 256;
+constexpr int kMaxUnits = 3;
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+#ifdef __CUDACC__
+// Exact-rounding arithmetic: the reference build has no FMA contraction
+// (SURVEY Appendix B), so every elementwise expression that must match it bit
+// for bit is spelled with the _rn intrinsics, which nvcc never fuses.
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+
+// ops.hpp:290-293: y = gamma * ((x - mean) * inv_std) + beta
+__device__ __forceinline__ float bn_train_apply(float x, float mean, float inv, float g, float b) {
+    return add(mul(g, mul(sub(x, mean), inv)), b);
+}
+// ops.hpp:304-321 inference affine: y = scale * x + shift
+__device__ __forceinline__ float bn_infer_apply(float x, float scale, float shift) {
+    return add(mul(scale, x), shift);
+}
+__device__ __forceinline__ float relu(float x) { return x > 0.0f ? x : 0.0f; }
+
+// Which task of a grouped launch owns this CTA (offs has nd+1 entries).
+__device__ __forceinline__ int find_task(const int* __restrict__ offs, int nd, int& local) {
+    int t = 0;
+    while (t + 1 < nd && static_cast<int>(blockIdx.x) >= offs[t + 1]) ++t;
+    local = static_cast<int>(blockIdx.x) - offs[t];
+    return t;
+}
+#endif  // __CUDACC__
+
+}  // namespace pbkd_gpu

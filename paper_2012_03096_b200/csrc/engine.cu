@@ -1,0 +1,1564 @@
+// engine.cu -- per-GPU distillation engine (see engine.hpp).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <sstream>
+
+#include "engine.hpp"
+#include "ops.cuh"
+#include "pbkd/dataset.hpp"
+#include "pbkd/replacement.hpp"
+
+namespace pbkd_gpu {
+
+using pbkd::Block;
+using pbkd::DistillTask;
+using pbkd::LayerKind;
+using pbkd::Network;
+using pbkd::SpecError;
+using pbkd::Tensor;
+
+namespace {
+
+constexpr int kScatterCtas = 148;
+
+// ------------------------------------------------------------ device memory
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        release();
+        p = o.p, bytes = o.bytes;
+        o.p = nullptr, o.bytes = 0;
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t n) {
+        release();
+        bytes = std::max<size_t>(n, 16);
+        PBKD_CUDA(cudaMalloc(&p, bytes));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    float* f() const { return static_cast<float*>(p); }
+    int* i() const { return static_cast<int*>(p); }
+    double* d() const { return static_cast<double*>(p); }
+};
+
+template <class T>
+DevBuf upload(const std::vector<T>& v, cudaStream_t st) {
+    DevBuf b(v.size() * sizeof(T));
+    if (!v.empty()) PBKD_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return b;
+}
+
+// ----------------------------------------------------------------- program
+// A recorded sequence of launches.  Grouped ops keep their descriptor arrays
+// in one device slab; the whole program can be captured into a CUDA graph.
+class Program {
+public:
+    template <class Op>
+    void grouped(void (*launch)(const Op*, int, int, cudaStream_t), std::vector<Op> ops,
+                 const std::function<int(const Op&)>& ctas) {
+        if (ops.empty()) return;
+        int total = 0;
+        for (Op& o : ops) {
+            o.cta_begin = total;
+            total += std::max(1, ctas(o));
+        }
+        const size_t off = (host_.size() + 63) & ~size_t(63);
+        host_.resize(off + ops.size() * sizeof(Op));
+        std::memcpy(host_.data() + off, ops.data(), ops.size() * sizeof(Op));
+        const int nd = static_cast<int>(ops.size());
+        steps_.push_back([launch, off, nd, total](cudaStream_t st, const uint8_t* slab) {
+            launch(reinterpret_cast<const Op*>(slab + off), nd, total, st);
+        });
+    }
+    void raw(std::function<void(cudaStream_t)> f) {
+        steps_.push_back([f](cudaStream_t st, const uint8_t*) { f(st); });
+    }
+    void finalize(cudaStream_t st) {
+        slab_.alloc(std::max<size_t>(host_.size(), 64));
+        if (!host_.empty())
+            PBKD_CUDA(cudaMemcpyAsync(slab_.p, host_.data(), host_.size(), cudaMemcpyHostToDevice, st));
+        PBKD_CUDA(cudaStreamSynchronize(st));
+        finalized_ = true;
+    }
+    void run(cudaStream_t st) {
+        if (!finalized_) finalize(st);
+        for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
+    }
+    void build_graph(cudaStream_t st) {
+        if (!finalized_) finalize(st);
+        cudaGraph_t g;
+        PBKD_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
+        PBKD_CUDA(cudaStreamEndCapture(st, &g));
+        PBKD_CUDA(cudaGraphInstantiate(&exec_, g, 0));
+        PBKD_CUDA(cudaGraphDestroy(g));
+    }
+    void launch_graph(cudaStream_t st) { PBKD_CUDA(cudaGraphLaunch(exec_, st)); }
+    bool has_graph() const { return exec_ != nullptr; }
+    size_t launches() const { return steps_.size(); }
+    ~Program() {
+        if (exec_) cudaGraphExecDestroy(exec_);
+    }
+
+private:
+    std::vector<uint8_t> host_;
+    DevBuf slab_;
+    std::vector<std::function<void(cudaStream_t, const uint8_t*)>> steps_;
+    bool finalized_ = false;
+    cudaGraphExec_t exec_ = nullptr;
+};
+
+// ------------------------------------------------------------- teacher dev
+struct ConvDev {
+    int cin = 0, cout = 0, k = 0, stride = 1, pad = 0;
+    DevBuf w;            // [cout][k*k][cin]
+    DevBuf scale, shift; // inference batch-norm affine (ops.hpp:304-321)
+};
+
+struct TBlockDev {
+    int kind = 0;  // 0 conv (3x3 or 1x1), 1 residual
+    int cin = 0, hin = 0, win = 0, cout = 0, hout = 0, wout = 0;
+    ConvDev c1, c2;
+    bool has_proj = false;
+    ConvDev proj;  // 1x1 stride projection, no affine
+    int mid_h = 0, mid_w = 0;
+};
+
+ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, cudaStream_t st) {
+    ConvDev d;
+    d.cin = conv.in_channels;
+    d.cout = conv.out_channels;
+    d.k = conv.kernel;
+    d.stride = conv.stride;
+    d.pad = conv.padding;
+    const int kk = d.k * d.k;
+    std::vector<float> w(static_cast<size_t>(d.cout) * kk * d.cin);
+    for (int o = 0; o < d.cout; ++o)
+        for (int j = 0; j < d.cin; ++j)
+            for (int t = 0; t < kk; ++t)
+                w[(static_cast<size_t>(o) * kk + t) * d.cin + j] =
+                    conv.weight.data[(static_cast<size_t>(o) * d.cin + j) * kk + t];
+    d.w = upload(w, st);
+    if (bn) {
+        std::vector<float> sc(d.cout), sh(d.cout);
+        for (int j = 0; j < d.cout; ++j) {  // ops.hpp:312-314, float arithmetic
+            volatile float s = bn->moving_var.data[j] + static_cast<float>(1e-5);
+            const float inv = 1.0f / std::sqrt(static_cast<float>(s));
+            volatile float scale = bn->gamma.data[j] * inv;
+            volatile float prod = bn->moving_mean.data[j] * scale;
+            sc[j] = scale;
+            sh[j] = bn->beta.data[j] - prod;
+        }
+        d.scale = upload(sc, st);
+        d.shift = upload(sh, st);
+    }
+    return d;
+}
+
+GemmOp conv_gemm(const ConvDev& c, const float* x, int n, int ih, int iw, float* y, bool affine,
+                 const float* skip, bool relu_out) {
+    GemmOp o{};
+    o.conv = 1;
+    o.ih = ih;
+    o.iw = iw;
+    o.ic = c.cin;
+    o.ksz = c.k;
+    o.cstride = c.stride;
+    o.cpad = c.pad;
+    o.oh = (ih + 2 * c.pad - c.k) / c.stride + 1;
+    o.ow = (iw + 2 * c.pad - c.k) / c.stride + 1;
+    o.M = n * o.oh * o.ow;
+    o.N = c.cout;
+    o.K = c.k * c.k * c.cin;
+    o.A = x;
+    o.B = c.w.f();
+    o.ldb = o.K;
+    o.b_kmajor = 1;
+    o.C = y;
+    o.ldc = c.cout;
+    o.epi = 0;
+    o.ksplit = 1;
+    o.kchunk = o.K;
+    o.tiles_m = ceil_div(o.M, kGemmBM);
+    o.tiles_n = ceil_div(o.N, kGemmBN);
+    if (affine) {
+        o.scale = c.scale.f();
+        o.shift = c.shift.f();
+    }
+    o.skip = skip;
+    o.relu = relu_out ? 1 : 0;
+    return o;
+}
+
+int gemm_ctas(const GemmOp& o) { return ctas_gemm(o); }
+
+// ------------------------------------------------------------- task state
+struct UnitDims {
+    int cin, hin, win, cout, ho, wo, stride;
+};
+
+struct TaskState {
+    DistillTask task;
+    int units = 2;
+    UnitDims u[kMaxUnits];
+    int k = 0;  // block index
+    int in_row = 0, out_row = 0;
+    long long total_steps = 0;
+    std::vector<int> steps_in_epoch;  // [epochs+1], index 0 unused
+    // parameters
+    size_t nparams = 0, nstats = 0;
+    size_t off_dw[kMaxUnits], off_pw[kMaxUnits], off_g[kMaxUnits], off_b[kMaxUnits];
+    DevBuf params, grads, vel, mstats, snapshot;
+    // streams
+    DevBuf in_stream, tgt_stream, pos, eval_in;
+    // workspace
+    DevBuf d[kMaxUnits], p[kMaxUnits], gp, gd, gy;
+    DevBuf cs0, cs1, psg, psgx, pgk, ploss, wsplit;
+    DevBuf mean, inv, sg, sgx;  // [units][cout]
+    DevBuf scale, shift;        // inference affine [units][cout]
+    // bookkeeping
+    DevBuf step_loss, epoch_loss, failed, best, take, eval_acc, baseline;
+    int n_evals_planned = 0;
+    std::vector<int> eval_epochs;
+    float* w_dw(int u) const { return params.f() + off_dw[u]; }
+    float* w_pw(int u) const { return params.f() + off_pw[u]; }
+    float* w_g(int u) const { return params.f() + off_g[u]; }
+    float* w_b(int u) const { return params.f() + off_b[u]; }
+    float* g_dw(int u) const { return grads.f() + off_dw[u]; }
+    float* g_pw(int u) const { return grads.f() + off_pw[u]; }
+    float* g_g(int u) const { return grads.f() + off_g[u]; }
+    float* g_b(int u) const { return grads.f() + off_b[u]; }
+    float* mm(int uu) const { return mstats.f() + static_cast<size_t>(uu) * 2 * u[0].cout; }
+    float* mv(int uu) const { return mstats.f() + (static_cast<size_t>(uu) * 2 + 1) * u[0].cout; }
+    float* mean_u(int uu) const { return mean.f() + static_cast<size_t>(uu) * u[0].cout; }
+    float* inv_u(int uu) const { return inv.f() + static_cast<size_t>(uu) * u[0].cout; }
+    float* sg_u(int uu) const { return sg.f() + static_cast<size_t>(uu) * u[0].cout; }
+    float* sgx_u(int uu) const { return sgx.f() + static_cast<size_t>(uu) * u[0].cout; }
+    float* scale_u(int uu) const { return scale.f() + static_cast<size_t>(uu) * u[0].cout; }
+    float* shift_u(int uu) const { return shift.f() + static_cast<size_t>(uu) * u[0].cout; }
+};
+
+int split_count(long long kdim) { return std::max(1, std::min(64, ceil_div(kdim, 512))); }
+int split_chunk(long long kdim, int ks) { return ((ceil_div(kdim, ks) + kGemmBK - 1) / kGemmBK) * kGemmBK; }
+
+}  // namespace
+
+// ================================================================= Impl ====
+struct Engine::Impl {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    bool has_teacher = false;
+    Network net;
+    std::vector<TBlockDev> tblocks;
+    // classifier
+    DevBuf cls_kinds, cls_w, cls_b;
+    int cls_layers = 0, cls_maxw = 0, cls_in_c = 0, cls_hw = 0;
+    // dataset
+    DevBuf images, labels, eval_labels;
+    int count = 0, dc = 0, dh = 0, dw = 0, classes = 0;
+    RunTiming timing;
+
+    explicit Impl(int device) : dev(device) {
+        PBKD_CUDA(cudaSetDevice(dev));
+        PBKD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    }
+    ~Impl() {
+        cudaSetDevice(dev);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    int max_row() const {
+        int m = net.in_c * net.in_h * net.in_w;
+        for (const TBlockDev& b : tblocks) m = std::max(m, b.cout * b.hout * b.wout);
+        for (const TBlockDev& b : tblocks) m = std::max(m, b.cout * b.mid_h * b.mid_w);
+        return m;
+    }
+
+    void load_teacher(const Network& n) {
+        PBKD_CUDA(cudaSetDevice(dev));
+        net = n;
+        tblocks.clear();
+        int c = n.in_c, h = n.in_h, w = n.in_w;
+        for (const Block& b : n.blocks) {
+            TBlockDev d;
+            d.cin = c;
+            d.hin = h;
+            d.win = w;
+            d.cout = b.out_channels;
+            if (b.spec_kind == "residual3x3") {
+                d.kind = 1;
+                d.c1 = conv_upload(b.layers[0], &b.layers[1], st);
+                d.c2 = conv_upload(b.layers[3], &b.layers[4], st);
+                const pbkd::LayerParams& add = b.layers[5];
+                if (!add.weight.data.empty()) {
+                    d.has_proj = true;
+                    pbkd::LayerParams pl = pbkd::make_conv_layer(LayerKind::Conv1x1, add.in_channels,
+                                                                 add.out_channels, 1, add.stride, 0);
+                    pl.weight = add.weight;
+                    d.proj = conv_upload(pl, nullptr, st);
+                }
+                d.mid_h = (h + 2 * d.c1.pad - 3) / d.c1.stride + 1;
+                d.mid_w = (w + 2 * d.c1.pad - 3) / d.c1.stride + 1;
+                d.hout = d.mid_h;
+                d.wout = d.mid_w;
+            } else {
+                d.kind = 0;
+                d.c1 = conv_upload(b.layers[0], &b.layers[1], st);
+                d.hout = (h + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
+                d.wout = (w + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
+            }
+            c = d.cout;
+            h = d.hout;
+            w = d.wout;
+            tblocks.push_back(std::move(d));
+        }
+        cls_in_c = c;
+        cls_hw = h * w;
+        std::vector<int> kinds;
+        std::vector<float> cw, cb;
+        int width = c;
+        cls_maxw = c;
+        for (const pbkd::LayerParams& l : n.classifier.layers) {
+            if (l.kind == LayerKind::GlobalAvgPool) {
+                kinds.push_back(0);
+                kinds.push_back(width);
+            } else if (l.kind == LayerKind::ReLU) {
+                kinds.push_back(1);
+                kinds.push_back(width);
+            } else {
+                kinds.push_back(2);
+                kinds.push_back(l.out_channels);
+                cw.insert(cw.end(), l.weight.data.begin(), l.weight.data.end());
+                cb.insert(cb.end(), l.bias.data.begin(), l.bias.data.end());
+                width = l.out_channels;
+                cls_maxw = std::max(cls_maxw, width);
+            }
+        }
+        cls_layers = static_cast<int>(n.classifier.layers.size());
+        cls_kinds = upload(kinds, st);
+        cls_w = upload(cw, st);
+        cls_b = upload(cb, st);
+        PBKD_CUDA(cudaStreamSynchronize(st));
+        has_teacher = true;
+    }
+
+    // Teacher block j (0-based) forward on n samples: x -> y.  scratch t1/sk.
+    void teacher_block(Program& P, int j, const float* x, float* y, int n, float* t1, float* sk) {
+        const TBlockDev& b = tblocks[static_cast<size_t>(j)];
+        auto one = [](const GemmOp& o) {
+            return std::vector<GemmOp>{o};
+        };
+        std::function<int(const GemmOp&)> cf = gemm_ctas;
+        if (b.kind == 0) {
+            P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.c1, x, n, b.hin, b.win, y, true, nullptr, true)), cf);
+            return;
+        }
+        P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true)), cf);
+        const float* skip = x;
+        if (b.has_proj) {
+            P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.proj, x, n, b.hin, b.win, sk, false, nullptr, false)), cf);
+            skip = sk;
+        }
+        P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.c2, t1, n, b.mid_h, b.mid_w, y, true, skip, true)), cf);
+    }
+
+    void load_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {
+        PBKD_CUDA(cudaSetDevice(dev));
+        const size_t sz = static_cast<size_t>(n) * c * h * w;
+        images.alloc(sz * sizeof(float));
+        PBKD_CUDA(cudaMemcpyAsync(images.p, img, sz * sizeof(float),
+                                  on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        labels.alloc(static_cast<size_t>(n) * sizeof(int));
+        PBKD_CUDA(cudaMemcpyAsync(labels.p, lab, static_cast<size_t>(n) * sizeof(int),
+                                  cudaMemcpyHostToDevice, st));
+        PBKD_CUDA(cudaStreamSynchronize(st));
+        count = n;
+        dc = c;
+        dh = h;
+        dw = w;
+        classes = cls;
+    }
+
+    // ------------------------------------------------------------ tasks --
+    void validate(const DistillTask& t) const {  // distill.cpp:86-100
+        if (t.epochs < 1) throw SpecError("epochs must be at least 1");
+        if (t.eval_every < 1) throw SpecError("eval_every must be at least 1");
+        if (t.batch_size < 1) throw SpecError("batch_size must be at least 1");
+        if (t.lambda_local < 0) throw SpecError("lambda_local must be non-negative");
+        if (t.threshold < 0.0 || t.threshold > 1.0) throw SpecError("threshold must lie in [0,1]");
+        if (t.max_steps < 0) throw SpecError("max_steps must be non-negative");
+        const std::vector<int> ok = pbkd::identify_replaceable(net);
+        if (!std::binary_search(ok.begin(), ok.end(), t.block_index))
+            throw SpecError("block " + std::to_string(t.block_index) + " of '" + net.name +
+                            "' is not replaceable");
+        if (t.loss_mode == pbkd::LossMode::Combined && !net.has_classifier())
+            throw SpecError("combined loss needs a network with a classifier");
+        if (t.loss_mode == pbkd::LossMode::Combined)
+            throw SpecError("combined loss mode is not implemented on the GPU path (LocalOnly only)");
+        if (t.kind == pbkd::CandidateKind::TwoLayerSkip || t.kind == pbkd::CandidateKind::ThreeLayerSkip)
+            throw SpecError(std::string("candidate ") + pbkd::candidate_kind_name(t.kind) +
+                            " is not implemented on the GPU path");
+    }
+
+    void init_task(TaskState& s, const DistillTask& t, int ntrain, int neval) {
+        s.task = t;
+        s.k = t.block_index;
+        const TBlockDev& tb = tblocks[static_cast<size_t>(s.k) - 1];
+        s.units = (t.kind == pbkd::CandidateKind::ThreeLayer) ? 3 : 2;
+        const int ho = (tb.hin - 1) / tb.c1.stride + 1, wo = (tb.win - 1) / tb.c1.stride + 1;
+        for (int u = 0; u < s.units; ++u)
+            s.u[u] = u == 0 ? UnitDims{tb.cin, tb.hin, tb.win, tb.cout, ho, wo, tb.c1.stride}
+                            : UnitDims{tb.cout, ho, wo, tb.cout, ho, wo, 1};
+        if (ho != tb.hout || wo != tb.wout) throw SpecError("candidate output shape differs from teacher block");
+        s.in_row = tb.cin * tb.hin * tb.win;
+        s.out_row = tb.cout * ho * wo;
+        const int B = t.batch_size;
+        const int spe = ceil_div(ntrain, B);
+        long long total = static_cast<long long>(t.epochs) * spe;
+        if (t.max_steps > 0) total = std::min<long long>(total, t.max_steps);
+        s.total_steps = total;
+        s.steps_in_epoch.assign(static_cast<size_t>(t.epochs) + 1, 0);
+        for (int e = 1; e <= t.epochs; ++e)
+            s.steps_in_epoch[e] = static_cast<int>(std::max<long long>(0, std::min<long long>(spe, total - static_cast<long long>(e - 1) * spe)));
+        s.eval_epochs.clear();
+        s.eval_epochs.push_back(0);
+        for (int e = 1; e <= t.epochs; ++e)
+            if (s.steps_in_epoch[e] > 0 && e % t.eval_every == 0) s.eval_epochs.push_back(e);
+        s.n_evals_planned = static_cast<int>(s.eval_epochs.size());
+
+        // parameters: candidate init on the host (bit-exact), device layout
+        pbkd::ReplacementBlock cand = pbkd::build_candidate(t.kind, tb.cin, tb.cout, tb.c1.stride,
+                                                            pbkd::mix_seed(t.seed, 0));
+        std::vector<float> host;
+        std::vector<float> stats;
+        size_t li = 0;
+        for (int u = 0; u < s.units; ++u) {
+            const pbkd::LayerParams& dwl = cand.block.layers[li];
+            const pbkd::LayerParams& pwl = cand.block.layers[li + 1];
+            const pbkd::LayerParams& bnl = cand.block.layers[li + 2];
+            li += 4;
+            const int ci = s.u[u].cin, co = s.u[u].cout;
+            s.off_dw[u] = host.size();
+            for (int tap = 0; tap < 9; ++tap)
+                for (int c = 0; c < ci; ++c) host.push_back(dwl.weight.data[static_cast<size_t>(c) * 9 + tap]);
+            s.off_pw[u] = host.size();
+            host.insert(host.end(), pwl.weight.data.begin(), pwl.weight.data.end());
+            s.off_g[u] = host.size();
+            host.insert(host.end(), bnl.gamma.data.begin(), bnl.gamma.data.end());
+            s.off_b[u] = host.size();
+            host.insert(host.end(), bnl.beta.data.begin(), bnl.beta.data.end());
+            (void)co;
+            stats.insert(stats.end(), bnl.moving_mean.data.begin(), bnl.moving_mean.data.end());
+            stats.insert(stats.end(), bnl.moving_var.data.begin(), bnl.moving_var.data.end());
+        }
+        while (host.size() % 4) host.push_back(0.0f);  // vector-friendly padding (never trained)
+        s.nparams = host.size();
+        s.nstats = stats.size();
+        s.params = upload(host, st);
+        s.grads.alloc(s.nparams * sizeof(float));
+        PBKD_CUDA(cudaMemsetAsync(s.grads.p, 0, s.nparams * sizeof(float), st));
+        s.vel.alloc(s.nparams * sizeof(float));
+        PBKD_CUDA(cudaMemsetAsync(s.vel.p, 0, s.nparams * sizeof(float), st));
+        s.mstats = upload(stats, st);
+        s.snapshot.alloc((s.nparams + s.nstats) * sizeof(float));
+
+        // streams and workspace
+        s.in_stream.alloc(static_cast<size_t>(ntrain) * s.in_row * sizeof(float));
+        s.tgt_stream.alloc(static_cast<size_t>(ntrain) * s.out_row * sizeof(float));
+        s.pos.alloc(static_cast<size_t>(ntrain) * sizeof(int));
+        s.eval_in.alloc(static_cast<size_t>(std::max(neval, 1)) * s.in_row * sizeof(float));
+        const long long M = static_cast<long long>(B) * ho * wo;
+        const int cin = tb.cin, cout = tb.cout, cmax = std::max(cin, cout);
+        for (int u = 0; u < s.units; ++u) {
+            s.d[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
+            s.p[u].alloc(static_cast<size_t>(M) * cout * sizeof(float));
+        }
+        s.gp.alloc(static_cast<size_t>(M) * cout * sizeof(float));
+        s.gd.alloc(static_cast<size_t>(M) * cmax * sizeof(float));
+        s.gy.alloc(static_cast<size_t>(M) * cout * sizeof(float));
+        const int tiles = ceil_div(M, kGemmBM);
+        s.cs0.alloc(static_cast<size_t>(tiles) * cout * sizeof(float));
+        s.cs1.alloc(static_cast<size_t>(tiles) * cout * sizeof(float));
+        int pc = 1;
+        for (int u = 0; u < s.units; ++u) pc = std::max(pc, rows_part_ctas(M, s.u[u].cin));
+        pc = std::max(pc, rows_part_ctas(M, cout));
+        s.psg.alloc(static_cast<size_t>(pc) * cout * sizeof(float));
+        s.psgx.alloc(static_cast<size_t>(pc) * cout * sizeof(float));
+        s.pgk.alloc(static_cast<size_t>(pc) * 9 * cmax * sizeof(float));
+        s.ploss.alloc(static_cast<size_t>(pc) * sizeof(float));
+        s.wsplit.alloc(static_cast<size_t>(split_count(M)) * cout * cmax * sizeof(float));
+        s.mean.alloc(static_cast<size_t>(s.units) * cout * sizeof(float));
+        s.inv.alloc(static_cast<size_t>(s.units) * cout * sizeof(float));
+        s.sg.alloc(static_cast<size_t>(s.units) * cout * sizeof(float));
+        s.sgx.alloc(static_cast<size_t>(s.units) * cout * sizeof(float));
+        s.scale.alloc(static_cast<size_t>(s.units) * cout * sizeof(float));
+        s.shift.alloc(static_cast<size_t>(s.units) * cout * sizeof(float));
+        s.step_loss.alloc(static_cast<size_t>(std::max<long long>(total, 1)) * sizeof(float));
+        PBKD_CUDA(cudaMemsetAsync(s.step_loss.p, 0, static_cast<size_t>(std::max<long long>(total, 1)) * sizeof(float), st));
+        s.epoch_loss.alloc(static_cast<size_t>(spe) * sizeof(float));
+        s.failed.alloc(sizeof(int));
+        PBKD_CUDA(cudaMemsetAsync(s.failed.p, 0, sizeof(int), st));
+        s.best.alloc(sizeof(double));
+        const double neg1 = -1.0;
+        PBKD_CUDA(cudaMemcpyAsync(s.best.p, &neg1, sizeof(double), cudaMemcpyHostToDevice, st));
+        s.take.alloc(sizeof(int));
+        s.eval_acc.alloc(static_cast<size_t>(s.n_evals_planned) * sizeof(double));
+        s.baseline.alloc(static_cast<size_t>(spe) * sizeof(double));
+    }
+
+    // ---------------------------------------------------------- step ops --
+    void add_step(Program& P, std::vector<TaskState*>& act, int step, long long gstep_unused, int ntrain,
+                  const std::vector<long long>& gsteps) {
+        (void)gstep_unused;
+        if (act.empty()) return;
+        const int U = act[0]->units;
+        struct Ctx {
+            TaskState* s;
+            int n;        // samples this step
+            long long M;  // rows
+            const float* x0;
+            const float* t;
+            const int* failed;
+            long long gstep;
+        };
+        std::vector<Ctx> cx;
+        for (size_t i = 0; i < act.size(); ++i) {
+            TaskState* s = act[i];
+            const int B = s->task.batch_size;
+            const int n = std::min(B, ntrain - step * B);
+            Ctx c{s, n, static_cast<long long>(n) * s->u[0].ho * s->u[0].wo,
+                  s->in_stream.f() + static_cast<size_t>(step) * B * s->in_row,
+                  s->tgt_stream.f() + static_cast<size_t>(step) * B * s->out_row, s->failed.i(), gsteps[i]};
+            cx.push_back(c);
+        }
+        std::function<int(const GemmOp&)> gc = gemm_ctas;
+        // ---- forward
+        for (int u = 0; u < U; ++u) {
+            std::vector<DwFwdOp> dws;
+            std::vector<GemmOp> gms;
+            std::vector<BnStatOp> bns;
+            for (Ctx& c : cx) {
+                TaskState& s = *c.s;
+                const UnitDims& d = s.u[u];
+                DwFwdOp o{};
+                o.x = u == 0 ? c.x0 : s.p[u - 1].f();
+                o.w = s.w_dw(u);
+                o.y = s.d[u].f();
+                o.n = c.n;
+                o.h = d.hin;
+                o.wd = d.win;
+                o.c = d.cin;
+                o.ho = d.ho;
+                o.wo = d.wo;
+                o.stride = d.stride;
+                o.pad = 1;
+                o.pro = u == 0 ? 0 : 1;
+                if (u > 0) {
+                    o.pa = s.mean_u(u - 1);
+                    o.pb = s.inv_u(u - 1);
+                    o.pc = s.w_g(u - 1);
+                    o.pd = s.w_b(u - 1);
+                }
+                o.failed = c.failed;
+                dws.push_back(o);
+                GemmOp g{};
+                g.M = static_cast<int>(c.M);
+                g.N = d.cout;
+                g.K = d.cin;
+                g.A = s.d[u].f();
+                g.lda = d.cin;
+                g.a_kmajor = 1;
+                g.B = s.w_pw(u);
+                g.ldb = d.cin;
+                g.b_kmajor = 1;
+                g.C = s.p[u].f();
+                g.ldc = d.cout;
+                g.epi = 1;
+                g.part0 = s.cs0.f();
+                g.part1 = s.cs1.f();
+                g.ksplit = 1;
+                g.kchunk = d.cin;
+                g.tiles_m = ceil_div(c.M, kGemmBM);
+                g.tiles_n = ceil_div(d.cout, kGemmBN);
+                g.failed = c.failed;
+                gms.push_back(g);
+                BnStatOp b{};
+                b.part_sum = s.cs0.f();
+                b.part_sq = s.cs1.f();
+                b.tiles = g.tiles_m;
+                b.c = d.cout;
+                b.m = c.M;
+                b.mean = s.mean_u(u);
+                b.inv = s.inv_u(u);
+                b.mm = s.mm(u);
+                b.mv = s.mv(u);
+                b.update_moving = 1;
+                b.failed = c.failed;
+                bns.push_back(b);
+            }
+            P.grouped<DwFwdOp>(launch_dw_fwd, dws, ctas_dw_fwd);
+            P.grouped<GemmOp>(launch_gemm, gms, gc);
+            P.grouped<BnStatOp>(launch_bn_stat, bns, [](const BnStatOp& o) { return ceil_div(o.c, kThreads); });
+        }
+        // ---- loss and last batch-norm backward sums
+        {
+            std::vector<LossOp> ls;
+            std::vector<BnBwdFinOp> fs;
+            for (Ctx& c : cx) {
+                TaskState& s = *c.s;
+                const int u = U - 1;
+                const int cout = s.u[u].cout;
+                LossOp o{};
+                o.p = s.p[u].f();
+                o.t = c.t;
+                o.mean = s.mean_u(u);
+                o.inv = s.inv_u(u);
+                o.gamma = s.w_g(u);
+                o.beta = s.w_b(u);
+                o.part_sg = s.psg.f();
+                o.part_sgx = s.psgx.f();
+                o.part_loss = s.ploss.f();
+                o.rows = static_cast<int>(c.M);
+                o.c = cout;
+                o.ctas = rows_part_ctas(c.M, cout);
+                o.rows_per = rows_part_per(c.M, o.ctas);
+                const size_t count = static_cast<size_t>(c.M) * cout;
+                o.kmse = (1.0f * 2.0f) / static_cast<float>(count);
+                o.failed = c.failed;
+                ls.push_back(o);
+                BnBwdFinOp f{};
+                f.part_sg = s.psg.f();
+                f.part_sgx = s.psgx.f();
+                f.part_loss = s.ploss.f();
+                f.ctas = o.ctas;
+                f.c = cout;
+                f.sg = s.sg_u(u);
+                f.sgx = s.sgx_u(u);
+                f.ggamma = s.g_g(u);
+                f.gbeta = s.g_b(u);
+                f.loss_out = s.epoch_loss.f() + step;
+                f.count = static_cast<double>(count);
+                f.failed = s.failed.i();
+                fs.push_back(f);
+            }
+            P.grouped<LossOp>(launch_loss, ls, [](const LossOp& o) { return o.ctas; });
+            P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fs, [](const BnBwdFinOp& o) { return ceil_div(o.c, kThreads); });
+        }
+        // ---- backward
+        for (int u = U - 1; u >= 0; --u) {
+            std::vector<BnBwdApplyOp> aps;
+            std::vector<GemmOp> dg, wg;
+            std::vector<ReduceOp> wr, kr;
+            std::vector<DwBwdOp> dbs;
+            std::vector<DwGkOp> gks;
+            std::vector<BnBwdFinOp> fins;
+            for (Ctx& c : cx) {
+                TaskState& s = *c.s;
+                const UnitDims& d = s.u[u];
+                BnBwdApplyOp a{};
+                a.p = s.p[u].f();
+                a.t = u == U - 1 ? c.t : nullptr;
+                a.gin = u == U - 1 ? nullptr : s.gy.f();
+                a.gout = s.gp.f();
+                a.mean = s.mean_u(u);
+                a.inv = s.inv_u(u);
+                a.gamma = s.w_g(u);
+                a.beta = s.w_b(u);
+                a.sg = s.sg_u(u);
+                a.sgx = s.sgx_u(u);
+                a.total = c.M * d.cout;
+                a.c = d.cout;
+                a.inv_m = 1.0f / static_cast<float>(c.M);
+                a.kmse = (1.0f * 2.0f) / static_cast<float>(static_cast<size_t>(c.M) * d.cout);
+                a.failed = c.failed;
+                aps.push_back(a);
+                // dgrad: gd[m][j] = sum_o gp[m][o] W[o][j]
+                GemmOp g{};
+                g.M = static_cast<int>(c.M);
+                g.N = d.cin;
+                g.K = d.cout;
+                g.A = s.gp.f();
+                g.lda = d.cout;
+                g.a_kmajor = 1;
+                g.B = s.w_pw(u);
+                g.ldb = d.cin;
+                g.b_kmajor = 0;
+                g.C = s.gd.f();
+                g.ldc = d.cin;
+                g.epi = 0;
+                g.ksplit = 1;
+                g.kchunk = d.cout;
+                g.tiles_m = ceil_div(c.M, kGemmBM);
+                g.tiles_n = ceil_div(d.cin, kGemmBN);
+                g.failed = c.failed;
+                dg.push_back(g);
+                // wgrad: gW[o][j] = sum_m gp[m][o] d[m][j]  (split-K over rows)
+                GemmOp w{};
+                w.M = d.cout;
+                w.N = d.cin;
+                w.K = static_cast<int>(c.M);
+                w.A = s.gp.f();
+                w.lda = d.cout;
+                w.a_kmajor = 0;
+                w.B = s.d[u].f();
+                w.ldb = d.cin;
+                w.b_kmajor = 0;
+                w.C = s.wsplit.f();
+                w.ldc = d.cin;
+                w.epi = 2;
+                w.ksplit = split_count(c.M);
+                w.kchunk = split_chunk(c.M, w.ksplit);
+                w.ksplit = ceil_div(c.M, w.kchunk);
+                w.tiles_m = ceil_div(d.cout, kGemmBM);
+                w.tiles_n = ceil_div(d.cin, kGemmBN);
+                w.failed = c.failed;
+                wg.push_back(w);
+                ReduceOp r{};
+                r.part = s.wsplit.f();
+                r.out = s.g_pw(u);
+                r.parts = w.ksplit;
+                r.width = d.cout * d.cin;
+                r.failed = c.failed;
+                wr.push_back(r);
+                if (u > 0) {
+                    DwBwdOp b{};
+                    b.gy = s.gd.f();
+                    b.xp = s.p[u - 1].f();
+                    b.w = s.w_dw(u);
+                    b.gyprev = s.gy.f();
+                    b.part_gk = s.pgk.f();
+                    b.part_sg = s.psg.f();
+                    b.part_sgx = s.psgx.f();
+                    b.mean = s.mean_u(u - 1);
+                    b.inv = s.inv_u(u - 1);
+                    b.gamma = s.w_g(u - 1);
+                    b.beta = s.w_b(u - 1);
+                    b.n = c.n;
+                    b.h = d.hin;
+                    b.wd = d.win;
+                    b.c = d.cin;
+                    b.ctas = rows_part_ctas(c.M, d.cin);
+                    b.rows_per = rows_part_per(c.M, b.ctas);
+                    b.failed = c.failed;
+                    dbs.push_back(b);
+                    ReduceOp kk{};
+                    kk.part = s.pgk.f();
+                    kk.out = s.g_dw(u);
+                    kk.parts = b.ctas;
+                    kk.width = 9 * d.cin;
+                    kk.failed = c.failed;
+                    kr.push_back(kk);
+                    BnBwdFinOp f{};
+                    f.part_sg = s.psg.f();
+                    f.part_sgx = s.psgx.f();
+                    f.ctas = b.ctas;
+                    f.c = d.cin;
+                    f.sg = s.sg_u(u - 1);
+                    f.sgx = s.sgx_u(u - 1);
+                    f.ggamma = s.g_g(u - 1);
+                    f.gbeta = s.g_b(u - 1);
+                    f.failed = s.failed.i();
+                    fins.push_back(f);
+                } else {
+                    DwGkOp b{};
+                    b.gy = s.gd.f();
+                    b.x = c.x0;
+                    b.part_gk = s.pgk.f();
+                    b.n = c.n;
+                    b.h = d.hin;
+                    b.wd = d.win;
+                    b.c = d.cin;
+                    b.ho = d.ho;
+                    b.wo = d.wo;
+                    b.stride = d.stride;
+                    b.pad = 1;
+                    b.ctas = rows_part_ctas(c.M, d.cin);
+                    b.rows_per = rows_part_per(c.M, b.ctas);
+                    b.failed = c.failed;
+                    gks.push_back(b);
+                    ReduceOp kk{};
+                    kk.part = s.pgk.f();
+                    kk.out = s.g_dw(u);
+                    kk.parts = b.ctas;
+                    kk.width = 9 * d.cin;
+                    kk.failed = c.failed;
+                    kr.push_back(kk);
+                }
+            }
+            auto red_ctas = [](const ReduceOp& o) { return ceil_div(o.width, kThreads); };
+            P.grouped<BnBwdApplyOp>(launch_bn_bwd_apply, aps, [](const BnBwdApplyOp& o) { return ctas_elem(o.total); });
+            P.grouped<GemmOp>(launch_gemm, dg, gc);
+            P.grouped<GemmOp>(launch_gemm, wg, gc);
+            P.grouped<ReduceOp>(launch_reduce, wr, red_ctas);
+            if (u > 0) {
+                P.grouped<DwBwdOp>(launch_dw_bwd, dbs, [](const DwBwdOp& o) { return o.ctas; });
+                P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
+                P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fins, [](const BnBwdFinOp& o) { return ceil_div(o.c, kThreads); });
+            } else {
+                P.grouped<DwGkOp>(launch_dw_gk, gks, [](const DwGkOp& o) { return o.ctas; });
+                P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
+            }
+        }
+        // ---- optimizer
+        std::vector<SgdOp> sg;
+        for (Ctx& c : cx) {
+            TaskState& s = *c.s;
+            SgdOp o{};
+            o.w = s.params.f();
+            o.v = s.vel.f();
+            o.g = s.grads.f();
+            o.n = static_cast<long long>(s.nparams);
+            o.lr = s.task.lr;
+            o.mom = s.task.momentum;
+            o.failed = c.failed;
+            sg.push_back(o);
+        }
+        P.grouped<SgdOp>(launch_sgd, sg, [](const SgdOp& o) { return ctas_elem(o.n); });
+    }
+
+    // Teacher pass over `n` samples (dataset indices at d_idx), scattering
+    // boundary activations: for each task, boundary k-1 -> its input stream,
+    // boundary k -> its target stream, rows placed at pos[t0 + i].
+    struct Sink {
+        int boundary;  // 0 = network input
+        float* dst;
+        const int* pos;
+        int width;
+    };
+    void add_teacher_pass(Program& P, const int* d_idx, int n, const std::vector<Sink>& sinks,
+                          int chunk, float* ping, float* pong, float* t1, float* sk) {
+        int kmax = 0;
+        for (const Sink& s : sinks) kmax = std::max(kmax, s.boundary);
+        const int in_c = net.in_c, in_h = net.in_h, in_w = net.in_w;
+        const float* img = images.f();
+        for (int t0 = 0; t0 < n; t0 += chunk) {
+            const int nc = std::min(chunk, n - t0);
+            const int* idx = d_idx + t0;
+            P.raw([=](cudaStream_t s) { launch_gather_nhwc(img, idx, nc, in_c, in_h, in_w, ping, s); });
+            float* cur = ping;
+            float* nxt = pong;
+            for (int j = 0; j <= kmax; ++j) {
+                if (j > 0) {
+                    teacher_block(P, j - 1, cur, nxt, nc, t1, sk);
+                    std::swap(cur, nxt);
+                }
+                std::vector<ScatterOp> sc;
+                for (const Sink& s : sinks)
+                    if (s.boundary == j) sc.push_back(ScatterOp{cur, s.dst, s.pos + t0, nc, s.width, 0});
+                P.grouped<ScatterOp>(launch_scatter, sc, [](const ScatterOp&) { return kScatterCtas; });
+            }
+        }
+    }
+
+    // Student inference over `rows_n` samples of x (task s), output into out.
+    void add_student_infer(Program& P, TaskState& s, const float* x, int nsamp, float* bufa,
+                           float* bufb, float* out) {
+        const int U = s.units;
+        for (int u = 0; u < U; ++u) {
+            const UnitDims& d = s.u[u];
+            const long long M = static_cast<long long>(nsamp) * d.ho * d.wo;
+            float* scale = s.scale_u(u);
+            float* shift = s.shift_u(u);
+            float* g = s.w_g(u);
+            float* b = s.w_b(u);
+            float* mmv = s.mm(u);
+            float* mvv = s.mv(u);
+            const int cout = d.cout;
+            P.raw([=](cudaStream_t st2) { launch_bn_infer_prep(g, b, mmv, mvv, cout, scale, shift, st2); });
+            DwFwdOp o{};
+            o.x = u == 0 ? x : bufb;
+            o.w = s.w_dw(u);
+            o.y = bufa;
+            o.n = nsamp;
+            o.h = d.hin;
+            o.wd = d.win;
+            o.c = d.cin;
+            o.ho = d.ho;
+            o.wo = d.wo;
+            o.stride = d.stride;
+            o.pad = 1;
+            o.pro = u == 0 ? 0 : 2;
+            if (u > 0) {
+                o.pa = s.scale_u(u - 1);
+                o.pb = s.shift_u(u - 1);
+            }
+            P.grouped<DwFwdOp>(launch_dw_fwd, {o}, ctas_dw_fwd);
+            GemmOp gm{};
+            gm.M = static_cast<int>(M);
+            gm.N = cout;
+            gm.K = d.cin;
+            gm.A = bufa;
+            gm.lda = d.cin;
+            gm.a_kmajor = 1;
+            gm.B = s.w_pw(u);
+            gm.ldb = d.cin;
+            gm.b_kmajor = 1;
+            gm.C = bufb;
+            gm.ldc = cout;
+            gm.ksplit = 1;
+            gm.kchunk = d.cin;
+            gm.tiles_m = ceil_div(M, kGemmBM);
+            gm.tiles_n = ceil_div(cout, kGemmBN);
+            std::function<int(const GemmOp&)> gc = gemm_ctas;
+            P.grouped<GemmOp>(launch_gemm, {gm}, gc);
+            if (u == U - 1) {
+                const long long tot = M * cout;
+                P.raw([=](cudaStream_t st2) { launch_bn_infer_relu(bufb, out, tot, cout, scale, shift, st2); });
+            }
+        }
+    }
+
+    std::vector<TaskOutcome> run(const std::vector<DistillTask>& tasks, const std::vector<int>& train_idx,
+                                 const std::vector<int>& eval_idx, const RunOptions& opt);
+    void run_group(std::vector<TaskState*>& ts, const std::vector<int>& train_idx,
+                   const std::vector<int>& eval_idx, const RunOptions& opt, DevBuf& d_train,
+                   DevBuf& d_eval, DevBuf& d_iota);
+};
+
+// =============================================================== run ======
+std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks,
+                                           const std::vector<int>& train_idx,
+                                           const std::vector<int>& eval_idx, const RunOptions& opt) {
+    PBKD_CUDA(cudaSetDevice(dev));
+    if (!has_teacher) throw std::logic_error("engine: no teacher loaded");
+    if (count == 0) throw std::logic_error("engine: no dataset loaded");
+    if (train_idx.empty()) throw SpecError("training split is empty");
+    if (eval_idx.empty()) throw SpecError("evaluation split is empty");
+    for (int i : train_idx)
+        if (i < 0 || i >= count) throw std::out_of_range("gather_batch: index out of range");
+    for (int i : eval_idx)
+        if (i < 0 || i >= count) throw std::out_of_range("gather_batch: index out of range");
+    if (dc != net.in_c || dh != net.in_h || dw != net.in_w)
+        throw pbkd::ShapeError("dataset image shape does not match the network input");
+    for (const DistillTask& t : tasks) validate(t);
+    const int ntrain = static_cast<int>(train_idx.size());
+    const int neval = static_cast<int>(eval_idx.size());
+    std::vector<std::unique_ptr<TaskState>> states;
+    for (const DistillTask& t : tasks) {
+        states.push_back(std::make_unique<TaskState>());
+        init_task(*states.back(), t, ntrain, neval);
+    }
+    DevBuf d_train = upload(train_idx, st), d_eval = upload(eval_idx, st);
+    std::vector<int> iota(static_cast<size_t>(std::max(ntrain, neval)));
+    std::iota(iota.begin(), iota.end(), 0);
+    DevBuf d_iota = upload(iota, st);
+    // group by (batch size, units) -- lockstep requires equal step geometry
+    std::map<std::pair<int, int>, std::vector<TaskState*>> groups;
+    for (auto& s : states) groups[{s->task.batch_size, s->units}].push_back(s.get());
+    timing = RunTiming{};
+    for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota);
+
+    // ---- read back and assemble train_block results
+    std::vector<TaskOutcome> out;
+    for (auto& sp : states) {
+        TaskState& s = *sp;
+        TaskOutcome r;
+        r.block_index = s.k;
+        r.kind = pbkd::candidate_kind_name(s.task.kind);
+        const int B = s.task.batch_size;
+        const int spe = ceil_div(ntrain, B);
+        std::vector<float> losses(static_cast<size_t>(std::max<long long>(s.total_steps, 1)));
+        PBKD_CUDA(cudaMemcpy(losses.data(), s.step_loss.p, losses.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        losses.resize(static_cast<size_t>(s.total_steps));
+        std::vector<double> accs(static_cast<size_t>(s.n_evals_planned));
+        PBKD_CUDA(cudaMemcpy(accs.data(), s.eval_acc.p, accs.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        std::vector<double> base(static_cast<size_t>(spe));
+        PBKD_CUDA(cudaMemcpy(base.data(), s.baseline.p, base.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        double best = -1.0;
+        PBKD_CUDA(cudaMemcpy(&best, s.best.p, sizeof(double), cudaMemcpyDeviceToHost));
+        std::vector<float> fin(s.nparams + s.nstats), snap(s.nparams + s.nstats);
+        PBKD_CUDA(cudaMemcpy(fin.data(), s.params.p, s.nparams * sizeof(float), cudaMemcpyDeviceToHost));
+        PBKD_CUDA(cudaMemcpy(fin.data() + s.nparams, s.mstats.p, s.nstats * sizeof(float), cudaMemcpyDeviceToHost));
+        PBKD_CUDA(cudaMemcpy(snap.data(), s.snapshot.p, snap.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        auto to_ref_order = [&](const std::vector<float>& flat) {
+            std::vector<float> o;
+            for (int u = 0; u < s.units; ++u) {
+                const int ci = s.u[u].cin, co = s.u[u].cout;
+                for (int c = 0; c < ci; ++c)
+                    for (int tap = 0; tap < 9; ++tap) o.push_back(flat[s.off_dw[u] + static_cast<size_t>(tap) * ci + c]);
+                o.insert(o.end(), flat.begin() + s.off_pw[u], flat.begin() + s.off_pw[u] + static_cast<size_t>(co) * ci);
+                o.insert(o.end(), flat.begin() + s.off_g[u], flat.begin() + s.off_g[u] + co);
+                o.insert(o.end(), flat.begin() + s.off_b[u], flat.begin() + s.off_b[u] + co);
+                const size_t st0 = s.nparams + static_cast<size_t>(u) * 2 * co;
+                o.insert(o.end(), flat.begin() + st0, flat.begin() + st0 + 2 * co);
+            }
+            return o;
+        };
+        r.final_block = to_ref_order(fin);
+        r.step_losses = losses;
+        if (opt.baseline_and_eval) {
+            // distill.cpp:166-192: mean over batches of float batch losses
+            double sum = 0.0;
+            for (int b = 0; b < spe; ++b) {
+                const int n = std::min(B, ntrain - b * B);
+                const double cnt = static_cast<double>(static_cast<size_t>(n) * s.out_row);
+                sum += static_cast<double>(static_cast<float>(base[b] / cnt));
+            }
+            r.loss_history.push_back(sum / spe);
+            r.final_local_loss = sum / spe;
+            r.eval_history.push_back({0, accs[0]});
+        }
+        long long g = 0;
+        size_t ev = 1;
+        for (int e = 1; e <= s.task.epochs; ++e) {
+            const int n = s.steps_in_epoch[e];
+            if (n == 0) break;
+            double sum = 0.0;
+            for (int b = 0; b < n; ++b) {
+                const float l = losses[static_cast<size_t>(g + b)];
+                if (!std::isfinite(l)) {  // distill.cpp:236-244
+                    std::ostringstream msg;
+                    msg << "block " << s.k << " diverged at epoch " << e << " batch " << b << " (loss "
+                        << static_cast<double>(l) << ")";
+                    r.failed = true;
+                    r.failure = msg.str();
+                    break;
+                }
+                sum += static_cast<double>(l);
+            }
+            if (r.failed) break;
+            g += n;
+            r.loss_history.push_back(sum / n);
+            r.final_local_loss = sum / n;
+            if (opt.baseline_and_eval && e % s.task.eval_every == 0 && ev < accs.size())
+                r.eval_history.push_back({e, accs[ev++]});
+        }
+        if (opt.baseline_and_eval) {
+            r.best_eval = best;
+            r.best_block = to_ref_order(snap);
+        }
+        r.wall_time_s = timing.epoch_ms_total * 1e-3;
+        out.push_back(std::move(r));
+    }
+    return out;
+}
+
+__global__ void eval_decide_kernel(const int* correct, int n_eval, double* best, int* take,
+                                   double* acc_out, const int* failed) {
+    if (failed && *failed) {
+        *take = 0;
+        return;
+    }
+    const double acc = static_cast<double>(*correct) / static_cast<double>(n_eval);
+    *acc_out = acc;
+    if (acc > *best) {  // strict >, distill.cpp:160-163
+        *best = acc;
+        *take = 1;
+    } else {
+        *take = 0;
+    }
+}
+
+__global__ void snapshot_kernel(float* dst, const float* params, size_t np, const float* stats,
+                                size_t ns, const int* take) {
+    if (!*take) return;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < np + ns;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        dst[i] = i < np ? params[i] : stats[i - np];
+}
+
+void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>& train_idx,
+                             const std::vector<int>& eval_idx, const RunOptions& opt, DevBuf& d_train,
+                             DevBuf& d_eval, DevBuf& d_iota) {
+    const int ntrain = static_cast<int>(train_idx.size());
+    const int neval = static_cast<int>(eval_idx.size());
+    const int B = ts[0]->task.batch_size;
+    const int spe = ceil_div(ntrain, B);
+    const int mrow = max_row();
+    const int chunk = std::max(1, std::min(ntrain, static_cast<int>((size_t(256) << 20) / (size_t(mrow) * 4))));
+    const int ichunk = std::max(B, (chunk / B) * B);
+    const size_t wsz = static_cast<size_t>(std::max(chunk, ichunk)) * mrow * sizeof(float);
+    DevBuf ping(wsz), pong(wsz), t1(wsz), sk(wsz), ia(wsz), ib(wsz), io(wsz);
+    DevBuf correct(sizeof(int) * ts.size());
+    int emax = 0;
+    for (TaskState* s : ts) emax = std::max(emax, s->task.epochs);
+
+    auto sinks_for = [&](bool identity) {
+        std::vector<Sink> v;
+        for (TaskState* s : ts) {
+            const int* pos = identity ? d_iota.i() : s->pos.i();
+            v.push_back({s->k - 1, s->in_stream.f(), pos, s->in_row});
+            v.push_back({s->k, s->tgt_stream.f(), pos, s->out_row});
+        }
+        return v;
+    };
+
+    auto run_eval = [&](const std::vector<TaskState*>& which, const std::vector<int>& eval_slot) {
+        PBKD_CUDA(cudaMemsetAsync(correct.p, 0, sizeof(int) * ts.size(), st));
+        Program P;
+        for (size_t i = 0; i < which.size(); ++i) {
+            TaskState& s = *which[i];
+            const size_t ti = static_cast<size_t>(std::find(ts.begin(), ts.end(), which[i]) - ts.begin());
+            int* corr = correct.i() + ti;
+            for (int e0 = 0; e0 < neval; e0 += ichunk) {
+                const int ne = std::min(ichunk, neval - e0);
+                add_student_infer(P, s, s.eval_in.f() + static_cast<size_t>(e0) * s.in_row, ne, ia.f(), ib.f(), io.f());
+                float* cur = io.f();
+                for (size_t j = static_cast<size_t>(s.k); j < tblocks.size(); ++j) {
+                    float* nxt = cur == ping.f() ? pong.f() : ping.f();
+                    teacher_block(P, static_cast<int>(j), cur, nxt, ne, t1.f(), sk.f());
+                    cur = nxt;
+                }
+                const int hw = cls_hw, cc = cls_in_c, nl = cls_layers, mw = cls_maxw;
+                const int* kinds = cls_kinds.i();
+                const float* w = cls_w.f();
+                const float* b = cls_b.f();
+                const int* labs = eval_labels.i() + e0;
+                const float* xin = cur;
+                P.raw([=](cudaStream_t s2) { launch_classifier_count(xin, ne, hw, cc, kinds, nl, w, b, mw, labs, corr, s2); });
+            }
+            double* accp = s.eval_acc.d() + eval_slot[i];
+            double* bestp = s.best.d();
+            int* takep = s.take.i();
+            const int* fl = s.failed.i();
+            float* snapp = s.snapshot.f();
+            const float* pp = s.params.f();
+            const float* sp = s.mstats.f();
+            const size_t np = s.nparams, ns = s.nstats;
+            P.raw([=](cudaStream_t s2) {
+                eval_decide_kernel<<<1, 1, 0, s2>>>(corr, neval, bestp, takep, accp, fl);
+                snapshot_kernel<<<64, 256, 0, s2>>>(snapp, pp, np, sp, ns, takep);
+            });
+        }
+        P.run(st);
+    };
+
+    // ---- labels of the eval split (for the classifier count)
+    {
+        std::vector<int> lab(static_cast<size_t>(neval));
+        std::vector<int> all(static_cast<size_t>(count));
+        PBKD_CUDA(cudaMemcpy(all.data(), labels.p, all.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < neval; ++i) lab[static_cast<size_t>(i)] = all[static_cast<size_t>(eval_idx[static_cast<size_t>(i)])];
+        eval_labels = upload(lab, st);
+    }
+
+    // ---- epoch 0: baseline losses and first evaluation
+    if (opt.baseline_and_eval) {
+        {  // eval-split prefix activations (once per run)
+            Program P;
+            std::vector<Sink> sk_eval;
+            for (TaskState* s : ts) sk_eval.push_back({s->k - 1, s->eval_in.f(), d_iota.i(), s->in_row});
+            add_teacher_pass(P, d_eval.i(), neval, sk_eval, chunk, ping.f(), pong.f(), t1.f(), sk.f());
+            P.run(st);
+        }
+        {
+            Program P;
+            add_teacher_pass(P, d_train.i(), ntrain, sinks_for(true), chunk, ping.f(), pong.f(), t1.f(), sk.f());
+            for (TaskState* s : ts) {
+                for (int r0 = 0; r0 < ntrain; r0 += ichunk) {
+                    const int nr = std::min(ichunk, ntrain - r0);
+                    add_student_infer(P, *s, s->in_stream.f() + static_cast<size_t>(r0) * s->in_row, nr, ia.f(), ib.f(), io.f());
+                    const float* tg = s->tgt_stream.f() + static_cast<size_t>(r0) * s->out_row;
+                    const float* so = io.f();
+                    const long long seg = static_cast<long long>(B) * s->out_row;
+                    const long long tot = static_cast<long long>(nr) * s->out_row;
+                    const int nseg = ceil_div(nr, B);
+                    double* outp = s->baseline.d() + r0 / B;
+                    P.raw([=](cudaStream_t s2) { launch_mse_segments(so, tg, seg, tot, nseg, outp, s2); });
+                }
+            }
+            P.run(st);
+        }
+        std::vector<int> slots(ts.size(), 0);
+        run_eval(ts, slots);
+    }
+
+    // ---- training epochs
+    std::map<std::vector<int>, std::unique_ptr<Program>> graphs;
+    cudaEvent_t e0, e1, t0, t1e;
+    PBKD_CUDA(cudaEventCreate(&e0));
+    PBKD_CUDA(cudaEventCreate(&e1));
+    PBKD_CUDA(cudaEventCreate(&t0));
+    PBKD_CUDA(cudaEventCreate(&t1e));
+    bool timed_started = false;
+    std::vector<long long> gbase(ts.size(), 0);
+    std::vector<int> evals_done(ts.size(), 1);
+    auto epoch_key = [&](int e) {
+        std::vector<int> key;
+        for (TaskState* s : ts) key.push_back(e <= s->task.epochs ? s->steps_in_epoch[e] : 0);
+        return key;
+    };
+    // host: epoch permutations (bit-exact std::shuffle) -> stream positions.
+    // Computed for epoch e+1 while the GPU runs epoch e.
+    std::vector<int> where(static_cast<size_t>(count), -1);
+    auto make_pos = [&](int e, const std::vector<int>& key) {
+        std::vector<std::vector<int>> out(ts.size());
+        for (size_t i = 0; i < ts.size(); ++i) {
+            if (key[i] == 0) continue;
+            const std::vector<int> order = pbkd::epoch_order(train_idx, ts[i]->task.seed, e);
+            for (int q = 0; q < ntrain; ++q) where[static_cast<size_t>(order[static_cast<size_t>(q)])] = q;
+            out[i].resize(static_cast<size_t>(ntrain));
+            for (int t = 0; t < ntrain; ++t)
+                out[i][static_cast<size_t>(t)] = where[static_cast<size_t>(train_idx[static_cast<size_t>(t)])];
+        }
+        return out;
+    };
+    std::vector<std::vector<int>> pos_next = make_pos(1, epoch_key(1));
+    for (int e = 1; e <= emax; ++e) {
+        const std::vector<int> key = epoch_key(e);
+        if (std::all_of(key.begin(), key.end(), [](int v) { return v == 0; })) break;
+        const bool timed = e >= opt.timed_from_epoch;
+        if (timed && !timed_started) {
+            PBKD_CUDA(cudaEventRecord(t0, st));
+            timed_started = true;
+        }
+        const std::vector<std::vector<int>> pos_now = std::move(pos_next);
+        for (size_t i = 0; i < ts.size(); ++i)
+            if (key[i] > 0)
+                PBKD_CUDA(cudaMemcpyAsync(ts[i]->pos.p, pos_now[i].data(), pos_now[i].size() * sizeof(int),
+                                          cudaMemcpyHostToDevice, st));
+        const std::vector<int>& gkey = key;
+        auto it = graphs.find(gkey);
+        if (it == graphs.end()) {
+            auto P = std::make_unique<Program>();
+            std::vector<Sink> sinks;
+            for (size_t i = 0; i < ts.size(); ++i) {
+                if (key[i] == 0) continue;
+                TaskState* s = ts[i];
+                sinks.push_back({s->k - 1, s->in_stream.f(), s->pos.i(), s->in_row});
+                sinks.push_back({s->k, s->tgt_stream.f(), s->pos.i(), s->out_row});
+            }
+            add_teacher_pass(*P, d_train.i(), ntrain, sinks, chunk, ping.f(), pong.f(), t1.f(), sk.f());
+            for (int step = 0; step < spe; ++step) {
+                std::vector<TaskState*> act;
+                std::vector<long long> gs;
+                for (size_t i = 0; i < ts.size(); ++i)
+                    if (step < key[i]) {
+                        act.push_back(ts[i]);
+                        gs.push_back(gbase[i] + step);
+                    }
+                add_step(*P, act, step, 0, ntrain, gs);
+            }
+            if (opt.use_graphs) P->build_graph(st);
+            it = graphs.emplace(gkey, std::move(P)).first;
+        }
+        PBKD_CUDA(cudaEventRecord(e0, st));
+        if (it->second->has_graph())
+            it->second->launch_graph(st);
+        else
+            it->second->run(st);
+        PBKD_CUDA(cudaEventRecord(e1, st));
+        for (size_t i = 0; i < ts.size(); ++i)  // epoch-local losses -> per-run history
+            if (key[i] > 0)
+                PBKD_CUDA(cudaMemcpyAsync(ts[i]->step_loss.f() + gbase[i], ts[i]->epoch_loss.p,
+                                          static_cast<size_t>(key[i]) * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        if (timed) timing.launches += static_cast<long long>(it->second->launches());
+        if (e + 1 <= emax) pos_next = make_pos(e + 1, epoch_key(e + 1));  // overlaps the GPU
+        PBKD_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        PBKD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        timing.epoch_ms_total += ms;
+        timing.epoch_ms.push_back(ms);
+        timing.epochs += 1;
+        if (timed) timing.timed_epochs += 1;
+        for (size_t i = 0; i < ts.size(); ++i) {
+            gbase[i] += key[i];
+            timing.student_steps = std::max<long long>(timing.student_steps, gbase[i]);
+        }
+        if (opt.baseline_and_eval) {
+            std::vector<TaskState*> which;
+            std::vector<int> slots;
+            for (size_t i = 0; i < ts.size(); ++i)
+                if (key[i] > 0 && e % ts[i]->task.eval_every == 0) {
+                    which.push_back(ts[i]);
+                    slots.push_back(evals_done[i]++);
+                }
+            if (!which.empty()) run_eval(which, slots);
+        }
+    }
+    if (timed_started) {
+        PBKD_CUDA(cudaEventRecord(t1e, st));
+        PBKD_CUDA(cudaEventSynchronize(t1e));
+        float ms = 0.0f;
+        PBKD_CUDA(cudaEventElapsedTime(&ms, t0, t1e));
+        timing.timed_ms += ms;
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1e);
+    PBKD_CUDA(cudaStreamSynchronize(st));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
+// ====================================================== kernel bench
+__global__ void fill_kernel(float* p, size_t n, float v) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = v * (1.0f + 0.001f * static_cast<float>(i % 97));
+}
+
+void Engine::bench_kernel(int which, int batch, int iters, double* ms, double* bytes, double* flops) {
+    Impl& m = *impl_;
+    PBKD_CUDA(cudaSetDevice(m.dev));
+    if (!m.has_teacher) throw std::logic_error("engine: no teacher loaded");
+    // the teacher block with the most MACs
+    size_t bi = 0;
+    double best = -1;
+    for (size_t j = 0; j < m.tblocks.size(); ++j) {
+        const TBlockDev& b = m.tblocks[j];
+        const double macs = static_cast<double>(b.hout) * b.wout * b.cout * b.cin * b.c1.k * b.c1.k;
+        if (macs > best) best = macs, bi = j;
+    }
+    const TBlockDev& b = m.tblocks[bi];
+    const int n = batch, c = b.cout, ho = b.hout, wo = b.wout;
+    const long long M = static_cast<long long>(n) * ho * wo;
+    const size_t big = static_cast<size_t>(std::max<long long>(M * std::max(c, b.cin) * 9LL, static_cast<long long>(n) * b.cin * b.hin * b.win));
+    DevBuf x(big * 4), y(big * 4), z(big * 4), w(static_cast<size_t>(c) * std::max(c, b.cin) * 9 * 4 + 64),
+        v(static_cast<size_t>(c) * 64 * 4 + 4096), parts(static_cast<size_t>(4096) * 9 * c * 4 + 4096);
+    for (DevBuf* d : {&x, &y, &z, &w, &v})
+        fill_kernel<<<1024, 256, 0, m.st>>>(d->f(), d->bytes / 4, 0.37f);
+    PBKD_LAUNCH_CHECK();
+    Program P;
+    double by = 0, fl = 0;
+    std::function<int(const GemmOp&)> gc = gemm_ctas;
+    if (which == 0) {
+        const ConvDev& cv = b.c1;
+        GemmOp o = conv_gemm(cv, x.f(), n, b.hin, b.win, y.f(), true, nullptr, true);
+        P.grouped<GemmOp>(launch_gemm, {o}, gc);
+        fl = 2.0 * o.M * o.N * o.K;
+        by = 4.0 * (static_cast<double>(n) * b.hin * b.win * b.cin + static_cast<double>(o.N) * o.K + static_cast<double>(o.M) * o.N);
+    } else if (which == 1) {
+        GemmOp g{};
+        g.M = static_cast<int>(M), g.N = c, g.K = c;
+        g.A = x.f(), g.lda = c, g.a_kmajor = 1, g.B = w.f(), g.ldb = c, g.b_kmajor = 1;
+        g.C = y.f(), g.ldc = c, g.epi = 1, g.part0 = parts.f(), g.part1 = parts.f() + static_cast<size_t>(2048) * c;
+        g.ksplit = 1, g.kchunk = c, g.tiles_m = ceil_div(M, kGemmBM), g.tiles_n = ceil_div(c, kGemmBN);
+        P.grouped<GemmOp>(launch_gemm, {g}, gc);
+        fl = 2.0 * M * c * c;
+        by = 4.0 * (2.0 * M * c + static_cast<double>(c) * c);
+    } else if (which == 2) {
+        DwFwdOp o{};
+        o.x = x.f(), o.w = w.f(), o.y = y.f(), o.n = n, o.h = ho, o.wd = wo, o.c = c, o.ho = ho, o.wo = wo;
+        o.stride = 1, o.pad = 1, o.pro = 1, o.pa = v.f(), o.pb = v.f(), o.pc = v.f(), o.pd = v.f();
+        P.grouped<DwFwdOp>(launch_dw_fwd, {o}, ctas_dw_fwd);
+        fl = 18.0 * M * c;
+        by = 4.0 * (2.0 * M * c + 9.0 * c);
+    } else if (which == 3) {
+        DwBwdOp o{};
+        o.gy = x.f(), o.xp = z.f(), o.w = w.f(), o.gyprev = y.f();
+        o.mean = v.f(), o.inv = v.f(), o.gamma = v.f(), o.beta = v.f();
+        o.n = n, o.h = ho, o.wd = wo, o.c = c;
+        o.ctas = rows_part_ctas(M, c), o.rows_per = rows_part_per(M, o.ctas);
+        o.part_gk = parts.f(), o.part_sg = parts.f(), o.part_sgx = parts.f();
+        P.grouped<DwBwdOp>(launch_dw_bwd, {o}, [](const DwBwdOp& q) { return q.ctas; });
+        fl = 36.0 * M * c;
+        by = 4.0 * (3.0 * M * c + 9.0 * c);
+    } else {
+        LossOp o{};
+        o.p = x.f(), o.t = z.f(), o.mean = v.f(), o.inv = v.f(), o.gamma = v.f(), o.beta = v.f();
+        o.rows = static_cast<int>(M), o.c = c, o.ctas = rows_part_ctas(M, c), o.rows_per = rows_part_per(M, o.ctas);
+        o.part_sg = parts.f(), o.part_sgx = parts.f(), o.part_loss = parts.f(), o.kmse = 1e-6f;
+        P.grouped<LossOp>(launch_loss, {o}, [](const LossOp& q) { return q.ctas; });
+        fl = 8.0 * M * c;
+        by = 4.0 * 2.0 * M * c;
+    }
+    P.finalize(m.st);
+    for (int i = 0; i < 3; ++i) P.run(m.st);  // warm-up
+    cudaEvent_t a, bev;
+    PBKD_CUDA(cudaEventCreate(&a));
+    PBKD_CUDA(cudaEventCreate(&bev));
+    PBKD_CUDA(cudaStreamSynchronize(m.st));
+    PBKD_CUDA(cudaEventRecord(a, m.st));
+    for (int i = 0; i < iters; ++i) P.run(m.st);
+    PBKD_CUDA(cudaEventRecord(bev, m.st));
+    PBKD_CUDA(cudaEventSynchronize(bev));
+    float t = 0.0f;
+    PBKD_CUDA(cudaEventElapsedTime(&t, a, bev));
+    cudaEventDestroy(a);
+    cudaEventDestroy(bev);
+    *ms = static_cast<double>(t) / iters;
+    *bytes = by;
+    *flops = fl;
+}
+
+// ====================================================== inference helpers
+namespace {
+Tensor nhwc_to_nchw(const std::vector<float>& v, int n, int c, int h, int w) {
+    Tensor t(n, c, h, w);
+    for (int i = 0; i < n; ++i)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x)
+                for (int ch = 0; ch < c; ++ch)
+                    t.data[t.idx(i, ch, y, x)] = v[((static_cast<size_t>(i) * h + y) * w + x) * c + ch];
+    return t;
+}
+std::vector<float> nchw_to_nhwc(const Tensor& t) {
+    std::vector<float> v(t.size());
+    for (int i = 0; i < t.n; ++i)
+        for (int ch = 0; ch < t.c; ++ch)
+            for (int y = 0; y < t.h; ++y)
+                for (int x = 0; x < t.w; ++x)
+                    v[((static_cast<size_t>(i) * t.h + y) * t.w + x) * t.c + ch] = t.data[t.idx(i, ch, y, x)];
+    return v;
+}
+}  // namespace
+
+Engine::Engine(int device) : impl_(std::make_unique<Impl>(device)) {}
+Engine::~Engine() = default;
+void Engine::set_teacher(const Network& net) { impl_->load_teacher(net); }
+const Network& Engine::teacher() const { return impl_->net; }
+bool Engine::has_teacher() const { return impl_->has_teacher; }
+void Engine::set_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {
+    impl_->load_dataset(img, lab, n, c, h, w, cls, on_dev);
+}
+std::vector<TaskOutcome> Engine::run(const std::vector<DistillTask>& t, const std::vector<int>& tr,
+                                     const std::vector<int>& ev, const RunOptions& o) {
+    return impl_->run(t, tr, ev, o);
+}
+const RunTiming& Engine::timing() const { return impl_->timing; }
+int Engine::device() const { return impl_->dev; }
+cudaStream_t Engine::stream() const { return impl_->st; }
+
+Tensor Engine::prefix_infer(const Tensor& x, int k, bool inclusive) {
+    Impl& m = *impl_;
+    PBKD_CUDA(cudaSetDevice(m.dev));
+    if (!m.has_teacher) throw std::logic_error("engine: no teacher loaded");
+    const int nb = static_cast<int>(m.tblocks.size());
+    if (k < 1 || k > nb) throw std::out_of_range("prefix_infer: k=" + std::to_string(k) + " out of range");
+    if (x.c != m.net.in_c || x.h != m.net.in_h || x.w != m.net.in_w)
+        throw pbkd::ShapeError("prefix_infer: input shape " + x.shape_str() + " does not match the network");
+    const int take = inclusive ? k : k - 1;
+    if (take == 0) return x;
+    const size_t wsz = static_cast<size_t>(x.n) * m.max_row() * sizeof(float);
+    DevBuf a(wsz), b(wsz), t1(wsz), sk(wsz);
+    const std::vector<float> in = nchw_to_nhwc(x);
+    PBKD_CUDA(cudaMemcpy(a.p, in.data(), in.size() * sizeof(float), cudaMemcpyHostToDevice));
+    Program P;
+    float* cur = a.f();
+    float* nxt = b.f();
+    for (int j = 0; j < take; ++j) {
+        m.teacher_block(P, j, cur, nxt, x.n, t1.f(), sk.f());
+        std::swap(cur, nxt);
+    }
+    P.run(m.st);
+    PBKD_CUDA(cudaStreamSynchronize(m.st));
+    const TBlockDev& lb = m.tblocks[static_cast<size_t>(take) - 1];
+    std::vector<float> out(static_cast<size_t>(x.n) * lb.cout * lb.hout * lb.wout);
+    PBKD_CUDA(cudaMemcpy(out.data(), cur, out.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    return nhwc_to_nchw(out, x.n, lb.cout, lb.hout, lb.wout);
+}
+
+int candidate_units(const Block& b) {
+    int u = 0;
+    for (const pbkd::LayerParams& l : b.layers)
+        if (l.kind == LayerKind::DepthwiseConv3x3) ++u;
+    return u;
+}
+
+Tensor Engine::candidate_infer(const Block& cand, const Tensor& x) {
+    Impl& m = *impl_;
+    PBKD_CUDA(cudaSetDevice(m.dev));
+    for (const pbkd::LayerParams& l : cand.layers)
+        if (l.kind == LayerKind::Add) throw SpecError("skip candidates are not implemented on the GPU path");
+    const int U = candidate_units(cand);
+    if (U < 1 || U > kMaxUnits) throw SpecError("not a depthwise-separable candidate block");
+    TaskState s;
+    s.units = U;
+    const int ho = (x.h - 1) / cand.stride + 1, wo = (x.w - 1) / cand.stride + 1;
+    std::vector<float> host, stats;
+    size_t li = 0;
+    for (int u = 0; u < U; ++u) {
+        const pbkd::LayerParams& dwl = cand.layers[li];
+        const pbkd::LayerParams& pwl = cand.layers[li + 1];
+        const pbkd::LayerParams& bnl = cand.layers[li + 2];
+        li += 4;
+        const int ci = dwl.in_channels, co = pwl.out_channels;
+        s.u[u] = u == 0 ? UnitDims{ci, x.h, x.w, co, ho, wo, cand.stride} : UnitDims{ci, ho, wo, co, ho, wo, 1};
+        s.off_dw[u] = host.size();
+        for (int tap = 0; tap < 9; ++tap)
+            for (int c = 0; c < ci; ++c) host.push_back(dwl.weight.data[static_cast<size_t>(c) * 9 + tap]);
+        s.off_pw[u] = host.size();
+        host.insert(host.end(), pwl.weight.data.begin(), pwl.weight.data.end());
+        s.off_g[u] = host.size();
+        host.insert(host.end(), bnl.gamma.data.begin(), bnl.gamma.data.end());
+        s.off_b[u] = host.size();
+        host.insert(host.end(), bnl.beta.data.begin(), bnl.beta.data.end());
+        stats.insert(stats.end(), bnl.moving_mean.data.begin(), bnl.moving_mean.data.end());
+        stats.insert(stats.end(), bnl.moving_var.data.begin(), bnl.moving_var.data.end());
+    }
+    if (x.c != s.u[0].cin) throw pbkd::ShapeError("candidate input channels do not match");
+    s.params = upload(host, m.st);
+    s.mstats = upload(stats, m.st);
+    const int cout = s.u[0].cout;
+    s.scale.alloc(static_cast<size_t>(U) * cout * sizeof(float));
+    s.shift.alloc(static_cast<size_t>(U) * cout * sizeof(float));
+    const int row = std::max(x.c * x.h * x.w, std::max(cout, x.c) * ho * wo);
+    const size_t wsz = static_cast<size_t>(x.n) * row * sizeof(float);
+    DevBuf in(wsz), a(wsz), b(wsz), o(wsz);
+    const std::vector<float> xin = nchw_to_nhwc(x);
+    PBKD_CUDA(cudaMemcpy(in.p, xin.data(), xin.size() * sizeof(float), cudaMemcpyHostToDevice));
+    Program P;
+    m.add_student_infer(P, s, in.f(), x.n, a.f(), b.f(), o.f());
+    P.run(m.st);
+    PBKD_CUDA(cudaStreamSynchronize(m.st));
+    std::vector<float> out(static_cast<size_t>(x.n) * cout * ho * wo);
+    PBKD_CUDA(cudaMemcpy(out.data(), o.p, out.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    return nhwc_to_nchw(out, x.n, cout, ho, wo);
+}
+
+double Engine::eval_with_student(int block_index, const Block& student, const std::vector<int>& eval_idx) {
+    Impl& m = *impl_;
+    PBKD_CUDA(cudaSetDevice(m.dev));
+    if (eval_idx.empty()) throw SpecError("evaluation split is empty");
+    if (block_index < 1 || block_index > static_cast<int>(m.tblocks.size()))
+        throw SpecError("block index " + std::to_string(block_index) + " out of range");
+    // prefix on host tensors, student, suffix + classifier on device
+    std::vector<int> lab;
+    pbkd::Dataset d;  // labels only
+    std::vector<int> all(static_cast<size_t>(m.count));
+    PBKD_CUDA(cudaMemcpy(all.data(), m.labels.p, all.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<float> img(static_cast<size_t>(m.count) * m.dc * m.dh * m.dw);
+    PBKD_CUDA(cudaMemcpy(img.data(), m.images.p, img.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    d.c = m.dc;
+    d.h = m.dh;
+    d.w = m.dw;
+    d.images = img;
+    d.labels = all;
+    const Tensor xb = pbkd::gather_batch(d, eval_idx);
+    const Tensor a = prefix_infer(xb, block_index, false);
+    const Tensor so = candidate_infer(student, a);
+    // suffix
+    const int n = xb.n;
+    const size_t wsz = static_cast<size_t>(n) * m.max_row() * sizeof(float);
+    DevBuf p0(wsz), p1(wsz), t1(wsz), sk(wsz);
+    const std::vector<float> sv = nchw_to_nhwc(so);
+    PBKD_CUDA(cudaMemcpy(p0.p, sv.data(), sv.size() * sizeof(float), cudaMemcpyHostToDevice));
+    Program P;
+    float* cur = p0.f();
+    float* nxt = p1.f();
+    for (size_t j = static_cast<size_t>(block_index); j < m.tblocks.size(); ++j) {
+        m.teacher_block(P, static_cast<int>(j), cur, nxt, n, t1.f(), sk.f());
+        std::swap(cur, nxt);
+    }
+    for (int i : eval_idx) lab.push_back(all[static_cast<size_t>(i)]);
+    DevBuf dl = upload(lab, m.st);
+    DevBuf corr(sizeof(int));
+    PBKD_CUDA(cudaMemsetAsync(corr.p, 0, sizeof(int), m.st));
+    const float* xin = cur;
+    P.raw([&, xin](cudaStream_t s2) {
+        launch_classifier_count(xin, n, m.cls_hw, m.cls_in_c, m.cls_kinds.i(), m.cls_layers, m.cls_w.f(),
+                                m.cls_b.f(), m.cls_maxw, dl.i(), corr.i(), s2);
+    });
+    P.run(m.st);
+    int c = 0;
+    PBKD_CUDA(cudaMemcpyAsync(&c, corr.p, sizeof(int), cudaMemcpyDeviceToHost, m.st));
+    PBKD_CUDA(cudaStreamSynchronize(m.st));
+    return static_cast<double>(c) / static_cast<double>(eval_idx.size());
+}
+
+}  // namespace pbkd_gpu

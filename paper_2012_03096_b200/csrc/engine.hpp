@@ -1,0 +1,102 @@
+// engine.hpp -- the per-GPU distillation engine behind the C ABI.
+//
+// One Engine owns one device.  run() executes a set of distillation tasks
+// (pbkd::DistillTask, distill.hpp:24-37) with train_block semantics
+// (distill.cpp:135-262) for every task, all tasks of the same batch size and
+// unit count advancing in lockstep as grouped launches:
+//
+//   per epoch:  teacher forward once per training sample, boundary activations
+//               scattered straight into each task's epoch-ordered stream
+//               (replaces prefix_infer per block per batch, distill.cpp:210-211)
+//            -> ceil(N/B) grouped student steps (fwd, MSE, bwd, SGD)
+//   the whole epoch is one CUDA graph; the host only uploads the epoch's
+//   permutation (std::shuffle + mt19937_64, bit-exact).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pbkd/distill.hpp"
+#include "pbkd/model.hpp"
+
+namespace pbkd_gpu {
+
+struct TaskOutcome {
+    int block_index = 0;
+    std::string kind;
+    bool failed = false;
+    std::string failure;
+    std::vector<float> best_block;   // for_each_block_array order (empty if none)
+    std::vector<float> final_block;  // weights after the last executed step
+    std::vector<pbkd::EvalPoint> eval_history;
+    std::vector<double> loss_history;
+    std::vector<float> step_losses;
+    double final_local_loss = 0.0;
+    double best_eval = -1.0;
+    double wall_time_s = 0.0;
+};
+
+struct RunOptions {
+    bool baseline_and_eval = true;  // epoch-0 baseline + evaluations (train_block semantics)
+    bool use_graphs = true;
+    int timed_from_epoch = 1;  // device events bracket epochs [timed_from_epoch, last]
+};
+
+// Timing of the last run (device events around the epoch graphs).
+struct RunTiming {
+    double epoch_ms_total = 0.0;  // sum over training epochs (teacher pass + steps)
+    std::vector<double> epoch_ms; // per training epoch (graph only)
+    double timed_ms = 0.0;        // events around epochs >= timed_from_epoch, host gaps included
+    int timed_epochs = 0;
+    int epochs = 0;
+    long long student_steps = 0;  // per task
+    long long launches = 0;       // kernel launches in the timed window
+};
+
+class Engine {
+public:
+    explicit Engine(int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void set_teacher(const pbkd::Network& net);
+    const pbkd::Network& teacher() const;
+    bool has_teacher() const;
+    void set_dataset(const float* images, const int* labels, int count, int c, int h, int w,
+                     int classes, bool images_on_device = false);
+    std::vector<TaskOutcome> run(const std::vector<pbkd::DistillTask>& tasks,
+                                 const std::vector<int>& train_idx,
+                                 const std::vector<int>& eval_idx, const RunOptions& opt);
+    const RunTiming& timing() const;
+
+    // Inference helpers (host NCHW in/out), used by the C ABI.
+    pbkd::Tensor prefix_infer(const pbkd::Tensor& x, int k, bool inclusive);
+    pbkd::Tensor candidate_infer(const pbkd::Block& cand, const pbkd::Tensor& x);
+    double eval_with_student(int block_index, const pbkd::Block& student,
+                             const std::vector<int>& eval_idx);
+    // Times one representative launch of a hot kernel in isolation (CUDA
+    // events on the engine stream).  which: 0 teacher conv implicit GEMM,
+    // 1 student pointwise GEMM (fwd), 2 depthwise fwd, 3 depthwise bwd
+    // (fused), 4 loss + batch-norm backward sums.  Shapes: the teacher block
+    // with the most MACs, `batch` samples.
+    void bench_kernel(int which, int batch, int iters, double* ms, double* bytes, double* flops);
+
+    int device() const;
+    cudaStream_t stream() const;
+
+    struct Impl;
+
+private:
+    std::unique_ptr<Impl> impl_;
+};
+
+// Flat conversions between pbkd::Block (reference array order / layouts) and
+// the engine's device layout ([9][C] depthwise, [Cout][Cin] pointwise).
+int candidate_units(const pbkd::Block& b);
+
+}  // namespace pbkd_gpu

@@ -1,0 +1,218 @@
+// ops.cuh -- operation descriptors for the grouped (multi-task) kernels.
+//
+// Every kernel of the student step runs as ONE launch for all distillation
+// tasks resident on the GPU: the host writes an array of per-task descriptors
+// (each carrying its own first-CTA index `cta_begin`), the kernel maps
+// blockIdx.x to its task with find_task().  Tiling and reduction partitions
+// depend only on a task's own shape, never on which other tasks share the
+// launch, so a block's bits do not depend on the schedule (the GPU analogue of
+// test_runtime.cpp:206-253).
+//
+// Layout: activations are channels-last (NHWC) rows; a "row" is one pixel of
+// one sample, channels contiguous.  Depthwise weights are tap-major [9][C];
+// pointwise weights keep the reference's [C_out][C_in] (model.cpp:157-171).
+#pragma once
+#include "common.cuh"
+
+namespace pbkd_gpu {
+
+// Depthwise 3x3 forward (ops.hpp:114-147), optional fused prologue that
+// rebuilds the input from the previous unit's pointwise output:
+//   pro 0: x as stored
+//   pro 1: relu(gamma*((x-mean)*inv)+beta)   (train-mode BN, ops.hpp:290-293)
+//   pro 2: relu(scale*x+shift)               (inference-mode BN, ops.hpp:304-321)
+struct DwFwdOp {
+    const float* x;
+    const float* w;  // [9][c]
+    float* y;
+    int n, h, wd, c, ho, wo, stride, pad;
+    int pro;
+    const float *pa, *pb, *pc, *pd;  // mean,inv,gamma,beta | scale,shift
+    const int* failed;
+    int cta_begin;
+};
+
+// Depthwise 3x3 backward of a stride-1 unit u>0 (ops.hpp:149-178) fused with
+// the ReLU (ops.hpp:387-393) and the batch-norm partial sums (ops.hpp:333-342)
+// of the previous unit:  gx -> gy_prev = gx * [y_prev > 0], partial sums
+// sum(gy_prev), sum(gy_prev * xhat_prev) and the weight gradient partials.
+struct DwBwdOp {
+    const float* gy;     // [rows][c] gradient wrt the dw output
+    const float* xp;     // previous unit's pointwise output (pre-BN)
+    const float* w;      // [9][c]
+    float* gyprev;       // [rows][c] gradient wrt previous BN output (masked)
+    float* part_gk;      // [ctas][9][c]
+    float* part_sg;      // [ctas][c]
+    float* part_sgx;     // [ctas][c]
+    const float *mean, *inv, *gamma, *beta;  // previous unit BN (train mode)
+    int n, h, wd, c;
+    int ctas, rows_per;
+    const int* failed;
+    int cta_begin;
+};
+
+// Depthwise weight-gradient partials only (unit 0, any stride; model.cpp:570
+// skips gx for the first layer).
+struct DwGkOp {
+    const float* gy;  // [n*ho*wo][c]
+    const float* x;   // [n*h*wd][c]
+    float* part_gk;   // [ctas][9][c]
+    int n, h, wd, c, ho, wo, stride, pad;
+    int ctas, rows_per;
+    const int* failed;
+    int cta_begin;
+};
+
+// Sum `parts` rows of width `width` in fixed order into out (optionally
+// through a per-element op).  Used for dw gk partials and split-K GEMM.
+struct ReduceOp {
+    const float* part;
+    float* out;
+    int parts, width;
+    int layout;  // 0: out[i] = sum ; 1: dw [9][c] -> out [9][c] (same)
+    const int* failed;
+    int cta_begin;
+};
+
+// Generic fp32 GEMM  C[m][n] = sum_k A(m,k) * B(n,k)
+//   A(m,k) = a_kmajor ? A[m*lda+k] : A[k*lda+m]   (or implicit conv, see conv)
+//   B(n,k) = b_kmajor ? B[n*ldb+k] : B[k*ldb+n]
+// epi 0: store C; 1: store C and per-(m-tile, column) partial sum / sum of
+// squares for batch-norm statistics; 2: split-K partial: C + split*M*ldc.
+// conv != 0: A is the implicit im2col of an NHWC input (teacher conv,
+// ops.hpp:37-75): k = tap*ic + j.  Teacher epilogue: y = scale*acc + shift
+// (+ skip), then optional relu (model.cpp:540-546, ops.hpp:460-466).
+struct GemmOp {
+    int M, N, K;
+    const float* A;
+    long long lda;
+    int a_kmajor;
+    const float* B;
+    long long ldb;
+    int b_kmajor;
+    float* C;
+    long long ldc;
+    int epi;
+    float *part0, *part1;
+    int ksplit, kchunk;
+    int tiles_m, tiles_n;
+    int conv, ih, iw, ic, oh, ow, ksz, cstride, cpad;
+    const float *scale, *shift, *skip;
+    int relu;
+    const int* failed;
+    int cta_begin;
+};
+
+// Batch-norm statistics from the GEMM column partials (ops.hpp:273-299):
+// mean, var = E[x^2]-mean^2 clamped, inv_std, moving-stat update.
+struct BnStatOp {
+    const float *part_sum, *part_sq;
+    int tiles, c;
+    long long m;  // rows in the batch
+    float *mean, *inv, *mm, *mv;
+    int update_moving;
+    const int* failed;
+    int cta_begin;
+};
+
+// Last unit: student output s = relu(bn(p)), loss partials sum (s-t)^2 and
+// batch-norm backward partials of g = [y>0] * k*(s-t) (ops.hpp:518-539,
+// 387-393, 333-342).  rows/ctas partition fixed per task shape.
+struct LossOp {
+    const float* p;
+    const float* t;
+    const float *mean, *inv, *gamma, *beta;
+    float* part_sg;
+    float* part_sgx;
+    float* part_loss;  // [ctas]
+    int rows, c, ctas, rows_per;
+    float kmse;        // (scale*2)/count
+    const int* failed;
+    int cta_begin;
+};
+
+// Reduce batch-norm backward partials -> sum_g, sum_gx, parameter gradients
+// (ggamma += sum_gx, gbeta += sum_g; ops.hpp:343-344); for the last unit also
+// the step loss, its non-finite check (distill.cpp:236-244) and failure flag.
+struct BnBwdFinOp {
+    const float *part_sg, *part_sgx, *part_loss;
+    int ctas, c;
+    float *sg, *sgx, *ggamma, *gbeta;
+    float* loss_out;   // nullptr unless last unit
+    double count;      // elements in the MSE
+    int* failed;       // written when loss is non-finite
+    int cta_begin;
+};
+
+// g_p = (gamma*inv) * ((g - inv_m*sum_g) - (xhat*inv_m)*sum_gx)  (ops.hpp:345-354)
+// with g either read (gin) or rebuilt from (p, t) for the last unit.
+struct BnBwdApplyOp {
+    const float* p;
+    const float* t;    // non-null -> last unit, g rebuilt from the MSE gradient
+    const float* gin;  // else the masked gradient from the dw backward
+    float* gout;
+    const float *mean, *inv, *gamma, *beta, *sg, *sgx;
+    long long total;   // rows*c
+    int c;
+    float inv_m, kmse;
+    const int* failed;
+    int cta_begin;
+};
+
+// Momentum SGD over a task's flat parameter buffer (ops.hpp:545-558).
+struct SgdOp {
+    float *w, *v;
+    const float* g;
+    long long n;
+    float lr, mom;
+    const int* failed;
+    int cta_begin;
+};
+
+// dst row pos[i] <- src row i   (activation streaming into a task's epoch order)
+struct ScatterOp {
+    const float* src;
+    float* dst;
+    const int* pos;
+    int rows, width;
+    int cta_begin;
+};
+
+// Host-side helpers (defined in ops.cu) ------------------------------------
+int rows_part_ctas(long long rows, int c);  // deterministic partition size
+int rows_part_per(long long rows, int ctas);
+constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
+
+void launch_dw_fwd(const DwFwdOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_dw_bwd(const DwBwdOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_dw_gk(const DwGkOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_reduce(const ReduceOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_gemm(const GemmOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_bn_stat(const BnStatOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_loss(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_bn_bwd_fin(const BnBwdFinOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_bn_bwd_apply(const BnBwdApplyOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_sgd(const SgdOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_scatter(const ScatterOp* d_ops, int nd, int ctas, cudaStream_t st);
+
+// CTA counts for one op (host)
+int ctas_dw_fwd(const DwFwdOp& o);
+int ctas_gemm(const GemmOp& o);
+int ctas_elem(long long total);
+
+// Non-grouped helpers used by evaluation / teacher / tests -----------------
+void launch_gather_nhwc(const float* images_nchw, const int* idx, int n, int c, int h, int w,
+                        float* out_nhwc, cudaStream_t st);
+void launch_bn_infer_prep(const float* gamma, const float* beta, const float* mm,
+                          const float* mv, int c, float* scale, float* shift, cudaStream_t st);
+void launch_bn_infer_relu(const float* x, float* y, long long total, int c, const float* scale,
+                          const float* shift, cudaStream_t st);
+// per-segment MSE sums (segment = one batch of the epoch-0 baseline)
+void launch_mse_segments(const float* s, const float* t, long long seg_elems, long long total,
+                         int nseg, double* out_sums, cudaStream_t st);
+// classifier head: GAP -> [relu] -> dense -> argmax (first max) == label
+void launch_classifier_count(const float* x_nhwc, int n, int hw, int c, const int* layer_kinds,
+                             int nlayers, const float* dense_w, const float* dense_b, int nout,
+                             const int* labels, int* correct, cudaStream_t st);
+
+}  // namespace pbkd_gpu

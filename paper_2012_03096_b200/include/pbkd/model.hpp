@@ -1,0 +1,116 @@
+#pragma once
+// pbkd-b200 host API: network graph.  Declarations match the reference's
+// include/pbkd/model.hpp:19-214 so a reference caller compiles unchanged; the
+// implementations live in csrc/host/model.cpp and, for execution, run on the
+// GPU behind the C ABI (include/pbkd_b200.h).
+#include <cstdint>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "pbkd/tensor.hpp"
+
+namespace pbkd {
+
+struct SpecError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+
+enum class LayerKind {
+    Conv3x3,
+    Conv1x1,
+    DepthwiseConv3x3,
+    PointwiseConv,
+    BatchNorm,
+    ReLU,
+    GlobalAvgPool,
+    Dense,
+    Add,
+};
+
+const char* layer_kind_name(LayerKind k);
+LayerKind layer_kind_from_name(const std::string& name);
+
+struct LayerParams {
+    LayerKind kind;
+    int in_channels = 0;
+    int out_channels = 0;
+    int kernel = 0;
+    int stride = 1;
+    int padding = 0;
+    Tensor weight;
+    Tensor bias;
+    Tensor gamma, beta, moving_mean, moving_var;
+};
+
+struct Block {
+    std::string name;
+    std::string spec_kind;
+    bool replaceable = false;
+    int in_channels = 0;
+    int out_channels = 0;
+    int stride = 1;
+    int padding = 1;
+    std::vector<LayerParams> layers;
+};
+
+struct Network {
+    std::string name;
+    int in_c = 0, in_h = 0, in_w = 0;
+    std::vector<Block> blocks;
+    Block classifier;
+    bool has_classifier() const { return !classifier.layers.empty(); }
+};
+
+LayerParams make_conv_layer(LayerKind kind, int in_c, int out_c, int kernel, int stride, int padding);
+LayerParams make_batchnorm_layer(int channels);
+LayerParams make_relu_layer(int channels);
+LayerParams make_gap_layer(int channels);
+LayerParams make_dense_layer(int in_features, int out_features);
+LayerParams make_add_layer(int in_c, int out_c, int stride);
+
+Network parse_model_spec(const std::string& text, const std::string& origin = "<memory>");
+Network load_model_spec_file(const std::string& path);
+
+Network subnetwork_prefix(const Network& net, int k, bool inclusive);
+std::vector<int> identify_replaceable(const Network& net);
+
+void init_block_weights(Block& b, std::mt19937_64& rng);
+void init_weights(Network& net, uint64_t seed);
+
+std::vector<Tensor*> collect_block_trainable(Block& b);
+std::vector<Tensor*> collect_trainable(Network& net);
+
+void for_each_array(Network& net, const std::function<void(const std::string&, Tensor&)>& fn);
+void for_each_block_array(Block& b, const std::function<void(const std::string&, Tensor&)>& fn);
+uint64_t network_weight_hash(const Network& net);
+
+// Shape bookkeeping used by the GPU driver: (c,h,w) at the entrance of block
+// k (1-based; k = blocks+1 gives the classifier input).
+void block_input_shape(const Network& net, int k, int& c, int& h, int& w);
+
+// Inference on the GPU (C ABI pbkd_prefix_infer / pbkd_block_infer).
+Tensor block_infer(const Block& b, const Tensor& x);
+Tensor prefix_infer(const Network& net, const Tensor& x, int k, bool inclusive);
+
+struct CostRow {
+    std::string layer;
+    LayerKind kind;
+    long long macs = 0;
+    long long params = 0;
+};
+
+struct CostTable {
+    std::vector<CostRow> rows;
+    long long total_macs = 0;
+    long long total_params = 0;
+    long long conv_macs() const;
+    long long conv_params() const;
+};
+
+CostTable count_block_cost(const Block& b, int c, int h, int w);
+CostTable count_macs_params(const Network& net, int c, int h, int w);
+CostTable count_macs_params(const Network& net);
+
+}  // namespace pbkd

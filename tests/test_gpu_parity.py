@@ -1,0 +1,317 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (fp32):
+  * bit-exact where the reference order is reproducible: depthwise forward,
+    depthwise input gradient, SGD, indices, plans, initial weights;
+  * reductions (GEMM K, batch-norm sums, weight gradients, MSE sum): relative
+    1e-4 per element against the serial-fp32 oracle (|a-b| <= 1e-4*|b| +
+    1e-5*max|b|), the bar BASELINE.json north_star states;
+  * N-step trajectories: per-step losses rel 1e-4, weights after N steps
+    rel 2e-4 of the tensor scale (drift compounds over steps).
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2012_03096_b200 as P  # noqa: E402
+from oracle.oracle import make_task as orc_task  # noqa: E402
+from tests.conftest import spec_text  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def close(a, b, rtol=1e-4, atol_frac=1e-5):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    scale = max(float(np.max(np.abs(b))), 1e-30)
+    err = np.abs(a - b) - (rtol * np.abs(b) + atol_frac * scale)
+    assert np.all(err <= 0), f"max excess {err.max():.3e} (max abs diff {np.abs(a-b).max():.3e}, scale {scale:.3e})"
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if not os.path.exists(P.LIB_PATH):
+        P.build()
+    return P.Context(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+def D(t):
+    return P.DevPtr(t.data_ptr())
+
+
+def nhwc(x):
+    return np.ascontiguousarray(np.transpose(x, (0, 2, 3, 1)))
+
+
+def nchw(x):
+    return np.ascontiguousarray(np.transpose(x, (0, 3, 1, 2)))
+
+
+def w9c(k):  # [C,1,3,3] -> [9][C]
+    return np.ascontiguousarray(k.reshape(k.shape[0], 9).T)
+
+
+# ------------------------------------------------------------ kernels ----
+@pytest.mark.parametrize("n,c,h,w,s", [(2, 3, 32, 32, 1), (4, 64, 32, 32, 2), (8, 512, 2, 2, 1),
+                                       (3, 13, 7, 9, 2), (32, 128, 16, 16, 1)])
+def test_dw_fwd_bit_exact(ctx, orc, n, c, h, w, s):
+    rng = np.random.default_rng(n * 1000 + c)
+    x = rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    k = rng.uniform(-1, 1, (c, 1, 3, 3)).astype(np.float32)
+    want = orc.dw_fwd(x, k, s, 1)
+    y = torch.zeros(want.shape[0], want.shape[2], want.shape[3], c, device="cuda")
+    xd, kd = dev(nhwc(x)), dev(w9c(k))
+    ctx.k("dw_fwd", D(xd), D(kd), D(y), n, h, w, c, s, 1)
+    assert np.array_equal(nchw(y.cpu().numpy()), want)
+
+
+@pytest.mark.parametrize("n,c,h,w", [(2, 64, 32, 32), (4, 512, 4, 4), (3, 12, 5, 7)])
+def test_dw_bwd_fused(ctx, orc, n, c, h, w):
+    rng = np.random.default_rng(c)
+    # p > 0 with mean 0, inv 1, gamma 1, beta 0: relu(bn(p)) = p, mask all-on
+    p = rng.uniform(0.01, 1, (n, c, h, w)).astype(np.float32)
+    k = rng.uniform(-1, 1, (c, 1, 3, 3)).astype(np.float32)
+    gy = rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    gx_want, gk_want = orc.dw_bwd(p, k, gy, 1, 1)
+    z, o = dev(np.zeros(c)), dev(np.ones(c))
+    gyp = torch.zeros(n, h, w, c, device="cuda")
+    gk = torch.zeros(9, c, device="cuda")
+    sg, sgx = torch.zeros(c, device="cuda"), torch.zeros(c, device="cuda")
+    gyd, pd, kd = dev(nhwc(gy)), dev(nhwc(p)), dev(w9c(k))
+    ctx.k("dw_bwd", D(gyd), D(pd), D(kd), D(z), D(o), D(o), D(z),
+          D(gyp), D(gk), D(sg), D(sgx), n, h, w, c)
+    assert np.array_equal(nchw(gyp.cpu().numpy()), gx_want)  # ordered gather: bit-exact
+    close(gk.cpu().numpy().T.reshape(c, 1, 3, 3), gk_want)
+    close(sg.cpu().numpy(), gx_want.sum(axis=(0, 2, 3)), rtol=1e-4, atol_frac=1e-5)
+
+
+@pytest.mark.parametrize("n,c,h,w,s", [(8, 3, 32, 32, 1), (4, 64, 32, 32, 2), (16, 512, 2, 2, 1)])
+def test_dw_gk(ctx, orc, n, c, h, w, s):
+    rng = np.random.default_rng(7 + c)
+    x = rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    k = rng.uniform(-1, 1, (c, 1, 3, 3)).astype(np.float32)
+    ho, wo = (h - 1) // s + 1, (w - 1) // s + 1
+    gy = rng.uniform(-1, 1, (n, c, ho, wo)).astype(np.float32)
+    _, gk_want = orc.dw_bwd(x, k, gy, s, 1)
+    gk = torch.zeros(9, c, device="cuda")
+    gyd, xd = dev(nhwc(gy)), dev(nhwc(x))
+    ctx.k("dw_gk", D(gyd), D(xd), D(gk), n, h, w, c, s, 1)
+    close(gk.cpu().numpy().T.reshape(c, 1, 3, 3), gk_want)
+
+
+@pytest.mark.parametrize("n,cin,cout,h", [(8, 3, 64, 32), (4, 64, 128, 16), (32, 512, 512, 2),
+                                          (5, 17, 33, 3)])
+def test_pointwise_fwd_bwd(ctx, orc, n, cin, cout, h):
+    rng = np.random.default_rng(cin * cout)
+    x = rng.uniform(-1, 1, (n, cin, h, h)).astype(np.float32)
+    wt = rng.uniform(-1, 1, (cout, cin, 1, 1)).astype(np.float32)
+    want = orc.pw_fwd(x, wt)
+    rows = n * h * h
+    y = torch.zeros(rows, cout, device="cuda")
+    cs, cq = torch.zeros(cout, device="cuda"), torch.zeros(cout, device="cuda")
+    xd, wd = dev(nhwc(x).reshape(rows, cin)), dev(wt.reshape(cout, cin))
+    ctx.k("pw_fwd", D(xd), D(wd), D(y), rows, cin, cout, D(cs), D(cq))
+    close(nchw(y.cpu().numpy().reshape(n, h, h, cout)), want)
+    w64 = want.astype(np.float64)
+    close(cs.cpu().numpy(), w64.sum(axis=(0, 2, 3)), atol_frac=1e-4)
+    close(cq.cpu().numpy(), (w64 ** 2).sum(axis=(0, 2, 3)))
+    gy = rng.uniform(-1, 1, want.shape).astype(np.float32)
+    gx_want, gw_want = orc.pw_bwd(x, wt, gy)
+    gx, gw = torch.zeros(rows, cin, device="cuda"), torch.zeros(cout, cin, device="cuda")
+    gyd = dev(nhwc(gy).reshape(rows, cout))
+    ctx.k("pw_bwd", D(xd), D(wd), D(gyd), D(gx), D(gw), rows, cin, cout)
+    close(nchw(gx.cpu().numpy().reshape(n, h, h, cin)), gx_want)
+    close(gw.cpu().numpy().reshape(cout, cin, 1, 1), gw_want)
+
+
+def test_sgd_bit_exact(ctx, orc):
+    rng = np.random.default_rng(1)
+    w = rng.standard_normal(10007).astype(np.float32)
+    g = rng.standard_normal(10007).astype(np.float32)
+    v = rng.standard_normal(10007).astype(np.float32)
+    w_want, v_want = orc.sgd(w, g, v, 0.05, 0.9)
+    wd, vd = dev(w), dev(v)
+    gd = dev(g)
+    ctx.k("sgd", D(wd), D(gd), D(vd), 10007, 0.05, 0.9)
+    assert np.array_equal(wd.cpu().numpy(), w_want) and np.array_equal(vd.cpu().numpy(), v_want)
+
+
+# ------------------------------------------------------------- teacher ----
+@pytest.mark.parametrize("name", ["vgg16_cifar", "resnet18_cifar", "resnet_blocks_demo"])
+def test_prefix_infer(ctx, orc, name):
+    spec = spec_text(name)
+    tw = orc.teacher_init(spec, 5)
+    ctx.teacher_load(spec, tw)
+    s = 16 if name == "resnet_blocks_demo" else 32
+    x = np.random.default_rng(3).random((3, 3, s, s), dtype=np.float32)
+    nb = orc.teacher_num_blocks(spec)
+    for k in sorted({1, 2, nb // 2, nb}):
+        want = orc.prefix_infer(spec, tw, x, k, True)
+        got = ctx.prefix_infer(x, k, True, want.size)
+        close(got, want, rtol=1e-4, atol_frac=1e-5)
+
+
+# ------------------------------------------------------- step replays ----
+def replay_case(ctx, orc, spec, teacher_seed, images, labels, k, batch, steps, kind=0, lr=0.05,
+                frac=0.1):
+    tw = orc.teacher_init(spec, teacher_seed)
+    tr, ev = orc.stratified_split(labels, frac, 17)
+    seed = orc.mix_seed(42, k)
+    ctx.teacher_load(spec, tw)
+    ctx.dataset_load(images, labels)
+    spe = -(-len(tr) // batch)
+    epochs = -(-steps // spe)
+    t = P.make_task(k, kind=kind, epochs=epochs, seed=seed, batch_size=batch, lr=lr,
+                    max_steps=steps)
+    got = ctx.run([t], tr, ev, flags=P.RUN_STEP_ONLY)["results"][0]
+    nf = len(got["final_block"])
+    o = orc_task(k, kind=kind, seed=seed, batch_size=batch, lr=lr)
+    losses, fw = orc.train_replay(spec, tw, images, labels, tr, ev, o, steps, nf)
+    return got, losses, fw
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_toy_step_replay(ctx, orc, k):
+    img, lab = orc.synthetic_dataset(60, 11, 2)
+    got, losses, fw = replay_case(ctx, orc, spec_text("toy_teacher"), 404, img, lab, k, 16, 8)
+    assert not got["failed"]
+    close(got["step_losses"], losses, rtol=1e-4)
+    close(got["final_block"], fw, rtol=2e-4, atol_frac=2e-4)
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 9, 13])
+def test_vgg16_step_replay(ctx, orc, k):
+    img = np.random.default_rng(7).random((40, 3, 32, 32), dtype=np.float32)
+    lab = (np.arange(40) % 10).astype(np.int32)
+    got, losses, fw = replay_case(ctx, orc, spec_text("vgg16_cifar"), orc.mix_seed(42, 0x7E11),
+                                  img, lab, k, 8, 3)
+    close(got["step_losses"], losses, rtol=1e-4)
+    close(got["final_block"], fw, rtol=2e-4, atol_frac=2e-4)
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_resnet18_step_replay(ctx, orc, k):
+    img = np.random.default_rng(9).random((30, 3, 32, 32), dtype=np.float32)
+    lab = (np.arange(30) % 10).astype(np.int32)
+    got, losses, fw = replay_case(ctx, orc, spec_text("resnet18_cifar"), 77, img, lab, k, 8, 2)
+    close(got["step_losses"], losses, rtol=1e-4)
+    close(got["final_block"], fw, rtol=2e-4, atol_frac=2e-4)
+
+
+def test_three_layer_candidate_replay(ctx, orc):
+    img, lab = orc.synthetic_dataset(60, 11, 2)
+    got, losses, fw = replay_case(ctx, orc, spec_text("toy_teacher"), 404, img, lab, 2, 16, 6,
+                                  kind=1)
+    close(got["step_losses"], losses, rtol=1e-4)
+    close(got["final_block"], fw, rtol=2e-4, atol_frac=2e-4)
+
+
+# ------------------------------------------------------- train_block ----
+def test_train_block_matches_golden(ctx, orc):
+    g = np.load(os.path.join(GOLD, "toy_train_block.npz"))
+    spec = spec_text("toy_teacher")
+    ctx.teacher_load(spec, g["teacher_w"])
+    ctx.dataset_load(g["images"], g["labels"])
+    t = P.make_task(2, epochs=4, eval_every=2, seed=1234, batch_size=16, lr=0.02)
+    r = ctx.run([t], g["train_idx"], g["eval_idx"])["results"][0]
+    assert not r["failed"]
+    close(r["loss_history"], g["loss_history"], rtol=1e-4)
+    ge = g["eval_history"]
+    assert [e for e, _ in r["eval_history"]] == [int(e) for e in ge[:, 0]]
+    # accuracies are integer counts over 10 eval samples; near-ties may flip one
+    assert np.max(np.abs(np.array([a for _, a in r["eval_history"]]) - ge[:, 1])) <= 0.1 + 1e-12
+    assert r["best_eval"] == pytest.approx(float(g["best_eval"]), abs=0.1 + 1e-12)
+    if np.allclose([a for _, a in r["eval_history"]], ge[:, 1]):
+        close(r["block"], g["block"], rtol=2e-4, atol_frac=2e-4)
+
+
+def test_eval_with_student_matches_oracle(ctx, orc):
+    spec = spec_text("toy_teacher")
+    tw = orc.teacher_init(spec, 404)
+    img, lab = orc.synthetic_dataset(60, 11, 2)
+    ctx.teacher_load(spec, tw)
+    ctx.dataset_load(img, lab)
+    _, ev = orc.stratified_split(lab, 0.2, 12)
+    for k, cin, cout, s in [(1, 3, 16, 1), (2, 16, 32, 2), (3, 32, 32, 1)]:
+        sw = orc.build_candidate(0, cin, cout, s, 5)
+        assert ctx.eval_with_student(k, 0, sw, ev, 16) == orc.eval_with_student(
+            spec, tw, img, lab, ev, k, 0, sw, 16)
+
+
+def test_candidate_infer_matches_oracle(ctx, orc):
+    for kind, cin, cout, s in [(0, 16, 32, 2), (1, 64, 64, 1)]:
+        bw = orc.build_candidate(kind, cin, cout, s, 3)
+        x = np.random.default_rng(1).random((4, cin, 8, 8), dtype=np.float32)
+        close(ctx.candidate_infer(kind, cin, cout, s, bw, x),
+              orc.candidate_infer(kind, cin, cout, s, bw, x), rtol=1e-4)
+
+
+# ------------------------------------------------------ run_parallel ----
+def _three_tasks():
+    return [P.make_task(k, epochs=2, eval_every=2, seed=P.mix_seed(99, k), batch_size=10, lr=0.02)
+            for k in (1, 2, 3)]
+
+
+def test_run_parallel_schedule_transparency(ctx, orc):
+    """test_runtime.cpp:206-253: identical block bits for every policy/width."""
+    spec = spec_text("toy_teacher")
+    ctx.teacher_load(spec, orc.teacher_init(spec, 2025))
+    img, lab = orc.synthetic_dataset(40, 21, 2)
+    ctx.dataset_load(img, lab)
+    tr, ev = orc.stratified_split(lab, 0.25, 3)
+    base = ctx.run(_three_tasks(), tr, ev, plan=P.round_robin([1, 2, 3], 1), workers=1)
+    for policy in ("round_robin", "wfd", "work_stealing"):
+        for workers in (2, 3):
+            plan = P.round_robin([1, 2, 3], workers)
+            r = ctx.run(_three_tasks(), tr, ev, plan=plan, workers=workers, policy=policy)
+            assert [x["block_index"] for x in r["results"]] == [1, 2, 3]
+            for a, b in zip(base["results"], r["results"]):
+                assert np.array_equal(a["block"], b["block"])
+                assert a["loss_history"] == b["loss_history"]
+            kinds = [e[3] for e in r["trace"]]
+            assert kinds.count(0) == 3 and kinds.count(1) == 3 and kinds.count(2) == 3
+            assert kinds.count(4) == 1
+    # a task alone gives the same bits as inside the group
+    alone = ctx.run([_three_tasks()[1]], tr, ev)["results"][0]
+    assert np.array_equal(alone["block"], base["results"][1]["block"])
+
+
+def test_run_parallel_failure_isolation_and_validation(ctx, orc):
+    spec = spec_text("toy_teacher")
+    ctx.teacher_load(spec, orc.teacher_init(spec, 77))
+    img, lab = orc.synthetic_dataset(30, 5, 2)
+    ctx.dataset_load(img, lab)
+    tr, ev = orc.stratified_split(lab, 0.2, 3)
+    tasks = _three_tasks()
+    tasks[1].loss_mode = 1  # combined: not on the GPU path -> failed result
+    r = ctx.run(tasks, tr, ev, plan=P.round_robin([1, 2, 3], 2), workers=2)
+    assert [x["failed"] for x in r["results"]] == [False, True, False]
+    with pytest.raises(ValueError):
+        ctx.run(_three_tasks(), tr, ev, plan=[[1, 9], [2, 3]], workers=2)
+    with pytest.raises(ValueError):
+        ctx.run(_three_tasks(), tr, ev, plan=[[1, 2]], workers=1)
+
+
+def test_task_validation(ctx, orc):
+    spec = spec_text("toy_teacher")
+    ctx.teacher_load(spec, orc.teacher_init(spec, 1))
+    img, lab = orc.synthetic_dataset(20, 1, 1)
+    ctx.dataset_load(img, lab)
+    tr, ev = orc.stratified_split(lab, 0.2, 1)
+    for bad in (dict(epochs=0), dict(eval_every=0), dict(batch_size=0), dict(threshold=1.5),
+                dict(max_steps=-1)):
+        t = P.make_task(1, **{**dict(epochs=1, batch_size=8), **bad})
+        with pytest.raises(ValueError):
+            ctx.run([t], tr, ev)
+    for k in (0, 4):
+        with pytest.raises(ValueError):
+            ctx.run([P.make_task(k, epochs=1, batch_size=8)], tr, ev)
