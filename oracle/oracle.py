@@ -338,14 +338,16 @@ class Oracle:
         }
 
     def train_replay(self, spec, tw, images, labels, train_idx, eval_idx, task, n_steps,
-                     n_block_floats):
+                     n_block_floats, with_f64=False):
+        """Returns (float losses, final weights) or, with_f64, also the fp64 losses."""
         ds = self._ds(images, labels)
         sp = self._split(train_idx, eval_idx)
         losses = np.zeros(n_steps, np.float32)
+        l64 = np.zeros(n_steps, np.float64)
         fw = np.zeros(n_block_floats, np.float32)
-        f = self.fn("train_replay", C.c_int, [C.c_char_p, F32P, C.POINTER(Dataset),
-                                               C.POINTER(Split), C.POINTER(Task), C.c_int, F32P,
-                                               F32P, C.c_size_t])
+        f = self.fn("train_replay_f64", C.c_int, [C.c_char_p, F32P, C.POINTER(Dataset),
+                                                   C.POINTER(Split), C.POINTER(Task), C.c_int,
+                                                   F32P, F64P, F32P, C.c_size_t])
         self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), C.byref(ds),
-                      C.byref(sp), C.byref(task), n_steps, losses, fw, fw.size))
-        return losses, fw
+                      C.byref(sp), C.byref(task), n_steps, losses, l64, fw, fw.size))
+        return (losses, fw, l64) if with_f64 else (losses, fw)

@@ -148,6 +148,13 @@ int ORC(train_replay)(const char* spec, const float* tw, const orc_dataset* d,
                       const orc_split* s, const orc_task* t, int n_steps, float* step_loss,
                       float* final_w, size_t cap);
 
+/* train_replay plus, per step, the MSE of the same student/teacher outputs
+ * accumulated in fp64 (the reference's float serial sum carries its own
+ * rounding error). */
+int ORC(train_replay_f64)(const char* spec, const float* tw, const orc_dataset* d,
+                          const orc_split* s, const orc_task* t, int n_steps, float* step_loss,
+                          double* step_loss64, float* final_w, size_t cap);
+
 #pragma GCC visibility pop
 #ifdef __cplusplus
 }

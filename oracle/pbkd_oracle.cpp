@@ -1273,6 +1273,12 @@ int orc_train_block(const char* spec, const float* tw, const orc_dataset* dd, co
 int orc_train_replay(const char* spec, const float* tw, const orc_dataset* dd, const orc_split* s,
                      const orc_task* t, int n_steps, float* step_loss, float* final_w,
                      size_t cap) {
+    return orc_train_replay_f64(spec, tw, dd, s, t, n_steps, step_loss, nullptr, final_w, cap);
+}
+
+int orc_train_replay_f64(const char* spec, const float* tw, const orc_dataset* dd, const orc_split* s,
+                         const orc_task* t, int n_steps, float* step_loss, double* loss64,
+                         float* final_w, size_t cap) {
     return guard([&] {
         Net net = load_net(spec, tw);
         const Data d = to_data(dd);
@@ -1293,6 +1299,14 @@ int orc_train_replay(const char* spec, const float* tw, const orc_dataset* dd, c
                 BlockCache cache;
                 const T4 so = block_forward(student, a, true, &cache);
                 step_loss[done] = mse(so.d.data(), tt.d.data(), so.d.size());
+                if (loss64) {
+                    double acc = 0.0;
+                    for (size_t q = 0; q < so.d.size(); ++q) {
+                        const double df = static_cast<double>(so.d[q]) - static_cast<double>(tt.d[q]);
+                        acc += df * df;
+                    }
+                    loss64[done] = acc / static_cast<double>(so.d.size());
+                }
                 T4 gs(so.n, so.c, so.h, so.w);
                 mse_bwd(so.d.data(), tt.d.data(), so.d.size(), 1.0f, gs.d.data());
                 opt.zero();
@@ -1304,5 +1318,6 @@ int orc_train_replay(const char* spec, const float* tw, const orc_dataset* dd, c
         block_store(student, final_w, cap);
     });
 }
+
 
 }  // extern "C"

@@ -359,6 +359,12 @@ int ref_train_block(const char* spec, const float* tw, const orc_dataset* d, con
 int ref_train_replay(const char* spec, const float* tw, const orc_dataset* d, const orc_split* s,
                      const orc_task* t, int n_steps, float* step_loss, float* final_w,
                      size_t cap) {
+    return ref_train_replay_f64(spec, tw, d, s, t, n_steps, step_loss, nullptr, final_w, cap);
+}
+
+int ref_train_replay_f64(const char* spec, const float* tw, const orc_dataset* d, const orc_split* s,
+                         const orc_task* t, int n_steps, float* step_loss, double* loss64,
+                         float* final_w, size_t cap) {
     // The train_block inner loop (distill.cpp:197-253) spelled through the
     // reference's public API, LocalOnly mode.
     return guard([&] {
@@ -386,6 +392,14 @@ int ref_train_replay(const char* spec, const float* tw, const orc_dataset* d, co
                 BlockCache cache;
                 const Tensor s_out = block_forward(student, a_prev, true, &cache);
                 step_loss[done] = ops::mse_local_loss(s_out, t_out);
+                if (loss64) {
+                    double acc = 0.0;
+                    for (size_t q = 0; q < s_out.data.size(); ++q) {
+                        const double df = static_cast<double>(s_out.data[q]) - t_out.data[q];
+                        acc += df * df;
+                    }
+                    loss64[done] = acc / static_cast<double>(s_out.data.size());
+                }
                 Tensor gs(s_out.n, s_out.c, s_out.h, s_out.w);
                 ops::mse_local_loss_bwd<float>(s_out, t_out, gs.data.data(), 1.0f);
                 opt.zero_grads();

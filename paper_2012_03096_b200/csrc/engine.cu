@@ -85,6 +85,23 @@ public:
             launch(reinterpret_cast<const Op*>(slab + off), nd, total, st);
         });
     }
+    // tcgen05 GEMMs: smem carve-up sized for the widest N tile of the launch
+    void gemm(std::vector<GemmOp> ops) {
+        if (ops.empty()) return;
+        int total = 0, bn_max = 16;
+        for (GemmOp& o : ops) {
+            o.cta_begin = total;
+            total += std::max(1, ctas_gemm(o));
+            bn_max = std::max(bn_max, o.bn);
+        }
+        const size_t off = (host_.size() + 63) & ~size_t(63);
+        host_.resize(off + ops.size() * sizeof(GemmOp));
+        std::memcpy(host_.data() + off, ops.data(), ops.size() * sizeof(GemmOp));
+        const int nd = static_cast<int>(ops.size());
+        steps_.push_back([off, nd, total, bn_max](cudaStream_t st, const uint8_t* slab) {
+            launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, bn_max, st);
+        });
+    }
     void raw(std::function<void(cudaStream_t)> f) {
         steps_.push_back([f](cudaStream_t st, const uint8_t*) { f(st); });
     }
@@ -193,19 +210,16 @@ GemmOp conv_gemm(const ConvDev& c, const float* x, int n, int ih, int iw, float*
     o.ldc = c.cout;
     o.epi = 0;
     o.ksplit = 1;
-    o.kchunk = o.K;
-    o.tiles_m = ceil_div(o.M, kGemmBM);
-    o.tiles_n = ceil_div(o.N, kGemmBN);
     if (affine) {
         o.scale = c.scale.f();
         o.shift = c.shift.f();
     }
     o.skip = skip;
     o.relu = relu_out ? 1 : 0;
+    gemm_finalize(o);
     return o;
 }
 
-int gemm_ctas(const GemmOp& o) { return ctas_gemm(o); }
 
 // ------------------------------------------------------------- task state
 struct UnitDims {
@@ -253,8 +267,12 @@ struct TaskState {
     float* shift_u(int uu) const { return shift.f() + static_cast<size_t>(uu) * u[0].cout; }
 };
 
+// parameter segments start on 16-byte boundaries (float4 loads)
+void pad4(std::vector<float>& v) {
+    while (v.size() % 4) v.push_back(0.0f);
+}
+
 int split_count(long long kdim) { return std::max(1, std::min(64, ceil_div(kdim, 512))); }
-int split_chunk(long long kdim, int ks) { return ((ceil_div(kdim, ks) + kGemmBK - 1) / kGemmBK) * kGemmBK; }
 
 }  // namespace
 
@@ -360,21 +378,17 @@ struct Engine::Impl {
     // Teacher block j (0-based) forward on n samples: x -> y.  scratch t1/sk.
     void teacher_block(Program& P, int j, const float* x, float* y, int n, float* t1, float* sk) {
         const TBlockDev& b = tblocks[static_cast<size_t>(j)];
-        auto one = [](const GemmOp& o) {
-            return std::vector<GemmOp>{o};
-        };
-        std::function<int(const GemmOp&)> cf = gemm_ctas;
         if (b.kind == 0) {
-            P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.c1, x, n, b.hin, b.win, y, true, nullptr, true)), cf);
+            P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, y, true, nullptr, true)});
             return;
         }
-        P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true)), cf);
+        P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true)});
         const float* skip = x;
         if (b.has_proj) {
-            P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.proj, x, n, b.hin, b.win, sk, false, nullptr, false)), cf);
+            P.gemm({conv_gemm(b.proj, x, n, b.hin, b.win, sk, false, nullptr, false)});
             skip = sk;
         }
-        P.grouped<GemmOp>(launch_gemm, one(conv_gemm(b.c2, t1, n, b.mid_h, b.mid_w, y, true, skip, true)), cf);
+        P.gemm({conv_gemm(b.c2, t1, n, b.mid_h, b.mid_w, y, true, skip, true)});
     }
 
     void load_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {
@@ -453,13 +467,17 @@ struct Engine::Impl {
             const pbkd::LayerParams& bnl = cand.block.layers[li + 2];
             li += 4;
             const int ci = s.u[u].cin, co = s.u[u].cout;
+            pad4(host);
             s.off_dw[u] = host.size();
             for (int tap = 0; tap < 9; ++tap)
                 for (int c = 0; c < ci; ++c) host.push_back(dwl.weight.data[static_cast<size_t>(c) * 9 + tap]);
+            pad4(host);
             s.off_pw[u] = host.size();
             host.insert(host.end(), pwl.weight.data.begin(), pwl.weight.data.end());
+            pad4(host);
             s.off_g[u] = host.size();
             host.insert(host.end(), bnl.gamma.data.begin(), bnl.gamma.data.end());
+            pad4(host);
             s.off_b[u] = host.size();
             host.insert(host.end(), bnl.beta.data.begin(), bnl.beta.data.end());
             (void)co;
@@ -491,7 +509,7 @@ struct Engine::Impl {
         s.gp.alloc(static_cast<size_t>(M) * cout * sizeof(float));
         s.gd.alloc(static_cast<size_t>(M) * cmax * sizeof(float));
         s.gy.alloc(static_cast<size_t>(M) * cout * sizeof(float));
-        const int tiles = ceil_div(M, kGemmBM);
+        const int tiles = ceil_div(M, 128);
         s.cs0.alloc(static_cast<size_t>(tiles) * cout * sizeof(float));
         s.cs1.alloc(static_cast<size_t>(tiles) * cout * sizeof(float));
         int pc = 1;
@@ -546,7 +564,6 @@ struct Engine::Impl {
                   s->tgt_stream.f() + static_cast<size_t>(step) * B * s->out_row, s->failed.i(), gsteps[i]};
             cx.push_back(c);
         }
-        std::function<int(const GemmOp&)> gc = gemm_ctas;
         // ---- forward
         for (int u = 0; u < U; ++u) {
             std::vector<DwFwdOp> dws;
@@ -592,9 +609,7 @@ struct Engine::Impl {
                 g.part0 = s.cs0.f();
                 g.part1 = s.cs1.f();
                 g.ksplit = 1;
-                g.kchunk = d.cin;
-                g.tiles_m = ceil_div(c.M, kGemmBM);
-                g.tiles_n = ceil_div(d.cout, kGemmBN);
+                gemm_finalize(g);
                 g.failed = c.failed;
                 gms.push_back(g);
                 BnStatOp b{};
@@ -612,8 +627,8 @@ struct Engine::Impl {
                 bns.push_back(b);
             }
             P.grouped<DwFwdOp>(launch_dw_fwd, dws, ctas_dw_fwd);
-            P.grouped<GemmOp>(launch_gemm, gms, gc);
-            P.grouped<BnStatOp>(launch_bn_stat, bns, [](const BnStatOp& o) { return ceil_div(o.c, kThreads); });
+            P.gemm(gms);
+            P.grouped<BnStatOp>(launch_bn_stat, bns, [](const BnStatOp& o) { return ctas_cols(o.c); });
         }
         // ---- loss and last batch-norm backward sums
         {
@@ -657,7 +672,7 @@ struct Engine::Impl {
                 fs.push_back(f);
             }
             P.grouped<LossOp>(launch_loss, ls, [](const LossOp& o) { return o.ctas; });
-            P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fs, [](const BnBwdFinOp& o) { return ceil_div(o.c, kThreads); });
+            P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fs, [](const BnBwdFinOp& o) { return ctas_cols(o.c); });
         }
         // ---- backward
         for (int u = U - 1; u >= 0; --u) {
@@ -702,9 +717,7 @@ struct Engine::Impl {
                 g.ldc = d.cin;
                 g.epi = 0;
                 g.ksplit = 1;
-                g.kchunk = d.cout;
-                g.tiles_m = ceil_div(c.M, kGemmBM);
-                g.tiles_n = ceil_div(d.cin, kGemmBN);
+                gemm_finalize(g);
                 g.failed = c.failed;
                 dg.push_back(g);
                 // wgrad: gW[o][j] = sum_m gp[m][o] d[m][j]  (split-K over rows)
@@ -722,10 +735,7 @@ struct Engine::Impl {
                 w.ldc = d.cin;
                 w.epi = 2;
                 w.ksplit = split_count(c.M);
-                w.kchunk = split_chunk(c.M, w.ksplit);
-                w.ksplit = ceil_div(c.M, w.kchunk);
-                w.tiles_m = ceil_div(d.cout, kGemmBM);
-                w.tiles_n = ceil_div(d.cin, kGemmBN);
+                gemm_finalize(w);
                 w.failed = c.failed;
                 wg.push_back(w);
                 ReduceOp r{};
@@ -802,13 +812,13 @@ struct Engine::Impl {
             }
             auto red_ctas = [](const ReduceOp& o) { return ceil_div(o.width, kThreads); };
             P.grouped<BnBwdApplyOp>(launch_bn_bwd_apply, aps, [](const BnBwdApplyOp& o) { return ctas_elem(o.total); });
-            P.grouped<GemmOp>(launch_gemm, dg, gc);
-            P.grouped<GemmOp>(launch_gemm, wg, gc);
+            P.gemm(dg);
+            P.gemm(wg);
             P.grouped<ReduceOp>(launch_reduce, wr, red_ctas);
             if (u > 0) {
                 P.grouped<DwBwdOp>(launch_dw_bwd, dbs, [](const DwBwdOp& o) { return o.ctas; });
                 P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
-                P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fins, [](const BnBwdFinOp& o) { return ceil_div(o.c, kThreads); });
+                P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fins, [](const BnBwdFinOp& o) { return ctas_cols(o.c); });
             } else {
                 P.grouped<DwGkOp>(launch_dw_gk, gks, [](const DwGkOp& o) { return o.ctas; });
                 P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
@@ -911,11 +921,8 @@ struct Engine::Impl {
             gm.C = bufb;
             gm.ldc = cout;
             gm.ksplit = 1;
-            gm.kchunk = d.cin;
-            gm.tiles_m = ceil_div(M, kGemmBM);
-            gm.tiles_n = ceil_div(cout, kGemmBN);
-            std::function<int(const GemmOp&)> gc = gemm_ctas;
-            P.grouped<GemmOp>(launch_gemm, {gm}, gc);
+            gemm_finalize(gm);
+            P.gemm({gm});
             if (u == U - 1) {
                 const long long tot = M * cout;
                 P.raw([=](cudaStream_t st2) { launch_bn_infer_relu(bufb, out, tot, cout, scale, shift, st2); });
@@ -1325,11 +1332,10 @@ void Engine::bench_kernel(int which, int batch, int iters, double* ms, double* b
     PBKD_LAUNCH_CHECK();
     Program P;
     double by = 0, fl = 0;
-    std::function<int(const GemmOp&)> gc = gemm_ctas;
     if (which == 0) {
         const ConvDev& cv = b.c1;
         GemmOp o = conv_gemm(cv, x.f(), n, b.hin, b.win, y.f(), true, nullptr, true);
-        P.grouped<GemmOp>(launch_gemm, {o}, gc);
+        P.gemm({o});
         fl = 2.0 * o.M * o.N * o.K;
         by = 4.0 * (static_cast<double>(n) * b.hin * b.win * b.cin + static_cast<double>(o.N) * o.K + static_cast<double>(o.M) * o.N);
     } else if (which == 1) {
@@ -1337,8 +1343,9 @@ void Engine::bench_kernel(int which, int batch, int iters, double* ms, double* b
         g.M = static_cast<int>(M), g.N = c, g.K = c;
         g.A = x.f(), g.lda = c, g.a_kmajor = 1, g.B = w.f(), g.ldb = c, g.b_kmajor = 1;
         g.C = y.f(), g.ldc = c, g.epi = 1, g.part0 = parts.f(), g.part1 = parts.f() + static_cast<size_t>(2048) * c;
-        g.ksplit = 1, g.kchunk = c, g.tiles_m = ceil_div(M, kGemmBM), g.tiles_n = ceil_div(c, kGemmBN);
-        P.grouped<GemmOp>(launch_gemm, {g}, gc);
+        g.ksplit = 1;
+        gemm_finalize(g);
+        P.gemm({g});
         fl = 2.0 * M * c * c;
         by = 4.0 * (2.0 * M * c + static_cast<double>(c) * c);
     } else if (which == 2) {
@@ -1479,14 +1486,18 @@ Tensor Engine::candidate_infer(const Block& cand, const Tensor& x) {
         li += 4;
         const int ci = dwl.in_channels, co = pwl.out_channels;
         s.u[u] = u == 0 ? UnitDims{ci, x.h, x.w, co, ho, wo, cand.stride} : UnitDims{ci, ho, wo, co, ho, wo, 1};
-        s.off_dw[u] = host.size();
+        pad4(host);
+            s.off_dw[u] = host.size();
         for (int tap = 0; tap < 9; ++tap)
             for (int c = 0; c < ci; ++c) host.push_back(dwl.weight.data[static_cast<size_t>(c) * 9 + tap]);
-        s.off_pw[u] = host.size();
+        pad4(host);
+            s.off_pw[u] = host.size();
         host.insert(host.end(), pwl.weight.data.begin(), pwl.weight.data.end());
-        s.off_g[u] = host.size();
+        pad4(host);
+            s.off_g[u] = host.size();
         host.insert(host.end(), bnl.gamma.data.begin(), bnl.gamma.data.end());
-        s.off_b[u] = host.size();
+        pad4(host);
+            s.off_b[u] = host.size();
         host.insert(host.end(), bnl.beta.data.begin(), bnl.beta.data.end());
         stats.insert(stats.end(), bnl.moving_mean.data.begin(), bnl.moving_mean.data.end());
         stats.insert(stats.end(), bnl.moving_var.data.begin(), bnl.moving_var.data.end());

@@ -633,9 +633,8 @@ int pbkd_k_pw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int r
         g.A = x, g.lda = cin, g.a_kmajor = 1;
         g.B = w, g.ldb = cin, g.b_kmajor = 1;
         g.C = y, g.ldc = cout;
-        g.ksplit = 1, g.kchunk = cin;
-        g.tiles_m = ceil_div(rows, kGemmBM);
-        g.tiles_n = ceil_div(cout, kGemmBN);
+        g.ksplit = 1;
+        gemm_finalize(g);
         cudaStream_t st = ctx->eng->stream();
         if (col_sum || col_sq) {
             Scratch p0(static_cast<size_t>(g.tiles_m) * cout), p1(static_cast<size_t>(g.tiles_m) * cout);
@@ -667,9 +666,8 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             g.A = gy, g.lda = cout, g.a_kmajor = 1;
             g.B = w, g.ldb = cin, g.b_kmajor = 0;
             g.C = gx, g.ldc = cin;
-            g.ksplit = 1, g.kchunk = cout;
-            g.tiles_m = ceil_div(rows, kGemmBM);
-            g.tiles_n = ceil_div(cin, kGemmBN);
+            g.ksplit = 1;
+            gemm_finalize(g);
             launch_one(st, launch_gemm, g, ctas_gemm(g));
         }
         if (gw) {
@@ -680,10 +678,7 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             g.ldc = cin;
             g.epi = 2;
             g.ksplit = std::max(1, std::min(64, ceil_div(rows, 512)));
-            g.kchunk = ((ceil_div(rows, g.ksplit) + kGemmBK - 1) / kGemmBK) * kGemmBK;
-            g.ksplit = ceil_div(rows, g.kchunk);
-            g.tiles_m = ceil_div(cout, kGemmBM);
-            g.tiles_n = ceil_div(cin, kGemmBN);
+            gemm_finalize(g);
             Scratch part(static_cast<size_t>(g.ksplit) * cout * cin);
             g.C = part.p;
             launch_one(st, launch_gemm, g, ctas_gemm(g));

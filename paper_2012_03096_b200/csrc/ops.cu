@@ -290,138 +290,40 @@ void launch_reduce(const ReduceOp* d, int nd, int ctas, cudaStream_t st) {
     PBKD_LAUNCH_CHECK();
 }
 
-// -------------------------------------------------------------- SIMT GEMM
-int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
-
-__device__ __forceinline__ float gemm_load_a(const GemmOp& o, int m, int k) {
-    if (m >= o.M || k >= o.K) return 0.0f;
-    if (o.conv) {
-        const int tap = k / o.ic, j = k - tap * o.ic;
-        const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
-        const int ox = m % o.ow;
-        const int t2 = m / o.ow;
-        const int oy = t2 % o.oh, n = t2 / o.oh;
-        const int iy = oy * o.cstride - o.cpad + ky, ix = ox * o.cstride - o.cpad + kx;
-        if (iy < 0 || iy >= o.ih || ix < 0 || ix >= o.iw) return 0.0f;
-        return o.A[((static_cast<long long>(n) * o.ih + iy) * o.iw + ix) * o.ic + j];
-    }
-    return o.a_kmajor ? o.A[m * o.lda + k] : o.A[static_cast<long long>(k) * o.lda + m];
-}
-__device__ __forceinline__ float gemm_load_b(const GemmOp& o, int n, int k) {
-    if (n >= o.N || k >= o.K) return 0.0f;
-    return o.b_kmajor ? o.B[n * o.ldb + k] : o.B[static_cast<long long>(k) * o.ldb + n];
-}
-
-__global__ void __launch_bounds__(kThreads) gemm_kernel(const GemmOp* __restrict__ ops, int nd) {
-    constexpr int BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
-    __shared__ __align__(16) float As[BK][BM + 4];
-    __shared__ __align__(16) float Bs[BK][BN + 4];
-    __shared__ float red0[16][BN], red1[16][BN];
-    int local;
-    const GemmOp& o = op_of(ops, nd, local);
-    if (is_failed(o.failed)) return;
-    const int tiles_mn = o.tiles_m * o.tiles_n;
-    const int split = local / tiles_mn;
-    const int rem = local - split * tiles_mn;
-    const int tm = rem / o.tiles_n, tn = rem - (rem / o.tiles_n) * o.tiles_n;
-    const int m0 = tm * BM, n0 = tn * BN;
-    const int kbeg = split * o.kchunk;
-    const int kend = min(o.K, kbeg + o.kchunk);
-    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-    float acc[4][4];
-    for (int i = 0; i < 4; ++i)
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-    const bool a_km = o.conv || o.a_kmajor;
-    for (int k0 = kbeg; k0 < kend; k0 += BK) {
-        // A tile (BM x BK)
-        if (a_km) {
-            const int m = tid / 4, kq = (tid % 4) * 4;
-            for (int q = 0; q < 4; ++q) {
-                const int k = k0 + kq + q;
-                As[kq + q][m] = (k < kend) ? gemm_load_a(o, m0 + m, k) : 0.0f;
-            }
-        } else {
-            const int k = tid / 16, mq = (tid % 16) * 4;
-            for (int q = 0; q < 4; ++q)
-                As[k][mq + q] = (k0 + k < kend) ? gemm_load_a(o, m0 + mq + q, k0 + k) : 0.0f;
-        }
-        if (o.b_kmajor) {
-            const int n = tid / 4, kq = (tid % 4) * 4;
-            for (int q = 0; q < 4; ++q) {
-                const int k = k0 + kq + q;
-                Bs[kq + q][n] = (k < kend) ? gemm_load_b(o, n0 + n, k) : 0.0f;
-            }
-        } else {
-            const int k = tid / 16, nq = (tid % 16) * 4;
-            for (int q = 0; q < 4; ++q)
-                Bs[k][nq + q] = (k0 + k < kend) ? gemm_load_b(o, n0 + nq + q, k0 + k) : 0.0f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < BK; ++k) {
-            const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
-            const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
-            const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-        }
-        __syncthreads();
-    }
-    // epilogue
-    float* C = o.C + (o.epi == 2 ? static_cast<long long>(split) * o.M * o.ldc : 0);
-    float cs[4] = {0, 0, 0, 0}, cq[4] = {0, 0, 0, 0};
-    for (int i = 0; i < 4; ++i) {
-        const int m = m0 + ty * 4 + i;
-        if (m >= o.M) continue;
-        for (int j = 0; j < 4; ++j) {
-            const int n = n0 + tx * 4 + j;
-            if (n >= o.N) continue;
-            float v = acc[i][j];
-            if (o.scale) v = bn_infer_apply(v, o.scale[n], o.shift[n]);
-            if (o.skip) v = add(v, o.skip[static_cast<long long>(m) * o.ldc + n]);
-            if (o.relu) v = relu(v);
-            C[static_cast<long long>(m) * o.ldc + n] = v;
-            cs[j] += v;
-            cq[j] += v * v;
-        }
-    }
-    if (o.epi == 1) {
-        for (int j = 0; j < 4; ++j) {
-            red0[ty][tx * 4 + j] = cs[j];
-            red1[ty][tx * 4 + j] = cq[j];
-        }
-        __syncthreads();
-        if (tid < BN && n0 + tid < o.N) {
-            float s = 0.0f, q = 0.0f;
-            for (int r = 0; r < 16; ++r) {
-                s += red0[r][tid];
-                q += red1[r][tid];
-            }
-            o.part0[static_cast<long long>(tm) * o.N + n0 + tid] = s;
-            o.part1[static_cast<long long>(tm) * o.N + n0 + tid] = q;
-        }
-    }
-}
-
-void launch_gemm(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
-    gemm_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
-    PBKD_LAUNCH_CHECK();
-}
-
 // ------------------------------------------------------------ BN statistics
+// Column sums of [parts][c] partials: a CTA owns 32 channels, 8 lanes stride
+// over the parts, lanes combine in fixed order (deterministic, latency-hidden).
+constexpr int kColLanes = kThreads / 32;
+int ctas_cols(int c) { return ceil_div(c, 32); }
+
+__device__ __forceinline__ float col_sum(const float* __restrict__ part, int parts, int c, int ch,
+                                         float (*red)[32]) {
+    const int lane = threadIdx.x / 32, col = threadIdx.x % 32;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (ch < c) {
+        int p = lane;
+        for (; p + 3 * kColLanes < parts; p += 4 * kColLanes)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] += part[static_cast<long long>(p + u * kColLanes) * c + ch];
+        for (; p < parts; p += kColLanes) acc[0] += part[static_cast<long long>(p) * c + ch];
+    }
+    red[lane][col] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    __syncthreads();
+    float s = 0.0f;
+    for (int l = 0; l < kColLanes; ++l) s += red[l][col];
+    __syncthreads();
+    return s;
+}
+
 __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __restrict__ ops, int nd) {
+    __shared__ float red[kColLanes][32];
     int local;
     const BnStatOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
-    const int ch = local * kThreads + threadIdx.x;
-    if (ch >= o.c) return;
-    float sum = 0.0f, sq = 0.0f;
-    for (int t = 0; t < o.tiles; ++t) {
-        sum += o.part_sum[static_cast<long long>(t) * o.c + ch];
-        sq += o.part_sq[static_cast<long long>(t) * o.c + ch];
-    }
+    const int ch = local * 32 + threadIdx.x % 32;
+    const float sum = col_sum(o.part_sum, o.tiles, o.c, ch, red);
+    const float sq = col_sum(o.part_sq, o.tiles, o.c, ch, red);
+    if (threadIdx.x >= 32 || ch >= o.c) return;
     const float fm = static_cast<float>(o.m);
     const float mean = __fdiv_rn(sum, fm);
     float var = sub(__fdiv_rn(sq, fm), mul(mean, mean));
@@ -494,23 +396,24 @@ void launch_loss(const LossOp* d, int nd, int ctas, cudaStream_t st) {
 }
 
 __global__ void __launch_bounds__(kThreads) bn_bwd_fin_kernel(const BnBwdFinOp* __restrict__ ops, int nd) {
+    __shared__ float red[kColLanes][32];
     int local;
     const BnBwdFinOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
-    const int ch = local * kThreads + threadIdx.x;
-    if (o.loss_out && local == 0 && threadIdx.x == 0) {
+    if (o.loss_out && local == 0 && threadIdx.x < 32) {  // one warp, fixed-order tree
         double s = 0.0;
-        for (int p = 0; p < o.ctas; ++p) s += static_cast<double>(o.part_loss[p]);
-        const float loss = static_cast<float>(s / o.count);
-        *o.loss_out = loss;
-        if (!isfinite(loss)) *o.failed = 1;
+        for (int p = threadIdx.x; p < o.ctas; p += 32) s += static_cast<double>(o.part_loss[p]);
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (threadIdx.x == 0) {
+            const float loss = static_cast<float>(s / o.count);
+            *o.loss_out = loss;
+            if (!isfinite(loss)) *o.failed = 1;
+        }
     }
-    if (ch >= o.c) return;
-    float a = 0.0f, b = 0.0f;
-    for (int p = 0; p < o.ctas; ++p) {
-        a += o.part_sg[static_cast<long long>(p) * o.c + ch];
-        b += o.part_sgx[static_cast<long long>(p) * o.c + ch];
-    }
+    const int ch = local * 32 + threadIdx.x % 32;
+    const float a = col_sum(o.part_sg, o.ctas, o.c, ch, red);
+    const float b = col_sum(o.part_sgx, o.ctas, o.c, ch, red);
+    if (threadIdx.x >= 32 || ch >= o.c) return;
     o.sg[ch] = a;
     o.sgx[ch] = b;
     o.gbeta[ch] = a;

@@ -99,9 +99,14 @@ struct GemmOp {
     int conv, ih, iw, ic, oh, ow, ksz, cstride, cpad;
     const float *scale, *shift, *skip;
     int relu;
+    int bn;              // N tile (multiple of 16, <= 256), set by gemm_finalize
+    int tf32x3, tf32x1;  // 3xTF32 split (fp32 parity, default) or plain TF32
     const int* failed;
     int cta_begin;
 };
+
+// Fills tiling fields (bn, tiles, kchunk/ksplit) of a GemmOp (umma.cu).
+void gemm_finalize(GemmOp& o);
 
 // Batch-norm statistics from the GEMM column partials (ops.hpp:273-299):
 // mean, var = E[x^2]-mean^2 clamped, inv_std, moving-stat update.
@@ -181,13 +186,13 @@ struct ScatterOp {
 // Host-side helpers (defined in ops.cu) ------------------------------------
 int rows_part_ctas(long long rows, int c);  // deterministic partition size
 int rows_part_per(long long rows, int ctas);
-constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
 
 void launch_dw_fwd(const DwFwdOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_dw_bwd(const DwBwdOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_dw_gk(const DwGkOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_reduce(const ReduceOp* d_ops, int nd, int ctas, cudaStream_t st);
-void launch_gemm(const GemmOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_gemm(const GemmOp* d_ops, int nd, int ctas, cudaStream_t st);  // bn_max 256
+void launch_gemm_bn(const GemmOp* d_ops, int nd, int ctas, int bn_max, cudaStream_t st);
 void launch_bn_stat(const BnStatOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_loss(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_bn_bwd_fin(const BnBwdFinOp* d_ops, int nd, int ctas, cudaStream_t st);
@@ -199,6 +204,7 @@ void launch_scatter(const ScatterOp* d_ops, int nd, int ctas, cudaStream_t st);
 int ctas_dw_fwd(const DwFwdOp& o);
 int ctas_gemm(const GemmOp& o);
 int ctas_elem(long long total);
+int ctas_cols(int c);  // bn_stat / bn_bwd_fin CTAs per task
 
 // Non-grouped helpers used by evaluation / teacher / tests -----------------
 void launch_gather_nhwc(const float* images_nchw, const int* idx, int n, int c, int h, int w,

@@ -1,0 +1,456 @@
+// umma.cu -- tcgen05 / TMEM GEMM for sm_100a (pointwise convs, teacher
+// implicit-GEMM conv, weight gradients).
+//
+//   C[m][n] = sum_k A(m,k) * B(n,k),   fp32 in / fp32 out
+//
+// Tensor-core path: kind::tf32 MMAs (M=128, N=BN<=128, K=8) issued by one
+// elected thread; accumulators live in TMEM and are read back with tcgen05.ld.
+//
+// fp32 parity (north_star: 1e-4 relative) with TF32 tensor cores:
+//  * 3xTF32 split  a*b ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi  (hi = tf32
+//    round-to-nearest, lo = tf32 of the exact remainder);
+//  * per-chunk drain: every 32-wide K chunk accumulates into its own TMEM slot
+//    (two slots, double buffered) and the chunk results are summed in fp32
+//    registers in chunk order.  Measured on B200, letting one TMEM accumulator
+//    absorb all K/8 MMA steps loses ~K/8 * 2^-23 (biased rounding inside the
+//    MMA); the drain keeps every accumulator short and the cross-chunk sum
+//    round-to-nearest.
+//
+// Operands are staged global -> registers -> shared by all 128 threads (one
+// row of the 128-row tile per thread) into the canonical K-major SWIZZLE_128B
+// layout: row r at (r/8)*1024 + (r%8)*128 bytes, its 16-byte chunk c at
+// ((c ^ r%8) * 16).  Register staging is what lets one kernel gather an
+// implicit im2col (teacher conv), transpose MN-major sources (dgrad/wgrad)
+// and split hi/lo with no host-side relayout.  Two smem stages / TMEM slots:
+// threads refill stage s^1 and drain slot s^1 while the tensor core runs on s.
+#include <algorithm>
+#include <cstdlib>
+
+#include "ops.cuh"
+
+namespace pbkd_gpu {
+
+namespace {
+
+constexpr int kBM = 128;  // MMA M (TMEM lanes)
+constexpr int kBK = 32;   // fp32 K per stage = one 128-byte swizzle row
+constexpr int kRowBytes = 128;
+constexpr int kStages = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Round fp32 to the nearest tf32 (ties to even) and clear the 13 dropped bits,
+// so the MMA's operand read is exact and x - hi is the exact remainder.
+// (Integer ops on purpose: measured on B200, the cvt.rna.tf32.f32 result kept
+// the low bits and the split degenerated to plain TF32.)
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    const uint32_t b = __float_as_uint(x);
+    return (b + 0xFFFu + ((b >> 13) & 1u)) & 0xFFFFE000u;
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 format):
+// start>>4 [0,14), LBO>>4 [16,30) (=1, unused for swizzled K-major),
+// SBO>>4 [32,46) (=1024 B between 8-row groups), version 1 [46,48),
+// layout type SWIZZLE_128B = 2 at [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M=128, N=n.
+__device__ __forceinline__ uint32_t instr_desc(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// acc[0..15] += TMEM row (this thread's lane), 16 columns at addr
+__device__ __forceinline__ void tmem_add16(uint32_t addr, float* acc) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = __fadd_rn(acc[i], __uint_as_float(r[i]));
+}
+
+// Store one 32-float K slice of a row (hi and lo parts) into a swizzled tile.
+__device__ __forceinline__ void put_row(uint8_t* hi, uint8_t* lo, int r, const float* v, bool split) {
+    const int base = (r >> 3) * 1024 + (r & 7) * kRowBytes;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float x = v[c * 4 + q];
+            h[q] = to_tf32(x);
+            l[q] = split ? to_tf32(__fsub_rn(x, __uint_as_float(h[q]))) : 0u;
+        }
+        const int off = base + ((c ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+        if (split) *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+}
+
+__device__ __forceinline__ void zero32(float* v) {
+#pragma unroll
+    for (int i = 0; i < kBK; ++i) v[i] = 0.0f;
+}
+
+__device__ __forceinline__ void load32_kmajor(const float* __restrict__ row, int k0, int kend, bool vec,
+                                              float* v) {
+    if (vec && k0 + kBK <= kend) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(row + k0) + c);
+            v[4 * c] = q.x, v[4 * c + 1] = q.y, v[4 * c + 2] = q.z, v[4 * c + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kBK; ++i) v[i] = (k0 + i < kend) ? __ldg(row + k0 + i) : 0.0f;
+    }
+}
+
+// MN-major source X(r, k) = X[k*ld + r]: lanes of a warp read consecutive r
+__device__ __forceinline__ void load32_mnmajor(const float* __restrict__ base, long long ld, int r, int k0,
+                                               int kend, float* v) {
+#pragma unroll
+    for (int i = 0; i < kBK; ++i) v[i] = (k0 + i < kend) ? __ldg(base + static_cast<long long>(k0 + i) * ld + r) : 0.0f;
+}
+
+// A(m, k0..k0+31) into v[32]
+__device__ __forceinline__ void load_a(const GemmOp& o, int m, int k0, int kend, float* v) {
+    if (m >= o.M) {
+        zero32(v);
+        return;
+    }
+    if (o.conv) {
+        const int ox = m % o.ow, t2 = m / o.ow;
+        const int oy = t2 % o.oh, n = t2 / o.oh;
+        if (o.ic % kBK == 0) {  // the 32 k values lie inside one tap: one 128-byte run
+            const int tap = k0 / o.ic, j0 = k0 - tap * o.ic;
+            const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
+            const int iy = oy * o.cstride - o.cpad + ky, ix = ox * o.cstride - o.cpad + kx;
+            if (k0 >= kend || iy < 0 || iy >= o.ih || ix < 0 || ix >= o.iw) {
+                zero32(v);
+                return;
+            }
+            const float* p = o.A + ((static_cast<long long>(n) * o.ih + iy) * o.iw + ix) * o.ic + j0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
+                v[4 * c] = q.x, v[4 * c + 1] = q.y, v[4 * c + 2] = q.z, v[4 * c + 3] = q.w;
+            }
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < kBK; ++i) {
+            const int k = k0 + i;
+            float x = 0.0f;
+            if (k < kend) {
+                const int tap = k / o.ic, j = k - tap * o.ic;
+                const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
+                const int iy = oy * o.cstride - o.cpad + ky, ix = ox * o.cstride - o.cpad + kx;
+                if (iy >= 0 && iy < o.ih && ix >= 0 && ix < o.iw)
+                    x = __ldg(o.A + ((static_cast<long long>(n) * o.ih + iy) * o.iw + ix) * o.ic + j);
+            }
+            v[i] = x;
+        }
+        return;
+    }
+    if (o.a_kmajor)
+        load32_kmajor(o.A + static_cast<long long>(m) * o.lda, k0, kend, (o.lda % 4) == 0, v);
+    else
+        load32_mnmajor(o.A, o.lda, m, k0, kend, v);
+}
+
+__device__ __forceinline__ void load_b(const GemmOp& o, int n, int k0, int kend, float* v) {
+    if (n >= o.N) {
+        zero32(v);
+        return;
+    }
+    if (o.b_kmajor)
+        load32_kmajor(o.B + static_cast<long long>(n) * o.ldb, k0, kend, (o.ldb % 4) == 0, v);
+    else
+        load32_mnmajor(o.B, o.ldb, n, k0, kend, v);
+}
+
+template <class Op>
+__device__ __forceinline__ const Op& op_of_u(const Op* ops, int nd, int& local) {
+    int t = 0;
+    while (t + 1 < nd && static_cast<int>(blockIdx.x) >= ops[t + 1].cta_begin) ++t;
+    local = static_cast<int>(blockIdx.x) - ops[t].cta_begin;
+    return ops[t];
+}
+
+}  // namespace
+
+// BN: N tile of this launch (16..128, multiple of 16), compile time so the
+// per-row fp32 sum stays in registers.
+template <int BN>
+__global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restrict__ ops, int nd) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bars[kStages];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ float red[4][32];
+    int local;
+    const GemmOp& o = op_of_u(ops, nd, local);
+    if (o.failed != nullptr && *o.failed != 0) return;
+
+    // 1024-byte aligned carve-up: [stage][A_hi | A_lo | B_hi | B_lo]
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int a_bytes = kBM * kRowBytes;
+    constexpr int b_bytes = BN * kRowBytes;
+    constexpr int stage_bytes = 2 * a_bytes + 2 * b_bytes;
+    constexpr int tmem_cols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : 256;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tiles_mn = o.tiles_m * o.tiles_n;
+    const int split = local / tiles_mn;
+    const int rem = local - split * tiles_mn;
+    const int tm = rem / o.tiles_n, tn = rem - tm * o.tiles_n;
+    const int m0 = tm * kBM, n0 = tn * BN;
+    const int kbeg = split * o.kchunk;
+    const int kend = min(o.K, kbeg + o.kchunk);
+    const int nchunks = max(1, (kend - kbeg + kBK - 1) / kBK);
+    const int terms = o.tf32x3;  // 1: tf32, 3: hi*hi+hi*lo+lo*hi, 4: + lo*lo
+    const bool split3 = terms > 1;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    const uint32_t idesc = instr_desc(BN);
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+    auto drain = [&](int kc) {  // chunk kc's slot into acc, in chunk order
+        mbar_wait(&bars[kc & 1], (kc >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) tmem_add16(tmem + lane_off + (kc & 1) * BN + c0, acc + c0);
+        tc_fence_before();
+    };
+
+    float v[kBK];
+    for (int kc = 0; kc < nchunks; ++kc) {
+        const int s = kc & 1;
+        const int k0 = kbeg + kc * kBK;
+        uint8_t* st = smem + s * stage_bytes;
+        uint8_t *a_hi = st, *a_lo = st + a_bytes, *b_hi = st + 2 * a_bytes, *b_lo = st + 2 * a_bytes + b_bytes;
+        if (kc >= kStages) drain(kc - kStages);  // frees smem stage s and TMEM slot s
+        load_a(o, m0 + tid, k0, kend, v);
+        put_row(a_hi, a_lo, tid, v, split3);
+#pragma unroll
+        for (int r = tid; r < BN; r += 128) {
+            load_b(o, n0 + r, k0, kend, v);
+            put_row(b_hi, b_lo, r, v, split3);
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (warp == 0) {
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+                const uint32_t d = tmem + s * BN;
+#pragma unroll
+                for (int kk = 0; kk < kBK / 8; ++kk) {
+                    const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+                    if (split3) {  // small terms first
+                        if (terms > 3) mma_tf32(d, smem_desc(al + off), smem_desc(bl + off), idesc, kk > 0 ? 1u : 0u);
+                        mma_tf32(d, smem_desc(ah + off), smem_desc(bl + off), idesc, (kk > 0 || terms > 3) ? 1u : 0u);
+                        mma_tf32(d, smem_desc(al + off), smem_desc(bh + off), idesc, 1u);
+                        mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), idesc, 1u);
+                    } else {
+                        mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), idesc, kk > 0 ? 1u : 0u);
+                    }
+                }
+                mma_commit(&bars[s]);
+            }
+            __syncwarp();
+        }
+    }
+    for (int kc = max(0, nchunks - kStages); kc < nchunks; ++kc) drain(kc);
+
+    // ------------------------------------------------------------ epilogue
+    const int row = m0 + warp * 32 + lane;
+    const bool row_ok = row < o.M;
+    float* C = o.C + (o.epi == 2 ? static_cast<long long>(split) * o.M * o.ldc : 0);
+    const bool vec_st = (o.ldc % 4) == 0;
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        float* val = acc + c0;
+        const int ncol = n0 + c0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int n = ncol + j;
+            float x = val[j];
+            if (row_ok && n < o.N) {
+                if (o.scale) x = bn_infer_apply(x, o.scale[n], o.shift[n]);
+                if (o.skip) x = add(x, o.skip[static_cast<long long>(row) * o.ldc + n]);
+                if (o.relu) x = relu(x);
+            } else {
+                x = 0.0f;
+            }
+            val[j] = x;
+        }
+        if (row_ok) {
+            float* dst = C + static_cast<long long>(row) * o.ldc + ncol;
+            if (vec_st && ncol + 16 <= o.N) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    reinterpret_cast<float4*>(dst)[q] = make_float4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (ncol + j < o.N) dst[j] = val[j];
+            }
+        }
+        if (o.epi == 1) {  // per-(m-tile, column) sum and sum of squares, fixed-order trees
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                float s = val[j], q = val[j] * val[j];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    s += __shfl_xor_sync(0xffffffffu, s, off);
+                    q += __shfl_xor_sync(0xffffffffu, q, off);
+                }
+                if (lane == 0) {
+                    red[warp][j] = s;
+                    red[warp][16 + j] = q;
+                }
+            }
+            __syncthreads();
+            if (tid < 16 && ncol + tid < o.N) {
+                const float s = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
+                const float q = (red[0][16 + tid] + red[1][16 + tid]) + (red[2][16 + tid] + red[3][16 + tid]);
+                o.part0[static_cast<long long>(tm) * o.N + ncol + tid] = s;
+                o.part1[static_cast<long long>(tm) * o.N + ncol + tid] = q;
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+}
+
+// ------------------------------------------------------------------- host
+namespace {
+int bn_for(int n) {
+    if (n <= 16) return 16;
+    if (n <= 32) return 32;
+    if (n <= 64) return 64;
+    return 128;
+}
+}  // namespace
+
+void gemm_finalize(GemmOp& o) {
+    o.bn = bn_for(o.N);
+    o.tiles_m = ceil_div(o.M, kBM);
+    o.tiles_n = ceil_div(o.N, o.bn);
+    if (o.ksplit < 1) o.ksplit = 1;
+    if (o.ksplit == 1) {
+        o.kchunk = ((o.K + kBK - 1) / kBK) * kBK;
+    } else {
+        o.kchunk = ((ceil_div(o.K, o.ksplit) + kBK - 1) / kBK) * kBK;
+        o.ksplit = ceil_div(o.K, o.kchunk);
+    }
+    if (o.tf32x3 == 0) {  // parity mode: split fp32 into tf32 hi+lo
+        static const int terms = [] {
+            const char* e = std::getenv("PBKD_TF32_TERMS");
+            return e ? std::atoi(e) : 3;
+        }();
+        o.tf32x3 = terms;
+    }
+}
+
+int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
+
+template <int BN>
+static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
+    constexpr size_t smem = 1024 + kStages * (2 * kBM * kRowBytes + 2 * BN * kRowBytes);
+    static bool attr = false;
+    if (!attr) {
+        PBKD_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        attr = true;
+    }
+    umma_gemm_kernel<BN><<<ctas, 128, smem, st>>>(d, nd);
+    PBKD_LAUNCH_CHECK();
+}
+
+// All ops of one launch run with the widest op's N tile (narrower ops pad
+// their B rows with zeros), because BN is a compile-time tile.
+void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int bn_max, cudaStream_t st) {
+    switch (bn_for(bn_max)) {
+        case 16: launch_bn_t<16>(d, nd, ctas, st); break;
+        case 32: launch_bn_t<32>(d, nd, ctas, st); break;
+        case 64: launch_bn_t<64>(d, nd, ctas, st); break;
+        default: launch_bn_t<128>(d, nd, ctas, st); break;
+    }
+}
+
+void launch_gemm(const GemmOp* d, int nd, int ctas, cudaStream_t st) { launch_gemm_bn(d, nd, ctas, 128, st); }
+
+}  // namespace pbkd_gpu
