@@ -85,22 +85,27 @@ public:
             launch(reinterpret_cast<const Op*>(slab + off), nd, total, st);
         });
     }
-    // tcgen05 GEMMs: smem carve-up sized for the widest N tile of the launch
-    void gemm(std::vector<GemmOp> ops) {
-        if (ops.empty()) return;
-        int total = 0, bn_max = 16;
-        for (GemmOp& o : ops) {
-            o.cta_begin = total;
-            total += std::max(1, ctas_gemm(o));
-            bn_max = std::max(bn_max, o.bn);
+    // tcgen05 GEMMs: one launch per N-tile class (the tile is a template
+    // parameter), all tasks of that class grouped in it
+    void gemm(std::vector<GemmOp> all) {
+        for (int cls : {32, 64, 128}) {
+            std::vector<GemmOp> ops;
+            for (const GemmOp& o : all)
+                if (gemm_bn_class(o) == cls) ops.push_back(o);
+            if (ops.empty()) continue;
+            int total = 0;
+            for (GemmOp& o : ops) {
+                o.cta_begin = total;
+                total += std::max(1, ctas_gemm(o));
+            }
+            const size_t off = (host_.size() + 63) & ~size_t(63);
+            host_.resize(off + ops.size() * sizeof(GemmOp));
+            std::memcpy(host_.data() + off, ops.data(), ops.size() * sizeof(GemmOp));
+            const int nd = static_cast<int>(ops.size());
+            steps_.push_back([off, nd, total, cls](cudaStream_t st, const uint8_t* slab) {
+                launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, cls, st);
+            });
         }
-        const size_t off = (host_.size() + 63) & ~size_t(63);
-        host_.resize(off + ops.size() * sizeof(GemmOp));
-        std::memcpy(host_.data() + off, ops.data(), ops.size() * sizeof(GemmOp));
-        const int nd = static_cast<int>(ops.size());
-        steps_.push_back([off, nd, total, bn_max](cudaStream_t st, const uint8_t* slab) {
-            launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, bn_max, st);
-        });
     }
     void raw(std::function<void(cudaStream_t)> f) {
         steps_.push_back([f](cudaStream_t st, const uint8_t*) { f(st); });

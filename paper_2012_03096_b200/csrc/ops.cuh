@@ -107,6 +107,7 @@ struct GemmOp {
 
 // Fills tiling fields (bn, tiles, kchunk/ksplit) of a GemmOp (umma.cu).
 void gemm_finalize(GemmOp& o);
+int gemm_bn_class(const GemmOp& o);  // N tile class of the launch that runs o
 
 // Batch-norm statistics from the GEMM column partials (ops.hpp:273-299):
 // mean, var = E[x^2]-mean^2 clamped, inv_std, moving-stat update.

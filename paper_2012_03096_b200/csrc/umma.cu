@@ -14,15 +14,18 @@
 //    registers in chunk order.  Measured on B200, letting one TMEM accumulator
 //    absorb all K/8 MMA steps loses ~K/8 * 2^-23 (biased rounding inside the
 //    MMA); the drain keeps every accumulator short and the cross-chunk sum
-//    round-to-nearest.
+//    round-to-nearest (tools/prec_probe.py: K=512 GEMM error 1.3e-5 vs 1.9e-5
+//    for numpy fp32).
 //
-// Operands are staged global -> registers -> shared by all 128 threads (one
-// row of the 128-row tile per thread) into the canonical K-major SWIZZLE_128B
-// layout: row r at (r/8)*1024 + (r%8)*128 bytes, its 16-byte chunk c at
-// ((c ^ r%8) * 16).  Register staging is what lets one kernel gather an
-// implicit im2col (teacher conv), transpose MN-major sources (dgrad/wgrad)
-// and split hi/lo with no host-side relayout.  Two smem stages / TMEM slots:
-// threads refill stage s^1 and drain slot s^1 while the tensor core runs on s.
+// 256 threads: two threads per tile row stage 16 of the chunk's 32 K values
+// each (global -> registers -> shared, into the canonical K-major
+// SWIZZLE_128B layout: row r at (r/8)*1024 + (r%8)*128 bytes, 16-byte chunk c
+// at ((c ^ r%8) * 16)); the 8 warps split the TMEM drain and the epilogue by
+// column halves (a warp may only touch TMEM lanes 32*(warp%4)..+31).  Register
+// staging lets one kernel gather an implicit im2col (teacher conv), transpose
+// MN-major sources (dgrad/wgrad) and split hi/lo, with no host relayout.
+// Two smem stages / TMEM slots: threads refill and drain slot s^1 while the
+// tensor core works on slot s.
 #include <algorithm>
 #include <cstdlib>
 
@@ -34,8 +37,10 @@ namespace {
 
 constexpr int kBM = 128;  // MMA M (TMEM lanes)
 constexpr int kBK = 32;   // fp32 K per stage = one 128-byte swizzle row
+constexpr int kKH = 16;   // K values staged per thread (half a row)
 constexpr int kRowBytes = 128;
 constexpr int kStages = 2;
+constexpr int kThreadsG = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -124,77 +129,77 @@ __device__ __forceinline__ void tmem_add16(uint32_t addr, float* acc) {
     for (int i = 0; i < 16; ++i) acc[i] = __fadd_rn(acc[i], __uint_as_float(r[i]));
 }
 
-// Store one 32-float K slice of a row (hi and lo parts) into a swizzled tile.
-__device__ __forceinline__ void put_row(uint8_t* hi, uint8_t* lo, int r, const float* v, bool split) {
+// Store 16 K values (chunks h*4..h*4+3 of row r) as tf32 hi / lo.
+__device__ __forceinline__ void put_half(uint8_t* hi, uint8_t* lo, int r, int h, const float* v, bool split) {
     const int base = (r >> 3) * 1024 + (r & 7) * kRowBytes;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        uint32_t h[4], l[4];
+    for (int cc = 0; cc < 4; ++cc) {
+        const int c = h * 4 + cc;
+        uint32_t hv[4], lv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const float x = v[c * 4 + q];
-            h[q] = to_tf32(x);
-            l[q] = split ? to_tf32(__fsub_rn(x, __uint_as_float(h[q]))) : 0u;
+            const float x = v[cc * 4 + q];
+            hv[q] = to_tf32(x);
+            lv[q] = split ? to_tf32(__fsub_rn(x, __uint_as_float(hv[q]))) : 0u;
         }
         const int off = base + ((c ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
-        if (split) *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+        *reinterpret_cast<uint4*>(hi + off) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        if (split) *reinterpret_cast<uint4*>(lo + off) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
     }
 }
 
-__device__ __forceinline__ void zero32(float* v) {
+__device__ __forceinline__ void zero16(float* v) {
 #pragma unroll
-    for (int i = 0; i < kBK; ++i) v[i] = 0.0f;
+    for (int i = 0; i < kKH; ++i) v[i] = 0.0f;
 }
 
-__device__ __forceinline__ void load32_kmajor(const float* __restrict__ row, int k0, int kend, bool vec,
-                                              float* v) {
-    if (vec && k0 + kBK <= kend) {
+__device__ __forceinline__ void load16_kmajor(const float* __restrict__ row, int k0, int kend, bool vec, float* v) {
+    if (vec && k0 + kKH <= kend) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 4; ++c) {
             const float4 q = __ldg(reinterpret_cast<const float4*>(row + k0) + c);
             v[4 * c] = q.x, v[4 * c + 1] = q.y, v[4 * c + 2] = q.z, v[4 * c + 3] = q.w;
         }
     } else {
 #pragma unroll
-        for (int i = 0; i < kBK; ++i) v[i] = (k0 + i < kend) ? __ldg(row + k0 + i) : 0.0f;
+        for (int i = 0; i < kKH; ++i) v[i] = (k0 + i < kend) ? __ldg(row + k0 + i) : 0.0f;
     }
 }
 
 // MN-major source X(r, k) = X[k*ld + r]: lanes of a warp read consecutive r
-__device__ __forceinline__ void load32_mnmajor(const float* __restrict__ base, long long ld, int r, int k0,
+__device__ __forceinline__ void load16_mnmajor(const float* __restrict__ base, long long ld, int r, int k0,
                                                int kend, float* v) {
 #pragma unroll
-    for (int i = 0; i < kBK; ++i) v[i] = (k0 + i < kend) ? __ldg(base + static_cast<long long>(k0 + i) * ld + r) : 0.0f;
+    for (int i = 0; i < kKH; ++i) v[i] = (k0 + i < kend) ? __ldg(base + static_cast<long long>(k0 + i) * ld + r) : 0.0f;
 }
 
-// A(m, k0..k0+31) into v[32]
+// A(m, k0..k0+15) into v[16]
 __device__ __forceinline__ void load_a(const GemmOp& o, int m, int k0, int kend, float* v) {
     if (m >= o.M) {
-        zero32(v);
+        zero16(v);
         return;
     }
     if (o.conv) {
         const int ox = m % o.ow, t2 = m / o.ow;
         const int oy = t2 % o.oh, n = t2 / o.oh;
-        if (o.ic % kBK == 0) {  // the 32 k values lie inside one tap: one 128-byte run
+        if (o.ic % kKH == 0) {  // the 16 k values lie inside one tap: one 64-byte run
             const int tap = k0 / o.ic, j0 = k0 - tap * o.ic;
             const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
             const int iy = oy * o.cstride - o.cpad + ky, ix = ox * o.cstride - o.cpad + kx;
             if (k0 >= kend || iy < 0 || iy >= o.ih || ix < 0 || ix >= o.iw) {
-                zero32(v);
+                zero16(v);
                 return;
             }
             const float* p = o.A + ((static_cast<long long>(n) * o.ih + iy) * o.iw + ix) * o.ic + j0;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
+            for (int c = 0; c < 4; ++c) {
                 const float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
                 v[4 * c] = q.x, v[4 * c + 1] = q.y, v[4 * c + 2] = q.z, v[4 * c + 3] = q.w;
             }
             return;
         }
 #pragma unroll
-        for (int i = 0; i < kBK; ++i) {
+        for (int i = 0; i < kKH; ++i) {
             const int k = k0 + i;
             float x = 0.0f;
             if (k < kend) {
@@ -209,20 +214,20 @@ __device__ __forceinline__ void load_a(const GemmOp& o, int m, int k0, int kend,
         return;
     }
     if (o.a_kmajor)
-        load32_kmajor(o.A + static_cast<long long>(m) * o.lda, k0, kend, (o.lda % 4) == 0, v);
+        load16_kmajor(o.A + static_cast<long long>(m) * o.lda, k0, kend, (o.lda % 4) == 0, v);
     else
-        load32_mnmajor(o.A, o.lda, m, k0, kend, v);
+        load16_mnmajor(o.A, o.lda, m, k0, kend, v);
 }
 
 __device__ __forceinline__ void load_b(const GemmOp& o, int n, int k0, int kend, float* v) {
     if (n >= o.N) {
-        zero32(v);
+        zero16(v);
         return;
     }
     if (o.b_kmajor)
-        load32_kmajor(o.B + static_cast<long long>(n) * o.ldb, k0, kend, (o.ldb % 4) == 0, v);
+        load16_kmajor(o.B + static_cast<long long>(n) * o.ldb, k0, kend, (o.ldb % 4) == 0, v);
     else
-        load32_mnmajor(o.B, o.ldb, n, k0, kend, v);
+        load16_mnmajor(o.B, o.ldb, n, k0, kend, v);
 }
 
 template <class Op>
@@ -236,13 +241,13 @@ __device__ __forceinline__ const Op& op_of_u(const Op* ops, int nd, int& local) 
 }  // namespace
 
 // BN: N tile of this launch (16..128, multiple of 16), compile time so the
-// per-row fp32 sum stays in registers.
+// per-row fp32 sums stay in registers.
 template <int BN>
-__global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restrict__ ops, int nd) {
+__global__ void __launch_bounds__(kThreadsG, 1) umma_gemm_kernel(const GemmOp* __restrict__ ops, int nd) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bars[kStages];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ float red[4][32];
+    __shared__ float red[8][32];
     int local;
     const GemmOp& o = op_of_u(ops, nd, local);
     if (o.failed != nullptr && *o.failed != 0) return;
@@ -253,8 +258,11 @@ __global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restr
     constexpr int b_bytes = BN * kRowBytes;
     constexpr int stage_bytes = 2 * a_bytes + 2 * b_bytes;
     constexpr int tmem_cols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : 256;
+    constexpr int HB = BN / 2;  // columns per warp half in drain / epilogue (>= 8)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int row_t = tid & (kBM - 1), half = tid >> 7;  // staging: row, K half
+    const int wq = warp & 3, wh = warp >> 2;               // TMEM lane quarter, column half
     const int tiles_mn = o.tiles_m * o.tiles_n;
     const int split = local / tiles_mn;
     const int rem = local - split * tiles_mn;
@@ -280,32 +288,33 @@ __global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restr
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
     const uint32_t idesc = instr_desc(BN);
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
 
-    float acc[BN];
+    float acc[HB];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+    for (int j = 0; j < HB; ++j) acc[j] = 0.0f;
     auto drain = [&](int kc) {  // chunk kc's slot into acc, in chunk order
         mbar_wait(&bars[kc & 1], (kc >> 1) & 1);
         tc_fence_after();
+        const uint32_t base = tmem + lane_off + (kc & 1) * BN + wh * HB;
+        static_assert(HB % 16 == 0, "BN >= 32");
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 16) tmem_add16(tmem + lane_off + (kc & 1) * BN + c0, acc + c0);
+        for (int c0 = 0; c0 < HB; c0 += 16) tmem_add16(base + c0, acc + c0);
         tc_fence_before();
     };
 
-    float v[kBK];
+    float v[kKH];
     for (int kc = 0; kc < nchunks; ++kc) {
         const int s = kc & 1;
-        const int k0 = kbeg + kc * kBK;
+        const int k0 = kbeg + kc * kBK + half * kKH;
         uint8_t* st = smem + s * stage_bytes;
         uint8_t *a_hi = st, *a_lo = st + a_bytes, *b_hi = st + 2 * a_bytes, *b_lo = st + 2 * a_bytes + b_bytes;
         if (kc >= kStages) drain(kc - kStages);  // frees smem stage s and TMEM slot s
-        load_a(o, m0 + tid, k0, kend, v);
-        put_row(a_hi, a_lo, tid, v, split3);
-#pragma unroll
-        for (int r = tid; r < BN; r += 128) {
-            load_b(o, n0 + r, k0, kend, v);
-            put_row(b_hi, b_lo, r, v, split3);
+        load_a(o, m0 + row_t, k0, kend, v);
+        put_half(a_hi, a_lo, row_t, half, v, split3);
+        if (row_t < BN) {
+            load_b(o, n0 + row_t, k0, kend, v);
+            put_half(b_hi, b_lo, row_t, half, v, split3);
         }
         fence_async_smem();
         __syncthreads();
@@ -334,16 +343,18 @@ __global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restr
     for (int kc = max(0, nchunks - kStages); kc < nchunks; ++kc) drain(kc);
 
     // ------------------------------------------------------------ epilogue
-    const int row = m0 + warp * 32 + lane;
+    // thread = (row wq*32+lane, columns wh*HB .. +HB)
+    const int row = m0 + wq * 32 + lane;
     const bool row_ok = row < o.M;
     float* C = o.C + (o.epi == 2 ? static_cast<long long>(split) * o.M * o.ldc : 0);
     const bool vec_st = (o.ldc % 4) == 0;
+    constexpr int SL = HB >= 16 ? 16 : HB;
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = 0; c0 < HB; c0 += SL) {
         float* val = acc + c0;
-        const int ncol = n0 + c0;
+        const int ncol = n0 + wh * HB + c0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < SL; ++j) {
             const int n = ncol + j;
             float x = val[j];
             if (row_ok && n < o.N) {
@@ -357,19 +368,19 @@ __global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restr
         }
         if (row_ok) {
             float* dst = C + static_cast<long long>(row) * o.ldc + ncol;
-            if (vec_st && ncol + 16 <= o.N) {
+            if (vec_st && ncol + SL <= o.N) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < SL / 4; ++q)
                     reinterpret_cast<float4*>(dst)[q] = make_float4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
             } else {
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
+                for (int j = 0; j < SL; ++j)
                     if (ncol + j < o.N) dst[j] = val[j];
             }
         }
-        if (o.epi == 1) {  // per-(m-tile, column) sum and sum of squares, fixed-order trees
+        if (o.epi == 1) {  // per-(m-tile, column) sum / sum of squares, fixed-order trees
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
+            for (int j = 0; j < SL; ++j) {
                 float s = val[j], q = val[j] * val[j];
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) {
@@ -382,11 +393,16 @@ __global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restr
                 }
             }
             __syncthreads();
-            if (tid < 16 && ncol + tid < o.N) {
-                const float s = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
-                const float q = (red[0][16 + tid] + red[1][16 + tid]) + (red[2][16 + tid] + red[3][16 + tid]);
-                o.part0[static_cast<long long>(tm) * o.N + ncol + tid] = s;
-                o.part1[static_cast<long long>(tm) * o.N + ncol + tid] = q;
+            if (tid < 2 * SL) {  // column (half h, j): 4 row quarters in order
+                const int h = tid / SL, j = tid % SL;
+                const int col = n0 + h * HB + c0 + j;
+                if (col < o.N) {
+                    const float s = (red[4 * h][j] + red[4 * h + 1][j]) + (red[4 * h + 2][j] + red[4 * h + 3][j]);
+                    const float q = (red[4 * h][16 + j] + red[4 * h + 1][16 + j]) +
+                                    (red[4 * h + 2][16 + j] + red[4 * h + 3][16 + j]);
+                    o.part0[static_cast<long long>(tm) * o.N + col] = s;
+                    o.part1[static_cast<long long>(tm) * o.N + col] = q;
+                }
             }
             __syncthreads();
         }
@@ -398,7 +414,6 @@ __global__ void __launch_bounds__(128, 1) umma_gemm_kernel(const GemmOp* __restr
 // ------------------------------------------------------------------- host
 namespace {
 int bn_for(int n) {
-    if (n <= 16) return 16;
     if (n <= 32) return 32;
     if (n <= 64) return 64;
     return 128;
@@ -426,6 +441,7 @@ void gemm_finalize(GemmOp& o) {
 }
 
 int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
+int gemm_bn_class(const GemmOp& o) { return bn_for(o.N); }
 
 template <int BN>
 static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
@@ -436,15 +452,14 @@ static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
                                        static_cast<int>(smem)));
         attr = true;
     }
-    umma_gemm_kernel<BN><<<ctas, 128, smem, st>>>(d, nd);
+    umma_gemm_kernel<BN><<<ctas, kThreadsG, smem, st>>>(d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
-// All ops of one launch run with the widest op's N tile (narrower ops pad
-// their B rows with zeros), because BN is a compile-time tile.
+// All ops of one launch share the N tile (the caller groups ops by
+// gemm_bn_class; narrower ops would pad their B rows with zeros).
 void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int bn_max, cudaStream_t st) {
     switch (bn_for(bn_max)) {
-        case 16: launch_bn_t<16>(d, nd, ctas, st); break;
         case 32: launch_bn_t<32>(d, nd, ctas, st); break;
         case 64: launch_bn_t<64>(d, nd, ctas, st); break;
         default: launch_bn_t<128>(d, nd, ctas, st); break;
