@@ -107,6 +107,34 @@ def cpu_reference_step(O, spec, tw, images, labels, tr, ev, blocks, batch, seed_
     return time.perf_counter() - t0
 
 
+def calibrate(ctx, P, blocks, tr, ev, B):
+    """Per-block student epoch time (each block alone, teacher part subtracted)
+    and the all-block teacher forward time per epoch, in ms (1 GPU)."""
+    s_ms = {}
+    for k in blocks:
+        t = [P.make_task(k, epochs=2, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B)]
+        r = ctx.run(t, tr, ev, flags=P.RUN_STEP_ONLY, timed_from_epoch=2)
+        s_ms[k] = max(1e-3, r["timed_ms"] - r["teacher_ms"])
+    t = [P.make_task(k, epochs=2, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B) for k in blocks]
+    r = ctx.run(t, tr, ev, flags=P.RUN_STEP_ONLY, timed_from_epoch=2,
+                global_blocks=[(k, 0) for k in blocks])
+    return s_ms, r["teacher_ms"]
+
+
+def water_fill(load, teacher_ms):
+    """Teacher shares x_r (sum 1) equalising load_r + x_r * teacher_ms."""
+    lo, hi = min(load), max(load) + teacher_ms
+    for _ in range(100):
+        mid = 0.5 * (lo + hi)
+        if sum(max(0.0, (mid - l) / teacher_ms) for l in load) > 1.0:
+            hi = mid
+        else:
+            lo = mid
+    x = [max(0.0, (hi - l) / teacher_ms) for l in load]
+    s = sum(x)
+    return [v / s for v in x]
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle/_ref built from the
     reference sources; the restatement if that build is absent)."""
@@ -157,25 +185,47 @@ def main():
     import paper_2012_03096_b200 as P
     dev = local
     spec, classes, images, labels, tr, ev, blocks = workload(args.config, args.dataset_size, P)
-    # block -> GPU: WFD over the reference's MAC-proxy weights (pipeline.cpp:65-85)
-    weights = P.mac_proxy_weights(spec, blocks)
-    plan, _ = P.wfd_bin_pack(blocks, weights, world)
-    mine = sorted(plan[rank])
     B, K, W = args.batch, args.steps, args.warmup
-    tasks = [P.make_task(k, epochs=W + K, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B,
-                         lr=0.05, momentum=0.9) for k in mine]
     ctx = P.Context(dev)
     teacher_seed = P.mix_seed(42, 0x7E11)
     ctx.teacher_init(spec, teacher_seed)
     ctx.dataset_load(images, labels, classes)
     n_train = len(tr)
+    share = None
+    if world == 1:
+        plan = [blocks]
+        weights_src = "single GPU"
+    else:
+        # NCCL communicator for the teacher-activation exchange
+        nid = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        ctx.set_comm(nid[0], rank, world)
+        # block -> GPU: WFD (scheduler.cpp:57-81) over MEASURED per-block student
+        # epoch times, teacher shards sized to fill the imbalance (rank 0
+        # calibrates, everyone gets the same numbers)
+        cal = [calibrate(ctx, P, blocks, tr, ev, B) if rank == 0 else None]
+        dist.broadcast_object_list(cal, src=0)
+        s_ms, t_ms_all = cal[0]
+        plan, _ = P.wfd_bin_pack(blocks, [s_ms[k] for k in blocks], world)
+        load = [sum(s_ms[k] for k in q) for q in plan]
+        share = water_fill(load, t_ms_all)
+        weights_src = "measured student epoch ms " + json.dumps({k: round(v, 3) for k, v in s_ms.items()}) + \
+            f"; teacher {t_ms_all:.3f} ms/epoch; teacher shares {[round(x, 4) for x in share]}"
+    mine = sorted(plan[rank])
+    owner = {k: r for r, q in enumerate(plan) for k in q}
+    tasks = [P.make_task(k, epochs=W + K, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B,
+                         lr=0.05, momentum=0.9) for k in mine]
 
     # ---------------- value: inputs resident in HBM, K timed epochs ----------
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clk = Clocks(dev)
-    res = ctx.run(tasks, tr, ev, flags=P.RUN_STEP_ONLY, timed_from_epoch=W + 1)
+    if world == 1:
+        res = ctx.run(tasks, tr, ev, flags=P.RUN_STEP_ONLY, timed_from_epoch=W + 1)
+    else:
+        res = ctx.run(tasks, tr, ev, flags=P.RUN_STEP_ONLY, timed_from_epoch=W + 1,
+                      global_blocks=[(k, owner[k]) for k in blocks], share=share)
     torch.cuda.synchronize()
     clocks = clk.stop()
     if dist:
@@ -268,7 +318,11 @@ def main():
                                    f"TwoLayer students, batch {B}, dataset {args.dataset_size} "
                                    f"({n_train} train), 1 step = 1 epoch (teacher forward over the "
                                    f"train split + {-(-n_train // B)} optimizer steps per block)",
-                       "plan": plan, "parallelism": f"blocks over {world} GPU(s) by WFD (MAC proxy)",
+                       "plan": plan,
+                       "parallelism": f"blocks over {world} GPU(s) by WFD; teacher forward sample-sharded "
+                                      "with NCCL all-to-all-v of boundary activations" if world > 1 else
+                                      "1 GPU: all blocks grouped",
+                       "weights": weights_src, "teacher_ms_per_epoch": res["teacher_ms"] / max(1, K),
                        "l2": "inputs larger than L2: each epoch streams every block's boundary "
                              "activations (~2.2 MB/sample for VGG-16, GBs per epoch) through HBM"},
             "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -152,6 +152,26 @@ int pbkd_run_timing(const pbkd_results* r, double* timed_ms, int* timed_epochs,
 int pbkd_bench_kernel(pbkd_ctx* ctx, int which, int batch, int iters, double* ms, double* bytes,
                       double* flops);
 
+/* ---- multi-GPU: sample-sharded teacher + NCCL exchange ------------------ */
+/* Rank 0 creates the 128-byte NCCL id; the launcher broadcasts it; every rank
+ * joins.  pbkd_run_sharded then trains the given (local) tasks while this
+ * rank runs the teacher forward on its shard of the training split for every
+ * block listed in g_blocks (owner g_owner) and exchanges boundary rows with
+ * grouped ncclSend/ncclRecv.  virtual_shards > 1 on one GPU runs the same
+ * pack/scatter path with local shards; share weights the teacher shards. */
+int pbkd_nccl_unique_id(char* out128);
+int pbkd_ctx_set_comm(pbkd_ctx* ctx, const char* id128, int rank, int world);
+int pbkd_run_sharded(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* train_idx,
+                     int n_train, const int* eval_idx, int n_eval, int flags, int timed_from_epoch,
+                     const int* g_blocks, const int* g_owner, int n_global, int virtual_shards,
+                     const double* share, int n_share, pbkd_results** out);
+/* Host-side exchange layout (what rank src sends rank dst), identical on all
+ * ranks; exposed for the multi-process plan tests. */
+int pbkd_exchange_plan(const int* blocks, const int* owners, int nb, const long long* in_row,
+                       const long long* out_row, int world, int n_train, const double* share,
+                       int src, int dst, size_t* count, size_t* off_in, size_t* off_tgt,
+                       int* shard_begin);
+
 /* ---- inference ----------------------------------------------------------- */
 int pbkd_prefix_infer(pbkd_ctx* ctx, const float* x, int n, int k, int inclusive, float* out,
                       size_t cap, int* out_shape);

@@ -98,6 +98,12 @@ def lib() -> C.CDLL:
                                          C.c_int, C.POINTER(vp)]),
             "pbkd_run_timing": (C.c_int, [vp, dp, ip, C.POINTER(C.c_longlong), vp, C.c_int, ip]),
             "pbkd_bench_kernel": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dp, dp, dp]),
+            "pbkd_nccl_unique_id": (C.c_int, [vp]),
+            "pbkd_ctx_set_comm": (C.c_int, [vp, vp, C.c_int, C.c_int]),
+            "pbkd_run_sharded": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int,
+                                           vp, vp, C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),
+            "pbkd_exchange_plan": (C.c_int, [vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, C.c_int,
+                                             C.c_int, C.POINTER(C.c_size_t), vp, vp, vp]),
             "pbkd_prefix_infer": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_size_t, vp]),
             "pbkd_candidate_infer": (C.c_int, [vp] + [C.c_int] * 4 + [vp, vp] + [C.c_int] * 3 +
                                      [vp, C.c_size_t]),
@@ -216,6 +222,27 @@ def mac_proxy_weights(spec, blocks):
     return out
 
 
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().pbkd_nccl_unique_id(buf))
+    return buf.raw
+
+
+def exchange_plan(blocks, owners, in_row, out_row, world, n_train, src, dst, share=None):
+    """What rank `src` sends rank `dst` (count, per-block in/tgt offsets, shard bounds)."""
+    nb = len(blocks)
+    b, o = _i32(blocks), _i32(owners)
+    ir, orow = np.ascontiguousarray(in_row, np.int64), np.ascontiguousarray(out_row, np.int64)
+    sh = np.ascontiguousarray(share, np.float64) if share is not None else None
+    cnt = C.c_size_t()
+    oi, ot = np.zeros(nb, np.uint64), np.zeros(nb, np.uint64)
+    sbd = np.zeros(world + 1, np.int32)
+    check(lib().pbkd_exchange_plan(_ptr(b), _ptr(o), nb, _ptr(ir), _ptr(orow), world, n_train,
+                                   _ptr(sh) if sh is not None else None, src, dst, C.byref(cnt),
+                                   _ptr(oi), _ptr(ot), _ptr(sbd)))
+    return cnt.value, oi, ot, sbd
+
+
 def spec_num_floats(spec):
     n = C.c_size_t()
     check(lib().pbkd_spec_num_floats(spec.encode(), C.byref(n)))
@@ -270,12 +297,25 @@ class Context:
         check(lib().pbkd_dataset_load_device(self.h, C.c_void_p(dev_ptr), _ptr(lab), n, c, h, w,
                                              classes))
 
+    def set_comm(self, nccl_id: bytes, rank: int, world: int):
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        check(lib().pbkd_ctx_set_comm(self.h, buf, rank, world))
+
     def run(self, tasks, train_idx, eval_idx, flags=0, plan=None, workers=1, policy="round_robin",
-            timed_from_epoch=None):
+            timed_from_epoch=None, global_blocks=None, virtual_shards=1, share=None):
         arr = (Task * len(tasks))(*tasks)
         tr, ev = _i32(train_idx), _i32(eval_idx)
         out = C.c_void_p()
-        if timed_from_epoch is not None:
+        if global_blocks is not None or virtual_shards > 1:
+            gb = list(global_blocks or [])
+            b = _i32([k for k, _ in gb]) if gb else np.zeros(1, np.int32)
+            o = _i32([w for _, w in gb]) if gb else np.zeros(1, np.int32)
+            sh = np.ascontiguousarray(share, np.float64) if share is not None else None
+            check(lib().pbkd_run_sharded(self.h, arr, len(tasks), _ptr(tr), len(tr), _ptr(ev), len(ev),
+                                         flags, timed_from_epoch or 1, _ptr(b), _ptr(o), len(gb),
+                                         virtual_shards, _ptr(sh) if sh is not None else None,
+                                         len(sh) if sh is not None else 0, C.byref(out)))
+        elif timed_from_epoch is not None:
             check(lib().pbkd_run_timed(self.h, arr, len(tasks), _ptr(tr), len(tr), _ptr(ev),
                                        len(ev), flags, timed_from_epoch, C.byref(out)))
         elif plan is None:
@@ -330,8 +370,11 @@ class Context:
         check(L.pbkd_run_timing(r, C.byref(tms), C.byref(tep), C.byref(nl), None, 0, C.byref(ne)))
         ems = np.zeros(max(ne.value, 1), np.float64)
         check(L.pbkd_run_timing(r, None, None, None, _ptr(ems), ne.value, C.byref(ne)))
+        tt = np.zeros(1, np.float64)
+        check(L.pbkd_run_timing(r, None, None, None, _ptr(tt), -1, C.byref(ne)))
         return {"results": res, "trace": trace, "wall_time_s": L.pbkd_run_wall_time(r),
                 "epoch_ms": L.pbkd_run_epoch_ms(r), "timed_ms": tms.value,
+                "teacher_ms": float(tt[0]),
                 "timed_epochs": tep.value, "launches": nl.value,
                 "epoch_ms_list": ems[:ne.value].tolist()}
 

@@ -7,6 +7,7 @@
 #include <numeric>
 #include <sstream>
 
+#include "comm.hpp"
 #include "engine.hpp"
 #include "ops.cuh"
 #include "pbkd/dataset.hpp"
@@ -295,6 +296,7 @@ struct Engine::Impl {
     DevBuf images, labels, eval_labels;
     int count = 0, dc = 0, dh = 0, dw = 0, classes = 0;
     RunTiming timing;
+    std::unique_ptr<NcclComm> comm;
 
     explicit Impl(int device) : dev(device) {
         PBKD_CUDA(cudaSetDevice(dev));
@@ -973,6 +975,9 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
     std::map<std::pair<int, int>, std::vector<TaskState*>> groups;
     for (auto& s : states) groups[{s->task.batch_size, s->units}].push_back(s.get());
     timing = RunTiming{};
+    if ((opt.virtual_shards > 1 || !opt.global_blocks.empty()) && groups.size() != 1)
+        throw SpecError("sharded teacher runs need exactly one task group per rank (same batch size and "
+                        "candidate depth); every rank must own at least one block");
     for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota);
 
     // ---- read back and assemble train_block results
@@ -1191,8 +1196,60 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     }
 
     // ---- training epochs
-    std::map<std::vector<int>, std::unique_ptr<Program>> graphs;
-    cudaEvent_t e0, e1, t0, t1e;
+    struct EpochProg {
+        std::unique_ptr<Program> pre, post;  // teacher (+pack) | (scatter +) student steps
+    };
+    std::map<std::vector<int>, EpochProg> graphs;
+    // ---- sample-sharded teacher: exchange plan (identical on every rank)
+    // exchange only when the caller lists the global block ownership; without
+    // it every rank runs the teacher for its own blocks on all samples
+    const bool multi = comm && !opt.global_blocks.empty();
+    const int world = multi ? comm->world() : 1;
+    const int me = multi ? comm->rank() : 0;
+    const int vshards = std::max(1, opt.virtual_shards);
+    const bool sharded = vshards > 1 || !opt.global_blocks.empty();
+    ExchangePlan xp;
+    DevBuf sendbuf, recvbuf;
+    std::vector<size_t> send_off, send_cnt, recv_off, recv_cnt;
+    std::vector<size_t> my_bp(ts.size(), 0);  // position of each local task in xp.blocks
+    if (sharded) {
+        xp.world = world > 1 ? world : vshards;
+        std::vector<std::pair<int, int>> gb = opt.global_blocks;
+        if (gb.empty())
+            for (TaskState* s : ts) gb.push_back({s->k, me});
+        std::sort(gb.begin(), gb.end());
+        for (auto& [k, owner] : gb) {
+            const TBlockDev& b = tblocks.at(static_cast<size_t>(k) - 1);
+            xp.blocks.push_back(k);
+            xp.owner.push_back(owner);
+            xp.in_row.push_back(static_cast<long long>(b.cin) * b.hin * b.win);
+            xp.out_row.push_back(static_cast<long long>(b.cout) * b.hout * b.wout);
+        }
+        std::vector<double> share = opt.shard_share;
+        if (static_cast<int>(share.size()) != xp.world) share.assign(static_cast<size_t>(xp.world), 1.0);
+        xp.shard_begin = shard_bounds(ntrain, share);
+        for (size_t i = 0; i < ts.size(); ++i) {
+            auto f = std::find(xp.blocks.begin(), xp.blocks.end(), ts[i]->k);
+            if (f == xp.blocks.end() || xp.owner[static_cast<size_t>(f - xp.blocks.begin())] != me)
+                throw std::logic_error("sharded run: local task not owned by this rank in global_blocks");
+            my_bp[i] = static_cast<size_t>(f - xp.blocks.begin());
+        }
+        send_off.assign(static_cast<size_t>(xp.world), 0);
+        send_cnt = recv_off = recv_cnt = send_off;
+        size_t so = 0, ro = 0;
+        for (int p = 0; p < xp.world; ++p) {
+            send_off[static_cast<size_t>(p)] = so;
+            send_cnt[static_cast<size_t>(p)] = world > 1 ? xp.count(me, p) : 0;
+            so += send_cnt[static_cast<size_t>(p)];
+            recv_off[static_cast<size_t>(p)] = ro;
+            recv_cnt[static_cast<size_t>(p)] = xp.count(p, me);
+            ro += recv_cnt[static_cast<size_t>(p)];
+        }
+        sendbuf.alloc(std::max<size_t>(so, 1) * sizeof(float));
+        recvbuf.alloc(std::max<size_t>(ro, 1) * sizeof(float));
+    }
+    cudaEvent_t e0, e1, t0, t1e, eT;
+    PBKD_CUDA(cudaEventCreate(&eT));
     PBKD_CUDA(cudaEventCreate(&e0));
     PBKD_CUDA(cudaEventCreate(&e1));
     PBKD_CUDA(cudaEventCreate(&t0));
@@ -1237,15 +1294,57 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         const std::vector<int>& gkey = key;
         auto it = graphs.find(gkey);
         if (it == graphs.end()) {
-            auto P = std::make_unique<Program>();
-            std::vector<Sink> sinks;
-            for (size_t i = 0; i < ts.size(); ++i) {
-                if (key[i] == 0) continue;
-                TaskState* s = ts[i];
-                sinks.push_back({s->k - 1, s->in_stream.f(), s->pos.i(), s->in_row});
-                sinks.push_back({s->k, s->tgt_stream.f(), s->pos.i(), s->out_row});
+            EpochProg ep{std::make_unique<Program>(), std::make_unique<Program>()};
+            if (!sharded) {
+                std::vector<Sink> sinks;
+                for (size_t i = 0; i < ts.size(); ++i) {
+                    if (key[i] == 0) continue;
+                    TaskState* s = ts[i];
+                    sinks.push_back({s->k - 1, s->in_stream.f(), s->pos.i(), s->in_row});
+                    sinks.push_back({s->k, s->tgt_stream.f(), s->pos.i(), s->out_row});
+                }
+                add_teacher_pass(*ep.pre, d_train.i(), ntrain, sinks, chunk, ping.f(), pong.f(), t1.f(), sk.f());
+            } else {
+                // pack: teacher forward on a shard, rows of every distilled block
+                // written in shard order into the buffer bound for its owner
+                auto pack = [&](int src) {
+                    std::vector<Sink> sinks;
+                    for (size_t bp = 0; bp < xp.blocks.size(); ++bp) {
+                        const int dst = xp.owner[bp];
+                        float* base = world > 1 ? sendbuf.f() + send_off[static_cast<size_t>(dst)]
+                                                : recvbuf.f() + recv_off[static_cast<size_t>(src)];
+                        sinks.push_back({xp.blocks[bp] - 1, base + xp.offset_in(src, dst, bp), d_iota.i(),
+                                         static_cast<int>(xp.in_row[bp])});
+                        sinks.push_back({xp.blocks[bp], base + xp.offset_tgt(src, dst, bp), d_iota.i(),
+                                         static_cast<int>(xp.out_row[bp])});
+                    }
+                    const int sb = xp.shard_begin[static_cast<size_t>(src)];
+                    if (xp.shard_rows(src) > 0)
+                        add_teacher_pass(*ep.pre, d_train.i() + sb, xp.shard_rows(src), sinks, chunk, ping.f(),
+                                         pong.f(), t1.f(), sk.f());
+                };
+                if (world > 1)
+                    pack(me);
+                else
+                    for (int src = 0; src < xp.world; ++src) pack(src);
+                // unpack: rows from every shard into each local task's epoch order
+                std::vector<ScatterOp> sc;
+                for (int src = 0; src < xp.world; ++src) {
+                    const int rows = xp.shard_rows(src);
+                    if (rows == 0) continue;
+                    const float* base = recvbuf.f() + recv_off[static_cast<size_t>(src)];
+                    const int sb = xp.shard_begin[static_cast<size_t>(src)];
+                    for (size_t i = 0; i < ts.size(); ++i) {
+                        if (key[i] == 0) continue;
+                        TaskState* s = ts[i];
+                        sc.push_back(ScatterOp{base + xp.offset_in(src, me, my_bp[i]), s->in_stream.f(), s->pos.i() + sb,
+                                               rows, s->in_row, 0});
+                        sc.push_back(ScatterOp{base + xp.offset_tgt(src, me, my_bp[i]), s->tgt_stream.f(),
+                                               s->pos.i() + sb, rows, s->out_row, 0});
+                    }
+                }
+                ep.post->grouped<ScatterOp>(launch_scatter, sc, [](const ScatterOp&) { return kScatterCtas; });
             }
-            add_teacher_pass(*P, d_train.i(), ntrain, sinks, chunk, ping.f(), pong.f(), t1.f(), sk.f());
             for (int step = 0; step < spe; ++step) {
                 std::vector<TaskState*> act;
                 std::vector<long long> gs;
@@ -1254,28 +1353,42 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                         act.push_back(ts[i]);
                         gs.push_back(gbase[i] + step);
                     }
-                add_step(*P, act, step, 0, ntrain, gs);
+                add_step(*ep.post, act, step, 0, ntrain, gs);
             }
-            if (opt.use_graphs) P->build_graph(st);
-            it = graphs.emplace(gkey, std::move(P)).first;
+            if (opt.use_graphs) {
+                ep.pre->build_graph(st);
+                ep.post->build_graph(st);
+            }
+            it = graphs.emplace(gkey, std::move(ep)).first;
         }
         PBKD_CUDA(cudaEventRecord(e0, st));
-        if (it->second->has_graph())
-            it->second->launch_graph(st);
-        else
-            it->second->run(st);
+        for (Program* pr : {it->second.pre.get(), it->second.post.get()}) {
+            if (pr->launches() == 0) continue;
+            if (pr->has_graph())
+                pr->launch_graph(st);
+            else
+                pr->run(st);
+            if (pr == it->second.pre.get() && world > 1)  // boundary rows to their owners
+                comm->all_to_all_v(sendbuf.f(), send_off, send_cnt, recvbuf.f(), recv_off, recv_cnt, st);
+            if (pr == it->second.pre.get()) PBKD_CUDA(cudaEventRecord(eT, st));
+        }
         PBKD_CUDA(cudaEventRecord(e1, st));
         for (size_t i = 0; i < ts.size(); ++i)  // epoch-local losses -> per-run history
             if (key[i] > 0)
                 PBKD_CUDA(cudaMemcpyAsync(ts[i]->step_loss.f() + gbase[i], ts[i]->epoch_loss.p,
                                           static_cast<size_t>(key[i]) * sizeof(float), cudaMemcpyDeviceToDevice, st));
-        if (timed) timing.launches += static_cast<long long>(it->second->launches());
+        if (timed) timing.launches += static_cast<long long>(it->second.pre->launches() + it->second.post->launches());
         if (e + 1 <= emax) pos_next = make_pos(e + 1, epoch_key(e + 1));  // overlaps the GPU
         PBKD_CUDA(cudaEventSynchronize(e1));
         float ms = 0.0f;
         PBKD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         timing.epoch_ms_total += ms;
         timing.epoch_ms.push_back(ms);
+        if (timed) {
+            float tms = 0.0f;
+            PBKD_CUDA(cudaEventElapsedTime(&tms, e0, eT));
+            timing.teacher_ms += tms;
+        }
         timing.epochs += 1;
         if (timed) timing.timed_epochs += 1;
         for (size_t i = 0; i < ts.size(); ++i) {
@@ -1302,6 +1415,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     }
     cudaEventDestroy(t0);
     cudaEventDestroy(t1e);
+    cudaEventDestroy(eT);
     PBKD_CUDA(cudaStreamSynchronize(st));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1434,6 +1548,13 @@ std::vector<TaskOutcome> Engine::run(const std::vector<DistillTask>& t, const st
 }
 const RunTiming& Engine::timing() const { return impl_->timing; }
 int Engine::device() const { return impl_->dev; }
+void Engine::set_comm(const char* id, int rank, int world) {
+    PBKD_CUDA(cudaSetDevice(impl_->dev));
+    impl_->comm.reset();
+    if (world > 1) impl_->comm = std::make_unique<NcclComm>(id, rank, world);
+}
+int Engine::comm_rank() const { return impl_->comm ? impl_->comm->rank() : 0; }
+int Engine::comm_world() const { return impl_->comm ? impl_->comm->world() : 1; }
 cudaStream_t Engine::stream() const { return impl_->st; }
 
 Tensor Engine::prefix_infer(const Tensor& x, int k, bool inclusive) {

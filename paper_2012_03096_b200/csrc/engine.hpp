@@ -44,6 +44,15 @@ struct RunOptions {
     bool baseline_and_eval = true;  // epoch-0 baseline + evaluations (train_block semantics)
     bool use_graphs = true;
     int timed_from_epoch = 1;  // device events bracket epochs [timed_from_epoch, last]
+    // Sample-sharded teacher (multi-GPU).  global_blocks lists every block
+    // being distilled on any rank with its owner; this engine trains only the
+    // tasks passed to run() (owner == rank), runs the teacher forward on its
+    // shard of the training split for ALL blocks, and exchanges boundary rows
+    // with NCCL (set_comm).  virtual_shards > 1 on a single GPU runs the same
+    // pack/scatter path with local shards (tests).
+    std::vector<std::pair<int, int>> global_blocks;  // (block index, owner rank)
+    int virtual_shards = 1;
+    std::vector<double> shard_share;  // teacher share per rank (empty: uniform)
 };
 
 // Timing of the last run (device events around the epoch graphs).
@@ -52,6 +61,7 @@ struct RunTiming {
     std::vector<double> epoch_ms; // per training epoch (graph only)
     double timed_ms = 0.0;        // events around epochs >= timed_from_epoch, host gaps included
     int timed_epochs = 0;
+    double teacher_ms = 0.0;      // timed epochs: teacher forward (+ pack + exchange) part
     int epochs = 0;
     long long student_steps = 0;  // per task
     long long launches = 0;       // kernel launches in the timed window
@@ -88,6 +98,10 @@ public:
 
     int device() const;
     cudaStream_t stream() const;
+    // join an NCCL communicator (id from nccl_unique_id on rank 0)
+    void set_comm(const char* nccl_id128, int rank, int world);
+    int comm_rank() const;
+    int comm_world() const;
 
     struct Impl;
 

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "pbkd_b200.h"
+#include "../comm.hpp"
 #include "../engine.hpp"
 #include "../ops.cuh"
 #include "pbkd/dataset.hpp"
@@ -228,6 +229,10 @@ int pbkd_run_timing(const pbkd_results* r, double* timed_ms, int* timed_epochs, 
                     double* epoch_ms, int cap, int* n_epochs) {
     return guard([&] {
         if (timed_ms) *timed_ms = r->timing.timed_ms;
+        if (epoch_ms && cap < 0) {  // cap < 0: epoch_ms[0] receives the teacher part instead
+            epoch_ms[0] = r->timing.teacher_ms;
+            return;
+        }
         if (timed_epochs) *timed_epochs = r->timing.timed_epochs;
         if (launches) *launches = r->timing.launches;
         if (n_epochs) *n_epochs = static_cast<int>(r->timing.epoch_ms.size());
@@ -259,6 +264,61 @@ int pbkd_run_timed(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int
 int pbkd_bench_kernel(pbkd_ctx* ctx, int which, int batch, int iters, double* ms, double* bytes,
                       double* flops) {
     return guard([&] { ctx->eng->bench_kernel(which, batch, iters, ms, bytes, flops); });
+}
+
+int pbkd_nccl_unique_id(char* out128) {
+    return guard([&] { nccl_unique_id(out128); });
+}
+
+int pbkd_ctx_set_comm(pbkd_ctx* ctx, const char* id128, int rank, int world) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank/world");
+        ctx->eng->set_comm(id128, rank, world);
+    });
+}
+
+int pbkd_run_sharded(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* tr, int n_tr, const int* ev,
+                     int n_ev, int flags, int timed_from_epoch, const int* g_blocks, const int* g_owner, int n_global,
+                     int virtual_shards, const double* share, int n_share, pbkd_results** out) {
+    return guard([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<pbkd::DistillTask> ts;
+        for (int i = 0; i < n_tasks; ++i) ts.push_back(to_task(tasks[i]));
+        RunOptions opt;
+        opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
+        opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
+        opt.timed_from_epoch = timed_from_epoch;
+        for (int i = 0; i < n_global; ++i) opt.global_blocks.push_back({g_blocks[i], g_owner[i]});
+        opt.virtual_shards = virtual_shards;
+        if (share) opt.shard_share.assign(share, share + n_share);
+        auto r = std::make_unique<pbkd_results>();
+        r->res = ctx->eng->run(ts, std::vector<int>(tr, tr + n_tr), std::vector<int>(ev, ev + n_ev), opt);
+        r->wall = now_s(t0);
+        r->epoch_ms = ctx->eng->timing().epoch_ms_total;
+        r->timing = ctx->eng->timing();
+        *out = r.release();
+    });
+}
+
+int pbkd_exchange_plan(const int* blocks, const int* owners, int nb, const long long* in_row,
+                       const long long* out_row, int world, int n_train, const double* share, int src, int dst,
+                       size_t* count, size_t* off_in, size_t* off_tgt, int* shard_begin) {
+    return guard([&] {
+        ExchangePlan xp;
+        xp.world = world;
+        xp.blocks.assign(blocks, blocks + nb);
+        xp.owner.assign(owners, owners + nb);
+        xp.in_row.assign(in_row, in_row + nb);
+        xp.out_row.assign(out_row, out_row + nb);
+        std::vector<double> sh = share ? std::vector<double>(share, share + world) : std::vector<double>(world, 1.0);
+        xp.shard_begin = shard_bounds(n_train, sh);
+        *count = xp.count(src, dst);
+        for (int b = 0; b < nb; ++b) {
+            off_in[b] = xp.offset_in(src, dst, static_cast<size_t>(b));
+            off_tgt[b] = xp.offset_tgt(src, dst, static_cast<size_t>(b));
+        }
+        for (int s = 0; s <= world; ++s) shard_begin[s] = xp.shard_begin[static_cast<size_t>(s)];
+    });
 }
 
 int pbkd_run_parallel(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* tr, int n_tr,
