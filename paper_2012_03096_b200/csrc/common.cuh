@@ -45,6 +45,24 @@ __device__ __forceinline__ float bn_infer_apply(float x, float scale, float shif
 }
 __device__ __forceinline__ float relu(float x) { return x > 0.0f ? x : 0.0f; }
 
+// Which op of a grouped launch owns work item t (ops sorted by cta_begin,
+// ops[0].cta_begin == 0).  Must be called by all 32 lanes of a warp with the
+// same t: lane l reads ops[l].cta_begin, one ballot -- a single global-load
+// latency instead of a chain of nd dependent loads.
+template <class Op>
+__device__ __forceinline__ int op_index(const Op* __restrict__ ops, int nd, int t) {
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    int idx = 0;
+    for (int base = 0; base < nd; base += 32) {
+        const int i = base + lane;
+        const bool ge = i < nd && t >= ops[i].cta_begin;
+        const unsigned b = __ballot_sync(0xffffffffu, ge);
+        idx += __popc(b);
+        if (b != 0xffffffffu) break;
+    }
+    return idx - 1;
+}
+
 // Which task of a grouped launch owns this CTA (offs has nd+1 entries).
 __device__ __forceinline__ int find_task(const int* __restrict__ offs, int nd, int& local) {
     int t = 0;

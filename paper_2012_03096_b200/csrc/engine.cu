@@ -2,6 +2,10 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cctype>
+#include <cstdio>
+#include <typeinfo>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -26,18 +30,42 @@ namespace {
 
 constexpr int kScatterCtas = 148;
 
+// PBKD_TRACE=1: host wall time of each phase of run() on stderr (synchronises
+// the stream at every mark, so only for diagnosis).
+struct PhaseTrace {
+    bool on = std::getenv("PBKD_TRACE") != nullptr;
+    cudaStream_t st = nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[pbkd] %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 // ------------------------------------------------------------ device memory
+// Buffers come from the device's stream-ordered memory pool on the engine
+// stream (release threshold: keep everything), so the per-run allocations of
+// activation streams and workspaces are pool hits after the first run instead
+// of cudaMalloc/cudaFree round trips.  g_alloc_stream is set by every Engine
+// entry point (thread-local: one engine per thread at a time).
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t s = nullptr;
     DevBuf() = default;
     explicit DevBuf(size_t n) { alloc(n); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr, o.bytes = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept {
         release();
-        p = o.p, bytes = o.bytes;
+        p = o.p, bytes = o.bytes, s = o.s;
         o.p = nullptr, o.bytes = 0;
         return *this;
     }
@@ -45,10 +73,11 @@ struct DevBuf {
     void alloc(size_t n) {
         release();
         bytes = std::max<size_t>(n, 16);
-        PBKD_CUDA(cudaMalloc(&p, bytes));
+        s = g_alloc_stream;
+        PBKD_CUDA(cudaMallocAsync(&p, bytes, s));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         bytes = 0;
     }
@@ -85,11 +114,12 @@ public:
         steps_.push_back([launch, off, nd, total](cudaStream_t st, const uint8_t* slab) {
             launch(reinterpret_cast<const Op*>(slab + off), nd, total, st);
         });
+        names_.push_back(op_name(typeid(Op).name()));
     }
-    // tcgen05 GEMMs: one launch per N-tile class (the tile is a template
-    // parameter), all tasks of that class grouped in it
+    // tcgen05 GEMMs: one launch per kernel / N-tile class (the tile is a
+    // template parameter), all tasks of that class grouped in it
     void gemm(std::vector<GemmOp> all) {
-        for (int cls : {32, 64, 128}) {
+        for (int cls : {32, 64, 128, kGemmClassTma + 32, kGemmClassTma + 64, kGemmClassTma + 128}) {
             std::vector<GemmOp> ops;
             for (const GemmOp& o : all)
                 if (gemm_bn_class(o) == cls) ops.push_back(o);
@@ -106,10 +136,14 @@ public:
             steps_.push_back([off, nd, total, cls](cudaStream_t st, const uint8_t* slab) {
                 launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, cls, st);
             });
+            const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
+            names_.push_back(std::string("gemm_") + kind + (cls >= kGemmClassTma ? "_tma" : "_reg") +
+                             std::to_string(cls % kGemmClassTma));
         }
     }
-    void raw(std::function<void(cudaStream_t)> f) {
+    void raw(std::function<void(cudaStream_t)> f, const char* name = "raw") {
         steps_.push_back([f](cudaStream_t st, const uint8_t*) { f(st); });
+        names_.push_back(name);
     }
     void finalize(cudaStream_t st) {
         slab_.alloc(std::max<size_t>(host_.size(), 64));
@@ -121,6 +155,27 @@ public:
     void run(cudaStream_t st) {
         if (!finalized_) finalize(st);
         for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
+    }
+    // Eager run with a CUDA event after every launch; adds each launch's
+    // device time to prof[name] (PBKD_PROFILE diagnosis).
+    void run_profiled(cudaStream_t st, std::map<std::string, std::pair<int, double>>& prof) {
+        if (!finalized_) finalize(st);
+        std::vector<cudaEvent_t> ev(steps_.size() + 1);
+        for (auto& e : ev) PBKD_CUDA(cudaEventCreate(&e));
+        PBKD_CUDA(cudaEventRecord(ev[0], st));
+        for (size_t i = 0; i < steps_.size(); ++i) {
+            steps_[i](st, static_cast<const uint8_t*>(slab_.p));
+            PBKD_CUDA(cudaEventRecord(ev[i + 1], st));
+        }
+        PBKD_CUDA(cudaEventSynchronize(ev.back()));
+        for (size_t i = 0; i < steps_.size(); ++i) {
+            float ms = 0.0f;
+            PBKD_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            auto& e = prof[names_[i]];
+            e.first += 1;
+            e.second += ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
     }
     void build_graph(cudaStream_t st) {
         if (!finalized_) finalize(st);
@@ -139,17 +194,39 @@ public:
     }
 
 private:
+    static std::string op_name(const char* mangled) {  // "N8pbkd_gpu7DwFwdOpE" -> "DwFwdOp"
+        std::string m(mangled), out;
+        size_t i = m.find("pbkd_gpu");
+        i = i == std::string::npos ? 0 : i + 8;
+        while (i < m.size() && std::isdigit(static_cast<unsigned char>(m[i]))) ++i;
+        while (i < m.size() && m[i] != 'E') out += m[i++];
+        return out.empty() ? m : out;
+    }
     std::vector<uint8_t> host_;
     DevBuf slab_;
     std::vector<std::function<void(cudaStream_t, const uint8_t*)>> steps_;
+    std::vector<std::string> names_;
     bool finalized_ = false;
     cudaGraphExec_t exec_ = nullptr;
 };
+
+void print_profile(const char* what, const std::map<std::string, std::pair<int, double>>& prof) {
+    double tot = 0.0;
+    for (auto& kv : prof) tot += kv.second.second;
+    std::vector<std::pair<double, std::string>> v;
+    for (auto& kv : prof) v.push_back({kv.second.second, kv.first});
+    std::sort(v.rbegin(), v.rend());
+    std::fprintf(stderr, "[pbkd-prof] %s: %.3f ms total (eager, events per launch)\n", what, tot);
+    for (auto& [ms, name] : v)
+        std::fprintf(stderr, "[pbkd-prof]   %-24s %5d launches %9.3f ms %5.1f%%  avg %8.1f us\n", name.c_str(),
+                     prof.at(name).first, ms, 100.0 * ms / tot, 1e3 * ms / prof.at(name).first);
+}
 
 // ------------------------------------------------------------- teacher dev
 struct ConvDev {
     int cin = 0, cout = 0, k = 0, stride = 1, pad = 0;
     DevBuf w;            // [cout][k*k][cin]
+    DevBuf w_hi, w_lo;   // the same, pre-split into tf32 hi / lo (3xTF32 operands)
     DevBuf scale, shift; // inference batch-norm affine (ops.hpp:304-321)
 };
 
@@ -177,6 +254,12 @@ ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, 
                 w[(static_cast<size_t>(o) * kk + t) * d.cin + j] =
                     conv.weight.data[(static_cast<size_t>(o) * d.cin + j) * kk + t];
     d.w = upload(w, st);
+    {
+        std::vector<float> hi(w.size()), lo(w.size());
+        tf32_split_host(w.data(), w.size(), hi.data(), lo.data());
+        d.w_hi = upload(hi, st);
+        d.w_lo = upload(lo, st);
+    }
     if (bn) {
         std::vector<float> sc(d.cout), sh(d.cout);
         for (int j = 0; j < d.cout; ++j) {  // ops.hpp:312-314, float arithmetic
@@ -210,6 +293,8 @@ GemmOp conv_gemm(const ConvDev& c, const float* x, int n, int ih, int iw, float*
     o.K = c.k * c.k * c.cin;
     o.A = x;
     o.B = c.w.f();
+    o.b_hi = c.w_hi.f();
+    o.b_lo = c.w_lo.f();
     o.ldb = o.K;
     o.b_kmajor = 1;
     o.C = y;
@@ -297,14 +382,28 @@ struct Engine::Impl {
     int count = 0, dc = 0, dh = 0, dw = 0, classes = 0;
     RunTiming timing;
     std::unique_ptr<NcclComm> comm;
+    PhaseTrace trace;
 
     explicit Impl(int device) : dev(device) {
         PBKD_CUDA(cudaSetDevice(dev));
+        g_alloc_stream = st;
         PBKD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        PBKD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = ~uint64_t(0);
+        PBKD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     ~Impl() {
         cudaSetDevice(dev);
-        if (st) cudaStreamDestroy(st);
+        g_alloc_stream = st;
+        // device buffers are freed on st, so before the stream goes away
+        tblocks.clear();
+        for (DevBuf* b : {&cls_kinds, &cls_w, &cls_b, &images, &labels, &eval_labels}) b->release();
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+        g_alloc_stream = nullptr;
     }
 
     int max_row() const {
@@ -316,6 +415,7 @@ struct Engine::Impl {
 
     void load_teacher(const Network& n) {
         PBKD_CUDA(cudaSetDevice(dev));
+        g_alloc_stream = st;
         net = n;
         tblocks.clear();
         int c = n.in_c, h = n.in_h, w = n.in_w;
@@ -400,6 +500,7 @@ struct Engine::Impl {
 
     void load_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {
         PBKD_CUDA(cudaSetDevice(dev));
+        g_alloc_stream = st;
         const size_t sz = static_cast<size_t>(n) * c * h * w;
         images.alloc(sz * sizeof(float));
         PBKD_CUDA(cudaMemcpyAsync(images.p, img, sz * sizeof(float),
@@ -949,6 +1050,8 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
                                            const std::vector<int>& train_idx,
                                            const std::vector<int>& eval_idx, const RunOptions& opt) {
     PBKD_CUDA(cudaSetDevice(dev));
+        g_alloc_stream = st;
+    trace.t = std::chrono::steady_clock::now();
     if (!has_teacher) throw std::logic_error("engine: no teacher loaded");
     if (count == 0) throw std::logic_error("engine: no dataset loaded");
     if (train_idx.empty()) throw SpecError("training split is empty");
@@ -960,6 +1063,7 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
     if (dc != net.in_c || dh != net.in_h || dw != net.in_w)
         throw pbkd::ShapeError("dataset image shape does not match the network input");
     for (const DistillTask& t : tasks) validate(t);
+    trace.st = st;
     const int ntrain = static_cast<int>(train_idx.size());
     const int neval = static_cast<int>(eval_idx.size());
     std::vector<std::unique_ptr<TaskState>> states;
@@ -967,6 +1071,7 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
         states.push_back(std::make_unique<TaskState>());
         init_task(*states.back(), t, ntrain, neval);
     }
+    trace.mark("run: init tasks");
     DevBuf d_train = upload(train_idx, st), d_eval = upload(eval_idx, st);
     std::vector<int> iota(static_cast<size_t>(std::max(ntrain, neval)));
     std::iota(iota.begin(), iota.end(), 0);
@@ -980,6 +1085,7 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
                         "candidate depth); every rank must own at least one block");
     for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota);
 
+    trace.mark("run: groups done");
     // ---- read back and assemble train_block results
     std::vector<TaskOutcome> out;
     for (auto& sp : states) {
@@ -1062,6 +1168,7 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
         r.wall_time_s = timing.epoch_ms_total * 1e-3;
         out.push_back(std::move(r));
     }
+    trace.mark("run: readback");
     return out;
 }
 
@@ -1163,6 +1270,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         for (int i = 0; i < neval; ++i) lab[static_cast<size_t>(i)] = all[static_cast<size_t>(eval_idx[static_cast<size_t>(i)])];
         eval_labels = upload(lab, st);
     }
+    trace.mark("group: workspace + labels");
 
     // ---- epoch 0: baseline losses and first evaluation
     if (opt.baseline_and_eval) {
@@ -1191,8 +1299,10 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             }
             P.run(st);
         }
+        trace.mark("group: epoch-0 baseline");
         std::vector<int> slots(ts.size(), 0);
         run_eval(ts, slots);
+        trace.mark("group: epoch-0 eval");
     }
 
     // ---- training epochs
@@ -1359,7 +1469,15 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 ep.pre->build_graph(st);
                 ep.post->build_graph(st);
             }
+            if (std::getenv("PBKD_PROFILE")) {  // one extra eager pass, timed per launch
+                std::map<std::string, std::pair<int, double>> pa, pb;
+                ep.pre->run_profiled(st, pa);
+                print_profile("teacher pass", pa);
+                ep.post->run_profiled(st, pb);
+                print_profile("student steps", pb);
+            }
             it = graphs.emplace(gkey, std::move(ep)).first;
+            trace.mark("epoch: build programs/graphs");
         }
         PBKD_CUDA(cudaEventRecord(e0, st));
         for (Program* pr : {it->second.pre.get(), it->second.post.get()}) {
@@ -1403,7 +1521,9 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                     which.push_back(ts[i]);
                     slots.push_back(evals_done[i]++);
                 }
+            trace.mark("epoch: run");
             if (!which.empty()) run_eval(which, slots);
+            trace.mark("epoch: eval");
         }
     }
     if (timed_started) {
@@ -1431,6 +1551,7 @@ __global__ void fill_kernel(float* p, size_t n, float v) {
 void Engine::bench_kernel(int which, int batch, int iters, double* ms, double* bytes, double* flops) {
     Impl& m = *impl_;
     PBKD_CUDA(cudaSetDevice(m.dev));
+    g_alloc_stream = m.st;
     if (!m.has_teacher) throw std::logic_error("engine: no teacher loaded");
     // the teacher block with the most MACs
     size_t bi = 0;
@@ -1550,6 +1671,7 @@ const RunTiming& Engine::timing() const { return impl_->timing; }
 int Engine::device() const { return impl_->dev; }
 void Engine::set_comm(const char* id, int rank, int world) {
     PBKD_CUDA(cudaSetDevice(impl_->dev));
+    g_alloc_stream = impl_->st;
     impl_->comm.reset();
     if (world > 1) impl_->comm = std::make_unique<NcclComm>(id, rank, world);
 }
@@ -1560,6 +1682,7 @@ cudaStream_t Engine::stream() const { return impl_->st; }
 Tensor Engine::prefix_infer(const Tensor& x, int k, bool inclusive) {
     Impl& m = *impl_;
     PBKD_CUDA(cudaSetDevice(m.dev));
+    g_alloc_stream = m.st;
     if (!m.has_teacher) throw std::logic_error("engine: no teacher loaded");
     const int nb = static_cast<int>(m.tblocks.size());
     if (k < 1 || k > nb) throw std::out_of_range("prefix_infer: k=" + std::to_string(k) + " out of range");
@@ -1596,6 +1719,7 @@ int candidate_units(const Block& b) {
 Tensor Engine::candidate_infer(const Block& cand, const Tensor& x) {
     Impl& m = *impl_;
     PBKD_CUDA(cudaSetDevice(m.dev));
+    g_alloc_stream = m.st;
     for (const pbkd::LayerParams& l : cand.layers)
         if (l.kind == LayerKind::Add) throw SpecError("skip candidates are not implemented on the GPU path");
     const int U = candidate_units(cand);
@@ -1651,6 +1775,7 @@ Tensor Engine::candidate_infer(const Block& cand, const Tensor& x) {
 double Engine::eval_with_student(int block_index, const Block& student, const std::vector<int>& eval_idx) {
     Impl& m = *impl_;
     PBKD_CUDA(cudaSetDevice(m.dev));
+    g_alloc_stream = m.st;
     if (eval_idx.empty()) throw SpecError("evaluation split is empty");
     if (block_index < 1 || block_index > static_cast<int>(m.tblocks.size()))
         throw SpecError("block index " + std::to_string(block_index) + " out of range");

@@ -115,6 +115,17 @@ void launch_one(cudaStream_t st, void (*launch)(const Op*, int, int, cudaStream_
     cudaFree(d);
 }
 
+void launch_gemm_one(cudaStream_t st, const GemmOp& g) {
+    GemmOp op = g;
+    op.cta_begin = 0;
+    GemmOp* d = nullptr;
+    PBKD_CUDA(cudaMalloc(&d, sizeof(GemmOp)));
+    PBKD_CUDA(cudaMemcpyAsync(d, &op, sizeof(GemmOp), cudaMemcpyHostToDevice, st));
+    launch_gemm_bn(d, 1, std::max(1, ctas_gemm(op)), gemm_bn_class(op), st);
+    PBKD_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d);
+}
+
 struct Scratch {
     float* p = nullptr;
     explicit Scratch(size_t n) { PBKD_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float))); }
@@ -699,7 +710,7 @@ int pbkd_k_pw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int r
         if (col_sum || col_sq) {
             Scratch p0(static_cast<size_t>(g.tiles_m) * cout), p1(static_cast<size_t>(g.tiles_m) * cout);
             g.epi = 1, g.part0 = p0.p, g.part1 = p1.p;
-            launch_one(st, launch_gemm, g, ctas_gemm(g));
+            launch_gemm_one(st, g);
             ReduceOp r{};
             r.parts = g.tiles_m, r.width = cout;
             if (col_sum) {
@@ -711,7 +722,7 @@ int pbkd_k_pw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int r
                 launch_one(st, launch_reduce, r, ceil_div(cout, kThreads));
             }
         } else {
-            launch_one(st, launch_gemm, g, ctas_gemm(g));
+            launch_gemm_one(st, g);
         }
     });
 }
@@ -728,7 +739,7 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             g.C = gx, g.ldc = cin;
             g.ksplit = 1;
             gemm_finalize(g);
-            launch_one(st, launch_gemm, g, ctas_gemm(g));
+            launch_gemm_one(st, g);
         }
         if (gw) {
             GemmOp g{};
@@ -741,7 +752,7 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             gemm_finalize(g);
             Scratch part(static_cast<size_t>(g.ksplit) * cout * cin);
             g.C = part.p;
-            launch_one(st, launch_gemm, g, ctas_gemm(g));
+            launch_gemm_one(st, g);
             ReduceOp r{};
             r.part = part.p, r.out = gw, r.parts = g.ksplit, r.width = cout * cin;
             launch_one(st, launch_reduce, r, ceil_div(r.width, kThreads));

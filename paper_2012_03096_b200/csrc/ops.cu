@@ -27,8 +27,7 @@ int ctas_elem(long long total) { return std::max(1, ceil_div(total, 256LL * 4));
 
 template <class Op>
 __device__ __forceinline__ const Op& op_of(const Op* ops, int nd, int& local) {
-    int t = 0;
-    while (t + 1 < nd && static_cast<int>(blockIdx.x) >= ops[t + 1].cta_begin) ++t;
+    const int t = op_index(ops, nd, static_cast<int>(blockIdx.x));
     local = static_cast<int>(blockIdx.x) - ops[t].cta_begin;
     return ops[t];
 }

@@ -12,6 +12,8 @@
 // one sample, channels contiguous.  Depthwise weights are tap-major [9][C];
 // pointwise weights keep the reference's [C_out][C_in] (model.cpp:157-171).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace pbkd_gpu {
@@ -103,11 +105,25 @@ struct GemmOp {
     int tf32x3, tf32x1;  // 3xTF32 split (fp32 parity, default) or plain TF32
     const int* failed;
     int cta_begin;
+    int tma;             // 1: umma_tma.cu kernel (tensor maps below valid)
+    // optional pre-split B (tf32 hi / lo bit patterns, same layout as B,
+    // K-major): the TMA kernel loads them straight into its MMA operand ring
+    const float *b_hi, *b_lo;
+    int b_presplit;      // set by gemm_finalize when b_hi/b_lo are usable
+    CUtensorMap map_a, map_b;     // 2-D fp32 maps of A and B (64-byte aligned)
+    CUtensorMap map_bh, map_bl;   // SWIZZLE_128B maps of b_hi / b_lo
 };
+
+// tf32 hi/lo split on the host, bit-identical to tc::to_tf32 on the device
+// (round to nearest even, 13 low bits cleared): hi = rne(x), lo = rne(x - hi).
+void tf32_split_host(const float* x, size_t n, float* hi, float* lo);
 
 // Fills tiling fields (bn, tiles, kchunk/ksplit) of a GemmOp (umma.cu).
 void gemm_finalize(GemmOp& o);
-int gemm_bn_class(const GemmOp& o);  // N tile class of the launch that runs o
+// Launch class of o: N tile (32/64/128), + kGemmClassTma for the TMA kernel.
+constexpr int kGemmClassTma = 1000;
+int gemm_bn_class(const GemmOp& o);
+bool gemm_tma_prepare(GemmOp& o);  // umma_tma.cu: tensor maps, false if ineligible
 
 // Batch-norm statistics from the GEMM column partials (ops.hpp:273-299):
 // mean, var = E[x^2]-mean^2 clamped, inv_std, moving-stat update.
@@ -192,8 +208,9 @@ void launch_dw_fwd(const DwFwdOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_dw_bwd(const DwBwdOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_dw_gk(const DwGkOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_reduce(const ReduceOp* d_ops, int nd, int ctas, cudaStream_t st);
-void launch_gemm(const GemmOp* d_ops, int nd, int ctas, cudaStream_t st);  // bn_max 256
-void launch_gemm_bn(const GemmOp* d_ops, int nd, int ctas, int bn_max, cudaStream_t st);
+// ctas: the ops' total tile count (sum of ctas_gemm); cls: gemm_bn_class
+void launch_gemm_bn(const GemmOp* d_ops, int nd, int ctas, int cls, cudaStream_t st);
+void launch_gemm_tma(const GemmOp* d_ops, int nd, int tiles, int bn, cudaStream_t st);
 void launch_bn_stat(const BnStatOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_loss(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_bn_bwd_fin(const BnBwdFinOp* d_ops, int nd, int ctas, cudaStream_t st);

@@ -1,0 +1,204 @@
+// tc.cuh -- sm_100a tcgen05 / TMEM / mbarrier / TMA helpers shared by the
+// GEMM kernels (umma.cu: register-staged, umma_tma.cu: TMA + warp roles).
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace pbkd_gpu {
+namespace tc {
+
+constexpr int kBM = 128;       // MMA M (TMEM lanes)
+constexpr int kBK = 32;        // fp32 K per stage = one 128-byte swizzle row
+constexpr int kRowBytes = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Round fp32 to the nearest tf32 (ties to even) with the 13 dropped bits
+// cleared, so the MMA's operand read is exact and x - hi is the exact
+// remainder.  cvt.rn.tf32.f32 is one F2FP.TF32.F32 instruction on sm_100a
+// (cvt.rna is emulated with 4); the mask makes the cleared low bits explicit.
+// tools/probes/tf32_cvt.cu checks it against the integer RNE formula
+// (b + 0xFFF + ((b >> 13) & 1)) & ~0x1FFF, which the host side uses.
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r & 0xFFFFE000u;
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 format):
+// start>>4 [0,14), LBO>>4 [16,30) (=1, unused for swizzled K-major),
+// SBO>>4 [32,46) (=1024 B between 8-row groups), version 1 [46,48),
+// layout type SWIZZLE_128B = 2 at [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+// Byte offset of 16-byte chunk c (0..7) of row r in a K-major SWIZZLE_128B
+// tile (rows of 128 bytes, 8-row groups of 1024 bytes).
+__device__ __forceinline__ int sw128(int r, int c) { return (r >> 3) * 1024 + (r & 7) * kRowBytes + ((c ^ (r & 7)) << 4); }
+
+// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M=128, N=n.
+__device__ __forceinline__ uint32_t instr_desc(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+// Spin on try_wait without a suspend-time hint: the pipeline hand-offs are
+// latency critical (a suspended waiter wakes late).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// 2-D TMA tile load global -> shared, completion counted on bar (bytes).
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// acc[0..15] += TMEM row (this thread's lane), 16 columns at addr
+__device__ __forceinline__ void tmem_add16(uint32_t addr, float* acc) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = __fadd_rn(acc[i], __uint_as_float(r[i]));
+}
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(p));
+    return p != 0;
+}
+
+// One 32-wide K chunk of the 3xTF32 split (hi*lo + lo*hi + hi*hi per 8-wide
+// k step, small terms first; the chunk's first MMA overwrites the TMEM slot)
+// as a single asm block: 12 tcgen05.mma with descriptors advanced in
+// registers, no per-instruction uniform moves or reconvergence.
+__device__ __forceinline__ void mma_chunk3(uint32_t d, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
+                                           uint32_t idesc) {
+    const uint64_t dah = smem_desc(ah), dal = smem_desc(al), dbh = smem_desc(bh), dbl = smem_desc(bl);
+    asm volatile(
+        "{\n\t"
+        ".reg .pred F, T;\n\t"
+        ".reg .b64 ah, al, bh, bl;\n\t"
+        "setp.ne.b32 F, 0, 0;\n\t"
+        "setp.eq.b32 T, 0, 0;\n\t"
+        "mov.b64 ah, %1;\n\tmov.b64 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, F;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
+        "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
+        "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
+        "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
+        "}\n" ::"r"(d),
+        "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(idesc)
+        : "memory");
+}
+
+// Issue one 32-wide K chunk (4 k-steps of 8) into TMEM column d:
+// terms 1: hi*hi; 3: hi*lo + lo*hi + hi*hi (small terms first); 4: + lo*lo.
+__device__ __forceinline__ void mma_chunk(uint32_t d, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
+                                          uint32_t idesc, int terms) {
+    if (terms == 3) {
+        mma_chunk3(d, ah, al, bh, bl, idesc);
+        return;
+    }
+#pragma unroll
+    for (int kk = 0; kk < kBK / 8; ++kk) {
+        const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+        if (terms > 1) {
+            if (terms > 3) mma_tf32(d, smem_desc(al + off), smem_desc(bl + off), idesc, kk > 0 ? 1u : 0u);
+            mma_tf32(d, smem_desc(ah + off), smem_desc(bl + off), idesc, (kk > 0 || terms > 3) ? 1u : 0u);
+            mma_tf32(d, smem_desc(al + off), smem_desc(bh + off), idesc, 1u);
+            mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), idesc, 1u);
+        } else {
+            mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), idesc, kk > 0 ? 1u : 0u);
+        }
+    }
+}
+
+}  // namespace tc
+}  // namespace pbkd_gpu

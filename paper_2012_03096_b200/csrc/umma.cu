@@ -29,109 +29,21 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "gemm_epi.cuh"
 #include "ops.cuh"
+#include "tc.cuh"
 
 namespace pbkd_gpu {
 
 namespace {
 
-constexpr int kBM = 128;  // MMA M (TMEM lanes)
-constexpr int kBK = 32;   // fp32 K per stage = one 128-byte swizzle row
+using namespace tc;
 constexpr int kKH = 16;   // K values staged per thread (half a row)
-constexpr int kRowBytes = 128;
 constexpr int kStages = 2;
 constexpr int kThreadsG = 256;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// Round fp32 to the nearest tf32 (ties to even) and clear the 13 dropped bits,
-// so the MMA's operand read is exact and x - hi is the exact remainder.
-// (Integer ops on purpose: measured on B200, the cvt.rna.tf32.f32 result kept
-// the low bits and the split degenerated to plain TF32.)
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    const uint32_t b = __float_as_uint(x);
-    return (b + 0xFFFu + ((b >> 13) & 1u)) & 0xFFFFE000u;
-}
-
-// K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 format):
-// start>>4 [0,14), LBO>>4 [16,30) (=1, unused for swizzled K-major),
-// SBO>>4 [32,46) (=1024 B between 8-row groups), version 1 [46,48),
-// layout type SWIZZLE_128B = 2 at [61,64).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
-    d |= static_cast<uint64_t>(1) << 16;
-    d |= static_cast<uint64_t>(1024 >> 4) << 32;
-    d |= static_cast<uint64_t>(1) << 46;
-    d |= static_cast<uint64_t>(2) << 61;
-    return d;
-}
-
-// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M=128, N=n.
-__device__ __forceinline__ uint32_t instr_desc(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-           (static_cast<uint32_t>(kBM >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@P1 bra DONE_%=;\n\t"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(0x989680u)
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-
-// acc[0..15] += TMEM row (this thread's lane), 16 columns at addr
-__device__ __forceinline__ void tmem_add16(uint32_t addr, float* acc) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = __fadd_rn(acc[i], __uint_as_float(r[i]));
-}
-
 // Store 16 K values (chunks h*4..h*4+3 of row r) as tf32 hi / lo.
 __device__ __forceinline__ void put_half(uint8_t* hi, uint8_t* lo, int r, int h, const float* v, bool split) {
-    const int base = (r >> 3) * 1024 + (r & 7) * kRowBytes;
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
         const int c = h * 4 + cc;
@@ -142,7 +54,7 @@ __device__ __forceinline__ void put_half(uint8_t* hi, uint8_t* lo, int r, int h,
             hv[q] = to_tf32(x);
             lv[q] = split ? to_tf32(__fsub_rn(x, __uint_as_float(hv[q]))) : 0u;
         }
-        const int off = base + ((c ^ (r & 7)) << 4);
+        const int off = sw128(r, c);
         *reinterpret_cast<uint4*>(hi + off) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
         if (split) *reinterpret_cast<uint4*>(lo + off) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
     }
@@ -232,8 +144,7 @@ __device__ __forceinline__ void load_b(const GemmOp& o, int n, int k0, int kend,
 
 template <class Op>
 __device__ __forceinline__ const Op& op_of_u(const Op* ops, int nd, int& local) {
-    int t = 0;
-    while (t + 1 < nd && static_cast<int>(blockIdx.x) >= ops[t + 1].cta_begin) ++t;
+    const int t = op_index(ops, nd, static_cast<int>(blockIdx.x));
     local = static_cast<int>(blockIdx.x) - ops[t].cta_begin;
     return ops[t];
 }
@@ -322,19 +233,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) umma_gemm_kernel(const GemmOp* _
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-                const uint32_t d = tmem + s * BN;
-#pragma unroll
-                for (int kk = 0; kk < kBK / 8; ++kk) {
-                    const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-                    if (split3) {  // small terms first
-                        if (terms > 3) mma_tf32(d, smem_desc(al + off), smem_desc(bl + off), idesc, kk > 0 ? 1u : 0u);
-                        mma_tf32(d, smem_desc(ah + off), smem_desc(bl + off), idesc, (kk > 0 || terms > 3) ? 1u : 0u);
-                        mma_tf32(d, smem_desc(al + off), smem_desc(bh + off), idesc, 1u);
-                        mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), idesc, 1u);
-                    } else {
-                        mma_tf32(d, smem_desc(ah + off), smem_desc(bh + off), idesc, kk > 0 ? 1u : 0u);
-                    }
-                }
+                mma_chunk(tmem + s * BN, ah, al, bh, bl, idesc, terms);
                 mma_commit(&bars[s]);
             }
             __syncwarp();
@@ -344,69 +243,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) umma_gemm_kernel(const GemmOp* _
 
     // ------------------------------------------------------------ epilogue
     // thread = (row wq*32+lane, columns wh*HB .. +HB)
-    const int row = m0 + wq * 32 + lane;
-    const bool row_ok = row < o.M;
-    float* C = o.C + (o.epi == 2 ? static_cast<long long>(split) * o.M * o.ldc : 0);
-    const bool vec_st = (o.ldc % 4) == 0;
-    constexpr int SL = HB >= 16 ? 16 : HB;
-#pragma unroll
-    for (int c0 = 0; c0 < HB; c0 += SL) {
-        float* val = acc + c0;
-        const int ncol = n0 + wh * HB + c0;
-#pragma unroll
-        for (int j = 0; j < SL; ++j) {
-            const int n = ncol + j;
-            float x = val[j];
-            if (row_ok && n < o.N) {
-                if (o.scale) x = bn_infer_apply(x, o.scale[n], o.shift[n]);
-                if (o.skip) x = add(x, o.skip[static_cast<long long>(row) * o.ldc + n]);
-                if (o.relu) x = relu(x);
-            } else {
-                x = 0.0f;
-            }
-            val[j] = x;
-        }
-        if (row_ok) {
-            float* dst = C + static_cast<long long>(row) * o.ldc + ncol;
-            if (vec_st && ncol + SL <= o.N) {
-#pragma unroll
-                for (int q = 0; q < SL / 4; ++q)
-                    reinterpret_cast<float4*>(dst)[q] = make_float4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < SL; ++j)
-                    if (ncol + j < o.N) dst[j] = val[j];
-            }
-        }
-        if (o.epi == 1) {  // per-(m-tile, column) sum / sum of squares, fixed-order trees
-#pragma unroll
-            for (int j = 0; j < SL; ++j) {
-                float s = val[j], q = val[j] * val[j];
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    s += __shfl_xor_sync(0xffffffffu, s, off);
-                    q += __shfl_xor_sync(0xffffffffu, q, off);
-                }
-                if (lane == 0) {
-                    red[warp][j] = s;
-                    red[warp][16 + j] = q;
-                }
-            }
-            __syncthreads();
-            if (tid < 2 * SL) {  // column (half h, j): 4 row quarters in order
-                const int h = tid / SL, j = tid % SL;
-                const int col = n0 + h * HB + c0 + j;
-                if (col < o.N) {
-                    const float s = (red[4 * h][j] + red[4 * h + 1][j]) + (red[4 * h + 2][j] + red[4 * h + 3][j]);
-                    const float q = (red[4 * h][16 + j] + red[4 * h + 1][16 + j]) +
-                                    (red[4 * h + 2][16 + j] + red[4 * h + 3][16 + j]);
-                    o.part0[static_cast<long long>(tm) * o.N + col] = s;
-                    o.part1[static_cast<long long>(tm) * o.N + col] = q;
-                }
-            }
-            __syncthreads();
-        }
-    }
+    gemm_epilogue<BN>(o, acc, tm, tn, split, wq, wh, lane, tid, red, [] { __syncthreads(); });
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
 }
@@ -438,10 +275,18 @@ void gemm_finalize(GemmOp& o) {
         }();
         o.tf32x3 = terms;
     }
+    // TMA + warp-specialised kernel for the plain (non-conv) GEMMs whose
+    // operands satisfy the tensor-map constraints (16-byte aligned rows);
+    // PBKD_GEMM_TMA=0 forces the register-staged kernel
+    static const bool tma_on = [] {
+        const char* e = std::getenv("PBKD_GEMM_TMA");
+        return !(e && e[0] == '0');
+    }();
+    o.tma = (tma_on && gemm_tma_prepare(o)) ? 1 : 0;
 }
 
 int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
-int gemm_bn_class(const GemmOp& o) { return bn_for(o.N); }
+int gemm_bn_class(const GemmOp& o) { return bn_for(o.N) + (o.tma ? kGemmClassTma : 0); }
 
 template <int BN>
 static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
@@ -456,16 +301,19 @@ static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
     PBKD_LAUNCH_CHECK();
 }
 
-// All ops of one launch share the N tile (the caller groups ops by
-// gemm_bn_class; narrower ops would pad their B rows with zeros).
-void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int bn_max, cudaStream_t st) {
-    switch (bn_for(bn_max)) {
+// All ops of one launch share the N tile and the kernel (the caller groups
+// ops by gemm_bn_class; narrower ops would pad their B rows with zeros).
+void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int cls, cudaStream_t st) {
+    if (cls >= kGemmClassTma) {
+        launch_gemm_tma(d, nd, ctas, cls - kGemmClassTma, st);
+        return;
+    }
+    switch (bn_for(cls)) {
         case 32: launch_bn_t<32>(d, nd, ctas, st); break;
         case 64: launch_bn_t<64>(d, nd, ctas, st); break;
         default: launch_bn_t<128>(d, nd, ctas, st); break;
     }
 }
 
-void launch_gemm(const GemmOp* d, int nd, int ctas, cudaStream_t st) { launch_gemm_bn(d, nd, ctas, 128, st); }
 
 }  // namespace pbkd_gpu

@@ -1,0 +1,528 @@
+// umma_tma.cu -- persistent, warp-specialised tcgen05 GEMM with TMA operand
+// loads, for the student pointwise convs (fwd / dgrad / wgrad).
+//
+//   C[m][n] = sum_k A(m,k) * B(n,k),   fp32 in / fp32 out, 3xTF32 split
+//
+// Same arithmetic as umma.cu (identical MMA sequence per 32-wide K chunk,
+// per-chunk TMEM drain summed in fp32 in chunk order), so both kernels give
+// the same bits; this one is built for the HBM-bound pointwise shapes
+// (arithmetic intensity <= 125 flop/B) where the register-staged kernel was
+// latency-bound.  Warp roles (448 threads):
+//
+//   warp 0      TMA producer: raw fp32 tiles (A 128x32, B BNx32) into a
+//               kR-deep ring, either orientation (K-major or MN-major
+//               source), zero fill out of bounds
+//   warp 1      TMEM allocator + MMA issuer (one elected lane)
+//   warps 2-5   converters: raw fp32 -> tf32 hi / lo in the canonical
+//               K-major SWIZZLE_128B layout (transposing MN-major sources),
+//               kS-deep operand ring
+//   warps 6-13  drain + epilogue: per chunk tcgen05.ld of the chunk's TMEM
+//               slot and fp32 add; at the tile end the epilogue (store,
+//               batch-norm partials, split-K partials)
+//
+// Persistent: grid = min(tiles, #SMs); CTA i takes tiles i, i+grid, ... of the
+// grouped launch (every task's tiles, cta_begin prefix), all rings continue
+// across tiles so the next tile's loads overlap this tile's epilogue.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "gemm_epi.cuh"
+#include "ops.cuh"
+#include "tc.cuh"
+
+namespace pbkd_gpu {
+
+using namespace tc;
+
+namespace {
+
+constexpr int kWarpsT = 15;
+constexpr int kBWarp = 14;  // loads pre-split B (tf32 hi/lo) straight into the operand ring
+constexpr int kThreadsT = kWarpsT * 32;
+constexpr int kConvThreads = 128;  // warps 2-5
+constexpr int kEpiWarp0 = 6;
+
+template <int BN>
+struct Cfg {
+    static constexpr int R = BN >= 128 ? 2 : BN >= 64 ? 3 : 4;  // raw (TMA) stages
+    static constexpr int S = BN >= 128 ? 2 : 3;  // converted operand stages
+    static constexpr int a_raw = kBM * kBK * 4;
+    static constexpr int b_raw = BN * kBK * 4;
+    static constexpr int raw_stage = a_raw + b_raw;
+    static constexpr int a_op = kBM * kRowBytes;
+    static constexpr int b_op = BN * kRowBytes;
+    static constexpr int op_stage = 2 * a_op + 2 * b_op;
+    static constexpr int smem = 1024 + R * raw_stage + S * op_stage;
+    static constexpr int A = 4;  // TMEM accumulator slots (one per K chunk in flight)
+    static constexpr int tmem_cols = (A * BN <= 128) ? 128 : (A * BN <= 256) ? 256 : 512;
+};
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+struct TileGeo {
+    int split, tm, tn, k0, nchunks;
+};
+struct TileInfo {
+    int op;  // -1: skip (the task's failure flag is set)
+    TileGeo g;
+};
+constexpr int kMaxTiles = 128;  // tiles per CTA (host sizes the grid)
+constexpr int kMaxOps = 128;    // ops per launch
+template <int BN>
+__device__ __forceinline__ TileGeo tile_geo(const GemmOp& o, int local) {
+    TileGeo g;
+    const int tiles_mn = o.tiles_m * o.tiles_n;
+    g.split = local / tiles_mn;
+    const int rem = local - g.split * tiles_mn;
+    g.tm = rem / o.tiles_n;
+    g.tn = rem - g.tm * o.tiles_n;
+    g.k0 = g.split * o.kchunk;
+    const int kend = min(o.K, g.k0 + o.kchunk);
+    g.nchunks = max(1, (kend - g.k0 + kBK - 1) / kBK);
+    return g;
+}
+
+__device__ __forceinline__ bool op_failed(const GemmOp& o) { return o.failed != nullptr && *o.failed != 0; }
+
+// raw tile (rows x 32 fp32) -> hi/lo K-major SW128.  kmajor: raw is
+// [rows][32] (128-byte rows); else raw is [32][rows] (MN contiguous).
+// Shared-space addresses (u32) so every access is LDS/STS.
+__device__ __forceinline__ void split4(const float* x, uint32_t* hv, uint32_t* lv, bool split) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        hv[q] = to_tf32(x[q]);
+        lv[q] = split ? to_tf32(__fsub_rn(x[q], __uint_as_float(hv[q]))) : 0u;
+    }
+}
+__device__ __forceinline__ void convert_tile(uint32_t raw, uint32_t hi, uint32_t lo, int rows, bool kmajor,
+                                             bool split, int ct) {
+    const int items = rows * 8;  // (row, 16-byte chunk)
+    if (kmajor) {
+#pragma unroll 4
+        for (int i = ct; i < items; i += kConvThreads) {
+            const int r = i >> 3, c = i & 7;
+            const float4 x = lds128(raw + r * kRowBytes + c * 16);
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+            uint32_t hv[4], lv[4];
+            split4(xs, hv, lv, split);
+            const int off = sw128(r, c);
+            sts128(hi + off, hv[0], hv[1], hv[2], hv[3]);
+            if (split) sts128(lo + off, lv[0], lv[1], lv[2], lv[3]);
+        }
+    } else {
+#pragma unroll 4
+        for (int i = ct; i < items; i += kConvThreads) {
+            const int r = i % rows, c = i / rows;
+            float xs[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) xs[q] = lds32(raw + ((4 * c + q) * rows + r) * 4);
+            uint32_t hv[4], lv[4];
+            split4(xs, hv, lv, split);
+            const int off = sw128(r, c);
+            sts128(hi + off, hv[0], hv[1], hv[2], hv[3]);
+            if (split) sts128(lo + off, lv[0], lv[1], lv[2], lv[3]);
+        }
+    }
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+}  // namespace
+
+template <int BN>
+__global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total, int dbg) {
+    using C = Cfg<BN>;
+    constexpr int R = C::R, S = C::S, HB = BN / 2;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t raw_full[R], raw_empty[R], op_full[S], op_empty[S], acc_full[C::A], acc_empty[C::A];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ float red[8][32];
+    __shared__ int begins[kMaxOps];
+    __shared__ TileInfo tiles_sh[kMaxTiles];
+
+    const uint32_t sbase = smem_u32(smem_raw);
+    const uint32_t pad = (1024u - (sbase & 1023u)) & 1023u;
+    uint8_t* raw_ring = smem_raw + pad;  // stays a shared-space pointer
+    uint8_t* op_ring = raw_ring + R * C::raw_stage;
+    const uint32_t raw_s = sbase + pad, op_s = raw_s + R * C::raw_stage;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(C::tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < R; ++i) {
+            mbar_init(&raw_full[i], 1);
+            mbar_init(&raw_empty[i], kConvThreads / 32);
+        }
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&op_full[i], kConvThreads / 32 + 1);  // + the B warp's arrive
+            mbar_init(&op_empty[i], 1);
+        }
+        for (int i = 0; i < C::A; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // decode this CTA's tiles once (all threads in parallel: one global-load
+    // latency instead of a dependent chain per tile per role)
+    for (int i = tid; i < nd; i += kThreadsT) begins[i] = ops[i].cta_begin;
+    __syncthreads();
+    const int ntiles = static_cast<int>(blockIdx.x) < total ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+    for (int j = tid; j < ntiles; j += kThreadsT) {
+        const int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+        int lo = 0, hi = nd - 1;  // last op with begins[op] <= t
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (begins[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const GemmOp& o = ops[lo];
+        TileInfo ti;
+        ti.op = op_failed(o) ? -1 : lo;
+        ti.g = tile_geo<BN>(o, t - begins[lo]);
+        tiles_sh[j] = ti;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const int m0 = g.tm * kBM, n0 = g.tn * BN;
+            const bool conv = o.conv != 0, akm = o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            int img = 0, y0 = 0;
+            if (conv) {  // tiles cover whole output rows / images (gemm_tma_prepare)
+                const int hw = o.oh * o.ow;
+                img = m0 / hw;
+                y0 = (m0 - img * hw) / o.ow * o.cstride - o.cpad;
+            }
+            if (lane == 0) {
+                for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                    const int r = it % R;
+                    mbar_wait(&raw_empty[r], ((it / R) & 1) ^ 1);
+                    uint8_t* st = raw_ring + r * C::raw_stage;
+                    if (dbg & 8) {  // diagnosis: no loads
+                        mbar_arrive(&raw_full[r]);
+                        continue;
+                    }
+                    mbar_arrive_expect_tx(&raw_full[r], o.b_presplit ? C::a_raw : C::raw_stage);
+                    const int k = g.k0 + kc * kBK;
+                    if (conv) {  // implicit im2col: tap (ky,kx), channels c0..c0+31
+                        const int tap = k / o.ic, c0 = k - tap * o.ic;
+                        const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
+                        tma_load_4d(st, &o.map_a, &raw_full[r], c0, kx - o.cpad, y0 + ky, img);
+                    } else if (akm) {
+                        tma_load_2d(st, &o.map_a, &raw_full[r], k, m0);
+                    } else {
+                        tma_load_2d(st, &o.map_a, &raw_full[r], m0, k);
+                    }
+                    if (o.b_presplit) {
+                        // B goes straight to the operand ring (warp kBWarp)
+                    } else if (bkm) {
+                        tma_load_2d(st + C::a_raw, &o.map_b, &raw_full[r], k, n0);
+                    } else {
+                        tma_load_2d(st + C::a_raw, &o.map_b, &raw_full[r], n0, k);
+                    }
+                }
+            } else {
+                it += g.nchunks;
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer
+        // whole warp waits (warp-uniform values), one elected lane issues
+        const uint32_t idesc = instr_desc(BN);
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const int terms = o.tf32x3;
+            for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                const int s = it % S, a = it % C::A;
+                mbar_wait(&op_full[s], (it / S) & 1);
+                mbar_wait(&acc_empty[a], ((it / C::A) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t ah = op_s + s * C::op_stage, al = ah + C::a_op, bh = al + C::a_op, bl = bh + C::b_op;
+                if (elect_one()) {
+                    if (!(dbg & 2)) mma_chunk(tmem + a * BN, ah, al, bh, bl, idesc, terms);
+                    mma_commit(&op_empty[s]);
+                    mma_commit(&acc_full[a]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == kBWarp) {
+        // ------------------------------------------------------ B (pre-split)
+        // one arrive per chunk on op_full (with the B bytes when pre-split),
+        // after the stage is free
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const int n0 = g.tn * BN;
+            const bool pre = o.b_presplit != 0;
+            if (lane == 0) {
+                for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
+                    if (pre && !(dbg & 8)) {
+                        uint8_t* os = op_ring + s * C::op_stage + 2 * C::a_op;
+                        mbar_arrive_expect_tx(&op_full[s], 2 * C::b_op);
+                        const int k = g.k0 + kc * kBK;
+                        tma_load_2d(os, &o.map_bh, &op_full[s], k, n0);
+                        tma_load_2d(os + C::b_op, &o.map_bl, &op_full[s], k, n0);
+                    } else {
+                        mbar_arrive(&op_full[s]);
+                    }
+                }
+            } else {
+                it += g.nchunks;
+            }
+            __syncwarp();
+        }
+    } else if (warp < kEpiWarp0) {
+        // ------------------------------------------------------ converters
+        const int ct = tid - 64;
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const bool split3 = o.tf32x3 > 1;
+            const bool akm = o.conv != 0 || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                const int r = it % R, s = it % S;
+                mbar_wait(&raw_full[r], (it / R) & 1);
+                mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
+                const uint32_t rs = raw_s + r * C::raw_stage;
+                const uint32_t os = op_s + s * C::op_stage;
+                if (!(dbg & 1)) convert_tile(rs, os, os + C::a_op, kBM, akm, split3, ct);
+                if (!o.b_presplit && !(dbg & 1))
+                    convert_tile(rs + C::a_raw, os + 2 * C::a_op, os + 2 * C::a_op + C::b_op, BN, bkm, split3, ct);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&raw_empty[r]);
+                    mbar_arrive(&op_full[s]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------ drain + epilogue
+        const int q = warp & 3, h = (warp - kEpiWarp0) >> 2, et = tid - kEpiWarp0 * 32;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            float acc[HB];
+#pragma unroll
+            for (int j = 0; j < HB; ++j) acc[j] = 0.0f;
+            for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                const int a = it % C::A;
+                mbar_wait(&acc_full[a], (it / C::A) & 1);
+                tc_fence_after();
+                const uint32_t base = tmem + lane_off + a * BN + h * HB;
+                if (!(dbg & 4)) {
+#pragma unroll
+                    for (int c0 = 0; c0 < HB; c0 += 16) tmem_add16(base + c0, acc + c0);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[a]);
+            }
+            if (!(dbg & 4)) gemm_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, [] { named_bar(1, 256); });
+        }
+    }
+    (void)op_ring;
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::tmem_cols));
+    }
+}
+
+// ------------------------------------------------------------------- host
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        PBKD_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (p == nullptr || q != cudaDriverEntryPointSuccess)
+            throw CudaError("cuTensorMapEncodeTiled is not available from the driver");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// 2-D fp32 tensor [outer][ld] (inner extent `inner` <= ld), box {bi, bo}.
+bool encode(CUtensorMap* m, const float* base, long long inner, long long outer, long long ld, int bi, int bo,
+            CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE) {
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * 4) % 16 != 0 || inner < 1 || outer < 1) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(bi), static_cast<cuuint32_t>(bo)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 0;
+        PBKD_CUDA(cudaGetDevice(&dev));
+        PBKD_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        return std::max(1, v);
+    }();
+    return n;
+}
+
+template <int BN>
+void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::smem));
+        attr = true;
+    }
+    if (nd > kMaxOps) throw CudaError("umma_tma: too many ops in one launch");
+    const int grid = std::max({1, std::min(total, num_sms()), (total + kMaxTiles - 1) / kMaxTiles});
+    // PBKD_GEMM_DBG (diagnosis only, wrong results): 1 skip conversion,
+    // 2 skip MMAs, 4 skip drain/epilogue, 8 skip TMA loads
+    static const int dbg = [] {
+        const char* e = std::getenv("PBKD_GEMM_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    umma_tma_kernel<BN><<<grid, kThreadsT, Cfg<BN>::smem, st>>>(d, nd, total, dbg);
+    PBKD_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// Implicit-im2col A operand of a teacher conv as a 4-D map over the NHWC
+// input {C, W, H, N}, box = one tap's 32 channels at the 128 output pixels
+// of a tile, traversal stride = conv stride, out-of-image taps zero filled.
+// Needs C % 32 == 0 and tiles made of whole output rows (ow | 128 and
+// (128/ow) | oh) or whole images (oh*ow | 128).
+bool encode_conv(CUtensorMap* m, const GemmOp& o) {
+    if (o.ic % kBK != 0 || (reinterpret_cast<uintptr_t>(o.A) & 15) != 0) return false;
+    const int hw = o.oh * o.ow;
+    int bw = o.ow, bh, bimg;
+    if (hw >= kBM) {
+        if (kBM % o.ow != 0 || o.oh % (kBM / o.ow) != 0) return false;
+        bh = kBM / o.ow, bimg = 1;
+    } else {
+        if (kBM % hw != 0) return false;
+        bh = o.oh, bimg = kBM / hw;
+    }
+    const int s = o.cstride;
+    const long long nimg = o.M / hw;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(o.ic), static_cast<cuuint64_t>(o.iw),
+                                static_cast<cuuint64_t>(o.ih), static_cast<cuuint64_t>(nimg)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(o.ic) * 4, static_cast<cuuint64_t>(o.iw) * o.ic * 4,
+                                   static_cast<cuuint64_t>(o.ih) * o.iw * o.ic * 4};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(bw * s),
+                               static_cast<cuuint32_t>(bh * s), static_cast<cuuint32_t>(bimg)};
+    const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(s), static_cast<cuuint32_t>(s), 1};
+    if (box[1] > 256 || box[2] > 256 || box[3] > 256) return false;
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(o.A), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// Pre-split B (K-major tf32 hi/lo arrays): 128-byte swizzled boxes land in
+// the MMA's canonical K-major SWIZZLE_128B layout with no conversion pass.
+void presplit_maps(GemmOp& o) {
+    o.b_presplit = 0;
+    if (!o.b_hi || !o.b_lo || !o.b_kmajor || o.tf32x3 < 2) return;
+    if (encode(&o.map_bh, o.b_hi, o.K, o.N, o.ldb, kBK, o.bn, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        encode(&o.map_bl, o.b_lo, o.K, o.N, o.ldb, kBK, o.bn, CU_TENSOR_MAP_SWIZZLE_128B))
+        o.b_presplit = 1;
+}
+
+// TMA eligibility + tensor maps (called from gemm_finalize).
+bool gemm_tma_prepare(GemmOp& o) {
+    const int bn = o.bn;
+    if (o.conv) {
+        static const bool conv_on = [] {
+            const char* e = std::getenv("PBKD_CONV_TMA");
+            return !(e && e[0] == '0');
+        }();
+        if (!conv_on || o.ksplit != 1 || !o.b_kmajor) return false;
+        if (!(encode_conv(&o.map_a, o) && encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn))) return false;
+        presplit_maps(o);
+        return true;
+    }
+    bool ok = o.a_kmajor ? encode(&o.map_a, o.A, o.K, o.M, o.lda, kBK, kBM) : encode(&o.map_a, o.A, o.M, o.K, o.lda, kBM, kBK);
+    ok = ok && (o.b_kmajor ? encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn) : encode(&o.map_b, o.B, o.N, o.K, o.ldb, bn, kBK));
+    if (ok) presplit_maps(o);
+    return ok;
+}
+
+void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
+    auto rne = [](float v) {
+        uint32_t b;
+        std::memcpy(&b, &v, 4);
+        b = (b + 0xFFFu + ((b >> 13) & 1u)) & 0xFFFFE000u;
+        float r;
+        std::memcpy(&r, &b, 4);
+        return r;
+    };
+    for (size_t i = 0; i < n; ++i) {
+        const float h = rne(x[i]);
+        volatile float d = x[i] - h;  // exact (Sterbenz), no contraction
+        hi[i] = h;
+        lo[i] = rne(d);
+    }
+}
+
+void launch_gemm_tma(const GemmOp* d, int nd, int total, int bn, cudaStream_t st) {
+    switch (bn) {
+        case 32: launch_tma_t<32>(d, nd, total, st); break;
+        case 64: launch_tma_t<64>(d, nd, total, st); break;
+        default: launch_tma_t<128>(d, nd, total, st); break;
+    }
+}
+
+}  // namespace pbkd_gpu

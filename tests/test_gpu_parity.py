@@ -333,3 +333,24 @@ def test_task_validation(ctx, orc):
     for k in (0, 4):
         with pytest.raises(ValueError):
             ctx.run([P.make_task(k, epochs=1, batch_size=8)], tr, ev)
+
+
+def test_gemm_kernels_agree_bitwise(ctx, tmp_path):
+    """The TMA warp-specialised GEMM (umma_tma.cu) and the register-staged one
+    (umma.cu) issue the same MMA sequence per 32-wide K chunk and drain the
+    chunks in the same order, so every pointwise fwd / dgrad / wgrad output
+    (incl. ragged M/N/K, MN-major operands, split-K) and every teacher conv
+    (implicit im2col, stride 1/2, 1x1 projections) must agree bit for bit;
+    both are also checked against fp64 (rel 1e-5) inside gemm_dump.py."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for tma in ("0", "1"):
+        path = str(tmp_path / f"g{tma}.npz")
+        env = dict(os.environ, PBKD_GEMM_TMA=tma, PBKD_CONV_TMA=tma, PYTHONPATH=root)
+        subprocess.run([sys.executable, os.path.join(root, "tests", "gemm_dump.py"), path], env=env, check=True,
+                       timeout=300)
+        outs[tma] = np.load(path)
+    for k in outs["0"].files:
+        assert np.array_equal(outs["0"][k], outs["1"][k]), k
