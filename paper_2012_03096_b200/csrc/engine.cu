@@ -28,7 +28,6 @@ using pbkd::Tensor;
 
 namespace {
 
-constexpr int kScatterCtas = 148;
 
 // PBKD_TRACE=1: host wall time of each phase of run() on stderr (synchronises
 // the stream at every mark, so only for diagnosis).
@@ -621,7 +620,10 @@ struct Engine::Impl {
         s.cs0.alloc(static_cast<size_t>(tiles) * cout * sizeof(float));
         s.cs1.alloc(static_cast<size_t>(tiles) * cout * sizeof(float));
         int pc = 1;
-        for (int u = 0; u < s.units; ++u) pc = std::max(pc, rows_part_ctas(M, s.u[u].cin));
+        for (int u = 0; u < s.units; ++u) {
+            pc = std::max(pc, rows_part_ctas(M, s.u[u].cin));
+            pc = std::max(pc, dw_tile(B, s.u[u].ho, s.u[u].wo, s.u[u].cin, s.u[u].stride, 2).tiles);
+        }
         pc = std::max(pc, rows_part_ctas(M, cout));
         s.psg.alloc(static_cast<size_t>(pc) * cout * sizeof(float));
         s.psgx.alloc(static_cast<size_t>(pc) * cout * sizeof(float));
@@ -700,6 +702,7 @@ struct Engine::Impl {
                     o.pd = s.w_b(u - 1);
                 }
                 o.failed = c.failed;
+                dw_fwd_finalize(o);
                 dws.push_back(o);
                 GemmOp g{};
                 g.M = static_cast<int>(c.M);
@@ -870,9 +873,8 @@ struct Engine::Impl {
                     b.h = d.hin;
                     b.wd = d.win;
                     b.c = d.cin;
-                    b.ctas = rows_part_ctas(c.M, d.cin);
-                    b.rows_per = rows_part_per(c.M, b.ctas);
                     b.failed = c.failed;
+                    dw_bwd_finalize(b);
                     dbs.push_back(b);
                     ReduceOp kk{};
                     kk.part = s.pgk.f();
@@ -905,9 +907,8 @@ struct Engine::Impl {
                     b.wo = d.wo;
                     b.stride = d.stride;
                     b.pad = 1;
-                    b.ctas = rows_part_ctas(c.M, d.cin);
-                    b.rows_per = rows_part_per(c.M, b.ctas);
                     b.failed = c.failed;
+                    dw_gk_finalize(b);
                     gks.push_back(b);
                     ReduceOp kk{};
                     kk.part = s.pgk.f();
@@ -918,17 +919,17 @@ struct Engine::Impl {
                     kr.push_back(kk);
                 }
             }
-            auto red_ctas = [](const ReduceOp& o) { return ceil_div(o.width, kThreads); };
+            auto red_ctas = ctas_reduce;
             P.grouped<BnBwdApplyOp>(launch_bn_bwd_apply, aps, [](const BnBwdApplyOp& o) { return ctas_elem(o.total); });
             P.gemm(dg);
             P.gemm(wg);
             P.grouped<ReduceOp>(launch_reduce, wr, red_ctas);
             if (u > 0) {
-                P.grouped<DwBwdOp>(launch_dw_bwd, dbs, [](const DwBwdOp& o) { return o.ctas; });
+                P.grouped<DwBwdOp>(launch_dw_bwd, dbs, ctas_dw_bwd);
                 P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
                 P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fins, [](const BnBwdFinOp& o) { return ctas_cols(o.c); });
             } else {
-                P.grouped<DwGkOp>(launch_dw_gk, gks, [](const DwGkOp& o) { return o.ctas; });
+                P.grouped<DwGkOp>(launch_dw_gk, gks, ctas_dw_gk);
                 P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
             }
         }
@@ -1015,6 +1016,7 @@ struct Engine::Impl {
                 o.pa = s.scale_u(u - 1);
                 o.pb = s.shift_u(u - 1);
             }
+            dw_fwd_finalize(o);
             P.grouped<DwFwdOp>(launch_dw_fwd, {o}, ctas_dw_fwd);
             GemmOp gm{};
             gm.M = static_cast<int>(M);
@@ -1592,6 +1594,7 @@ void Engine::bench_kernel(int which, int batch, int iters, double* ms, double* b
         DwFwdOp o{};
         o.x = x.f(), o.w = w.f(), o.y = y.f(), o.n = n, o.h = ho, o.wd = wo, o.c = c, o.ho = ho, o.wo = wo;
         o.stride = 1, o.pad = 1, o.pro = 1, o.pa = v.f(), o.pb = v.f(), o.pc = v.f(), o.pd = v.f();
+        dw_fwd_finalize(o);
         P.grouped<DwFwdOp>(launch_dw_fwd, {o}, ctas_dw_fwd);
         fl = 18.0 * M * c;
         by = 4.0 * (2.0 * M * c + 9.0 * c);
@@ -1600,9 +1603,9 @@ void Engine::bench_kernel(int which, int batch, int iters, double* ms, double* b
         o.gy = x.f(), o.xp = z.f(), o.w = w.f(), o.gyprev = y.f();
         o.mean = v.f(), o.inv = v.f(), o.gamma = v.f(), o.beta = v.f();
         o.n = n, o.h = ho, o.wd = wo, o.c = c;
-        o.ctas = rows_part_ctas(M, c), o.rows_per = rows_part_per(M, o.ctas);
+        dw_bwd_finalize(o);
         o.part_gk = parts.f(), o.part_sg = parts.f(), o.part_sgx = parts.f();
-        P.grouped<DwBwdOp>(launch_dw_bwd, {o}, [](const DwBwdOp& q) { return q.ctas; });
+        P.grouped<DwBwdOp>(launch_dw_bwd, {o}, ctas_dw_bwd);
         fl = 36.0 * M * c;
         by = 4.0 * (3.0 * M * c + 9.0 * c);
     } else {

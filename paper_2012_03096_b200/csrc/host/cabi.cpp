@@ -626,6 +626,7 @@ int pbkd_k_dw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int n
         o.wo = (wd + 2 * pad - 3) / stride + 1;
         o.stride = stride;
         o.pad = pad;
+        dw_fwd_finalize(o);
         launch_one(ctx->eng->stream(), launch_dw_fwd, o, ctas_dw_fwd(o));
     });
 }
@@ -649,22 +650,21 @@ int pbkd_k_dw_bwd(pbkd_ctx* ctx, const float* gy, const float* p, const float* w
         o.h = h;
         o.wd = wd;
         o.c = c;
-        o.ctas = rows_part_ctas(rows, c);
-        o.rows_per = rows_part_per(rows, o.ctas);
+        dw_bwd_finalize(o);
         Scratch pgk(static_cast<size_t>(o.ctas) * 9 * c), psg(static_cast<size_t>(o.ctas) * c),
             psgx(static_cast<size_t>(o.ctas) * c);
         o.part_gk = pgk.p;
         o.part_sg = psg.p;
         o.part_sgx = psgx.p;
         cudaStream_t st = ctx->eng->stream();
-        launch_one(st, launch_dw_bwd, o, o.ctas);
+        launch_one(st, launch_dw_bwd, o, ctas_dw_bwd(o));
         ReduceOp r{};
         r.part = pgk.p, r.out = gk, r.parts = o.ctas, r.width = 9 * c;
-        launch_one(st, launch_reduce, r, ceil_div(r.width, kThreads));
+        launch_one(st, launch_reduce, r, ctas_reduce(r));
         r.part = psg.p, r.out = sg, r.width = c;
-        launch_one(st, launch_reduce, r, ceil_div(c, kThreads));
+        launch_one(st, launch_reduce, r, ctas_reduce(r));
         r.part = psgx.p, r.out = sgx;
-        launch_one(st, launch_reduce, r, ceil_div(c, kThreads));
+        launch_one(st, launch_reduce, r, ctas_reduce(r));
     });
 }
 
@@ -684,15 +684,14 @@ int pbkd_k_dw_gk(pbkd_ctx* ctx, const float* gy, const float* x, float* gk, int 
         o.stride = stride;
         o.pad = pad;
         const long long rows = static_cast<long long>(n) * o.ho * o.wo;
-        o.ctas = rows_part_ctas(rows, c);
-        o.rows_per = rows_part_per(rows, o.ctas);
+        dw_gk_finalize(o);
         Scratch pgk(static_cast<size_t>(o.ctas) * 9 * c);
         o.part_gk = pgk.p;
         cudaStream_t st = ctx->eng->stream();
-        launch_one(st, launch_dw_gk, o, o.ctas);
+        launch_one(st, launch_dw_gk, o, ctas_dw_gk(o));
         ReduceOp r{};
         r.part = pgk.p, r.out = gk, r.parts = o.ctas, r.width = 9 * c;
-        launch_one(st, launch_reduce, r, ceil_div(r.width, kThreads));
+        launch_one(st, launch_reduce, r, ctas_reduce(r));
     });
 }
 
@@ -715,11 +714,11 @@ int pbkd_k_pw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int r
             r.parts = g.tiles_m, r.width = cout;
             if (col_sum) {
                 r.part = p0.p, r.out = col_sum;
-                launch_one(st, launch_reduce, r, ceil_div(cout, kThreads));
+                launch_one(st, launch_reduce, r, ctas_reduce(r));
             }
             if (col_sq) {
                 r.part = p1.p, r.out = col_sq;
-                launch_one(st, launch_reduce, r, ceil_div(cout, kThreads));
+                launch_one(st, launch_reduce, r, ctas_reduce(r));
             }
         } else {
             launch_gemm_one(st, g);
@@ -755,7 +754,7 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             launch_gemm_one(st, g);
             ReduceOp r{};
             r.part = part.p, r.out = gw, r.parts = g.ksplit, r.width = cout * cin;
-            launch_one(st, launch_reduce, r, ceil_div(r.width, kThreads));
+            launch_one(st, launch_reduce, r, ctas_reduce(r));
         }
     });
 }

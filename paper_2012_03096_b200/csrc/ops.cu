@@ -76,218 +76,348 @@ __device__ void cta_reduce_rows(float* red, const float* v, const Geo& g, int rr
     __syncthreads();
 }
 
-// ---------------------------------------------------------- depthwise fwd
-int ctas_dw_fwd(const DwFwdOp& o) {
-    const int V = (o.c % 4 == 0) ? 4 : 1;
-    return std::max(1, ceil_div(static_cast<long long>(o.n) * o.ho * o.wo * (o.c / V), kThreads));
+// ------------------------------------------------------- depthwise tiling
+// A CTA stages ni images x tr rows x tw cols x 32 channels of its input(s) in
+// shared memory ([pixel][32], zero halo), then thread (channel = tid % 32,
+// pixel lane = tid / 32) walks the tile's output pixels.  Warps read 32
+// consecutive words (conflict-free); global loads/stores are 128-byte rows.
+constexpr int kDwC = 32;             // channels per CTA
+constexpr int kDwLanes = kThreads / kDwC;
+constexpr int kDwTileBytes = 48 * 1024;  // per staged array
+
+DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays) {
+    DwTile t{};
+    const int target = 256;  // output pixels per CTA
+    if (ho * wo >= target) {
+        t.ni = 1;
+        t.th = std::max(1, std::min(ho, target / wo));
+    } else {
+        t.th = ho;
+        t.ni = std::max(1, std::min(n, target / (ho * wo)));
+    }
+    auto fp = [&](const DwTile& q) {
+        return static_cast<long long>(q.ni) * ((q.th - 1) * stride + 3) * ((wo - 1) * stride + 3) * kDwC * 4;
+    };
+    while (fp(t) > kDwTileBytes / std::max(1, arrays - 1) && (t.ni > 1 || t.th > 1)) {
+        if (t.ni > 1) t.ni = (t.ni + 1) / 2;
+        else t.th = (t.th + 1) / 2;
+    }
+    t.tr = (t.th - 1) * stride + 3;
+    t.tw = (wo - 1) * stride + 3;
+    t.tiles_y = ceil_div(ho, t.th);
+    t.tiles = ceil_div(n, t.ni) * t.tiles_y;
+    t.cslices = ceil_div(c, kDwC);
+    return t;
+}
+static size_t dw_smem(const DwTile& t) { return static_cast<size_t>(t.ni) * t.tr * t.tw * kDwC * sizeof(float); }
+
+void dw_fwd_finalize(DwFwdOp& o) { o.tile = dw_tile(o.n, o.ho, o.wo, o.c, o.stride, 1); }
+void dw_bwd_finalize(DwBwdOp& o) {
+    o.tile = dw_tile(o.n, o.h, o.wd, o.c, 1, 2);
+    o.ctas = o.tile.tiles;
+    o.rows_per = 0;
+}
+void dw_gk_finalize(DwGkOp& o) {
+    o.tile = dw_tile(o.n, o.ho, o.wo, o.c, o.stride, 2);
+    o.ctas = o.tile.tiles;
+    o.rows_per = 0;
+}
+int ctas_dw_fwd(const DwFwdOp& o) { return o.tile.tiles * o.tile.cslices; }
+int ctas_dw_bwd(const DwBwdOp& o) { return o.tile.tiles * o.tile.cslices; }
+int ctas_dw_gk(const DwGkOp& o) { return o.tile.tiles * o.tile.cslices; }
+
+// Stage a [ni][tr][tw][32] tile of an NHWC tensor (n, h, w, c), origin
+// (n0, iy0, ix0, c0) with cp.async (all loads in flight at once; zero fill
+// for out-of-range pixels / channels, the reference's padding).  16-byte
+// copies when the 32-channel slice is whole and aligned, else 4-byte.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
+// Staged rows: R = i*tr + rr (image i of the tile, input row rr); a warp
+// takes whole rows, lanes walk the row's 16-byte chunks (col*8 + q), so the
+// only index math per chunk is a shift and a mask.
+__device__ __forceinline__ void dw_stage(float* dst, const float* __restrict__ src, const DwTile& t, int n, int h,
+                                         int w, int c, int n0, int iy0, int ix0, int c0) {
+    const uint32_t sd = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows = t.ni * t.tr;
+    const bool vec = (c % 4 == 0) && (c0 + kDwC <= c);
+    for (int R = warp; R < rows; R += kThreads / 32) {
+        const int i = R / t.tr, rr = R - i * t.tr;
+        const int nn = n0 + i, iy = iy0 + rr;
+        const bool row_in = nn < n && iy >= 0 && iy < h;
+        const float* rowp = src + (static_cast<long long>(nn) * h + iy) * w * c;
+        const uint32_t drow = sd + R * t.tw * kDwC * 4;
+        if (vec) {
+            for (int it = lane; it < t.tw * 8; it += 32) {
+                const int col = it >> 3, q = it & 7, ix = ix0 + col;
+                const bool in = row_in && ix >= 0 && ix < w;
+                cp_async16(drow + it * 16, in ? rowp + static_cast<long long>(ix) * c + c0 + q * 4 : src, in ? 16 : 0);
+            }
+        } else {
+            const bool cin = c0 + lane < c;
+            for (int col = 0; col < t.tw; ++col) {
+                const int ix = ix0 + col;
+                const bool in = row_in && cin && ix >= 0 && ix < w;
+                cp_async4(drow + (col * kDwC + lane) * 4, in ? rowp + static_cast<long long>(ix) * c + c0 + lane : src,
+                          in ? 4 : 0);
+            }
+        }
+    }
+    cp_async_wait_all();
+}
+
+// In-place prologue f on the staged in-range pixels (padding stays 0); the
+// caller synchronises before and after.  Warp = staged row, lane = channel.
+template <class F>
+__device__ __forceinline__ void dw_map(float* buf, const DwTile& t, int n, int h, int w, int n0, int iy0, int ix0,
+                                       F f) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int R = warp; R < t.ni * t.tr; R += kThreads / 32) {
+        const int i = R / t.tr, rr = R - i * t.tr;
+        const int iy = iy0 + rr;
+        if (n0 + i >= n || iy < 0 || iy >= h) continue;
+        float* row = buf + R * t.tw * kDwC + lane;
+        const int cb = max(0, -ix0), ce = min(t.tw, w - ix0);
+        for (int col = cb; col < ce; ++col) row[col * kDwC] = f(row[col * kDwC]);
+    }
+}
+
+struct DwPos {
+    int n0, y0, c0, tile;
+};
+__device__ __forceinline__ DwPos dw_pos(const DwTile& t, int local) {
+    DwPos q;
+    const int cs = local % t.cslices;
+    q.tile = local / t.cslices;
+    q.n0 = (q.tile / t.tiles_y) * t.ni;
+    q.y0 = (q.tile % t.tiles_y) * t.th;
+    q.c0 = cs * kDwC;
+    return q;
+}
+
+// ---------------------------------------------------------- depthwise fwd
+// Warp = output row (image i, row oy) of the tile, lane = channel.
 __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restrict__ ops, int nd) {
+    extern __shared__ float xs[];
     int local;
     const DwFwdOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
-    const int V = (o.c % 4 == 0) ? 4 : 1;
-    const int G = o.c / V;
-    const long long idx = static_cast<long long>(local) * kThreads + threadIdx.x;
-    const long long total = static_cast<long long>(o.n) * o.ho * o.wo * G;
-    if (idx >= total) return;
-    const int g = static_cast<int>(idx % G);
-    const long long r = idx / G;
-    const int ox = static_cast<int>(r % o.wo);
-    const int oy = static_cast<int>((r / o.wo) % o.ho);
-    const int n = static_cast<int>(r / (static_cast<long long>(o.wo) * o.ho));
-    const int c0 = g * V;
-    float pa[4], pb[4], pc[4], pd[4];
-    if (o.pro != 0) {
-        load_v(o.pa + c0, V, pa);
-        load_v(o.pb + c0, V, pb);
-        if (o.pro == 1) {
-            load_v(o.pc + c0, V, pc);
-            load_v(o.pd + c0, V, pd);
+    const DwTile t = o.tile;
+    const DwPos q = dw_pos(t, local);
+    const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5, c = q.c0 + ch;
+    const bool cok = c < o.c;
+    float pa = 0, pb = 0, pc = 0, pd = 0;
+    if (o.pro != 0 && cok) {
+        pa = o.pa[c], pb = o.pb[c];
+        if (o.pro == 1) pc = o.pc[c], pd = o.pd[c];
+    }
+    const int pro = o.pro;
+    const int iy0 = q.y0 * o.stride - o.pad;
+    float wk[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wk[k] = cok ? o.w[k * o.c + c] : 0.0f;
+    dw_stage(xs, o.x, t, o.n, o.h, o.wd, o.c, q.n0, iy0, -o.pad, q.c0);
+    __syncthreads();
+    if (pro == 1) {
+        dw_map(xs, t, o.n, o.h, o.wd, q.n0, iy0, -o.pad, [&](float v) { return relu(bn_train_apply(v, pa, pb, pc, pd)); });
+        __syncthreads();
+    } else if (pro == 2) {
+        dw_map(xs, t, o.n, o.h, o.wd, q.n0, iy0, -o.pad, [&](float v) { return relu(bn_infer_apply(v, pa, pb)); });
+        __syncthreads();
+    }
+    if (!cok) return;
+    const int s = o.stride;
+    for (int R = warp; R < t.ni * t.th; R += kThreads / 32) {
+        const int i = R / t.th, oy = R - i * t.th;
+        const int nn = q.n0 + i, yy = q.y0 + oy;
+        if (nn >= o.n || yy >= o.ho) continue;
+        const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
+        float* out = o.y + ((static_cast<long long>(nn) * o.ho + yy) * o.wo) * o.c + c;
+#pragma unroll 2
+        for (int ox = 0; ox < o.wo; ++ox) {
+            const float* b = base + ox * s * kDwC;
+            float acc = 0.0f;  // 9-term serial sum in (ky, kx) order (ops.hpp:131-140)
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                for (int kx = 0; kx < 3; ++kx) acc = add(acc, mul(b[(ky * t.tw + kx) * kDwC], wk[ky * 3 + kx]));
+            out[static_cast<long long>(ox) * o.c] = acc;
         }
     }
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    for (int ky = 0; ky < 3; ++ky) {
-        const int iy = oy * o.stride - o.pad + ky;
-        if (iy < 0 || iy >= o.h) continue;
-        for (int kx = 0; kx < 3; ++kx) {
-            const int ix = ox * o.stride - o.pad + kx;
-            if (ix < 0 || ix >= o.wd) continue;
-            float xv[4], wv[4];
-            load_v(o.x + ((static_cast<long long>(n) * o.h + iy) * o.wd + ix) * o.c + c0, V, xv);
-            load_v(o.w + (ky * 3 + kx) * o.c + c0, V, wv);
-            for (int q = 0; q < V; ++q) {
-                float v = xv[q];
-                if (o.pro == 1) v = relu(bn_train_apply(v, pa[q], pb[q], pc[q], pd[q]));
-                else if (o.pro == 2) v = relu(bn_infer_apply(v, pa[q], pb[q]));
-                acc[q] = add(acc[q], mul(v, wv[q]));
-            }
-        }
-    }
-    store_v(o.y + r * o.c + c0, V, acc);
 }
 
 void launch_dw_fwd(const DwFwdOp* d, int nd, int ctas, cudaStream_t st) {
-    dw_fwd_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    dw_fwd_kernel<<<ctas, kThreads, kDwTileBytes, st>>>(d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
+// CTA-level fixed-order sum of per-thread values v[k] (k < nv) over the 8
+// pixel lanes; thread ch of the result gets out[k] for its channel.
+template <int NV>
+__device__ __forceinline__ void dw_lane_sum(float* red, const float* v, float* out) {
+    const int ch = threadIdx.x % kDwC, lane = threadIdx.x / kDwC;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[(lane * NV + k) * kDwC + ch] = v[k];
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            float acc = 0.0f;
+            for (int l = 0; l < kDwLanes; ++l) acc += red[(l * NV + k) * kDwC + ch];
+            out[k] = acc;
+        }
+    }
+}
+
 // ------------------------------------------- depthwise bwd (unit > 0, s=1)
+// gy (dw output gradient) and the previous unit's activation relu(bn(p)) are
+// staged with halos; per pixel: the input gradient gathered in ascending
+// (oy, ox) order with zero terms skipped (ops.hpp:156-174), the weight-
+// gradient terms, the previous ReLU mask and batch-norm partial sums.
 __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restrict__ ops, int nd) {
-    extern __shared__ float red[];
+    extern __shared__ float sm[];
     int local;
     const DwBwdOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
-    const Geo g = geo_of(o.c);
-    const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
-    const bool lane_ok = rr < g.RP;
-    const long long rows = static_cast<long long>(o.n) * o.h * o.wd;
-    const long long r0 = static_cast<long long>(local) * o.rows_per;
-    const long long r1 = min(rows, r0 + o.rows_per);
-    const int c0 = gg * g.V;
-    float mean[4], inv[4], gam[4], bet[4], wk[9][4];
-    float gk[9][4], sg[4], sgx[4];
-    if (lane_ok) {
-        load_v(o.mean + c0, g.V, mean);
-        load_v(o.inv + c0, g.V, inv);
-        load_v(o.gamma + c0, g.V, gam);
-        load_v(o.beta + c0, g.V, bet);
-        for (int t = 0; t < 9; ++t) load_v(o.w + t * o.c + c0, g.V, wk[t]);
-    }
-    for (int t = 0; t < 9; ++t)
-        for (int q = 0; q < 4; ++q) gk[t][q] = 0.0f;
-    for (int q = 0; q < 4; ++q) sg[q] = sgx[q] = 0.0f;
-    if (lane_ok) {
-        for (long long r = r0 + rr; r < r1; r += g.RP) {
-            const int x = static_cast<int>(r % o.wd);
-            const int y = static_cast<int>((r / o.wd) % o.h);
-            const long long nbase = (r / (static_cast<long long>(o.wd) * o.h)) * o.h;
-            // (a) input gradient: outputs touching (y,x) in ascending (oy,ox)
-            //     order, tap (1-dy, 1-dx) (ops.hpp:156-174, skip g == 0)
-            float gx[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-            float gyc[4];
-            load_v(o.gy + r * o.c + c0, g.V, gyc);
-            for (int dy = -1; dy <= 1; ++dy) {
-                const int oy = y + dy;
-                if (oy < 0 || oy >= o.h) continue;
-                for (int dx = -1; dx <= 1; ++dx) {
-                    const int ox = x + dx;
-                    if (ox < 0 || ox >= o.wd) continue;
-                    float gv[4];
-                    load_v(o.gy + ((nbase + oy) * o.wd + ox) * o.c + c0, g.V, gv);
-                    const int tap = (1 - dy) * 3 + (1 - dx);
-                    for (int q = 0; q < g.V; ++q)
-                        if (gv[q] != 0.0f) gx[q] = add(gx[q], mul(gv[q], wk[tap][q]));
-                }
-            }
-            // (b) weight-gradient partials: this output times its 9 inputs,
-            //     inputs rebuilt as relu(bn(p_prev))
-            for (int ky = 0; ky < 3; ++ky) {
-                const int iy = y - 1 + ky;
-                if (iy < 0 || iy >= o.h) continue;
-                for (int kx = 0; kx < 3; ++kx) {
-                    const int ix = x - 1 + kx;
-                    if (ix < 0 || ix >= o.wd) continue;
-                    float pv[4];
-                    load_v(o.xp + ((nbase + iy) * o.wd + ix) * o.c + c0, g.V, pv);
-                    for (int q = 0; q < g.V; ++q) {
-                        const float xin = relu(bn_train_apply(pv[q], mean[q], inv[q], gam[q], bet[q]));
-                        if (gyc[q] != 0.0f) gk[ky * 3 + kx][q] += gyc[q] * xin;
+    const DwTile t = o.tile;
+    const DwPos q = dw_pos(t, local);
+    const int ch = threadIdx.x % kDwC, c = q.c0 + ch;
+    const bool cok = c < o.c;
+    float mean = 0, inv = 0, gam = 0, bet = 0;
+    if (cok) mean = o.mean[c], inv = o.inv[c], gam = o.gamma[c], bet = o.beta[c];
+    float* gs = sm;
+    float* xs = sm + static_cast<size_t>(t.ni) * t.tr * t.tw * kDwC;
+    float wk[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wk[k] = cok ? o.w[k * o.c + c] : 0.0f;
+    dw_stage(gs, o.gy, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 - 1, -1, q.c0);
+    dw_stage(xs, o.xp, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 - 1, -1, q.c0);
+    __syncthreads();
+    // xs keeps the raw pre-BN p for the centre (xhat, mask); the relu(bn(p))
+    // view the weight gradient needs is formed per tap below
+
+    float acc[11];  // gk[9], sg, sgx
+#pragma unroll
+    for (int k = 0; k < 11; ++k) acc[k] = 0.0f;
+    if (cok) {
+        const int warp = threadIdx.x >> 5;
+        for (int R = warp; R < t.ni * t.th; R += kThreads / 32) {
+            const int i = R / t.th, y = R - i * t.th;
+            const int nn = q.n0 + i, yy = q.y0 + y;
+            if (nn >= o.n || yy >= o.h) continue;
+            const long long grow = ((static_cast<long long>(nn) * o.h + yy) * o.wd) * o.c + c;
+            for (int x = 0; x < o.wd; ++x) {
+                const int ctr = ((i * t.tr + y + 1) * t.tw + x + 1) * kDwC + ch;
+                float gx = 0.0f;
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const float gv = gs[ctr + (dy * t.tw + dx) * kDwC];
+                        if (gv != 0.0f) gx = add(gx, mul(gv, wk[(1 - dy) * 3 + (1 - dx)]));
+                    }
+                const float gyc = gs[ctr];
+                if (gyc != 0.0f) {
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) {
+                        const int iy = yy + ky - 1;
+#pragma unroll
+                        for (int kx = 0; kx < 3; ++kx) {
+                            const int ix = x + kx - 1;
+                            if (iy < 0 || iy >= o.h || ix < 0 || ix >= o.wd) continue;  // padded input is 0
+                            const float xin =
+                                relu(bn_train_apply(xs[ctr + ((ky - 1) * t.tw + kx - 1) * kDwC], mean, inv, gam, bet));
+                            acc[ky * 3 + kx] += gyc * xin;
+                        }
                     }
                 }
+                const float xh = mul(sub(xs[ctr], mean), inv);
+                const float yv = add(mul(gam, xh), bet);
+                const float gm = yv > 0.0f ? add(0.0f, gx) : 0.0f;
+                o.gyprev[grow + static_cast<long long>(x) * o.c] = gm;
+                acc[9] += gm;
+                acc[10] += gm * xh;
             }
-            // (c) previous unit's ReLU mask and batch-norm partial sums
-            float pc[4], outv[4];
-            load_v(o.xp + r * o.c + c0, g.V, pc);
-            for (int q = 0; q < g.V; ++q) {
-                const float xh = mul(sub(pc[q], mean[q]), inv[q]);
-                const float yv = add(mul(gam[q], xh), bet[q]);
-                const float gm = yv > 0.0f ? add(0.0f, gx[q]) : 0.0f;
-                outv[q] = gm;
-                sg[q] += gm;
-                sgx[q] += gm * xh;
-            }
-            store_v(o.gyprev + r * o.c + c0, g.V, outv);
         }
     }
-    for (int t = 0; t < 9; ++t)
-        cta_reduce_rows(red, gk[t], g, rr, gg, lane_ok, o.c,
-                        o.part_gk + (static_cast<long long>(local) * 9 + t) * o.c);
-    cta_reduce_rows(red, sg, g, rr, gg, lane_ok, o.c, o.part_sg + static_cast<long long>(local) * o.c);
-    cta_reduce_rows(red, sgx, g, rr, gg, lane_ok, o.c, o.part_sgx + static_cast<long long>(local) * o.c);
+    __syncthreads();  // staging buffers are reused for the reduction
+    float out[11];
+    dw_lane_sum<11>(sm, acc, out);
+    if (threadIdx.x < kDwC && cok) {
+        for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * o.c + c] = out[k];
+        o.part_sg[static_cast<long long>(q.tile) * o.c + c] = out[9];
+        o.part_sgx[static_cast<long long>(q.tile) * o.c + c] = out[10];
+    }
 }
 
-static size_t red_smem(int cmax) { return static_cast<size_t>(kThreads) * 4 * sizeof(float) + cmax * 0; }
-
 void launch_dw_bwd(const DwBwdOp* d, int nd, int ctas, cudaStream_t st) {
-    // RP*c <= kThreads*V <= 1024 floats
-    dw_bwd_kernel<<<ctas, kThreads, red_smem(0), st>>>(d, nd);
+    static bool attr = false;
+    if (!attr) {
+        PBKD_CUDA(cudaFuncSetAttribute(dw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDwTileBytes));
+        attr = true;
+    }
+    dw_bwd_kernel<<<ctas, kThreads, 2 * kDwTileBytes, st>>>(d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
 // ------------------------------------------- depthwise weight grad (unit 0)
+// model.cpp:570 skips the input gradient of the block's first layer.
 __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restrict__ ops, int nd) {
-    extern __shared__ float red[];
+    extern __shared__ float sm[];
     int local;
     const DwGkOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
-    const Geo g = geo_of(o.c);
-    const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
-    const bool lane_ok = rr < g.RP;
-    const long long rows = static_cast<long long>(o.n) * o.ho * o.wo;
-    const long long r0 = static_cast<long long>(local) * o.rows_per;
-    const long long r1 = min(rows, r0 + o.rows_per);
-    const int c0 = gg * g.V;
-    float gk[9][4];
-    for (int t = 0; t < 9; ++t)
-        for (int q = 0; q < 4; ++q) gk[t][q] = 0.0f;
-    if (lane_ok) {
-        for (long long r = r0 + rr; r < r1; r += g.RP) {
-            const int ox = static_cast<int>(r % o.wo);
-            const int oy = static_cast<int>((r / o.wo) % o.ho);
-            const long long n = r / (static_cast<long long>(o.wo) * o.ho);
-            float gv[4];
-            load_v(o.gy + r * o.c + c0, g.V, gv);
-            for (int ky = 0; ky < 3; ++ky) {
-                const int iy = oy * o.stride - o.pad + ky;
-                if (iy < 0 || iy >= o.h) continue;
-                for (int kx = 0; kx < 3; ++kx) {
-                    const int ix = ox * o.stride - o.pad + kx;
-                    if (ix < 0 || ix >= o.wd) continue;
-                    float xv[4];
-                    load_v(o.x + ((n * o.h + iy) * o.wd + ix) * o.c + c0, g.V, xv);
-                    for (int q = 0; q < g.V; ++q)
-                        if (gv[q] != 0.0f) gk[ky * 3 + kx][q] += gv[q] * xv[q];
-                }
+    const DwTile t = o.tile;
+    const DwPos q = dw_pos(t, local);
+    const int ch = threadIdx.x % kDwC, c = q.c0 + ch;
+    const bool cok = c < o.c;
+    float* xs = sm;
+    dw_stage(xs, o.x, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 * o.stride - o.pad, -o.pad, q.c0);
+    __syncthreads();
+    float acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = 0.0f;
+    if (cok) {
+        const int s = o.stride, warp = threadIdx.x >> 5;
+        for (int R = warp; R < t.ni * t.th; R += kThreads / 32) {
+            const int i = R / t.th, oy = R - i * t.th;
+            const int nn = q.n0 + i, yy = q.y0 + oy;
+            if (nn >= o.n || yy >= o.ho) continue;
+            const float* gyr = o.gy + ((static_cast<long long>(nn) * o.ho + yy) * o.wo) * o.c + c;
+            const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
+#pragma unroll 2
+            for (int ox = 0; ox < o.wo; ++ox) {
+                const float gv = __ldg(gyr + static_cast<long long>(ox) * o.c);
+                if (gv == 0.0f) continue;
+                const float* b = base + ox * s * kDwC;
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                    for (int kx = 0; kx < 3; ++kx) acc[ky * 3 + kx] += gv * b[(ky * t.tw + kx) * kDwC];
             }
         }
     }
-    for (int t = 0; t < 9; ++t)
-        cta_reduce_rows(red, gk[t], g, rr, gg, lane_ok, o.c,
-                        o.part_gk + (static_cast<long long>(local) * 9 + t) * o.c);
+    __syncthreads();
+    float out[9];
+    dw_lane_sum<9>(sm, acc, out);
+    if (threadIdx.x < kDwC && cok)
+        for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * o.c + c] = out[k];
 }
 
 void launch_dw_gk(const DwGkOp* d, int nd, int ctas, cudaStream_t st) {
-    dw_gk_kernel<<<ctas, kThreads, red_smem(0), st>>>(d, nd);
+    dw_gk_kernel<<<ctas, kThreads, kDwTileBytes, st>>>(d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
-// --------------------------------------------------------- fixed-order sums
-__global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __restrict__ ops, int nd) {
-    int local;
-    const ReduceOp& o = op_of(ops, nd, local);
-    if (is_failed(o.failed)) return;
-    const int i = local * kThreads + threadIdx.x;
-    if (i >= o.width) return;
-    float s = 0.0f;
-    for (int p = 0; p < o.parts; ++p) s += o.part[static_cast<long long>(p) * o.width + i];
-    o.out[i] = s;
-}
-
-void launch_reduce(const ReduceOp* d, int nd, int ctas, cudaStream_t st) {
-    reduce_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
-    PBKD_LAUNCH_CHECK();
-}
+static size_t red_smem(int) { return static_cast<size_t>(kThreads) * 4 * sizeof(float); }
 
 // ------------------------------------------------------------ BN statistics
 // Column sums of [parts][c] partials: a CTA owns 32 channels, 8 lanes stride
@@ -303,8 +433,8 @@ __device__ __forceinline__ float col_sum(const float* __restrict__ part, int par
         int p = lane;
         for (; p + 3 * kColLanes < parts; p += 4 * kColLanes)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] += part[static_cast<long long>(p + u * kColLanes) * c + ch];
-        for (; p < parts; p += kColLanes) acc[0] += part[static_cast<long long>(p) * c + ch];
+            for (int u = 0; u < 4; ++u) acc[u] += __ldg(part + static_cast<long long>(p + u * kColLanes) * c + ch);
+        for (; p < parts; p += kColLanes) acc[0] += __ldg(part + static_cast<long long>(p) * c + ch);
     }
     red[lane][col] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     __syncthreads();
@@ -337,6 +467,26 @@ __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __res
     }
 }
 
+// --------------------------------------------------------- fixed-order sums
+// out[i] = sum over parts of part[p][i]: a CTA owns 32 columns, 8 lanes
+// stride over the parts (col_sum): the order depends only on `parts`.
+int ctas_reduce(const ReduceOp& o) { return std::max(1, ceil_div(o.width, 32)); }
+
+__global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __restrict__ ops, int nd) {
+    __shared__ float red[kColLanes][32];
+    int local;
+    const ReduceOp& o = op_of(ops, nd, local);
+    if (is_failed(o.failed)) return;
+    const int col = local * 32 + threadIdx.x % 32;
+    const float v = col_sum(o.part, o.parts, o.width, col, red);
+    if (threadIdx.x < 32 && col < o.width) o.out[col] = v;
+}
+
+void launch_reduce(const ReduceOp* d, int nd, int ctas, cudaStream_t st) {
+    reduce_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    PBKD_LAUNCH_CHECK();
+}
+
 void launch_bn_stat(const BnStatOp* d, int nd, int ctas, cudaStream_t st) {
     bn_stat_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
     PBKD_LAUNCH_CHECK();
@@ -363,6 +513,7 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
         load_v(o.inv + c0, g.V, inv);
         load_v(o.gamma + c0, g.V, gam);
         load_v(o.beta + c0, g.V, bet);
+#pragma unroll 4
         for (long long r = r0 + rr; r < r1; r += g.RP) {
             float pv[4], tv[4];
             load_v(o.p + r * o.c + c0, g.V, pv);
@@ -424,28 +575,59 @@ void launch_bn_bwd_fin(const BnBwdFinOp* d, int nd, int ctas, cudaStream_t st) {
     PBKD_LAUNCH_CHECK();
 }
 
+// Each thread owns 4 consecutive elements (one channel quad when c % 4 == 0,
+// per-channel parameters as float4); every load is issued before any store.
+struct BnBwdPar {
+    float mean, inv, gamma, beta, sg, sgx;
+};
+__device__ __forceinline__ float bn_bwd_one(const BnBwdApplyOp& o, const BnBwdPar& q, float p, float tg) {
+    const float xh = mul(sub(p, q.mean), q.inv);
+    float gy;
+    if (o.t) {
+        const float y = add(mul(q.gamma, xh), q.beta);
+        const float d = sub(relu(y), tg);
+        gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
+    } else {
+        gy = tg;
+    }
+    const float kk = mul(q.gamma, q.inv);
+    const float inner = sub(sub(gy, mul(o.inv_m, q.sg)), mul(mul(xh, o.inv_m), q.sgx));
+    return add(0.0f, mul(kk, inner));
+}
+__device__ __forceinline__ BnBwdPar bn_bwd_par(const BnBwdApplyOp& o, int ch) {
+    return {o.mean[ch], o.inv[ch], o.gamma[ch], o.beta[ch], o.sg[ch], o.sgx[ch]};
+}
+
 __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApplyOp* __restrict__ ops, int nd) {
     int local;
     const BnBwdApplyOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
     const long long base = (static_cast<long long>(local) * kThreads + threadIdx.x) * 4;
-    for (int q = 0; q < 4; ++q) {
-        const long long i = base + q;
-        if (i >= o.total) return;
-        const int ch = static_cast<int>(i % o.c);
-        const float xh = mul(sub(o.p[i], o.mean[ch]), o.inv[ch]);
-        float gy;
-        if (o.t) {
-            const float y = add(mul(o.gamma[ch], xh), o.beta[ch]);
-            const float d = sub(relu(y), o.t[i]);
-            gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
-        } else {
-            gy = o.gin[i];
-        }
-        const float kk = mul(o.gamma[ch], o.inv[ch]);
-        const float inner = sub(sub(gy, mul(o.inv_m, o.sg[ch])), mul(mul(xh, o.inv_m), o.sgx[ch]));
-        o.gout[i] = add(0.0f, mul(kk, inner));
+    if (base >= o.total) return;
+    const float* tg = o.t ? o.t : o.gin;
+    if ((o.c & 3) == 0 && base + 4 <= o.total) {
+        const int ch = static_cast<int>(base % o.c);
+        const float4 p = __ldg(reinterpret_cast<const float4*>(o.p + base));
+        const float4 g = __ldg(reinterpret_cast<const float4*>(tg + base));
+        const float4 mn = __ldg(reinterpret_cast<const float4*>(o.mean + ch));
+        const float4 iv = __ldg(reinterpret_cast<const float4*>(o.inv + ch));
+        const float4 gm = __ldg(reinterpret_cast<const float4*>(o.gamma + ch));
+        const float4 bt = __ldg(reinterpret_cast<const float4*>(o.beta + ch));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(o.sg + ch));
+        const float4 s2 = __ldg(reinterpret_cast<const float4*>(o.sgx + ch));
+        float4 r;
+        r.x = bn_bwd_one(o, {mn.x, iv.x, gm.x, bt.x, s1.x, s2.x}, p.x, g.x);
+        r.y = bn_bwd_one(o, {mn.y, iv.y, gm.y, bt.y, s1.y, s2.y}, p.y, g.y);
+        r.z = bn_bwd_one(o, {mn.z, iv.z, gm.z, bt.z, s1.z, s2.z}, p.z, g.z);
+        r.w = bn_bwd_one(o, {mn.w, iv.w, gm.w, bt.w, s1.w, s2.w}, p.w, g.w);
+        *reinterpret_cast<float4*>(o.gout + base) = r;
+        return;
     }
+    float pv[4], gv[4], rv[4];
+    const int cnt = static_cast<int>(min(4LL, o.total - base));
+    for (int q = 0; q < cnt; ++q) pv[q] = o.p[base + q], gv[q] = tg[base + q];
+    for (int q = 0; q < cnt; ++q) rv[q] = bn_bwd_one(o, bn_bwd_par(o, static_cast<int>((base + q) % o.c)), pv[q], gv[q]);
+    for (int q = 0; q < cnt; ++q) o.gout[base + q] = rv[q];
 }
 
 void launch_bn_bwd_apply(const BnBwdApplyOp* d, int nd, int ctas, cudaStream_t st) {
@@ -459,9 +641,22 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__
     const SgdOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
     const long long base = (static_cast<long long>(local) * kThreads + threadIdx.x) * 4;
-    for (int q = 0; q < 4; ++q) {
-        const long long i = base + q;
-        if (i >= o.n) return;
+    if (base >= o.n) return;
+    // v = m*v + g; w = w - lr*v   (ops.hpp:554-557, two roundings each)
+    if (base + 4 <= o.n) {  // flat parameter buffers are 16-byte aligned, n % 4 == 0
+        const float4 v = *reinterpret_cast<const float4*>(o.v + base);
+        const float4 g = *reinterpret_cast<const float4*>(o.g + base);
+        const float4 w = *reinterpret_cast<const float4*>(o.w + base);
+        float4 nv, nw;
+        nv.x = add(mul(o.mom, v.x), g.x), nv.y = add(mul(o.mom, v.y), g.y);
+        nv.z = add(mul(o.mom, v.z), g.z), nv.w = add(mul(o.mom, v.w), g.w);
+        nw.x = sub(w.x, mul(o.lr, nv.x)), nw.y = sub(w.y, mul(o.lr, nv.y));
+        nw.z = sub(w.z, mul(o.lr, nv.z)), nw.w = sub(w.w, mul(o.lr, nv.w));
+        *reinterpret_cast<float4*>(o.v + base) = nv;
+        *reinterpret_cast<float4*>(o.w + base) = nw;
+        return;
+    }
+    for (long long i = base; i < o.n; ++i) {
         const float v = add(mul(o.mom, o.v[i]), o.g[i]);
         o.v[i] = v;
         o.w[i] = sub(o.w[i], mul(o.lr, v));
@@ -477,18 +672,34 @@ void launch_sgd(const SgdOp* d, int nd, int ctas, cudaStream_t st) {
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const ScatterOp* __restrict__ ops, int nd) {
     int local;
     const ScatterOp& o = op_of(ops, nd, local);
-    const bool v4 = (o.width % 4) == 0;
-    const int wv = v4 ? o.width / 4 : o.width;
-    const long long total = static_cast<long long>(o.rows) * wv;
-    for (long long i = static_cast<long long>(local) * kThreads + threadIdx.x; i < total;
-         i += static_cast<long long>(kThreads) * 64) {
-        const long long r = i / wv, j = i - r * wv;
-        const long long dr = o.pos[r];
-        if (v4)
-            reinterpret_cast<float4*>(o.dst + dr * o.width)[j] =
-                reinterpret_cast<const float4*>(o.src + r * o.width)[j];
-        else
-            o.dst[dr * o.width + j] = o.src[r * o.width + j];
+    const long long step = static_cast<long long>(kThreads) * kScatterCtas;
+    if ((o.width % 4) == 0) {
+        const int wv = o.width / 4;
+        const long long total = static_cast<long long>(o.rows) * wv;
+        const float4* src = reinterpret_cast<const float4*>(o.src);
+        float4* dst = reinterpret_cast<float4*>(o.dst);
+        for (long long i = static_cast<long long>(local) * kThreads + threadIdx.x; i < total; i += 4 * step) {
+            float4 v[4];
+            long long d[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // all loads first
+                const long long ii = i + u * step;
+                if (ii < total) {
+                    const long long r = ii / wv;
+                    d[u] = static_cast<long long>(__ldg(o.pos + r)) * wv + (ii - r * wv);
+                    v[u] = __ldg(src + ii);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + u * step < total) dst[d[u]] = v[u];
+        }
+        return;
+    }
+    const long long total = static_cast<long long>(o.rows) * o.width;
+    for (long long i = static_cast<long long>(local) * kThreads + threadIdx.x; i < total; i += step) {
+        const long long r = i / o.width, j = i - r * o.width;
+        o.dst[static_cast<long long>(o.pos[r]) * o.width + j] = o.src[i];
     }
 }
 

@@ -18,6 +18,18 @@
 
 namespace pbkd_gpu {
 
+// Spatial tiling of the depthwise kernels: a CTA owns `ni` images x `th`
+// output rows x all columns x 32 channels, staged (with the 1-pixel halo,
+// zero padded) in shared memory as [pixel][32 channels].  Depends only on the
+// op's own shape (schedule-independent partials).
+struct DwTile {
+    int ni, th;         // images, output rows per tile
+    int tiles_y, tiles; // row tiles per image group, spatial tiles
+    int cslices;        // 32-channel slices
+    int tr, tw;         // staged input rows / cols (halo included)
+};
+DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays);
+
 // Depthwise 3x3 forward (ops.hpp:114-147), optional fused prologue that
 // rebuilds the input from the previous unit's pointwise output:
 //   pro 0: x as stored
@@ -32,6 +44,7 @@ struct DwFwdOp {
     const float *pa, *pb, *pc, *pd;  // mean,inv,gamma,beta | scale,shift
     const int* failed;
     int cta_begin;
+    DwTile tile;  // set by dw_fwd_finalize
 };
 
 // Depthwise 3x3 backward of a stride-1 unit u>0 (ops.hpp:149-178) fused with
@@ -48,9 +61,10 @@ struct DwBwdOp {
     float* part_sgx;     // [ctas][c]
     const float *mean, *inv, *gamma, *beta;  // previous unit BN (train mode)
     int n, h, wd, c;
-    int ctas, rows_per;
+    int ctas, rows_per;  // ctas: partial rows (= spatial tiles, dw_bwd_finalize)
     const int* failed;
     int cta_begin;
+    DwTile tile;
 };
 
 // Depthwise weight-gradient partials only (unit 0, any stride; model.cpp:570
@@ -60,9 +74,10 @@ struct DwGkOp {
     const float* x;   // [n*h*wd][c]
     float* part_gk;   // [ctas][9][c]
     int n, h, wd, c, ho, wo, stride, pad;
-    int ctas, rows_per;
+    int ctas, rows_per;  // ctas: partial rows (= spatial tiles, dw_gk_finalize)
     const int* failed;
     int cta_begin;
+    DwTile tile;
 };
 
 // Sum `parts` rows of width `width` in fixed order into out (optionally
@@ -191,7 +206,9 @@ struct SgdOp {
     int cta_begin;
 };
 
-// dst row pos[i] <- src row i   (activation streaming into a task's epoch order)
+// dst row pos[i] <- src row i   (activation streaming into a task's epoch order);
+// kScatterCtas CTAs per op
+constexpr int kScatterCtas = 148;
 struct ScatterOp {
     const float* src;
     float* dst;
@@ -220,6 +237,13 @@ void launch_scatter(const ScatterOp* d_ops, int nd, int ctas, cudaStream_t st);
 
 // CTA counts for one op (host)
 int ctas_dw_fwd(const DwFwdOp& o);
+int ctas_reduce(const ReduceOp& o);
+int ctas_dw_bwd(const DwBwdOp& o);
+int ctas_dw_gk(const DwGkOp& o);
+// fill the tile geometry (and partial-row count `ctas` for bwd / gk)
+void dw_fwd_finalize(DwFwdOp& o);
+void dw_bwd_finalize(DwBwdOp& o);
+void dw_gk_finalize(DwGkOp& o);
 int ctas_gemm(const GemmOp& o);
 int ctas_elem(long long total);
 int ctas_cols(int c);  // bn_stat / bn_bwd_fin CTAs per task
