@@ -45,6 +45,14 @@ __device__ __forceinline__ float bn_infer_apply(float x, float scale, float shif
 }
 __device__ __forceinline__ float relu(float x) { return x > 0.0f ? x : 0.0f; }
 
+// tf32 hi part of x: round to nearest even, 13 low bits cleared (one F2FP);
+// identical to tc::to_tf32 and tf32_split_host.  lo = hi(x - hi).
+__device__ __forceinline__ uint32_t tc_split_hi(float x) {
+    uint32_t r;
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r & 0xFFFFE000u;
+}
+
 // Which op of a grouped launch owns work item t (ops sorted by cta_begin,
 // ops[0].cta_begin == 0).  Must be called by all 32 lanes of a warp with the
 // same t: lane l reads ops[l].cta_begin, one ballot -- a single global-load

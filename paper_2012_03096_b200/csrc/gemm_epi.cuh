@@ -14,36 +14,49 @@
 namespace pbkd_gpu {
 
 // sync(): barrier over the 256 epilogue threads.  red: [8][32] shared floats.
+// The op's fields are copied to registers first: the C stores could alias the
+// descriptor as far as the compiler knows, which would force a reload of every
+// field after every store.
 template <int BN, class Sync>
-__device__ __forceinline__ void gemm_epilogue(const GemmOp& o, float* acc, int tm, int tn, int split, int q,
+__device__ __forceinline__ void gemm_epilogue(const GemmOp& op, float* acc, int tm, int tn, int split, int q,
                                               int h, int lane, int et, float (*red)[32], Sync sync) {
     constexpr int HB = BN / 2;
+    const int M = op.M, N = op.N, epi = op.epi, relu_on = op.relu;
+    const long long ldc = op.ldc;
+    const float* __restrict__ scale = op.scale;
+    const float* __restrict__ shift = op.shift;
+    const float* __restrict__ skip = op.skip;
+    float* __restrict__ part0 = op.part0;
+    float* __restrict__ part1 = op.part1;
     const int m0 = tm * tc::kBM, n0 = tn * BN;
     const int row = m0 + q * 32 + lane;
-    const bool row_ok = row < o.M;
-    float* C = o.C + (o.epi == 2 ? static_cast<long long>(split) * o.M * o.ldc : 0);
-    const bool vec_st = (o.ldc % 4) == 0;
+    const bool row_ok = row < M;
+    float* __restrict__ C = op.C + (epi == 2 ? static_cast<long long>(split) * M * ldc : 0);
+    const bool vec_st = (ldc % 4) == 0;
     constexpr int SL = HB >= 16 ? 16 : HB;
 #pragma unroll
     for (int c0 = 0; c0 < HB; c0 += SL) {
         float* val = acc + c0;
         const int ncol = n0 + h * HB + c0;
+        if (scale || skip || relu_on) {
 #pragma unroll
-        for (int j = 0; j < SL; ++j) {
-            const int n = ncol + j;
-            float x = val[j];
-            if (row_ok && n < o.N) {
-                if (o.scale) x = bn_infer_apply(x, o.scale[n], o.shift[n]);
-                if (o.skip) x = add(x, o.skip[static_cast<long long>(row) * o.ldc + n]);
-                if (o.relu) x = relu(x);
-            } else {
-                x = 0.0f;
+            for (int j = 0; j < SL; ++j) {
+                const int n = ncol + j;
+                float x = val[j];
+                if (row_ok && n < N) {
+                    if (scale) x = bn_infer_apply(x, __ldg(scale + n), __ldg(shift + n));
+                    if (skip) x = add(x, __ldg(skip + static_cast<long long>(row) * ldc + n));
+                    if (relu_on) x = relu(x);
+                }
+                val[j] = x;
             }
-            val[j] = x;
         }
+#pragma unroll
+        for (int j = 0; j < SL; ++j)
+            if (!(row_ok && ncol + j < N)) val[j] = 0.0f;
         if (row_ok) {
-            float* dst = C + static_cast<long long>(row) * o.ldc + ncol;
-            if (vec_st && ncol + SL <= o.N) {
+            float* dst = C + static_cast<long long>(row) * ldc + ncol;
+            if (vec_st && ncol + SL <= N) {
 #pragma unroll
                 for (int qq = 0; qq < SL / 4; ++qq)
                     reinterpret_cast<float4*>(dst)[qq] =
@@ -51,10 +64,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& o, float* acc, int t
             } else {
 #pragma unroll
                 for (int j = 0; j < SL; ++j)
-                    if (ncol + j < o.N) dst[j] = val[j];
+                    if (ncol + j < N) dst[j] = val[j];
             }
         }
-        if (o.epi == 1) {  // per-(m-tile, column) sum / sum of squares, fixed-order trees
+        if (epi == 1) {  // per-(m-tile, column) sum / sum of squares, fixed-order trees
 #pragma unroll
             for (int j = 0; j < SL; ++j) {
                 float s = val[j], sq = val[j] * val[j];
@@ -72,12 +85,12 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& o, float* acc, int t
             if (et < 2 * SL) {  // column (half hh, j): 4 row quarters in order
                 const int hh = et / SL, j = et % SL;
                 const int col = n0 + hh * HB + c0 + j;
-                if (col < o.N) {
+                if (col < N) {
                     const float s = (red[4 * hh][j] + red[4 * hh + 1][j]) + (red[4 * hh + 2][j] + red[4 * hh + 3][j]);
                     const float sq = (red[4 * hh][16 + j] + red[4 * hh + 1][16 + j]) +
                                      (red[4 * hh + 2][16 + j] + red[4 * hh + 3][16 + j]);
-                    o.part0[static_cast<long long>(tm) * o.N + col] = s;
-                    o.part1[static_cast<long long>(tm) * o.N + col] = sq;
+                    part0[static_cast<long long>(tm) * N + col] = s;
+                    part1[static_cast<long long>(tm) * N + col] = sq;
                 }
             }
             sync();

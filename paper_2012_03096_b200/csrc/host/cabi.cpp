@@ -695,17 +695,40 @@ int pbkd_k_dw_gk(pbkd_ctx* ctx, const float* gy, const float* x, float* gk, int 
     });
 }
 
+// PBKD_GEMM_PRESPLIT=1 (tests): hand the GEMMs pre-split tf32 planes of
+// their operands, exercising the TMA kernel's no-conversion paths (K-major
+// and MN-major); results must be bitwise those of the converting paths.
+struct Planes {
+    std::unique_ptr<Scratch> hi, lo;
+    const float* h = nullptr;
+    const float* l = nullptr;
+    Planes(const float* x, size_t n, cudaStream_t st) {
+        static const bool on = [] {
+            const char* e = std::getenv("PBKD_GEMM_PRESPLIT");
+            return e && e[0] == '1';
+        }();
+        if (!on || !x) return;
+        hi = std::make_unique<Scratch>(n);
+        lo = std::make_unique<Scratch>(n);
+        launch_tf32_split(x, static_cast<long long>(n), hi->p, lo->p, st);
+        h = hi->p;
+        l = lo->p;
+    }
+};
+
 int pbkd_k_pw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int rows, int cin, int cout,
                   float* col_sum, float* col_sq) {
     return guard([&] {
+        cudaStream_t st = ctx->eng->stream();
+        Planes px(x, static_cast<size_t>(rows) * cin, st), pw(w, static_cast<size_t>(cout) * cin, st);
         GemmOp g{};
         g.M = rows, g.N = cout, g.K = cin;
         g.A = x, g.lda = cin, g.a_kmajor = 1;
         g.B = w, g.ldb = cin, g.b_kmajor = 1;
+        g.a_hi = px.h, g.a_lo = px.l, g.b_hi = pw.h, g.b_lo = pw.l;
         g.C = y, g.ldc = cout;
         g.ksplit = 1;
         gemm_finalize(g);
-        cudaStream_t st = ctx->eng->stream();
         if (col_sum || col_sq) {
             Scratch p0(static_cast<size_t>(g.tiles_m) * cout), p1(static_cast<size_t>(g.tiles_m) * cout);
             g.epi = 1, g.part0 = p0.p, g.part1 = p1.p;
@@ -730,11 +753,14 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
                   int rows, int cin, int cout) {
     return guard([&] {
         cudaStream_t st = ctx->eng->stream();
+        Planes px(x, static_cast<size_t>(rows) * cin, st), pw(w, static_cast<size_t>(cout) * cin, st),
+            pg(gy, static_cast<size_t>(rows) * cout, st);
         if (gx) {
             GemmOp g{};
             g.M = rows, g.N = cin, g.K = cout;
             g.A = gy, g.lda = cout, g.a_kmajor = 1;
             g.B = w, g.ldb = cin, g.b_kmajor = 0;
+            g.a_hi = pg.h, g.a_lo = pg.l, g.b_hi = pw.h, g.b_lo = pw.l;
             g.C = gx, g.ldc = cin;
             g.ksplit = 1;
             gemm_finalize(g);
@@ -745,6 +771,7 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             g.M = cout, g.N = cin, g.K = rows;
             g.A = gy, g.lda = cout, g.a_kmajor = 0;
             g.B = x, g.ldb = cin, g.b_kmajor = 0;
+            g.a_hi = pg.h, g.a_lo = pg.l, g.b_hi = px.h, g.b_lo = px.l;
             g.ldc = cin;
             g.epi = 2;
             g.ksplit = std::max(1, std::min(64, ceil_div(rows, 512)));

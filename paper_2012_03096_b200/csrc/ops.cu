@@ -709,6 +709,24 @@ void launch_scatter(const ScatterOp* d, int nd, int ctas, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------- non-grouped ---
+// tf32 hi / lo planes of x (RNE split, as the GEMM converters do it)
+__global__ void tf32_split_kernel(const float* __restrict__ x, long long n, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const float v = x[i];
+        const float h = __uint_as_float(tc_split_hi(v));
+        hi[i] = h;
+        lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(v, h)));
+    }
+}
+
+void launch_tf32_split(const float* x, long long n, float* hi, float* lo, cudaStream_t st) {
+    const int blocks = static_cast<int>(std::min<long long>(4096, (n + 255) / 256));
+    tf32_split_kernel<<<std::max(1, blocks), 256, 0, st>>>(x, n, hi, lo);
+    PBKD_LAUNCH_CHECK();
+}
+
 __global__ void gather_nhwc_kernel(const float* __restrict__ img, const int* __restrict__ idx, int n,
                                    int c, int h, int w, float* __restrict__ out) {
     const long long total = static_cast<long long>(n) * c * h * w;

@@ -121,12 +121,14 @@ struct GemmOp {
     const int* failed;
     int cta_begin;
     int tma;             // 1: umma_tma.cu kernel (tensor maps below valid)
-    // optional pre-split B (tf32 hi / lo bit patterns, same layout as B,
-    // K-major): the TMA kernel loads them straight into its MMA operand ring
-    const float *b_hi, *b_lo;
-    int b_presplit;      // set by gemm_finalize when b_hi/b_lo are usable
+    // optional pre-split operands: tf32 hi / lo planes (RNE split, same
+    // layout and leading dimension as A / B; for conv, as the NHWC input).
+    // The TMA kernel loads them straight into its MMA operand ring.
+    const float *a_hi, *a_lo, *b_hi, *b_lo;
+    int a_presplit, b_presplit;   // set by gemm_finalize when usable
     CUtensorMap map_a, map_b;     // 2-D fp32 maps of A and B (64-byte aligned)
-    CUtensorMap map_bh, map_bl;   // SWIZZLE_128B maps of b_hi / b_lo
+    CUtensorMap map_ah, map_al;   // SWIZZLE_128B maps of the planes
+    CUtensorMap map_bh, map_bl;
 };
 
 // tf32 hi/lo split on the host, bit-identical to tc::to_tf32 on the device
@@ -255,6 +257,8 @@ void launch_bn_infer_prep(const float* gamma, const float* beta, const float* mm
                           const float* mv, int c, float* scale, float* shift, cudaStream_t st);
 void launch_bn_infer_relu(const float* x, float* y, long long total, int c, const float* scale,
                           const float* shift, cudaStream_t st);
+// tf32 hi / lo planes of n floats (the 3xTF32 operand split)
+void launch_tf32_split(const float* x, long long n, float* hi, float* lo, cudaStream_t st);
 // per-segment MSE sums (segment = one batch of the epoch-0 baseline)
 void launch_mse_segments(const float* s, const float* t, long long seg_elems, long long total,
                          int nseg, double* out_sums, cudaStream_t st);

@@ -42,14 +42,31 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     return d;
 }
 
+// MN-major descriptor for 32-bit (tf32) operands.  The only MN-major layout
+// the tensor core takes for tf32 is SWIZZLE_128B_BASE32B (layout type 1;
+// CUTLASS sm100_common.inl): atoms of 32 MN elements (128 B) x 4 K rows
+// (512 B), 32-byte chunks XOR-swizzled by the row; LBO = byte stride between
+// MN atoms, SBO = between 4-row K groups (make_umma_desc<Major::MN>).  The
+// TMA twin is CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(1) << 61;
+    return d;
+}
+
 // Byte offset of 16-byte chunk c (0..7) of row r in a K-major SWIZZLE_128B
 // tile (rows of 128 bytes, 8-row groups of 1024 bytes).
 __device__ __forceinline__ int sw128(int r, int c) { return (r >> 3) * 1024 + (r & 7) * kRowBytes + ((c ^ (r & 7)) << 4); }
 
-// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M=128, N=n.
-__device__ __forceinline__ uint32_t instr_desc(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-           (static_cast<uint32_t>(kBM >> 4) << 24);
+// Instruction descriptor: kind::tf32, D fp32, M=128, N=n; A/B K-major unless
+// a_mn / b_mn (bits 15 / 16: MN-major operand).
+__device__ __forceinline__ uint32_t instr_desc(int n, bool a_mn = false, bool b_mn = false) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn ? 1u << 15 : 0u) | (b_mn ? 1u << 16 : 0u) |
+           (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -148,9 +165,8 @@ __device__ __forceinline__ bool elect_one() {
 // k step, small terms first; the chunk's first MMA overwrites the TMEM slot)
 // as a single asm block: 12 tcgen05.mma with descriptors advanced in
 // registers, no per-instruction uniform moves or reconvergence.
-__device__ __forceinline__ void mma_chunk3(uint32_t d, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
-                                           uint32_t idesc) {
-    const uint64_t dah = smem_desc(ah), dal = smem_desc(al), dbh = smem_desc(bh), dbl = smem_desc(bl);
+__device__ __forceinline__ void mma_chunk3d(uint32_t d, uint64_t dah, uint64_t dal, uint64_t dbh, uint64_t dbl,
+                                            uint64_t inc_a, uint64_t inc_b, uint32_t idesc) {
     asm volatile(
         "{\n\t"
         ".reg .pred F, T;\n\t"
@@ -161,21 +177,27 @@ __device__ __forceinline__ void mma_chunk3(uint32_t d, uint32_t ah, uint32_t al,
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, F;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
-        "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+        "add.s64 ah, ah, %6;\n\tadd.s64 al, al, %6;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, T;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
-        "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+        "add.s64 ah, ah, %6;\n\tadd.s64 al, al, %6;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, T;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
-        "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+        "add.s64 ah, ah, %6;\n\tadd.s64 al, al, %6;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, T;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, T;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, T;\n\t"
         "}\n" ::"r"(d),
-        "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(idesc)
+        "l"(dah), "l"(dal), "l"(dbh), "l"(dbl), "r"(idesc), "l"(inc_a), "l"(inc_b)
         : "memory");
+}
+
+// K-major SW128 operands: the k-step advances 32 bytes (+2 in the >>4 field).
+__device__ __forceinline__ void mma_chunk3(uint32_t d, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
+                                           uint32_t idesc) {
+    mma_chunk3d(d, smem_desc(ah), smem_desc(al), smem_desc(bh), smem_desc(bl), 2, 2, idesc);
 }
 
 // Issue one 32-wide K chunk (4 k-steps of 8) into TMEM column d:

@@ -27,7 +27,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "gemm_epi.cuh"
 #include "ops.cuh"
@@ -152,7 +154,8 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 }  // namespace
 
 template <int BN>
-__global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total, int dbg) {
+__global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total, int dbg,
+                                                                 unsigned long long* __restrict__ trace) {
     using C = Cfg<BN>;
     constexpr int R = C::R, S = C::S, HB = BN / 2;
     extern __shared__ uint8_t smem_raw[];
@@ -162,6 +165,16 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     __shared__ int begins[kMaxOps];
     __shared__ TileInfo tiles_sh[kMaxTiles];
 
+    // PBKD_GEMM_TRACE: CTA 0 timestamps (globaltimer ns) per pipeline event
+    const bool tr_on = trace != nullptr && blockIdx.x == 0;
+    auto mark = [&](int ev, uint32_t i) {
+        if (tr_on && i < 512) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[ev * 512 + i] = t;
+        }
+    };
+    if (threadIdx.x == 0) mark(5, 0);
     const uint32_t sbase = smem_u32(smem_raw);
     const uint32_t pad = (1024u - (sbase & 1023u)) & 1023u;
     uint8_t* raw_ring = smem_raw + pad;  // stays a shared-space pointer
@@ -212,6 +225,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    if (threadIdx.x == 0) mark(5, 1);
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -237,9 +251,16 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                         mbar_arrive(&raw_full[r]);
                         continue;
                     }
-                    mbar_arrive_expect_tx(&raw_full[r], o.b_presplit ? C::a_raw : C::raw_stage);
+                    const uint32_t bytes = (o.a_presplit ? 0 : C::a_raw) + (o.b_presplit ? 0 : C::b_raw);
+                    if (bytes == 0) {  // both operands go straight to the operand ring
+                        mbar_arrive(&raw_full[r]);
+                        continue;
+                    }
+                    mbar_arrive_expect_tx(&raw_full[r], bytes);
                     const int k = g.k0 + kc * kBK;
-                    if (conv) {  // implicit im2col: tap (ky,kx), channels c0..c0+31
+                    if (o.a_presplit) {
+                        // A goes straight to the operand ring (warp kBWarp)
+                    } else if (conv) {  // implicit im2col: tap (ky,kx), channels c0..c0+31
                         const int tap = k / o.ic, c0 = k - tap * o.ic;
                         const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
                         tma_load_4d(st, &o.map_a, &raw_full[r], c0, kx - o.cpad, y0 + ky, img);
@@ -248,6 +269,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     } else {
                         tma_load_2d(st, &o.map_a, &raw_full[r], m0, k);
                     }
+                    mark(0, it);
                     if (o.b_presplit) {
                         // B goes straight to the operand ring (warp kBWarp)
                     } else if (bkm) {
@@ -264,13 +286,15 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer
         // whole warp waits (warp-uniform values), one elected lane issues
-        const uint32_t idesc = instr_desc(BN);
         uint32_t it = 0;
         for (int j = 0; j < ntiles; ++j) {
             if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
             const int terms = o.tf32x3;
+            // pre-split MN-major operands stay MN-major in shared memory
+            const bool amn = o.a_presplit && !o.conv && !o.a_kmajor, bmn = o.b_presplit && !o.b_kmajor;
+            const uint32_t idesc = instr_desc(BN, amn, bmn);
             for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                 const int s = it % S, a = it % C::A;
                 mbar_wait(&op_full[s], (it / S) & 1);
@@ -278,36 +302,87 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                 tc_fence_after();
                 const uint32_t ah = op_s + s * C::op_stage, al = ah + C::a_op, bh = al + C::a_op, bl = bh + C::b_op;
                 if (elect_one()) {
-                    if (!(dbg & 2)) mma_chunk(tmem + a * BN, ah, al, bh, bl, idesc, terms);
+                    if (dbg & 2) {
+                    } else if ((amn || bmn) && terms == 3) {
+                        // MN-major (BASE32B): atoms of 32 MN x 4 K (512 B), MN atoms
+                        // 4096 B apart (one TMA box each); a k-step of 8 advances 1024 B
+                        constexpr uint32_t lbo = 4096, sbo = 512;
+                        const uint64_t dah = amn ? smem_desc_mn(ah, lbo, sbo) : smem_desc(ah);
+                        const uint64_t dal = amn ? smem_desc_mn(al, lbo, sbo) : smem_desc(al);
+                        const uint64_t dbh = bmn ? smem_desc_mn(bh, lbo, sbo) : smem_desc(bh);
+                        const uint64_t dbl = bmn ? smem_desc_mn(bl, lbo, sbo) : smem_desc(bl);
+                        mma_chunk3d(tmem + a * BN, dah, dal, dbh, dbl, amn ? 64 : 2, bmn ? 64 : 2, idesc);
+                    } else {
+                        mma_chunk(tmem + a * BN, ah, al, bh, bl, idesc, terms);
+                    }
                     mma_commit(&op_empty[s]);
                     mma_commit(&acc_full[a]);
+                    mark(2, it);
                 }
                 __syncwarp();
             }
         }
     } else if (warp == kBWarp) {
-        // ------------------------------------------------------ B (pre-split)
-        // one arrive per chunk on op_full (with the B bytes when pre-split),
-        // after the stage is free
+        // ------------------------------------------------------ operand loader
+        // pre-split (tf32 hi / lo) operands straight into the operand ring:
+        // K-major as one 128-byte-swizzled box per plane, MN-major as one
+        // {32 MN, 32 K} swizzled box per 32-wide MN atom.  One arrive per chunk
+        // on op_full (with the bytes), after the stage is free.
         uint32_t it = 0;
         for (int j = 0; j < ntiles; ++j) {
             if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
-            const int n0 = g.tn * BN;
-            const bool pre = o.b_presplit != 0;
+            const int m0 = g.tm * kBM, n0 = g.tn * BN;
+            const bool apre = o.a_presplit != 0 && !(dbg & 8), bpre = o.b_presplit != 0 && !(dbg & 8);
+            const bool akm = o.conv != 0 || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            int img = 0, y0 = 0;
+            if (o.conv) {
+                const int hw = o.oh * o.ow;
+                img = m0 / hw;
+                y0 = (m0 - img * hw) / o.ow * o.cstride - o.cpad;
+            }
             if (lane == 0) {
                 for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                     const int s = it % S;
                     mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
-                    if (pre && !(dbg & 8)) {
-                        uint8_t* os = op_ring + s * C::op_stage + 2 * C::a_op;
-                        mbar_arrive_expect_tx(&op_full[s], 2 * C::b_op);
-                        const int k = g.k0 + kc * kBK;
-                        tma_load_2d(os, &o.map_bh, &op_full[s], k, n0);
-                        tma_load_2d(os + C::b_op, &o.map_bl, &op_full[s], k, n0);
-                    } else {
+                    const uint32_t bytes = (apre ? 2 * C::a_op : 0) + (bpre ? 2 * C::b_op : 0);
+                    if (bytes == 0) {
                         mbar_arrive(&op_full[s]);
+                        continue;
+                    }
+                    mbar_arrive_expect_tx(&op_full[s], bytes);
+                    uint8_t* os = op_ring + s * C::op_stage;
+                    const int k = g.k0 + kc * kBK;
+                    if (apre) {
+                        if (o.conv) {
+                            const int tap = k / o.ic, c0 = k - tap * o.ic;
+                            const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
+                            tma_load_4d(os, &o.map_ah, &op_full[s], c0, kx - o.cpad, y0 + ky, img);
+                            tma_load_4d(os + C::a_op, &o.map_al, &op_full[s], c0, kx - o.cpad, y0 + ky, img);
+                        } else if (akm) {
+                            tma_load_2d(os, &o.map_ah, &op_full[s], k, m0);
+                            tma_load_2d(os + C::a_op, &o.map_al, &op_full[s], k, m0);
+                        } else {
+#pragma unroll
+                            for (int at = 0; at < kBM / 32; ++at) {
+                                tma_load_2d(os + at * 4096, &o.map_ah, &op_full[s], m0 + 32 * at, k);
+                                tma_load_2d(os + C::a_op + at * 4096, &o.map_al, &op_full[s], m0 + 32 * at, k);
+                            }
+                        }
+                    }
+                    if (bpre) {
+                        uint8_t* ob = os + 2 * C::a_op;
+                        if (bkm) {
+                            tma_load_2d(ob, &o.map_bh, &op_full[s], k, n0);
+                            tma_load_2d(ob + C::b_op, &o.map_bl, &op_full[s], k, n0);
+                        } else {
+#pragma unroll
+                            for (int at = 0; at < BN / 32; ++at) {
+                                tma_load_2d(ob + at * 4096, &o.map_bh, &op_full[s], n0 + 32 * at, k);
+                                tma_load_2d(ob + C::b_op + at * 4096, &o.map_bl, &op_full[s], n0 + 32 * at, k);
+                            }
+                        }
                     }
                 }
             } else {
@@ -328,17 +403,22 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                 const int r = it % R, s = it % S;
                 mbar_wait(&raw_full[r], (it / R) & 1);
+                if (warp == 2 && lane == 0) mark(6, it);
                 mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
+                if (warp == 2 && lane == 0) mark(7, it);
                 const uint32_t rs = raw_s + r * C::raw_stage;
                 const uint32_t os = op_s + s * C::op_stage;
-                if (!(dbg & 1)) convert_tile(rs, os, os + C::a_op, kBM, akm, split3, ct);
+                if (!(dbg & 1) && !o.a_presplit) convert_tile(rs, os, os + C::a_op, kBM, akm, split3, ct);
+                if (warp == 2 && lane == 0) mark(8, it);
                 if (!o.b_presplit && !(dbg & 1))
                     convert_tile(rs + C::a_raw, os + 2 * C::a_op, os + 2 * C::a_op + C::b_op, BN, bkm, split3, ct);
+                if (warp == 2 && lane == 0) mark(9, it);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&raw_empty[r]);
                     mbar_arrive(&op_full[s]);
+                    if (warp == 2) mark(1, it);
                 }
             }
         }
@@ -365,9 +445,13 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[a]);
+                if (lane == 0) {
+                    mbar_arrive(&acc_empty[a]);
+                    if (warp == kEpiWarp0) mark(3, it);
+                }
             }
             if (!(dbg & 4)) gemm_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, [] { named_bar(1, 256); });
+            if (warp == kEpiWarp0 && lane == 0) mark(4, j);
         }
     }
     (void)op_ring;
@@ -433,8 +517,36 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         const char* e = std::getenv("PBKD_GEMM_DBG");
         return e ? std::atoi(e) : 0;
     }();
-    umma_tma_kernel<BN><<<grid, kThreadsT, Cfg<BN>::smem, st>>>(d, nd, total, dbg);
+    static const bool trace_on = std::getenv("PBKD_GEMM_TRACE") != nullptr;
+    static unsigned long long* trace = nullptr;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (trace_on) PBKD_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (trace_on && cap == cudaStreamCaptureStatusNone && !trace)
+        PBKD_CUDA(cudaMalloc(&trace, 10 * 512 * sizeof(unsigned long long)));
+    unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
+    if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, 10 * 512 * sizeof(unsigned long long), st));
+    umma_tma_kernel<BN><<<grid, kThreadsT, Cfg<BN>::smem, st>>>(d, nd, total, dbg, tr);
     PBKD_LAUNCH_CHECK();
+    static const int trace_from = [] {
+        const char* e = std::getenv("PBKD_GEMM_TRACE");
+        return e ? std::atoi(e) : 0;
+    }();
+    static int launch_no = 0;
+    if (tr) ++launch_no;
+    if (tr && launch_no >= trace_from && launch_no < trace_from + 8) {  // diagnosis: CTA 0 timeline on stderr
+        std::vector<unsigned long long> h(10 * 512);
+        PBKD_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        PBKD_CUDA(cudaStreamSynchronize(st));
+        const unsigned long long t0 = h[5 * 512];
+        auto rel = [&](int ev, int i) { return h[ev * 512 + i] ? static_cast<long long>(h[ev * 512 + i] - t0) : -1LL; };
+        std::fprintf(stderr, "[gemm-trace] launch %d BN=%d grid=%d tiles=%d nd=%d setup=%lld ns\n", launch_no, BN, grid,
+                     total, nd, rel(5, 1));
+        for (int i = 0; i < 512 && h[i]; ++i)
+            std::fprintf(stderr, "[gemm-trace]   chunk %3d: tma %8lld raw_full %8lld op_empty %8lld A %8lld B %8lld fence %8lld mma %8lld drain %8lld\n",
+                         i, rel(0, i), rel(6, i), rel(7, i), rel(8, i), rel(9, i), rel(1, i), rel(2, i), rel(3, i));
+        for (int j = 0; j < 512 && h[4 * 512 + j]; ++j)
+            std::fprintf(stderr, "[gemm-trace]   tile %3d epilogue end %8lld\n", j, rel(4, j));
+    }
 }
 
 }  // namespace
@@ -444,7 +556,7 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
 // of a tile, traversal stride = conv stride, out-of-image taps zero filled.
 // Needs C % 32 == 0 and tiles made of whole output rows (ow | 128 and
 // (128/ow) | oh) or whole images (oh*ow | 128).
-bool encode_conv(CUtensorMap* m, const GemmOp& o) {
+bool encode_conv(CUtensorMap* m, const GemmOp& o, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE) {
     if (o.ic % kBK != 0 || (reinterpret_cast<uintptr_t>(o.A) & 15) != 0) return false;
     const int hw = o.oh * o.ow;
     int bw = o.ow, bh, bimg;
@@ -466,19 +578,40 @@ bool encode_conv(CUtensorMap* m, const GemmOp& o) {
     const cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(s), static_cast<cuuint32_t>(s), 1};
     if (box[1] > 256 || box[2] > 256 || box[3] > 256) return false;
     const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(o.A), dims, strides, box,
-                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-// Pre-split B (K-major tf32 hi/lo arrays): 128-byte swizzled boxes land in
-// the MMA's canonical K-major SWIZZLE_128B layout with no conversion pass.
+// Pre-split operands (tf32 hi / lo planes with the operand's own layout and
+// leading dimension): 128-byte swizzled boxes land in the MMA's canonical
+// SWIZZLE_128B layout (K-major: box {32 K, rows}; MN-major: box {32 MN, 32 K}
+// per MN atom) with no conversion pass.  Only with the 3xTF32 split.
+bool presplit_pair(CUtensorMap* mh, CUtensorMap* ml, const float* hi, const float* lo, bool kmajor, long long mn,
+                   long long k, long long ld, int rows) {
+    const auto sw = CU_TENSOR_MAP_SWIZZLE_128B;
+    if (kmajor) return encode(mh, hi, k, mn, ld, kBK, rows, sw) && encode(ml, lo, k, mn, ld, kBK, rows, sw);
+    const auto sw32 = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;  // tf32 MN-major smem layout
+    return encode(mh, hi, mn, k, ld, 32, kBK, sw32) && encode(ml, lo, mn, k, ld, 32, kBK, sw32);
+}
+
 void presplit_maps(GemmOp& o) {
     o.b_presplit = 0;
-    if (!o.b_hi || !o.b_lo || !o.b_kmajor || o.tf32x3 < 2) return;
-    if (encode(&o.map_bh, o.b_hi, o.K, o.N, o.ldb, kBK, o.bn, CU_TENSOR_MAP_SWIZZLE_128B) &&
-        encode(&o.map_bl, o.b_lo, o.K, o.N, o.ldb, kBK, o.bn, CU_TENSOR_MAP_SWIZZLE_128B))
+    if (o.tf32x3 == 3 && o.b_hi && o.b_lo &&
+        presplit_pair(&o.map_bh, &o.map_bl, o.b_hi, o.b_lo, o.b_kmajor != 0, o.N, o.K, o.ldb, o.bn))
         o.b_presplit = 1;
+    o.a_presplit = 0;
+    if (o.tf32x3 != 3 || !o.a_hi || !o.a_lo) return;
+    if (o.conv) {
+        GemmOp t = o;
+        t.A = o.a_hi;
+        if (!encode_conv(&o.map_ah, t, CU_TENSOR_MAP_SWIZZLE_128B)) return;
+        t.A = o.a_lo;
+        if (!encode_conv(&o.map_al, t, CU_TENSOR_MAP_SWIZZLE_128B)) return;
+        o.a_presplit = 1;
+    } else if (presplit_pair(&o.map_ah, &o.map_al, o.a_hi, o.a_lo, o.a_kmajor != 0, o.M, o.K, o.lda, kBM)) {
+        o.a_presplit = 1;
+    }
 }
 
 // TMA eligibility + tensor maps (called from gemm_finalize).

@@ -37,7 +37,9 @@ def main(out):
             got = res[f"{key}_{name}"].astype(np.float64)
             err = np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-30)
             if err > 1e-5:
-                raise SystemExit(f"{key} {name}: rel err {err:.2e} vs fp64")
+                raise SystemExit(f"{key} {name}: rel err {err:.2e} vs fp64 (max|got| {np.max(np.abs(got)):.3e}, "
+                                 f"max|want| {np.max(np.abs(want)):.3e}, got[0,:4] {got.ravel()[:4]}, "
+                                 f"want[0,:4] {want.ravel()[:4]})")
     # teacher implicit-GEMM convs (register-staged vs TMA 4-D im2col boxes):
     # every boundary of VGG-16 and ResNet-18 on 5 samples
     import os

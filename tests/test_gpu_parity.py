@@ -340,17 +340,21 @@ def test_gemm_kernels_agree_bitwise(ctx, tmp_path):
     (umma.cu) issue the same MMA sequence per 32-wide K chunk and drain the
     chunks in the same order, so every pointwise fwd / dgrad / wgrad output
     (incl. ragged M/N/K, MN-major operands, split-K) and every teacher conv
-    (implicit im2col, stride 1/2, 1x1 projections) must agree bit for bit;
+    (implicit im2col, stride 1/2, 1x1 projections) must agree bit for bit,
+    also when the operands arrive as pre-split tf32 planes (no conversion,
+    K-major and MN-major shared-memory descriptors);
     both are also checked against fp64 (rel 1e-5) inside gemm_dump.py."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    for tma in ("0", "1"):
-        path = str(tmp_path / f"g{tma}.npz")
-        env = dict(os.environ, PBKD_GEMM_TMA=tma, PBKD_CONV_TMA=tma, PYTHONPATH=root)
+    # register-staged | TMA with converter warps | TMA on pre-split tf32 planes
+    for name, tma, pre in (("reg", "0", "0"), ("tma", "1", "0"), ("pre", "1", "1")):
+        path = str(tmp_path / f"g{name}.npz")
+        env = dict(os.environ, PBKD_GEMM_TMA=tma, PBKD_CONV_TMA=tma, PBKD_GEMM_PRESPLIT=pre, PYTHONPATH=root)
         subprocess.run([sys.executable, os.path.join(root, "tests", "gemm_dump.py"), path], env=env, check=True,
                        timeout=300)
-        outs[tma] = np.load(path)
-    for k in outs["0"].files:
-        assert np.array_equal(outs["0"][k], outs["1"][k]), k
+        outs[name] = np.load(path)
+    for k in outs["reg"].files:
+        assert np.array_equal(outs["reg"][k], outs["tma"][k]), k
+        assert np.array_equal(outs["reg"][k], outs["pre"][k]), k
