@@ -332,6 +332,14 @@ struct TaskState {
     DevBuf in_stream, tgt_stream, pos, eval_in;
     // workspace
     DevBuf d[kMaxUnits], p[kMaxUnits], gp, gd, gy;
+    // tf32 hi / lo planes of the pointwise GEMM operands (3xTF32 split),
+    // written by their producers when the TMA GEMM consumes them pre-split:
+    // dw outputs (fwd A, wgrad B), BN-backward outputs (dgrad A, wgrad A),
+    // parameters (pw weights: fwd B, dgrad B)
+    // planes[u]: unit u's GEMMs (fwd, dgrad, wgrad) all take TMA pre-split
+    // operands, so its dw output and BN gradient are written as planes only
+    bool planes_d[kMaxUnits] = {false, false, false}, planes_w = false;
+    DevBuf d_hi[kMaxUnits], d_lo[kMaxUnits], gp_hi, gp_lo, params_hi, params_lo;
     DevBuf cs0, cs1, psg, psgx, pgk, ploss, wsplit;
     DevBuf mean, inv, sg, sgx;  // [units][cout]
     DevBuf scale, shift;        // inference affine [units][cout]
@@ -595,6 +603,14 @@ struct Engine::Impl {
         s.nparams = host.size();
         s.nstats = stats.size();
         s.params = upload(host, st);
+        s.planes_w = false;
+        for (int u = 0; u < s.units; ++u) s.planes_w = s.planes_w || gemm_presplit_ok(s.u[u].cin);
+        if (s.planes_w) {
+            std::vector<float> hi(host.size()), lo(host.size());
+            tf32_split_host(host.data(), host.size(), hi.data(), lo.data());
+            s.params_hi = upload(hi, st);
+            s.params_lo = upload(lo, st);
+        }
         s.grads.alloc(s.nparams * sizeof(float));
         PBKD_CUDA(cudaMemsetAsync(s.grads.p, 0, s.nparams * sizeof(float), st));
         s.vel.alloc(s.nparams * sizeof(float));
@@ -611,9 +627,18 @@ struct Engine::Impl {
         const int cin = tb.cin, cout = tb.cout, cmax = std::max(cin, cout);
         for (int u = 0; u < s.units; ++u) {
             s.d[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
+            s.planes_d[u] = gemm_presplit_ok(s.u[u].cin) && gemm_presplit_ok(s.u[u].cout) && s.planes_w;
+            if (s.planes_d[u]) {
+                s.d_hi[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
+                s.d_lo[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
+            }
             s.p[u].alloc(static_cast<size_t>(M) * cout * sizeof(float));
         }
         s.gp.alloc(static_cast<size_t>(M) * cout * sizeof(float));
+        if (s.planes_w && gemm_presplit_ok(cout)) {
+            s.gp_hi.alloc(static_cast<size_t>(M) * cout * sizeof(float));
+            s.gp_lo.alloc(static_cast<size_t>(M) * cout * sizeof(float));
+        }
         s.gd.alloc(static_cast<size_t>(M) * cmax * sizeof(float));
         s.gy.alloc(static_cast<size_t>(M) * cout * sizeof(float));
         const int tiles = ceil_div(M, 128);
@@ -686,6 +711,7 @@ struct Engine::Impl {
                 o.x = u == 0 ? c.x0 : s.p[u - 1].f();
                 o.w = s.w_dw(u);
                 o.y = s.d[u].f();
+                if (s.planes_d[u]) o.y_hi = s.d_hi[u].f(), o.y_lo = s.d_lo[u].f();
                 o.n = c.n;
                 o.h = d.hin;
                 o.wd = d.win;
@@ -709,6 +735,8 @@ struct Engine::Impl {
                 g.N = d.cout;
                 g.K = d.cin;
                 g.A = s.d[u].f();
+                if (s.planes_d[u]) g.a_hi = s.d_hi[u].f(), g.a_lo = s.d_lo[u].f();
+                if (s.planes_w) g.b_hi = s.params_hi.f() + s.off_pw[u], g.b_lo = s.params_lo.f() + s.off_pw[u];
                 g.lda = d.cin;
                 g.a_kmajor = 1;
                 g.B = s.w_pw(u);
@@ -721,6 +749,7 @@ struct Engine::Impl {
                 g.part1 = s.cs1.f();
                 g.ksplit = 1;
                 gemm_finalize(g);
+                if (s.planes_d[u] && !g.a_presplit) throw std::logic_error("pre-split dw output not consumed by the fwd GEMM");
                 g.failed = c.failed;
                 gms.push_back(g);
                 BnStatOp b{};
@@ -801,6 +830,7 @@ struct Engine::Impl {
                 a.t = u == U - 1 ? c.t : nullptr;
                 a.gin = u == U - 1 ? nullptr : s.gy.f();
                 a.gout = s.gp.f();
+                if (s.planes_d[u]) a.gout_hi = s.gp_hi.f(), a.gout_lo = s.gp_lo.f();
                 a.mean = s.mean_u(u);
                 a.inv = s.inv_u(u);
                 a.gamma = s.w_g(u);
@@ -819,6 +849,8 @@ struct Engine::Impl {
                 g.N = d.cin;
                 g.K = d.cout;
                 g.A = s.gp.f();
+                if (s.planes_d[u]) g.a_hi = s.gp_hi.f(), g.a_lo = s.gp_lo.f();
+                if (s.planes_w) g.b_hi = s.params_hi.f() + s.off_pw[u], g.b_lo = s.params_lo.f() + s.off_pw[u];
                 g.lda = d.cout;
                 g.a_kmajor = 1;
                 g.B = s.w_pw(u);
@@ -829,6 +861,7 @@ struct Engine::Impl {
                 g.epi = 0;
                 g.ksplit = 1;
                 gemm_finalize(g);
+                if (s.planes_d[u] && !g.a_presplit) throw std::logic_error("pre-split BN gradient not consumed by dgrad");
                 g.failed = c.failed;
                 dg.push_back(g);
                 // wgrad: gW[o][j] = sum_m gp[m][o] d[m][j]  (split-K over rows)
@@ -837,9 +870,11 @@ struct Engine::Impl {
                 w.N = d.cin;
                 w.K = static_cast<int>(c.M);
                 w.A = s.gp.f();
+                if (s.planes_d[u]) w.a_hi = s.gp_hi.f(), w.a_lo = s.gp_lo.f();
                 w.lda = d.cout;
                 w.a_kmajor = 0;
                 w.B = s.d[u].f();
+                if (s.planes_d[u]) w.b_hi = s.d_hi[u].f(), w.b_lo = s.d_lo[u].f();
                 w.ldb = d.cin;
                 w.b_kmajor = 0;
                 w.C = s.wsplit.f();
@@ -847,15 +882,21 @@ struct Engine::Impl {
                 w.epi = 2;
                 w.ksplit = split_count(c.M);
                 gemm_finalize(w);
+                if (s.planes_d[u] && !(w.a_presplit && w.b_presplit))
+                    throw std::logic_error("pre-split operands not consumed by wgrad");
                 w.failed = c.failed;
+                if (w.ksplit == 1) {  // no split: the GEMM writes the gradient itself
+                    w.C = s.g_pw(u);
+                } else {
+                    ReduceOp r{};
+                    r.part = s.wsplit.f();
+                    r.out = s.g_pw(u);
+                    r.parts = w.ksplit;
+                    r.width = d.cout * d.cin;
+                    r.failed = c.failed;
+                    wr.push_back(r);
+                }
                 wg.push_back(w);
-                ReduceOp r{};
-                r.part = s.wsplit.f();
-                r.out = s.g_pw(u);
-                r.parts = w.ksplit;
-                r.width = d.cout * d.cin;
-                r.failed = c.failed;
-                wr.push_back(r);
                 if (u > 0) {
                     DwBwdOp b{};
                     b.gy = s.gd.f();
@@ -939,6 +980,7 @@ struct Engine::Impl {
             TaskState& s = *c.s;
             SgdOp o{};
             o.w = s.params.f();
+            if (s.planes_w) o.w_hi = s.params_hi.f(), o.w_lo = s.params_lo.f();
             o.v = s.vel.f();
             o.g = s.grads.f();
             o.n = static_cast<long long>(s.nparams);

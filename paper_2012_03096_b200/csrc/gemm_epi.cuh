@@ -32,6 +32,8 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& op, float* acc, int 
     const int row = m0 + q * 32 + lane;
     const bool row_ok = row < M;
     float* __restrict__ C = op.C + (epi == 2 ? static_cast<long long>(split) * M * ldc : 0);
+    float* __restrict__ Ch = op.c_hi;  // tf32 planes of the output for the next GEMM
+    float* __restrict__ Cl = op.c_lo;
     const bool vec_st = (ldc % 4) == 0;
     constexpr int SL = HB >= 16 ? 16 : HB;
 #pragma unroll
@@ -55,7 +57,8 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& op, float* acc, int 
         for (int j = 0; j < SL; ++j)
             if (!(row_ok && ncol + j < N)) val[j] = 0.0f;
         if (row_ok) {
-            float* dst = C + static_cast<long long>(row) * ldc + ncol;
+            const long long off = static_cast<long long>(row) * ldc + ncol;
+            float* dst = C + off;
             if (vec_st && ncol + SL <= N) {
 #pragma unroll
                 for (int qq = 0; qq < SL / 4; ++qq)
@@ -65,6 +68,15 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& op, float* acc, int 
 #pragma unroll
                 for (int j = 0; j < SL; ++j)
                     if (ncol + j < N) dst[j] = val[j];
+            }
+            if (Ch) {
+#pragma unroll
+                for (int j = 0; j < SL; ++j)
+                    if (ncol + j < N) {
+                        const float hv = __uint_as_float(tc_split_hi(val[j]));
+                        Ch[off + j] = hv;
+                        Cl[off + j] = __uint_as_float(tc_split_hi(__fsub_rn(val[j], hv)));
+                    }
             }
         }
         if (epi == 1) {  // per-(m-tile, column) sum / sum of squares, fixed-order trees

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
         const int nn = q.n0 + i, yy = q.y0 + oy;
         if (nn >= o.n || yy >= o.ho) continue;
         const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
-        float* out = o.y + ((static_cast<long long>(nn) * o.ho + yy) * o.wo) * o.c + c;
+        const long long obase = ((static_cast<long long>(nn) * o.ho + yy) * o.wo) * o.c + c;
 #pragma unroll 2
         for (int ox = 0; ox < o.wo; ++ox) {
             const float* b = base + ox * s * kDwC;
@@ -249,7 +249,14 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
             for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
                 for (int kx = 0; kx < 3; ++kx) acc = add(acc, mul(b[(ky * t.tw + kx) * kDwC], wk[ky * 3 + kx]));
-            out[static_cast<long long>(ox) * o.c] = acc;
+            const long long oi = obase + static_cast<long long>(ox) * o.c;
+            if (o.y_hi) {  // tf32 planes for the pointwise GEMMs (3xTF32 operand split)
+                const float hv = __uint_as_float(tc_split_hi(acc));
+                o.y_hi[oi] = hv;
+                o.y_lo[oi] = __uint_as_float(tc_split_hi(__fsub_rn(acc, hv)));
+            } else {
+                o.y[oi] = acc;
+            }
         }
     }
 }
@@ -468,18 +475,29 @@ __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __res
 }
 
 // --------------------------------------------------------- fixed-order sums
-// out[i] = sum over parts of part[p][i]: a CTA owns 32 columns, 8 lanes
-// stride over the parts (col_sum): the order depends only on `parts`.
-int ctas_reduce(const ReduceOp& o) { return std::max(1, ceil_div(o.width, 32)); }
+// out[i] = sum over parts of part[p][i]: one column per thread, four
+// independent accumulators (p mod 4) combined as (a0+a1)+(a2+a3) -- the order
+// depends only on `parts`; the loads of four parts are in flight at once.
+int ctas_reduce(const ReduceOp& o) { return std::max(1, ceil_div(o.width, kThreads)); }
 
 __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __restrict__ ops, int nd) {
-    __shared__ float red[kColLanes][32];
     int local;
     const ReduceOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
-    const int col = local * 32 + threadIdx.x % 32;
-    const float v = col_sum(o.part, o.parts, o.width, col, red);
-    if (threadIdx.x < 32 && col < o.width) o.out[col] = v;
+    const int col = local * kThreads + threadIdx.x;
+    if (col >= o.width) return;
+    const float* __restrict__ p = o.part + col;
+    const long long w = o.width;
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    int q = 0;
+    for (; q + 3 < o.parts; q += 4) {
+        a0 += __ldg(p + q * w);
+        a1 += __ldg(p + (q + 1) * w);
+        a2 += __ldg(p + (q + 2) * w);
+        a3 += __ldg(p + (q + 3) * w);
+    }
+    for (; q < o.parts; ++q) a0 += __ldg(p + q * w);
+    o.out[col] = (a0 + a1) + (a2 + a3);
 }
 
 void launch_reduce(const ReduceOp* d, int nd, int ctas, cudaStream_t st) {
@@ -620,14 +638,32 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApply
         r.y = bn_bwd_one(o, {mn.y, iv.y, gm.y, bt.y, s1.y, s2.y}, p.y, g.y);
         r.z = bn_bwd_one(o, {mn.z, iv.z, gm.z, bt.z, s1.z, s2.z}, p.z, g.z);
         r.w = bn_bwd_one(o, {mn.w, iv.w, gm.w, bt.w, s1.w, s2.w}, p.w, g.w);
-        *reinterpret_cast<float4*>(o.gout + base) = r;
+        if (o.gout_hi) {
+            float4 h, l;
+            h.x = __uint_as_float(tc_split_hi(r.x)), l.x = __uint_as_float(tc_split_hi(__fsub_rn(r.x, h.x)));
+            h.y = __uint_as_float(tc_split_hi(r.y)), l.y = __uint_as_float(tc_split_hi(__fsub_rn(r.y, h.y)));
+            h.z = __uint_as_float(tc_split_hi(r.z)), l.z = __uint_as_float(tc_split_hi(__fsub_rn(r.z, h.z)));
+            h.w = __uint_as_float(tc_split_hi(r.w)), l.w = __uint_as_float(tc_split_hi(__fsub_rn(r.w, h.w)));
+            *reinterpret_cast<float4*>(o.gout_hi + base) = h;
+            *reinterpret_cast<float4*>(o.gout_lo + base) = l;
+        } else {
+            *reinterpret_cast<float4*>(o.gout + base) = r;
+        }
         return;
     }
     float pv[4], gv[4], rv[4];
     const int cnt = static_cast<int>(min(4LL, o.total - base));
     for (int q = 0; q < cnt; ++q) pv[q] = o.p[base + q], gv[q] = tg[base + q];
     for (int q = 0; q < cnt; ++q) rv[q] = bn_bwd_one(o, bn_bwd_par(o, static_cast<int>((base + q) % o.c)), pv[q], gv[q]);
-    for (int q = 0; q < cnt; ++q) o.gout[base + q] = rv[q];
+    for (int q = 0; q < cnt; ++q) {
+        if (o.gout_hi) {
+            const float hv = __uint_as_float(tc_split_hi(rv[q]));
+            o.gout_hi[base + q] = hv;
+            o.gout_lo[base + q] = __uint_as_float(tc_split_hi(__fsub_rn(rv[q], hv)));
+        } else {
+            o.gout[base + q] = rv[q];
+        }
+    }
 }
 
 void launch_bn_bwd_apply(const BnBwdApplyOp* d, int nd, int ctas, cudaStream_t st) {
@@ -654,12 +690,27 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__
         nw.z = sub(w.z, mul(o.lr, nv.z)), nw.w = sub(w.w, mul(o.lr, nv.w));
         *reinterpret_cast<float4*>(o.v + base) = nv;
         *reinterpret_cast<float4*>(o.w + base) = nw;
+        if (o.w_hi) {
+            float4 h, l;
+            h.x = __uint_as_float(tc_split_hi(nw.x)), l.x = __uint_as_float(tc_split_hi(__fsub_rn(nw.x, h.x)));
+            h.y = __uint_as_float(tc_split_hi(nw.y)), l.y = __uint_as_float(tc_split_hi(__fsub_rn(nw.y, h.y)));
+            h.z = __uint_as_float(tc_split_hi(nw.z)), l.z = __uint_as_float(tc_split_hi(__fsub_rn(nw.z, h.z)));
+            h.w = __uint_as_float(tc_split_hi(nw.w)), l.w = __uint_as_float(tc_split_hi(__fsub_rn(nw.w, h.w)));
+            *reinterpret_cast<float4*>(o.w_hi + base) = h;
+            *reinterpret_cast<float4*>(o.w_lo + base) = l;
+        }
         return;
     }
     for (long long i = base; i < o.n; ++i) {
         const float v = add(mul(o.mom, o.v[i]), o.g[i]);
         o.v[i] = v;
-        o.w[i] = sub(o.w[i], mul(o.lr, v));
+        const float w = sub(o.w[i], mul(o.lr, v));
+        o.w[i] = w;
+        if (o.w_hi) {
+            const float hv = __uint_as_float(tc_split_hi(w));
+            o.w_hi[i] = hv;
+            o.w_lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(w, hv)));
+        }
     }
 }
 

@@ -38,7 +38,8 @@ DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays);
 struct DwFwdOp {
     const float* x;
     const float* w;  // [9][c]
-    float* y;
+    float* y;        // fp32 output, or (y_hi, y_lo) tf32 planes when set
+    float *y_hi, *y_lo;
     int n, h, wd, c, ho, wo, stride, pad;
     int pro;
     const float *pa, *pb, *pc, *pd;  // mean,inv,gamma,beta | scale,shift
@@ -126,6 +127,7 @@ struct GemmOp {
     // The TMA kernel loads them straight into its MMA operand ring.
     const float *a_hi, *a_lo, *b_hi, *b_lo;
     int a_presplit, b_presplit;   // set by gemm_finalize when usable
+    float *c_hi, *c_lo;           // optional tf32 planes of the output (epi 0)
     CUtensorMap map_a, map_b;     // 2-D fp32 maps of A and B (64-byte aligned)
     CUtensorMap map_ah, map_al;   // SWIZZLE_128B maps of the planes
     CUtensorMap map_bh, map_bl;
@@ -141,6 +143,10 @@ void gemm_finalize(GemmOp& o);
 constexpr int kGemmClassTma = 1000;
 int gemm_bn_class(const GemmOp& o);
 bool gemm_tma_prepare(GemmOp& o);  // umma_tma.cu: tensor maps, false if ineligible
+// Whether GEMM operands with leading dimension `ld` (floats) will be consumed
+// as pre-split tf32 planes (TMA kernel on, 3xTF32, 16-byte rows): producers
+// then write planes instead of fp32.
+bool gemm_presplit_ok(long long ld);
 
 // Batch-norm statistics from the GEMM column partials (ops.hpp:273-299):
 // mean, var = E[x^2]-mean^2 clamped, inv_std, moving-stat update.
@@ -189,7 +195,8 @@ struct BnBwdApplyOp {
     const float* p;
     const float* t;    // non-null -> last unit, g rebuilt from the MSE gradient
     const float* gin;  // else the masked gradient from the dw backward
-    float* gout;
+    float* gout;       // fp32 output, or (gout_hi, gout_lo) tf32 planes when set
+    float *gout_hi, *gout_lo;
     const float *mean, *inv, *gamma, *beta, *sg, *sgx;
     long long total;   // rows*c
     int c;
@@ -206,6 +213,7 @@ struct SgdOp {
     float lr, mom;
     const int* failed;
     int cta_begin;
+    float *w_hi, *w_lo;  // optional tf32 planes of the updated w (GEMM operands)
 };
 
 // dst row pos[i] <- src row i   (activation streaming into a task's epoch order);

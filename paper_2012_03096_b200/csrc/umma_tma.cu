@@ -583,6 +583,16 @@ bool encode_conv(CUtensorMap* m, const GemmOp& o, CUtensorMapSwizzle sw = CU_TEN
     return r == CUDA_SUCCESS;
 }
 
+bool gemm_presplit_ok(long long ld) {
+    static const bool on = [] {
+        const char* t = std::getenv("PBKD_GEMM_TMA");
+        const char* p = std::getenv("PBKD_PRESPLIT");
+        const char* e = std::getenv("PBKD_TF32_TERMS");
+        return !(t && t[0] == '0') && !(p && p[0] == '0') && (!e || std::atoi(e) == 3);
+    }();
+    return on && (ld * 4) % 16 == 0;
+}
+
 // Pre-split operands (tf32 hi / lo planes with the operand's own layout and
 // leading dimension): 128-byte swizzled boxes land in the MMA's canonical
 // SWIZZLE_128B layout (K-major: box {32 K, rows}; MN-major: box {32 MN, 32 K}
