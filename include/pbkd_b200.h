@@ -49,6 +49,9 @@ extern "C" {
 
 #define PBKD_RUN_STEP_ONLY 1 /* skip epoch-0 baseline and evaluations */
 #define PBKD_RUN_NO_GRAPH 2  /* launch eagerly instead of CUDA graphs */
+#define PBKD_RUN_PROFILE 4   /* after the last epoch, replay it once eagerly with an
+                                event per launch: per-kernel-class device time and
+                                algorithmic bytes / flops (measurement runs only) */
 
 typedef struct pbkd_ctx pbkd_ctx;
 typedef struct pbkd_results pbkd_results;
@@ -137,6 +140,11 @@ int pbkd_run_trace(const pbkd_results* r, pbkd_trace_event* out, int cap, int* n
 double pbkd_run_wall_time(const pbkd_results* r);
 double pbkd_run_epoch_ms(const pbkd_results* r); /* device time of the training epochs */
 void pbkd_run_free(pbkd_results* r);
+/* PBKD_RUN_PROFILE results: per kernel class (name), launches, device ms,
+ * compulsory fp32 bytes and flops of those launches. */
+int pbkd_run_profile_count(const pbkd_results* r);
+int pbkd_run_profile_entry(const pbkd_results* r, int i, char* name, size_t cap, int* launches, double* ms,
+                           double* bytes, double* flops);
 /* Same as pbkd_run; device events bracket epochs >= timed_from_epoch (host
  * gaps between epochs included), read back with pbkd_run_timing. */
 int pbkd_run_timed(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* train_idx,

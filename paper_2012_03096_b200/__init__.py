@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(HERE, "libpbkd_b200.so")
 
 KINDS = {"two_layer": 0, "three_layer": 1, "two_layer_skip": 2, "three_layer_skip": 3}
 POLICIES = {"round_robin": 0, "wfd": 1, "work_stealing": 2}
-RUN_STEP_ONLY, RUN_NO_GRAPH = 1, 2
+RUN_STEP_ONLY, RUN_NO_GRAPH, RUN_PROFILE = 1, 2, 4
 ERR_KINDS = {1: ValueError, 2: ValueError, 3: IndexError, 4: RuntimeError, 5: RuntimeError,
              6: RuntimeError}
 
@@ -97,6 +97,8 @@ def lib() -> C.CDLL:
             "pbkd_run_timed": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int,
                                          C.c_int, C.POINTER(vp)]),
             "pbkd_run_timing": (C.c_int, [vp, dp, ip, C.POINTER(C.c_longlong), vp, C.c_int, ip]),
+            "pbkd_run_profile_count": (C.c_int, [vp]),
+            "pbkd_run_profile_entry": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, ip, dp, dp, dp]),
             "pbkd_bench_kernel": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dp, dp, dp]),
             "pbkd_nccl_unique_id": (C.c_int, [vp]),
             "pbkd_ctx_set_comm": (C.c_int, [vp, vp, C.c_int, C.c_int]),
@@ -372,11 +374,18 @@ class Context:
         check(L.pbkd_run_timing(r, None, None, None, _ptr(ems), ne.value, C.byref(ne)))
         tt = np.zeros(1, np.float64)
         check(L.pbkd_run_timing(r, None, None, None, _ptr(tt), -1, C.byref(ne)))
+        prof = {}
+        for i in range(L.pbkd_run_profile_count(r)):
+            name = C.create_string_buffer(64)
+            nlch, ms, by, fl = C.c_int(), C.c_double(), C.c_double(), C.c_double()
+            check(L.pbkd_run_profile_entry(r, i, name, 64, C.byref(nlch), C.byref(ms), C.byref(by), C.byref(fl)))
+            prof[name.value.decode()] = {"launches": nlch.value, "ms": ms.value, "bytes": by.value,
+                                         "flops": fl.value}
         return {"results": res, "trace": trace, "wall_time_s": L.pbkd_run_wall_time(r),
                 "epoch_ms": L.pbkd_run_epoch_ms(r), "timed_ms": tms.value,
                 "teacher_ms": float(tt[0]),
                 "timed_epochs": tep.value, "launches": nl.value,
-                "epoch_ms_list": ems[:ne.value].tolist()}
+                "epoch_ms_list": ems[:ne.value].tolist(), "profile": prof}
 
     def bench_kernel(self, which, batch, iters=20):
         ms, by, fl = C.c_double(), C.c_double(), C.c_double()

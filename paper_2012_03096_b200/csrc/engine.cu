@@ -92,6 +92,33 @@ DevBuf upload(const std::vector<T>& v, cudaStream_t st) {
     return b;
 }
 
+// ------------------------------------------------------- algorithmic work
+// Compulsory fp32 bytes and flops of one op: what the kernel must
+// move / compute at minimum, not what it does move (pre-split operand planes,
+// halo re-reads and partial sums are overheads against these).
+using Work = std::pair<double, double>;
+double el(long long a, long long b = 1, long long c = 1, long long d = 1) {
+    return static_cast<double>(a) * static_cast<double>(b) * static_cast<double>(c) * static_cast<double>(d);
+}
+Work op_work(const DwFwdOp& o) {
+    return {4.0 * (el(o.n, o.h, o.wd, o.c) + el(o.n, o.ho, o.wo, o.c)), 18.0 * el(o.n, o.ho, o.wo, o.c)};
+}
+Work op_work(const DwBwdOp& o) { return {12.0 * el(o.n, o.h, o.wd, o.c), 36.0 * el(o.n, o.h, o.wd, o.c)}; }
+Work op_work(const DwGkOp& o) {
+    return {4.0 * (el(o.n, o.h, o.wd, o.c) + el(o.n, o.ho, o.wo, o.c)), 18.0 * el(o.n, o.ho, o.wo, o.c)};
+}
+Work op_work(const ReduceOp& o) { return {4.0 * (el(o.parts, o.width) + o.width), el(o.parts, o.width)}; }
+Work op_work(const BnStatOp& o) { return {8.0 * el(o.tiles, o.c), 2.0 * el(o.tiles, o.c)}; }
+Work op_work(const LossOp& o) { return {8.0 * el(o.rows, o.c), 12.0 * el(o.rows, o.c)}; }
+Work op_work(const BnBwdFinOp& o) { return {8.0 * el(o.ctas, o.c), 2.0 * el(o.ctas, o.c)}; }
+Work op_work(const BnBwdApplyOp& o) { return {12.0 * static_cast<double>(o.total), 12.0 * static_cast<double>(o.total)}; }
+Work op_work(const SgdOp& o) { return {20.0 * static_cast<double>(o.n), 4.0 * static_cast<double>(o.n)}; }
+Work op_work(const ScatterOp& o) { return {8.0 * el(o.rows, o.width), 0.0}; }
+Work op_work(const GemmOp& o) {
+    const double a = o.conv ? el(o.M / (o.oh * o.ow), o.ih, o.iw, o.ic) : el(o.M, o.K);
+    return {4.0 * (a + el(o.K, o.N) + el(o.M, o.N)), 2.0 * el(o.M, o.N, o.K)};
+}
+
 // ----------------------------------------------------------------- program
 // A recorded sequence of launches.  Grouped ops keep their descriptor arrays
 // in one device slab; the whole program can be captured into a CUDA graph.
@@ -114,6 +141,12 @@ public:
             launch(reinterpret_cast<const Op*>(slab + off), nd, total, st);
         });
         names_.push_back(op_name(typeid(Op).name()));
+        KernelStat w;
+        for (const Op& o : ops) {
+            const auto bf = op_work(o);
+            w.bytes += bf.first, w.flops += bf.second;
+        }
+        work_.push_back(w);
     }
     // tcgen05 GEMMs: one launch per kernel / N-tile class (the tile is a
     // template parameter), all tasks of that class grouped in it
@@ -138,11 +171,20 @@ public:
             const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
             names_.push_back(std::string("gemm_") + kind + (cls >= kGemmClassTma ? "_tma" : "_reg") +
                              std::to_string(cls % kGemmClassTma));
+            KernelStat w;
+            for (const GemmOp& o : ops) {
+                const auto bf = op_work(o);
+                w.bytes += bf.first, w.flops += bf.second;
+            }
+            work_.push_back(w);
         }
     }
-    void raw(std::function<void(cudaStream_t)> f, const char* name = "raw") {
+    void raw(std::function<void(cudaStream_t)> f, const char* name = "raw", double bytes = 0.0) {
         steps_.push_back([f](cudaStream_t st, const uint8_t*) { f(st); });
         names_.push_back(name);
+        KernelStat w;
+        w.bytes = bytes;
+        work_.push_back(w);
     }
     void finalize(cudaStream_t st) {
         slab_.alloc(std::max<size_t>(host_.size(), 64));
@@ -156,8 +198,8 @@ public:
         for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
     }
     // Eager run with a CUDA event after every launch; adds each launch's
-    // device time to prof[name] (PBKD_PROFILE diagnosis).
-    void run_profiled(cudaStream_t st, std::map<std::string, std::pair<int, double>>& prof) {
+    // device time and algorithmic work to prof[name].
+    void run_profiled(cudaStream_t st, std::map<std::string, KernelStat>& prof) {
         if (!finalized_) finalize(st);
         std::vector<cudaEvent_t> ev(steps_.size() + 1);
         for (auto& e : ev) PBKD_CUDA(cudaEventCreate(&e));
@@ -170,9 +212,11 @@ public:
         for (size_t i = 0; i < steps_.size(); ++i) {
             float ms = 0.0f;
             PBKD_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-            auto& e = prof[names_[i]];
-            e.first += 1;
-            e.second += ms;
+            KernelStat& e = prof[names_[i]];
+            e.launches += 1;
+            e.ms += ms;
+            e.bytes += work_[i].bytes;
+            e.flops += work_[i].flops;
         }
         for (auto& e : ev) cudaEventDestroy(e);
     }
@@ -205,20 +249,24 @@ private:
     DevBuf slab_;
     std::vector<std::function<void(cudaStream_t, const uint8_t*)>> steps_;
     std::vector<std::string> names_;
+    std::vector<KernelStat> work_;
     bool finalized_ = false;
     cudaGraphExec_t exec_ = nullptr;
 };
 
-void print_profile(const char* what, const std::map<std::string, std::pair<int, double>>& prof) {
+void print_profile(const char* what, const std::map<std::string, KernelStat>& prof) {
     double tot = 0.0;
-    for (auto& kv : prof) tot += kv.second.second;
+    for (auto& kv : prof) tot += kv.second.ms;
     std::vector<std::pair<double, std::string>> v;
-    for (auto& kv : prof) v.push_back({kv.second.second, kv.first});
+    for (auto& kv : prof) v.push_back({kv.second.ms, kv.first});
     std::sort(v.rbegin(), v.rend());
     std::fprintf(stderr, "[pbkd-prof] %s: %.3f ms total (eager, events per launch)\n", what, tot);
-    for (auto& [ms, name] : v)
-        std::fprintf(stderr, "[pbkd-prof]   %-24s %5d launches %9.3f ms %5.1f%%  avg %8.1f us\n", name.c_str(),
-                     prof.at(name).first, ms, 100.0 * ms / tot, 1e3 * ms / prof.at(name).first);
+    for (auto& [ms, name] : v) {
+        const KernelStat& k = prof.at(name);
+        std::fprintf(stderr, "[pbkd-prof]   %-22s %5d launches %9.3f ms %5.1f%%  avg %8.1f us  %7.0f GB/s %7.1f TF/s\n",
+                     name.c_str(), k.launches, ms, 100.0 * ms / tot, 1e3 * ms / k.launches, k.bytes / ms / 1e6,
+                     k.flops / ms / 1e9);
+    }
 }
 
 // ------------------------------------------------------------- teacher dev
@@ -1514,7 +1562,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 ep.post->build_graph(st);
             }
             if (std::getenv("PBKD_PROFILE")) {  // one extra eager pass, timed per launch
-                std::map<std::string, std::pair<int, double>> pa, pb;
+                std::map<std::string, KernelStat> pa, pb;
                 ep.pre->run_profiled(st, pa);
                 print_profile("teacher pass", pa);
                 ep.post->run_profiled(st, pb);
@@ -1576,6 +1624,14 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         float ms = 0.0f;
         PBKD_CUDA(cudaEventElapsedTime(&ms, t0, t1e));
         timing.timed_ms += ms;
+    }
+    // outside the timed window
+    if (opt.profile && !graphs.empty()) {  // last epoch's programs once more, per launch
+        EpochProg& ep = graphs.rbegin()->second;
+        ep.pre->run_profiled(st, timing.prof);
+        if (world > 1)
+            comm->all_to_all_v(sendbuf.f(), send_off, send_cnt, recvbuf.f(), recv_off, recv_cnt, st);
+        ep.post->run_profiled(st, timing.prof);
     }
     cudaEventDestroy(t0);
     cudaEventDestroy(t1e);

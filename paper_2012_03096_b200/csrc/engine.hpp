@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -53,6 +54,18 @@ struct RunOptions {
     std::vector<std::pair<int, int>> global_blocks;  // (block index, owner rank)
     int virtual_shards = 1;
     std::vector<double> shard_share;  // teacher share per rank (empty: uniform)
+    // after the last epoch, replay that epoch's programs once more eagerly
+    // with a CUDA event after every launch (per-kernel-class device time and
+    // algorithmic work, RunTiming::prof); training state moves on by one
+    // epoch, so only for measurement runs
+    bool profile = false;
+};
+
+// Per kernel class of a profiled epoch: launches, device ms (events on the
+// engine stream), algorithmic bytes / flops of those launches.
+struct KernelStat {
+    int launches = 0;
+    double ms = 0.0, bytes = 0.0, flops = 0.0;
 };
 
 // Timing of the last run (device events around the epoch graphs).
@@ -65,6 +78,7 @@ struct RunTiming {
     int epochs = 0;
     long long student_steps = 0;  // per task
     long long launches = 0;       // kernel launches in the timed window
+    std::map<std::string, KernelStat> prof;  // RunOptions::profile
 };
 
 class Engine {

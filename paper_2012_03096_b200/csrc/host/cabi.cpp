@@ -227,6 +227,7 @@ int pbkd_run(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* tr, 
         RunOptions opt;
         opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
         opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
+        opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
         auto r = std::make_unique<pbkd_results>();
         r->res = ctx->eng->run(ts, std::vector<int>(tr, tr + n_tr), std::vector<int>(ev, ev + n_ev), opt);
         r->wall = now_s(t0);
@@ -262,6 +263,7 @@ int pbkd_run_timed(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int
         RunOptions opt;
         opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
         opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
+        opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
         opt.timed_from_epoch = timed_from_epoch;
         auto r = std::make_unique<pbkd_results>();
         r->res = ctx->eng->run(ts, std::vector<int>(tr, tr + n_tr), std::vector<int>(ev, ev + n_ev), opt);
@@ -298,6 +300,7 @@ int pbkd_run_sharded(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const i
         RunOptions opt;
         opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
         opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
+        opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
         opt.timed_from_epoch = timed_from_epoch;
         for (int i = 0; i < n_global; ++i) opt.global_blocks.push_back({g_blocks[i], g_owner[i]});
         opt.virtual_shards = virtual_shards;
@@ -394,6 +397,8 @@ int pbkd_run_parallel(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const 
             RunOptions opt;
             opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
             opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
+            opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
+        opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
             std::vector<TaskOutcome> res =
                 ctx->eng->run(ok, std::vector<int>(tr, tr + n_tr), std::vector<int>(ev, ev + n_ev), opt);
             for (TaskOutcome& o : res) outcome[o.block_index] = std::move(o);
@@ -410,6 +415,25 @@ int pbkd_run_parallel(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const 
 }
 
 int pbkd_run_count(const pbkd_results* r) { return r ? static_cast<int>(r->res.size()) : 0; }
+
+int pbkd_run_profile_count(const pbkd_results* r) { return r ? static_cast<int>(r->timing.prof.size()) : 0; }
+
+int pbkd_run_profile_entry(const pbkd_results* r, int i, char* name, size_t cap, int* launches, double* ms,
+                           double* bytes, double* flops) {
+    return guard([&] {
+        need(i >= 0 && i < static_cast<int>(r->timing.prof.size()), "profile entry out of range");
+        auto it = r->timing.prof.begin();
+        std::advance(it, i);
+        if (name && cap) {
+            std::strncpy(name, it->first.c_str(), cap - 1);
+            name[cap - 1] = 0;
+        }
+        *launches = it->second.launches;
+        *ms = it->second.ms;
+        *bytes = it->second.bytes;
+        *flops = it->second.flops;
+    });
+}
 
 int pbkd_run_info(const pbkd_results* r, int i, pbkd_result_info* info) {
     return guard([&] {
