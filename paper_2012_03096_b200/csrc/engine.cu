@@ -151,7 +151,11 @@ public:
     // tcgen05 GEMMs: one launch per kernel / N-tile class (the tile is a
     // template parameter), all tasks of that class grouped in it
     void gemm(std::vector<GemmOp> all) {
-        for (int cls : {32, 64, 128, kGemmClassTma + 32, kGemmClassTma + 64, kGemmClassTma + 128}) {
+        std::vector<int> classes;
+        for (const GemmOp& o : all) classes.push_back(gemm_bn_class(o));
+        std::sort(classes.begin(), classes.end());
+        classes.erase(std::unique(classes.begin(), classes.end()), classes.end());
+        for (int cls : classes) {
             std::vector<GemmOp> ops;
             for (const GemmOp& o : all)
                 if (gemm_bn_class(o) == cls) ops.push_back(o);
@@ -169,7 +173,8 @@ public:
                 launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, cls, st);
             });
             const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
-            names_.push_back(std::string("gemm_") + kind + (cls >= kGemmClassTma ? "_tma" : "_reg") +
+            names_.push_back(std::string("gemm_") + kind +
+                             (cls >= 2 * kGemmClassTma ? "_pre" : cls >= kGemmClassTma ? "_tma" : "_reg") +
                              std::to_string(cls % kGemmClassTma));
             KernelStat w;
             for (const GemmOp& o : ops) {
@@ -925,17 +930,17 @@ struct Engine::Impl {
                 if (s.planes_d[u]) w.b_hi = s.d_hi[u].f(), w.b_lo = s.d_lo[u].f();
                 w.ldb = d.cin;
                 w.b_kmajor = 0;
-                w.C = s.wsplit.f();
                 w.ldc = d.cin;
                 w.epi = 2;
                 w.ksplit = split_count(c.M);
+                // no split: the GEMM writes the gradient itself (C must be final
+                // before gemm_finalize, which builds the TMA store map from it)
+                w.C = w.ksplit == 1 ? s.g_pw(u) : s.wsplit.f();
                 gemm_finalize(w);
                 if (s.planes_d[u] && !(w.a_presplit && w.b_presplit))
                     throw std::logic_error("pre-split operands not consumed by wgrad");
                 w.failed = c.failed;
-                if (w.ksplit == 1) {  // no split: the GEMM writes the gradient itself
-                    w.C = s.g_pw(u);
-                } else {
+                if (w.ksplit > 1) {
                     ReduceOp r{};
                     r.part = s.wsplit.f();
                     r.out = s.g_pw(u);

@@ -82,11 +82,11 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& op, float* acc, int 
         if (epi == 1) {  // per-(m-tile, column) sum / sum of squares, fixed-order trees
 #pragma unroll
             for (int j = 0; j < SL; ++j) {
-                float s = val[j], sq = val[j] * val[j];
+                float s = val[j], sq = __fmul_rn(val[j], val[j]);
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) {
-                    s += __shfl_xor_sync(0xffffffffu, s, off);
-                    sq += __shfl_xor_sync(0xffffffffu, sq, off);
+                    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+                    sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, off));
                 }
                 if (lane == 0) {
                     red[h * 4 + q][j] = s;
@@ -98,9 +98,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& op, float* acc, int 
                 const int hh = et / SL, j = et % SL;
                 const int col = n0 + hh * HB + c0 + j;
                 if (col < N) {
-                    const float s = (red[4 * hh][j] + red[4 * hh + 1][j]) + (red[4 * hh + 2][j] + red[4 * hh + 3][j]);
-                    const float sq = (red[4 * hh][16 + j] + red[4 * hh + 1][16 + j]) +
-                                     (red[4 * hh + 2][16 + j] + red[4 * hh + 3][16 + j]);
+                    const float s = __fadd_rn(__fadd_rn(red[4 * hh][j], red[4 * hh + 1][j]),
+                                              __fadd_rn(red[4 * hh + 2][j], red[4 * hh + 3][j]));
+                    const float sq = __fadd_rn(__fadd_rn(red[4 * hh][16 + j], red[4 * hh + 1][16 + j]),
+                                               __fadd_rn(red[4 * hh + 2][16 + j], red[4 * hh + 3][16 + j]));
                     part0[static_cast<long long>(tm) * N + col] = s;
                     part1[static_cast<long long>(tm) * N + col] = sq;
                 }

@@ -791,6 +791,8 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             launch_gemm_one(st, g);
         }
         if (gw) {
+            const int splits = std::max(1, std::min(64, ceil_div(rows, 512)));
+            Scratch part(static_cast<size_t>(splits) * cout * cin);
             GemmOp g{};
             g.M = cout, g.N = cin, g.K = rows;
             g.A = gy, g.lda = cout, g.a_kmajor = 0;
@@ -798,10 +800,9 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             g.a_hi = pg.h, g.a_lo = pg.l, g.b_hi = px.h, g.b_lo = px.l;
             g.ldc = cin;
             g.epi = 2;
-            g.ksplit = std::max(1, std::min(64, ceil_div(rows, 512)));
-            gemm_finalize(g);
-            Scratch part(static_cast<size_t>(g.ksplit) * cout * cin);
+            g.ksplit = splits;
             g.C = part.p;
+            gemm_finalize(g);
             launch_gemm_one(st, g);
             ReduceOp r{};
             r.part = part.p, r.out = gw, r.parts = g.ksplit, r.width = cout * cin;

@@ -131,6 +131,8 @@ struct GemmOp {
     CUtensorMap map_a, map_b;     // 2-D fp32 maps of A and B (64-byte aligned)
     CUtensorMap map_ah, map_al;   // SWIZZLE_128B maps of the planes
     CUtensorMap map_bh, map_bl;
+    int c_tma;                    // epilogue stores C through shared memory + TMA
+    CUtensorMap map_c;            // 3-D {N, M, ksplit} SWIZZLE_128B map of C
 };
 
 // tf32 hi/lo split on the host, bit-identical to tc::to_tf32 on the device

@@ -286,7 +286,10 @@ void gemm_finalize(GemmOp& o) {
 }
 
 int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
-int gemm_bn_class(const GemmOp& o) { return bn_for(o.N) + (o.tma ? kGemmClassTma : 0); }
+// + kGemmClassTma: TMA kernel; + 2 kGemmClassTma: TMA kernel, both operands pre-split
+int gemm_bn_class(const GemmOp& o) {
+    return bn_for(o.N) + (o.tma ? kGemmClassTma : 0) + (o.tma && o.a_presplit && o.b_presplit ? kGemmClassTma : 0);
+}
 
 template <int BN>
 static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {

@@ -47,19 +47,25 @@ constexpr int kThreadsT = kWarpsT * 32;
 constexpr int kConvThreads = 128;  // warps 2-5
 constexpr int kEpiWarp0 = 6;
 
-template <int BN>
+// PS: every op of the launch takes both operands pre-split (no raw ring, no
+// conversion: deeper operand ring).  cs: C staging for the TMA-store
+// epilogue, one column half (BN/2 columns x 128 rows, 128-byte swizzled
+// 32-column blocks).
+template <int BN, bool PS>
 struct Cfg {
-    static constexpr int R = BN >= 128 ? 2 : BN >= 64 ? 3 : 4;  // raw (TMA) stages
-    static constexpr int S = BN >= 128 ? 2 : 3;  // converted operand stages
+    static constexpr int R = PS ? 0 : (BN >= 64 ? 2 : 4);  // raw (TMA) stages
+    static constexpr int S = PS ? (BN >= 128 ? 3 : BN >= 64 ? 4 : 5) : (BN >= 128 ? 2 : 3);  // operand stages
     static constexpr int a_raw = kBM * kBK * 4;
     static constexpr int b_raw = BN * kBK * 4;
     static constexpr int raw_stage = a_raw + b_raw;
     static constexpr int a_op = kBM * kRowBytes;
     static constexpr int b_op = BN * kRowBytes;
     static constexpr int op_stage = 2 * a_op + 2 * b_op;
-    static constexpr int smem = 1024 + R * raw_stage + S * op_stage;
+    static constexpr int cs = kBM * 32 * 4;  // one 32-column block
+    static constexpr int smem = 1024 + R * raw_stage + S * op_stage + cs;
     static constexpr int A = 4;  // TMEM accumulator slots (one per K chunk in flight)
     static constexpr int tmem_cols = (A * BN <= 128) ? 128 : (A * BN <= 256) ? 256 : 512;
+    static constexpr int RB = R > 0 ? R : 1;  // barrier array sizes
 };
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
@@ -83,8 +89,8 @@ struct TileInfo {
     int op;  // -1: skip (the task's failure flag is set)
     TileGeo g;
 };
-constexpr int kMaxTiles = 128;  // tiles per CTA (host sizes the grid)
-constexpr int kMaxOps = 128;    // ops per launch
+constexpr int kMaxTiles = 64;  // tiles per CTA (host sizes the grid)
+constexpr int kMaxOps = 64;    // ops per launch
 template <int BN>
 __device__ __forceinline__ TileGeo tile_geo(const GemmOp& o, int local) {
     TileGeo g;
@@ -142,6 +148,116 @@ __device__ __forceinline__ void convert_tile(uint32_t raw, uint32_t hi, uint32_t
     }
 }
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Epilogue through shared memory: each column half (BN/2 columns) of the
+// tile is staged as 128-byte-swizzled 32-column blocks (conflict-free
+// thread-per-row 16-byte stores) and written by TMA (whole 128-byte lines,
+// tails clipped per split).  The batch-norm partial sums (epi 1) are taken
+// from the staged tile with the same butterfly tree and quarter order as
+// gemm_epilogue, so both epilogues give identical bits.
+template <int BN>
+__device__ __forceinline__ void staged_epilogue(const GemmOp& op, float* acc, int tm, int tn, int split, int q, int h,
+                                                int lane, int et, float (*red)[4][32], uint32_t cs, int& stores) {
+    constexpr int HB = BN / 2;
+    const int M = op.M, N = op.N, epi = op.epi, relu_on = op.relu;
+    const long long ldc = op.ldc;
+    const float* __restrict__ scale = op.scale;
+    const float* __restrict__ shift = op.shift;
+    const float* __restrict__ skip = op.skip;
+    const int m0 = tm * kBM, n0 = tn * BN;
+    const int r = q * 32 + lane, row = m0 + r;
+    const bool row_ok = row < M;
+#pragma unroll
+    for (int j = 0; j < HB; ++j) {
+        const int n = n0 + h * HB + j;
+        float x = acc[j];
+        if (row_ok && n < N) {
+            if (scale) x = bn_infer_apply(x, __ldg(scale + n), __ldg(shift + n));
+            if (skip) x = add(x, __ldg(skip + static_cast<long long>(row) * ldc + n));
+            if (relu_on) x = relu(x);
+        } else {
+            x = 0.0f;
+        }
+        acc[j] = x;
+    }
+    if (op.c_hi && row_ok) {  // tf32 planes of the output (next GEMM's pre-split operand)
+        const long long off = static_cast<long long>(row) * ldc + n0 + h * HB;
+#pragma unroll
+        for (int j = 0; j < HB; ++j)
+            if (n0 + h * HB + j < N) {
+                const float hv = __uint_as_float(tc_split_hi(acc[j]));
+                op.c_hi[off + j] = hv;
+                op.c_lo[off + j] = __uint_as_float(tc_split_hi(__fsub_rn(acc[j], hv)));
+            }
+    }
+    // 32-column passes (one swizzled 16 KB block each); a pass's 16-byte
+    // chunks belong to whichever column half holds them
+#pragma unroll
+    for (int pass = 0; pass < BN / 32; ++pass) {
+        if (et == 0 && stores) tma_store_wait_read();  // staging block free again
+        named_bar(1, 256);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int col = pass * 32 + 4 * c;  // tile column (compile time)
+            const int hh = col / HB;
+            if (h == hh) {
+                const int j = col - hh * HB;
+                sts128(cs + r * 128 + ((c ^ (r & 7)) << 4), __float_as_uint(acc[j]), __float_as_uint(acc[j + 1]),
+                       __float_as_uint(acc[j + 2]), __float_as_uint(acc[j + 3]));
+            }
+        }
+        fence_async_smem();
+        named_bar(1, 256);
+        if (et == 0) {
+            tma_store_3d(&op.map_c, cs, n0 + pass * 32, m0, epi == 2 ? split : 0);
+            tma_store_commit();
+            stores = 1;
+        }
+        if (epi == 1) {
+            const int col = et & 31, qq = et >> 5;
+            if (qq < 4) {
+                float t[32], u[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int rr = qq * 32 + i;
+                    t[i] = lds32(cs + rr * 128 + ((((col >> 2) ^ (rr & 7))) << 4) + (col & 3) * 4);
+                    u[i] = __fmul_rn(t[i], t[i]);
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                    for (int i = 0; i < off; ++i) {
+                        t[i] = __fadd_rn(t[i], t[i + off]);
+                        u[i] = __fadd_rn(u[i], u[i + off]);
+                    }
+                red[0][qq][col] = t[0];
+                red[1][qq][col] = u[0];
+            }
+            named_bar(1, 256);
+            if (et < 32) {
+                const int cg = n0 + pass * 32 + et;
+                if (cg < N) {
+                    op.part0[static_cast<long long>(tm) * N + cg] =
+                        __fadd_rn(__fadd_rn(red[0][0][et], red[0][1][et]), __fadd_rn(red[0][2][et], red[0][3][et]));
+                    op.part1[static_cast<long long>(tm) * N + cg] =
+                        __fadd_rn(__fadd_rn(red[1][0][et], red[1][1][et]), __fadd_rn(red[1][2][et], red[1][3][et]));
+                }
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
     asm volatile(
@@ -153,15 +269,16 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 
 }  // namespace
 
-template <int BN>
+template <int BN, bool PS>
 __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total, int dbg,
                                                                  unsigned long long* __restrict__ trace) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, PS>;
     constexpr int R = C::R, S = C::S, HB = BN / 2;
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t raw_full[R], raw_empty[R], op_full[S], op_empty[S], acc_full[C::A], acc_empty[C::A];
+    __shared__ uint64_t raw_full[C::RB], raw_empty[C::RB], op_full[S], op_empty[S], acc_full[C::A], acc_empty[C::A];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ float red[8][32];
+    __shared__ float red_buf[256];  // [8][32] (gemm_epilogue) or [2][4][32] (staged_epilogue)
+    auto red = reinterpret_cast<float(*)[4][32]>(red_buf);
     __shared__ int begins[kMaxOps];
     __shared__ TileInfo tiles_sh[kMaxTiles];
 
@@ -180,6 +297,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     uint8_t* raw_ring = smem_raw + pad;  // stays a shared-space pointer
     uint8_t* op_ring = raw_ring + R * C::raw_stage;
     const uint32_t raw_s = sbase + pad, op_s = raw_s + R * C::raw_stage;
+    const uint32_t cs_s = op_s + S * C::op_stage;  // epilogue staging (C::cs bytes)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (warp == 1) {
@@ -193,7 +311,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             mbar_init(&raw_empty[i], kConvThreads / 32);
         }
         for (int i = 0; i < S; ++i) {
-            mbar_init(&op_full[i], kConvThreads / 32 + 1);  // + the B warp's arrive
+            mbar_init(&op_full[i], PS ? 1 : kConvThreads / 32 + 1);  // converters + the loader warp
             mbar_init(&op_empty[i], 1);
         }
         for (int i = 0; i < C::A; ++i) {
@@ -229,6 +347,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
+        if (PS) goto done;  // nothing to convert: no raw loads
         uint32_t it = 0;
         for (int j = 0; j < ntiles; ++j) {
             if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
@@ -352,6 +471,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                         continue;
                     }
                     mbar_arrive_expect_tx(&op_full[s], bytes);
+                    mark(0, it);
                     uint8_t* os = op_ring + s * C::op_stage;
                     const int k = g.k0 + kc * kBK;
                     if (apre) {
@@ -392,6 +512,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
         }
     } else if (warp < kEpiWarp0) {
         // ------------------------------------------------------ converters
+        if (PS) goto done;
         const int ct = tid - 64;
         uint32_t it = 0;
         for (int j = 0; j < ntiles; ++j) {
@@ -426,6 +547,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
         // ------------------------------------------------------ drain + epilogue
         const int q = warp & 3, h = (warp - kEpiWarp0) >> 2, et = tid - kEpiWarp0 * 32;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        int stores = 0;  // TMA store groups in flight (elected thread)
         uint32_t it = 0;
         for (int j = 0; j < ntiles; ++j) {
             if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
@@ -450,11 +572,21 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     if (warp == kEpiWarp0) mark(3, it);
                 }
             }
-            if (!(dbg & 4)) gemm_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, [] { named_bar(1, 256); });
+            if (!(dbg & 4)) {
+                if (o.c_tma)
+                    staged_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
+                else
+                    gemm_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, reinterpret_cast<float(*)[32]>(red_buf),
+                                      [] { named_bar(1, 256); });
+            }
             if (warp == kEpiWarp0 && lane == 0) mark(4, j);
         }
     }
+    // the thread that issued the TMA stores waits for them before the CTA's
+    // shared memory goes away (bulk async-groups are per thread)
+    if (tid == kEpiWarp0 * 32) tma_store_wait_all();
     (void)op_ring;
+done:
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -502,11 +634,12 @@ int num_sms() {
     return n;
 }
 
-template <int BN>
+template <int BN, bool PS>
 void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::smem));
+        PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg<BN, PS>::smem));
         attr = true;
     }
     if (nd > kMaxOps) throw CudaError("umma_tma: too many ops in one launch");
@@ -525,7 +658,7 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         PBKD_CUDA(cudaMalloc(&trace, 10 * 512 * sizeof(unsigned long long)));
     unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
     if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, 10 * 512 * sizeof(unsigned long long), st));
-    umma_tma_kernel<BN><<<grid, kThreadsT, Cfg<BN>::smem, st>>>(d, nd, total, dbg, tr);
+    umma_tma_kernel<BN, PS><<<grid, kThreadsT, Cfg<BN, PS>::smem, st>>>(d, nd, total, dbg, tr);
     PBKD_LAUNCH_CHECK();
     static const int trace_from = [] {
         const char* e = std::getenv("PBKD_GEMM_TRACE");
@@ -624,6 +757,21 @@ void presplit_maps(GemmOp& o) {
     }
 }
 
+// C written through shared memory + TMA store: 3-D {N, M, ksplit} map with
+// 128-byte swizzle (32-column boxes of 128 rows, clipped per split).
+bool encode_c(GemmOp& o) {
+    if (!o.C || (reinterpret_cast<uintptr_t>(o.C) & 15) != 0 || (o.ldc * 4) % 16 != 0) return false;
+    const long long splits = o.epi == 2 ? o.ksplit : 1;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(o.N), static_cast<cuuint64_t>(o.M),
+                                static_cast<cuuint64_t>(splits)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(o.ldc) * 4, static_cast<cuuint64_t>(o.ldc) * o.M * 4};
+    const cuuint32_t box[3] = {32, static_cast<cuuint32_t>(kBM), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode_fn()(&o.map_c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, o.C, dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // TMA eligibility + tensor maps (called from gemm_finalize).
 bool gemm_tma_prepare(GemmOp& o) {
     const int bn = o.bn;
@@ -635,11 +783,15 @@ bool gemm_tma_prepare(GemmOp& o) {
         if (!conv_on || o.ksplit != 1 || !o.b_kmajor) return false;
         if (!(encode_conv(&o.map_a, o) && encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn))) return false;
         presplit_maps(o);
+        o.c_tma = encode_c(o) ? 1 : 0;
         return true;
     }
     bool ok = o.a_kmajor ? encode(&o.map_a, o.A, o.K, o.M, o.lda, kBK, kBM) : encode(&o.map_a, o.A, o.M, o.K, o.lda, kBM, kBK);
     ok = ok && (o.b_kmajor ? encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn) : encode(&o.map_b, o.B, o.N, o.K, o.ldb, bn, kBK));
-    if (ok) presplit_maps(o);
+    if (ok) {
+        presplit_maps(o);
+        o.c_tma = encode_c(o) ? 1 : 0;
+    }
     return ok;
 }
 
@@ -660,11 +812,15 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
     }
 }
 
+// bn: N tile, + kGemmClassTma when every op of the launch is fully pre-split
 void launch_gemm_tma(const GemmOp* d, int nd, int total, int bn, cudaStream_t st) {
     switch (bn) {
-        case 32: launch_tma_t<32>(d, nd, total, st); break;
-        case 64: launch_tma_t<64>(d, nd, total, st); break;
-        default: launch_tma_t<128>(d, nd, total, st); break;
+        case 32: launch_tma_t<32, false>(d, nd, total, st); break;
+        case 64: launch_tma_t<64, false>(d, nd, total, st); break;
+        case 128: launch_tma_t<128, false>(d, nd, total, st); break;
+        case kGemmClassTma + 32: launch_tma_t<32, true>(d, nd, total, st); break;
+        case kGemmClassTma + 64: launch_tma_t<64, true>(d, nd, total, st); break;
+        default: launch_tma_t<128, true>(d, nd, total, st); break;
     }
 }
 

@@ -11,7 +11,7 @@ import torch
 import paper_2012_03096_b200 as P
 
 SHAPES = [(32768, 64, 64), (8192, 64, 128), (2048, 128, 256), (512, 256, 512), (128, 512, 512),
-          (1000, 20, 48), (300, 96, 40), (4096, 3, 64)]
+          (1000, 20, 48), (300, 96, 40), (4096, 3, 64), (2048, 16, 16), (1000, 24, 20), (2048, 16, 32)]
 
 
 def main(out):
@@ -33,7 +33,8 @@ def main(out):
             res[f"{key}_{name}"] = t.cpu().numpy()
         # fp64 reference for the dump's own sanity
         xd, wd, gyd = (t.double().cpu().numpy() for t in (x, w, gy))
-        for name, want in (("y", xd @ wd.T), ("gx", gyd @ wd), ("gw", gyd.T @ xd)):
+        yd = xd @ wd.T
+        for name, want in (("y", yd), ("gx", gyd @ wd), ("gw", gyd.T @ xd), ("cs", yd.sum(0)), ("cq", (yd * yd).sum(0))):
             got = res[f"{key}_{name}"].astype(np.float64)
             err = np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-30)
             if err > 1e-5:
