@@ -158,63 +158,64 @@ __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk
 __device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// Epilogue through shared memory: each column half (BN/2 columns) of the
-// tile is staged as 128-byte-swizzled 32-column blocks (conflict-free
-// thread-per-row 16-byte stores) and written by TMA (whole 128-byte lines,
-// tails clipped per split).  The batch-norm partial sums (epi 1) are taken
-// from the staged tile with the same butterfly tree and quarter order as
-// gemm_epilogue, so both epilogues give identical bits.
+// Epilogue through shared memory, in 32-column passes: the pass's block of
+// the tile (128 rows x 32 columns, 128-byte swizzled: conflict-free
+// thread-per-row 16-byte stores) is staged, optionally transformed in place
+// (teacher conv: BN affine, skip add, ReLU, tf32 planes of the output),
+// written by one TMA store (whole 128-byte lines, tails clipped per split)
+// and, for epi 1, reduced into the batch-norm partial sums: warp-level
+// butterflies over each 32-row quarter and the quarter order of
+// gemm_epilogue, so both epilogues give identical bits.  Loops that need no
+// register arrays stay rolled: the kernel's code must fit the instruction
+// cache next to the producer / MMA roles.
+__device__ __forceinline__ uint32_t cs_addr(uint32_t cs, int r, int col) {  // element (r, col) of a block
+    return cs + r * 128 + ((((col >> 2) ^ (r & 7))) << 4) + (col & 3) * 4;
+}
+
 template <int BN>
-__device__ __forceinline__ void staged_epilogue(const GemmOp& op, float* acc, int tm, int tn, int split, int q, int h,
-                                                int lane, int et, float (*red)[4][32], uint32_t cs, int& stores) {
+__device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* acc, int tm, int tn, int split, int q,
+                                                int h, int lane, int et, float (*red)[4][32], uint32_t cs,
+                                                int& stores) {
     constexpr int HB = BN / 2;
-    const int M = op.M, N = op.N, epi = op.epi, relu_on = op.relu;
-    const long long ldc = op.ldc;
-    const float* __restrict__ scale = op.scale;
-    const float* __restrict__ shift = op.shift;
-    const float* __restrict__ skip = op.skip;
+    const int warp8 = et >> 5;
+    const int M = op.M, N = op.N, epi = op.epi;
     const int m0 = tm * kBM, n0 = tn * BN;
-    const int r = q * 32 + lane, row = m0 + r;
-    const bool row_ok = row < M;
-#pragma unroll
-    for (int j = 0; j < HB; ++j) {
-        const int n = n0 + h * HB + j;
-        float x = acc[j];
-        if (row_ok && n < N) {
-            if (scale) x = bn_infer_apply(x, __ldg(scale + n), __ldg(shift + n));
-            if (skip) x = add(x, __ldg(skip + static_cast<long long>(row) * ldc + n));
-            if (relu_on) x = relu(x);
-        } else {
-            x = 0.0f;
-        }
-        acc[j] = x;
-    }
-    if (op.c_hi && row_ok) {  // tf32 planes of the output (next GEMM's pre-split operand)
-        const long long off = static_cast<long long>(row) * ldc + n0 + h * HB;
-#pragma unroll
-        for (int j = 0; j < HB; ++j)
-            if (n0 + h * HB + j < N) {
-                const float hv = __uint_as_float(tc_split_hi(acc[j]));
-                op.c_hi[off + j] = hv;
-                op.c_lo[off + j] = __uint_as_float(tc_split_hi(__fsub_rn(acc[j], hv)));
-            }
-    }
-    // 32-column passes (one swizzled 16 KB block each); a pass's 16-byte
-    // chunks belong to whichever column half holds them
+    const int r = q * 32 + lane;
+    const bool xform = op.scale || op.skip || op.relu || op.c_hi;
 #pragma unroll
     for (int pass = 0; pass < BN / 32; ++pass) {
         if (et == 0 && stores) tma_store_wait_read();  // staging block free again
         named_bar(1, 256);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            constexpr int dummy = 0;
-            (void)dummy;
             const int col = pass * 32 + 4 * c;  // tile column (compile time)
             const int hh = col / HB;
             if (h == hh) {
                 const int j = col - hh * HB;
                 sts128(cs + r * 128 + ((c ^ (r & 7)) << 4), __float_as_uint(acc[j]), __float_as_uint(acc[j + 1]),
                        __float_as_uint(acc[j + 2]), __float_as_uint(acc[j + 3]));
+            }
+        }
+        if (xform) {  // thread = column (lane), rows strided by warp
+            named_bar(1, 256);
+            const int n = n0 + pass * 32 + lane;
+            const long long ldc = op.ldc;
+            float sc = 1.0f, sh = 0.0f;
+            if (op.scale && n < N) sc = __ldg(op.scale + n), sh = __ldg(op.shift + n);
+            for (int rr = warp8; rr < kBM; rr += 8) {
+                const int row = m0 + rr;
+                if (row >= M || n >= N) continue;
+                const uint32_t a = cs_addr(cs, rr, lane);
+                float x = lds32(a);
+                if (op.scale) x = bn_infer_apply(x, sc, sh);
+                if (op.skip) x = add(x, __ldg(op.skip + static_cast<long long>(row) * ldc + n));
+                if (op.relu) x = relu(x);
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
+                if (op.c_hi) {
+                    const float hv = __uint_as_float(tc_split_hi(x));
+                    op.c_hi[static_cast<long long>(row) * ldc + n] = hv;
+                    op.c_lo[static_cast<long long>(row) * ldc + n] = __uint_as_float(tc_split_hi(__fsub_rn(x, hv)));
+                }
             }
         }
         fence_async_smem();
@@ -225,24 +226,20 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, float* acc, in
             stores = 1;
         }
         if (epi == 1) {
-            const int col = et & 31, qq = et >> 5;
-            if (qq < 4) {
-                float t[32], u[32];
+            // (column, quarter) pairs over the 8 warps; lane = row of the quarter
+            for (int pq = warp8; pq < 128; pq += 8) {
+                const int col = pq & 31, qq = pq >> 5;
+                const float v = lds32(cs_addr(cs, qq * 32 + lane, col));
+                float sv = v, sq = __fmul_rn(v, v);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int rr = qq * 32 + i;
-                    t[i] = lds32(cs + rr * 128 + ((((col >> 2) ^ (rr & 7))) << 4) + (col & 3) * 4);
-                    u[i] = __fmul_rn(t[i], t[i]);
+                for (int off = 16; off > 0; off >>= 1) {
+                    sv = __fadd_rn(sv, __shfl_xor_sync(0xffffffffu, sv, off));
+                    sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, off));
                 }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-                    for (int i = 0; i < off; ++i) {
-                        t[i] = __fadd_rn(t[i], t[i + off]);
-                        u[i] = __fadd_rn(u[i], u[i + off]);
-                    }
-                red[0][qq][col] = t[0];
-                red[1][qq][col] = u[0];
+                if (lane == 0) {
+                    red[0][qq][col] = sv;
+                    red[1][qq][col] = sq;
+                }
             }
             named_bar(1, 256);
             if (et < 32) {
@@ -270,7 +267,7 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 }  // namespace
 
 template <int BN, bool PS>
-__global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total, int dbg,
+__global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total,
                                                                  unsigned long long* __restrict__ trace) {
     using C = Cfg<BN, PS>;
     constexpr int R = C::R, S = C::S, HB = BN / 2;
@@ -282,7 +279,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     __shared__ int begins[kMaxOps];
     __shared__ TileInfo tiles_sh[kMaxTiles];
 
-    // PBKD_GEMM_TRACE: CTA 0 timestamps (globaltimer ns) per pipeline event
+    // Pipeline tracer (build with -DPBKD_GEMM_TRACE_BUILD, run with
+    // PBKD_GEMM_TRACE=<launch>): CTA 0 globaltimer stamps per event.
+#ifdef PBKD_GEMM_TRACE_BUILD
     const bool tr_on = trace != nullptr && blockIdx.x == 0;
     auto mark = [&](int ev, uint32_t i) {
         if (tr_on && i < 512) {
@@ -291,6 +290,10 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             trace[ev * 512 + i] = t;
         }
     };
+#else
+    auto mark = [](int, uint32_t) {};
+    (void)trace;
+#endif
     if (threadIdx.x == 0) mark(5, 0);
     const uint32_t sbase = smem_u32(smem_raw);
     const uint32_t pad = (1024u - (sbase & 1023u)) & 1023u;
@@ -366,10 +369,6 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     const int r = it % R;
                     mbar_wait(&raw_empty[r], ((it / R) & 1) ^ 1);
                     uint8_t* st = raw_ring + r * C::raw_stage;
-                    if (dbg & 8) {  // diagnosis: no loads
-                        mbar_arrive(&raw_full[r]);
-                        continue;
-                    }
                     const uint32_t bytes = (o.a_presplit ? 0 : C::a_raw) + (o.b_presplit ? 0 : C::b_raw);
                     if (bytes == 0) {  // both operands go straight to the operand ring
                         mbar_arrive(&raw_full[r]);
@@ -421,8 +420,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                 tc_fence_after();
                 const uint32_t ah = op_s + s * C::op_stage, al = ah + C::a_op, bh = al + C::a_op, bl = bh + C::b_op;
                 if (elect_one()) {
-                    if (dbg & 2) {
-                    } else if ((amn || bmn) && terms == 3) {
+                    if ((amn || bmn) && terms == 3) {
                         // MN-major (BASE32B): atoms of 32 MN x 4 K (512 B), MN atoms
                         // 4096 B apart (one TMA box each); a k-step of 8 advances 1024 B
                         constexpr uint32_t lbo = 4096, sbo = 512;
@@ -453,7 +451,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
             const int m0 = g.tm * kBM, n0 = g.tn * BN;
-            const bool apre = o.a_presplit != 0 && !(dbg & 8), bpre = o.b_presplit != 0 && !(dbg & 8);
+            const bool apre = o.a_presplit != 0, bpre = o.b_presplit != 0;
             const bool akm = o.conv != 0 || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
             int img = 0, y0 = 0;
             if (o.conv) {
@@ -529,9 +527,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                 if (warp == 2 && lane == 0) mark(7, it);
                 const uint32_t rs = raw_s + r * C::raw_stage;
                 const uint32_t os = op_s + s * C::op_stage;
-                if (!(dbg & 1) && !o.a_presplit) convert_tile(rs, os, os + C::a_op, kBM, akm, split3, ct);
+                if (!o.a_presplit) convert_tile(rs, os, os + C::a_op, kBM, akm, split3, ct);
                 if (warp == 2 && lane == 0) mark(8, it);
-                if (!o.b_presplit && !(dbg & 1))
+                if (!o.b_presplit)
                     convert_tile(rs + C::a_raw, os + 2 * C::a_op, os + 2 * C::a_op + C::b_op, BN, bkm, split3, ct);
                 if (warp == 2 && lane == 0) mark(9, it);
                 fence_async_smem();
@@ -561,10 +559,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                 mbar_wait(&acc_full[a], (it / C::A) & 1);
                 tc_fence_after();
                 const uint32_t base = tmem + lane_off + a * BN + h * HB;
-                if (!(dbg & 4)) {
 #pragma unroll
-                    for (int c0 = 0; c0 < HB; c0 += 16) tmem_add16(base + c0, acc + c0);
-                }
+                for (int c0 = 0; c0 < HB; c0 += 16) tmem_add16(base + c0, acc + c0);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
@@ -572,13 +568,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     if (warp == kEpiWarp0) mark(3, it);
                 }
             }
-            if (!(dbg & 4)) {
-                if (o.c_tma)
-                    staged_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
-                else
-                    gemm_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, reinterpret_cast<float(*)[32]>(red_buf),
-                                      [] { named_bar(1, 256); });
-            }
+            staged_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
             if (warp == kEpiWarp0 && lane == 0) mark(4, j);
         }
     }
@@ -644,12 +634,6 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     }
     if (nd > kMaxOps) throw CudaError("umma_tma: too many ops in one launch");
     const int grid = std::max({1, std::min(total, num_sms()), (total + kMaxTiles - 1) / kMaxTiles});
-    // PBKD_GEMM_DBG (diagnosis only, wrong results): 1 skip conversion,
-    // 2 skip MMAs, 4 skip drain/epilogue, 8 skip TMA loads
-    static const int dbg = [] {
-        const char* e = std::getenv("PBKD_GEMM_DBG");
-        return e ? std::atoi(e) : 0;
-    }();
     static const bool trace_on = std::getenv("PBKD_GEMM_TRACE") != nullptr;
     static unsigned long long* trace = nullptr;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -658,7 +642,7 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         PBKD_CUDA(cudaMalloc(&trace, 10 * 512 * sizeof(unsigned long long)));
     unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
     if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, 10 * 512 * sizeof(unsigned long long), st));
-    umma_tma_kernel<BN, PS><<<grid, kThreadsT, Cfg<BN, PS>::smem, st>>>(d, nd, total, dbg, tr);
+    umma_tma_kernel<BN, PS><<<grid, kThreadsT, Cfg<BN, PS>::smem, st>>>(d, nd, total, tr);
     PBKD_LAUNCH_CHECK();
     static const int trace_from = [] {
         const char* e = std::getenv("PBKD_GEMM_TRACE");
@@ -679,6 +663,9 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
                          i, rel(0, i), rel(6, i), rel(7, i), rel(8, i), rel(9, i), rel(1, i), rel(2, i), rel(3, i));
         for (int j = 0; j < 512 && h[4 * 512 + j]; ++j)
             std::fprintf(stderr, "[gemm-trace]   tile %3d epilogue end %8lld\n", j, rel(4, j));
+        std::fprintf(stderr, "[gemm-trace]   tile 0 epilogue: staged start %lld passes", rel(9, 0));
+        for (int p = 0; p < 4; ++p) std::fprintf(stderr, " %lld", rel(8, p));
+        std::fprintf(stderr, "\n");
     }
 }
 
@@ -784,7 +771,7 @@ bool gemm_tma_prepare(GemmOp& o) {
         if (!(encode_conv(&o.map_a, o) && encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn))) return false;
         presplit_maps(o);
         o.c_tma = encode_c(o) ? 1 : 0;
-        return true;
+        return o.c_tma != 0;
     }
     bool ok = o.a_kmajor ? encode(&o.map_a, o.A, o.K, o.M, o.lda, kBK, kBM) : encode(&o.map_a, o.A, o.M, o.K, o.lda, kBM, kBK);
     ok = ok && (o.b_kmajor ? encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn) : encode(&o.map_b, o.B, o.N, o.K, o.ldb, bn, kBK));
@@ -792,7 +779,7 @@ bool gemm_tma_prepare(GemmOp& o) {
         presplit_maps(o);
         o.c_tma = encode_c(o) ? 1 : 0;
     }
-    return ok;
+    return ok && o.c_tma != 0;  // the TMA kernel's epilogue stores through the C map
 }
 
 void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
