@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cctype>
 #include <cstdio>
+#include <thread>
 #include <typeinfo>
 #include <cstdlib>
 #include <cstring>
@@ -299,18 +300,13 @@ ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, 
     d.stride = conv.stride;
     d.pad = conv.padding;
     const int kk = d.k * d.k;
-    std::vector<float> w(static_cast<size_t>(d.cout) * kk * d.cin);
-    for (int o = 0; o < d.cout; ++o)
-        for (int j = 0; j < d.cin; ++j)
-            for (int t = 0; t < kk; ++t)
-                w[(static_cast<size_t>(o) * kk + t) * d.cin + j] =
-                    conv.weight.data[(static_cast<size_t>(o) * d.cin + j) * kk + t];
-    d.w = upload(w, st);
-    {
-        std::vector<float> hi(w.size()), lo(w.size());
-        tf32_split_host(w.data(), w.size(), hi.data(), lo.data());
-        d.w_hi = upload(hi, st);
-        d.w_lo = upload(lo, st);
+    const size_t nw = static_cast<size_t>(d.cout) * kk * d.cin;
+    {  // relayout [cout][cin][kk] -> [cout][kk][cin] and tf32 split on the device
+        DevBuf raw = upload(conv.weight.data, st);
+        d.w.alloc(nw * sizeof(float));
+        d.w_hi.alloc(nw * sizeof(float));
+        d.w_lo.alloc(nw * sizeof(float));
+        launch_conv_weight_prep(raw.f(), d.cout, d.cin, kk, d.w.f(), d.w_hi.f(), d.w_lo.f(), st);
     }
     if (bn) {
         std::vector<float> sc(d.cout), sh(d.cout);
@@ -398,6 +394,9 @@ struct TaskState {
     DevBuf scale, shift;        // inference affine [units][cout]
     // bookkeeping
     DevBuf step_loss, epoch_loss, failed, best, take, eval_acc, baseline;
+    // host copy of the initial parameters / moving stats (init_task_host)
+    std::vector<float> host_params, host_stats;
+    bool host_ready = false;
     int n_evals_planned = 0;
     std::vector<int> eval_epochs;
     float* w_dw(int u) const { return params.f() + off_dw[u]; }
@@ -443,6 +442,8 @@ struct Engine::Impl {
     RunTiming timing;
     std::unique_ptr<NcclComm> comm;
     PhaseTrace trace;
+    void* pinned = nullptr;  // readback staging (grows as needed)
+    size_t pinned_bytes = 0;
 
     explicit Impl(int device) : dev(device) {
         PBKD_CUDA(cudaSetDevice(dev));
@@ -463,6 +464,7 @@ struct Engine::Impl {
             cudaStreamSynchronize(st);
             cudaStreamDestroy(st);
         }
+        if (pinned) cudaFreeHost(pinned);
         g_alloc_stream = nullptr;
     }
 
@@ -473,10 +475,11 @@ struct Engine::Impl {
         return m;
     }
 
-    void load_teacher(const Network& n) {
+    void load_teacher(Network n_in) {
         PBKD_CUDA(cudaSetDevice(dev));
         g_alloc_stream = st;
-        net = n;
+        net = std::move(n_in);
+        const Network& n = net;
         tblocks.clear();
         int c = n.in_c, h = n.in_h, w = n.in_w;
         for (const Block& b : n.blocks) {
@@ -597,7 +600,8 @@ struct Engine::Impl {
                             " is not implemented on the GPU path");
     }
 
-    void init_task(TaskState& s, const DistillTask& t, int ntrain, int neval) {
+    // task, block index, unit geometry (what init_task_host needs)
+    void task_dims(TaskState& s, const DistillTask& t) const {
         s.task = t;
         s.k = t.block_index;
         const TBlockDev& tb = tblocks[static_cast<size_t>(s.k) - 1];
@@ -606,6 +610,12 @@ struct Engine::Impl {
         for (int u = 0; u < s.units; ++u)
             s.u[u] = u == 0 ? UnitDims{tb.cin, tb.hin, tb.win, tb.cout, ho, wo, tb.c1.stride}
                             : UnitDims{tb.cout, ho, wo, tb.cout, ho, wo, 1};
+    }
+
+    void init_task(TaskState& s, const DistillTask& t, int ntrain, int neval) {
+        task_dims(s, t);
+        const TBlockDev& tb = tblocks[static_cast<size_t>(s.k) - 1];
+        const int ho = s.u[0].ho, wo = s.u[0].wo;
         if (ho != tb.hout || wo != tb.wout) throw SpecError("candidate output shape differs from teacher block");
         s.in_row = tb.cin * tb.hin * tb.win;
         s.out_row = tb.cout * ho * wo;
@@ -623,11 +633,39 @@ struct Engine::Impl {
             if (s.steps_in_epoch[e] > 0 && e % t.eval_every == 0) s.eval_epochs.push_back(e);
         s.n_evals_planned = static_cast<int>(s.eval_epochs.size());
 
-        // parameters: candidate init on the host (bit-exact), device layout
-        pbkd::ReplacementBlock cand = pbkd::build_candidate(t.kind, tb.cin, tb.cout, tb.c1.stride,
+        if (!s.host_ready) init_task_host(s);
+        std::vector<float>& host = s.host_params;
+        std::vector<float>& stats = s.host_stats;
+        s.nparams = host.size();
+        s.nstats = stats.size();
+        s.params = upload(host, st);
+        s.planes_w = false;
+        for (int u = 0; u < s.units; ++u) s.planes_w = s.planes_w || gemm_presplit_ok(s.u[u].cin);
+        if (s.planes_w) {
+            s.params_hi.alloc(host.size() * sizeof(float));
+            s.params_lo.alloc(host.size() * sizeof(float));
+            launch_tf32_split(s.params.f(), static_cast<long long>(host.size()), s.params_hi.f(), s.params_lo.f(), st);
+        }
+        s.grads.alloc(s.nparams * sizeof(float));
+        PBKD_CUDA(cudaMemsetAsync(s.grads.p, 0, s.nparams * sizeof(float), st));
+        s.vel.alloc(s.nparams * sizeof(float));
+        PBKD_CUDA(cudaMemsetAsync(s.vel.p, 0, s.nparams * sizeof(float), st));
+        s.mstats = upload(stats, st);
+        s.snapshot.alloc((s.nparams + s.nstats) * sizeof(float));
+        init_task_device(s, B, ho, wo, tb, ntrain, neval, total, spe);
+    }
+
+    // Host half of init_task (no CUDA calls; run for all tasks in parallel):
+    // the candidate's seeded init (build_candidate, bit-exact) in the device
+    // parameter layout.
+    static void init_task_host(TaskState& s) {
+        const DistillTask& t = s.task;
+        pbkd::ReplacementBlock cand = pbkd::build_candidate(t.kind, s.u[0].cin, s.u[0].cout, s.u[0].stride,
                                                             pbkd::mix_seed(t.seed, 0));
-        std::vector<float> host;
-        std::vector<float> stats;
+        std::vector<float>& host = s.host_params;
+        std::vector<float>& stats = s.host_stats;
+        host.clear();
+        stats.clear();
         size_t li = 0;
         for (int u = 0; u < s.units; ++u) {
             const pbkd::LayerParams& dwl = cand.block.layers[li];
@@ -653,24 +691,11 @@ struct Engine::Impl {
             stats.insert(stats.end(), bnl.moving_var.data.begin(), bnl.moving_var.data.end());
         }
         while (host.size() % 4) host.push_back(0.0f);  // vector-friendly padding (never trained)
-        s.nparams = host.size();
-        s.nstats = stats.size();
-        s.params = upload(host, st);
-        s.planes_w = false;
-        for (int u = 0; u < s.units; ++u) s.planes_w = s.planes_w || gemm_presplit_ok(s.u[u].cin);
-        if (s.planes_w) {
-            std::vector<float> hi(host.size()), lo(host.size());
-            tf32_split_host(host.data(), host.size(), hi.data(), lo.data());
-            s.params_hi = upload(hi, st);
-            s.params_lo = upload(lo, st);
-        }
-        s.grads.alloc(s.nparams * sizeof(float));
-        PBKD_CUDA(cudaMemsetAsync(s.grads.p, 0, s.nparams * sizeof(float), st));
-        s.vel.alloc(s.nparams * sizeof(float));
-        PBKD_CUDA(cudaMemsetAsync(s.vel.p, 0, s.nparams * sizeof(float), st));
-        s.mstats = upload(stats, st);
-        s.snapshot.alloc((s.nparams + s.nstats) * sizeof(float));
+        s.host_ready = true;
+    }
 
+    void init_task_device(TaskState& s, int B, int ho, int wo, const TBlockDev& tb, int ntrain, int neval,
+                          long long total, int spe) {
         // streams and workspace
         s.in_stream.alloc(static_cast<size_t>(ntrain) * s.in_row * sizeof(float));
         s.tgt_stream.alloc(static_cast<size_t>(ntrain) * s.out_row * sizeof(float));
@@ -1166,8 +1191,14 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
     std::vector<std::unique_ptr<TaskState>> states;
     for (const DistillTask& t : tasks) {
         states.push_back(std::make_unique<TaskState>());
-        init_task(*states.back(), t, ntrain, neval);
+        task_dims(*states.back(), t);
     }
+    {  // candidate inits (host RNG, bit-exact) for all tasks in parallel
+        std::vector<std::thread> pool;
+        for (auto& sp : states) pool.emplace_back([p = sp.get()] { init_task_host(*p); });
+        for (std::thread& th : pool) th.join();
+    }
+    for (size_t i = 0; i < tasks.size(); ++i) init_task(*states[i], tasks[i], ntrain, neval);
     trace.mark("run: init tasks");
     DevBuf d_train = upload(train_idx, st), d_eval = upload(eval_idx, st);
     std::vector<int> iota(static_cast<size_t>(std::max(ntrain, neval)));
@@ -1183,28 +1214,68 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
     for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota);
 
     trace.mark("run: groups done");
-    // ---- read back and assemble train_block results
+    // ---- read back and assemble train_block results: every task's arrays
+    // in one batch of async copies into a persistent pinned buffer, one sync
+    struct Rb {
+        size_t losses, accs, base, best, fin, snap;
+    };
+    std::vector<Rb> rb(states.size());
+    size_t rb_bytes = 0;
+    auto take = [&](size_t n) {
+        const size_t o = rb_bytes;
+        rb_bytes += (n + 7) & ~size_t(7);
+        return o;
+    };
+    for (size_t i = 0; i < states.size(); ++i) {
+        TaskState& s = *states[i];
+        const int spe = ceil_div(ntrain, s.task.batch_size);
+        rb[i].losses = take(static_cast<size_t>(std::max<long long>(s.total_steps, 1)) * sizeof(float));
+        rb[i].accs = take(static_cast<size_t>(s.n_evals_planned) * sizeof(double));
+        rb[i].base = take(static_cast<size_t>(spe) * sizeof(double));
+        rb[i].best = take(sizeof(double));
+        rb[i].fin = take((s.nparams + s.nstats) * sizeof(float));
+        rb[i].snap = take((s.nparams + s.nstats) * sizeof(float));
+    }
+    if (rb_bytes > pinned_bytes) {
+        if (pinned) cudaFreeHost(pinned);
+        PBKD_CUDA(cudaMallocHost(&pinned, rb_bytes));
+        pinned_bytes = rb_bytes;
+    }
+    uint8_t* hb = static_cast<uint8_t*>(pinned);
+    for (size_t i = 0; i < states.size(); ++i) {
+        TaskState& s = *states[i];
+        const int spe = ceil_div(ntrain, s.task.batch_size);
+        auto cp = [&](size_t off, const void* src, size_t n) {
+            if (n) PBKD_CUDA(cudaMemcpyAsync(hb + off, src, n, cudaMemcpyDeviceToHost, st));
+        };
+        cp(rb[i].losses, s.step_loss.p, static_cast<size_t>(std::max<long long>(s.total_steps, 1)) * sizeof(float));
+        cp(rb[i].accs, s.eval_acc.p, static_cast<size_t>(s.n_evals_planned) * sizeof(double));
+        cp(rb[i].base, s.baseline.p, static_cast<size_t>(spe) * sizeof(double));
+        cp(rb[i].best, s.best.p, sizeof(double));
+        cp(rb[i].fin, s.params.p, s.nparams * sizeof(float));
+        cp(rb[i].fin + s.nparams * sizeof(float), s.mstats.p, s.nstats * sizeof(float));
+        cp(rb[i].snap, s.snapshot.p, (s.nparams + s.nstats) * sizeof(float));
+    }
+    PBKD_CUDA(cudaStreamSynchronize(st));
     std::vector<TaskOutcome> out;
-    for (auto& sp : states) {
-        TaskState& s = *sp;
+    for (size_t si = 0; si < states.size(); ++si) {
+        TaskState& s = *states[si];
         TaskOutcome r;
         r.block_index = s.k;
         r.kind = pbkd::candidate_kind_name(s.task.kind);
         const int B = s.task.batch_size;
         const int spe = ceil_div(ntrain, B);
-        std::vector<float> losses(static_cast<size_t>(std::max<long long>(s.total_steps, 1)));
-        PBKD_CUDA(cudaMemcpy(losses.data(), s.step_loss.p, losses.size() * sizeof(float), cudaMemcpyDeviceToHost));
-        losses.resize(static_cast<size_t>(s.total_steps));
-        std::vector<double> accs(static_cast<size_t>(s.n_evals_planned));
-        PBKD_CUDA(cudaMemcpy(accs.data(), s.eval_acc.p, accs.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        std::vector<double> base(static_cast<size_t>(spe));
-        PBKD_CUDA(cudaMemcpy(base.data(), s.baseline.p, base.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        double best = -1.0;
-        PBKD_CUDA(cudaMemcpy(&best, s.best.p, sizeof(double), cudaMemcpyDeviceToHost));
-        std::vector<float> fin(s.nparams + s.nstats), snap(s.nparams + s.nstats);
-        PBKD_CUDA(cudaMemcpy(fin.data(), s.params.p, s.nparams * sizeof(float), cudaMemcpyDeviceToHost));
-        PBKD_CUDA(cudaMemcpy(fin.data() + s.nparams, s.mstats.p, s.nstats * sizeof(float), cudaMemcpyDeviceToHost));
-        PBKD_CUDA(cudaMemcpy(snap.data(), s.snapshot.p, snap.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        const float* lp = reinterpret_cast<const float*>(hb + rb[si].losses);
+        std::vector<float> losses(lp, lp + s.total_steps);
+        const double* ap = reinterpret_cast<const double*>(hb + rb[si].accs);
+        std::vector<double> accs(ap, ap + s.n_evals_planned);
+        const double* bp = reinterpret_cast<const double*>(hb + rb[si].base);
+        std::vector<double> base(bp, bp + spe);
+        const double best = *reinterpret_cast<const double*>(hb + rb[si].best);
+        const float* fp = reinterpret_cast<const float*>(hb + rb[si].fin);
+        std::vector<float> fin(fp, fp + s.nparams + s.nstats);
+        const float* sp = reinterpret_cast<const float*>(hb + rb[si].snap);
+        std::vector<float> snap(sp, sp + s.nparams + s.nstats);
         auto to_ref_order = [&](const std::vector<float>& flat) {
             std::vector<float> o;
             for (int u = 0; u < s.units; ++u) {
@@ -1269,14 +1340,17 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
     return out;
 }
 
-__global__ void eval_decide_kernel(const int* correct, int n_eval, double* best, int* take,
-                                   double* acc_out, const int* failed) {
+// acc_out[*slot] = accuracy, *slot += 1 (the slot advances on the device so
+// the evaluation program can be replayed as a graph)
+__global__ void eval_decide_kernel(const int* correct, int n_eval, double* best, int* take, double* acc_out,
+                                   int* slot, const int* failed) {
+    const int k = (*slot)++;
     if (failed && *failed) {
         *take = 0;
         return;
     }
     const double acc = static_cast<double>(*correct) / static_cast<double>(n_eval);
-    *acc_out = acc;
+    acc_out[k] = acc;
     if (acc > *best) {  // strict >, distill.cpp:160-163
         *best = acc;
         *take = 1;
@@ -1319,9 +1393,21 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         return v;
     };
 
-    auto run_eval = [&](const std::vector<TaskState*>& which, const std::vector<int>& eval_slot) {
+    // Evaluation programs are identical from one eval to the next (the
+    // eval_acc slot advances on the device), so each task set's program is
+    // captured into a CUDA graph once and replayed.
+    std::map<std::vector<TaskState*>, std::unique_ptr<Program>> eval_progs;
+    DevBuf eval_slots(sizeof(int) * ts.size());
+    PBKD_CUDA(cudaMemsetAsync(eval_slots.p, 0, sizeof(int) * ts.size(), st));
+    auto run_eval = [&](const std::vector<TaskState*>& which) {
         PBKD_CUDA(cudaMemsetAsync(correct.p, 0, sizeof(int) * ts.size(), st));
-        Program P;
+        auto found = eval_progs.find(which);
+        if (found != eval_progs.end()) {
+            found->second->launch_graph(st);
+            return;
+        }
+        auto prog = std::make_unique<Program>();
+        Program& P = *prog;
         for (size_t i = 0; i < which.size(); ++i) {
             TaskState& s = *which[i];
             const size_t ti = static_cast<size_t>(std::find(ts.begin(), ts.end(), which[i]) - ts.begin());
@@ -1343,7 +1429,8 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 const float* xin = cur;
                 P.raw([=](cudaStream_t s2) { launch_classifier_count(xin, ne, hw, cc, kinds, nl, w, b, mw, labs, corr, s2); });
             }
-            double* accp = s.eval_acc.d() + eval_slot[i];
+            double* accp = s.eval_acc.d();
+            int* slotp = eval_slots.i() + ti;
             double* bestp = s.best.d();
             int* takep = s.take.i();
             const int* fl = s.failed.i();
@@ -1352,11 +1439,17 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             const float* sp = s.mstats.f();
             const size_t np = s.nparams, ns = s.nstats;
             P.raw([=](cudaStream_t s2) {
-                eval_decide_kernel<<<1, 1, 0, s2>>>(corr, neval, bestp, takep, accp, fl);
+                eval_decide_kernel<<<1, 1, 0, s2>>>(corr, neval, bestp, takep, accp, slotp, fl);
                 snapshot_kernel<<<64, 256, 0, s2>>>(snapp, pp, np, sp, ns, takep);
             });
         }
-        P.run(st);
+        if (opt.use_graphs) {
+            P.build_graph(st);
+            P.launch_graph(st);
+            eval_progs.emplace(which, std::move(prog));
+        } else {
+            P.run(st);
+        }
     };
 
     // ---- labels of the eval split (for the classifier count)
@@ -1397,8 +1490,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             P.run(st);
         }
         trace.mark("group: epoch-0 baseline");
-        std::vector<int> slots(ts.size(), 0);
-        run_eval(ts, slots);
+        run_eval(ts);
         trace.mark("group: epoch-0 eval");
     }
 
@@ -1463,7 +1555,6 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     PBKD_CUDA(cudaEventCreate(&t1e));
     bool timed_started = false;
     std::vector<long long> gbase(ts.size(), 0);
-    std::vector<int> evals_done(ts.size(), 1);
     auto epoch_key = [&](int e) {
         std::vector<int> key;
         for (TaskState* s : ts) key.push_back(e <= s->task.epochs ? s->steps_in_epoch[e] : 0);
@@ -1612,14 +1703,10 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         }
         if (opt.baseline_and_eval) {
             std::vector<TaskState*> which;
-            std::vector<int> slots;
             for (size_t i = 0; i < ts.size(); ++i)
-                if (key[i] > 0 && e % ts[i]->task.eval_every == 0) {
-                    which.push_back(ts[i]);
-                    slots.push_back(evals_done[i]++);
-                }
+                if (key[i] > 0 && e % ts[i]->task.eval_every == 0) which.push_back(ts[i]);
             trace.mark("epoch: run");
-            if (!which.empty()) run_eval(which, slots);
+            if (!which.empty()) run_eval(which);
             trace.mark("epoch: eval");
         }
     }
@@ -1764,6 +1851,7 @@ std::vector<float> nchw_to_nhwc(const Tensor& t) {
 Engine::Engine(int device) : impl_(std::make_unique<Impl>(device)) {}
 Engine::~Engine() = default;
 void Engine::set_teacher(const Network& net) { impl_->load_teacher(net); }
+void Engine::set_teacher(Network&& net) { impl_->load_teacher(std::move(net)); }
 const Network& Engine::teacher() const { return impl_->net; }
 bool Engine::has_teacher() const { return impl_->has_teacher; }
 void Engine::set_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {

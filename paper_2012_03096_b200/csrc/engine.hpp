@@ -89,6 +89,7 @@ public:
     Engine& operator=(const Engine&) = delete;
 
     void set_teacher(const pbkd::Network& net);
+    void set_teacher(pbkd::Network&& net);
     const pbkd::Network& teacher() const;
     bool has_teacher() const;
     void set_dataset(const float* images, const int* labels, int count, int c, int h, int w,

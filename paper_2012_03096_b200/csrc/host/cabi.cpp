@@ -176,7 +176,7 @@ int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec, const float* w, size_t n)
             std::copy(w + at, w + at + t.data.size(), t.data.begin());
             at += t.data.size();
         });
-        ctx->eng->set_teacher(net);
+        ctx->eng->set_teacher(std::move(net));
         ctx->spec = spec;
     });
 }
@@ -185,7 +185,7 @@ int pbkd_teacher_init(pbkd_ctx* ctx, const char* spec, uint64_t seed) {
     return guard([&] {
         pbkd::Network net = spec_net(spec);
         pbkd::init_weights(net, seed);
-        ctx->eng->set_teacher(net);
+        ctx->eng->set_teacher(std::move(net));
         ctx->spec = spec;
     });
 }

@@ -772,6 +772,33 @@ __global__ void tf32_split_kernel(const float* __restrict__ x, long long n, floa
     }
 }
 
+// Teacher conv weights [cout][cin][kk] (model.cpp layout) -> implicit-GEMM
+// layout [cout][kk][cin] (K index = tap * cin + j) plus its tf32 planes.
+__global__ void conv_weight_prep_kernel(const float* __restrict__ raw, int cout, int cin, int kk,
+                                        float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo) {
+    const long long n = static_cast<long long>(cout) * cin * kk;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i % cin);
+        const long long r = i / cin;
+        const int t = static_cast<int>(r % kk);
+        const long long o = r / kk;
+        const float v = raw[(o * cin + j) * kk + t];
+        const float h = __uint_as_float(tc_split_hi(v));
+        w[i] = v;
+        hi[i] = h;
+        lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(v, h)));
+    }
+}
+
+void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, float* w, float* hi, float* lo,
+                             cudaStream_t st) {
+    const long long n = static_cast<long long>(cout) * cin * kk;
+    const int blocks = static_cast<int>(std::min<long long>(4096, (n + 255) / 256));
+    conv_weight_prep_kernel<<<std::max(1, blocks), 256, 0, st>>>(raw, cout, cin, kk, w, hi, lo);
+    PBKD_LAUNCH_CHECK();
+}
+
 void launch_tf32_split(const float* x, long long n, float* hi, float* lo, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>(4096, (n + 255) / 256));
     tf32_split_kernel<<<std::max(1, blocks), 256, 0, st>>>(x, n, hi, lo);

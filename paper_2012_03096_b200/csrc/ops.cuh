@@ -267,6 +267,9 @@ void launch_bn_infer_prep(const float* gamma, const float* beta, const float* mm
                           const float* mv, int c, float* scale, float* shift, cudaStream_t st);
 void launch_bn_infer_relu(const float* x, float* y, long long total, int c, const float* scale,
                           const float* shift, cudaStream_t st);
+// teacher conv weights [cout][cin][kk] -> [cout][kk][cin] + tf32 planes
+void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, float* w, float* hi, float* lo,
+                             cudaStream_t st);
 // tf32 hi / lo planes of n floats (the 3xTF32 operand split)
 void launch_tf32_split(const float* x, long long n, float* hi, float* lo, cudaStream_t st);
 // per-segment MSE sums (segment = one batch of the epoch-0 baseline)
