@@ -324,9 +324,17 @@ ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, 
     return d;
 }
 
+// tf32 planes of an activation buffer (null: none)
+struct Planes2 {
+    float* hi = nullptr;
+    float* lo = nullptr;
+};
+
 GemmOp conv_gemm(const ConvDev& c, const float* x, int n, int ih, int iw, float* y, bool affine,
-                 const float* skip, bool relu_out) {
+                 const float* skip, bool relu_out, Planes2 xp = {}, Planes2 yp = {}) {
     GemmOp o{};
+    o.a_hi = xp.hi, o.a_lo = xp.lo;  // input planes: the conv runs on pre-split A
+    o.c_hi = yp.hi, o.c_lo = yp.lo;  // output planes for the next conv
     o.conv = 1;
     o.ih = ih;
     o.iw = iw;
@@ -546,19 +554,29 @@ struct Engine::Impl {
     }
 
     // Teacher block j (0-based) forward on n samples: x -> y.  scratch t1/sk.
+    // tf32 planes registered for activation buffers (teacher ping / pong /
+    // t1 of a run): convs reading such a buffer take pre-split A, convs
+    // writing one also emit its planes
+    std::map<const float*, Planes2> act_planes;
+    Planes2 planes_for(const float* p) const {
+        auto it = act_planes.find(p);
+        return it == act_planes.end() ? Planes2{} : it->second;
+    }
+
     void teacher_block(Program& P, int j, const float* x, float* y, int n, float* t1, float* sk) {
         const TBlockDev& b = tblocks[static_cast<size_t>(j)];
+        const Planes2 xp = planes_for(x), yp = planes_for(y), tp = planes_for(t1);
         if (b.kind == 0) {
-            P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, y, true, nullptr, true)});
+            P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, y, true, nullptr, true, xp, yp)});
             return;
         }
-        P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true)});
+        P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true, xp, tp)});
         const float* skip = x;
         if (b.has_proj) {
-            P.gemm({conv_gemm(b.proj, x, n, b.hin, b.win, sk, false, nullptr, false)});
+            P.gemm({conv_gemm(b.proj, x, n, b.hin, b.win, sk, false, nullptr, false, xp)});
             skip = sk;
         }
-        P.gemm({conv_gemm(b.c2, t1, n, b.mid_h, b.mid_w, y, true, skip, true)});
+        P.gemm({conv_gemm(b.c2, t1, n, b.mid_h, b.mid_w, y, true, skip, true, tp, yp)});
     }
 
     void load_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {
@@ -1344,6 +1362,7 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
 // the evaluation program can be replayed as a graph)
 __global__ void eval_decide_kernel(const int* correct, int n_eval, double* best, int* take, double* acc_out,
                                    int* slot, const int* failed) {
+    pdl_enter();
     const int k = (*slot)++;
     if (failed && *failed) {
         *take = 0;
@@ -1361,6 +1380,7 @@ __global__ void eval_decide_kernel(const int* correct, int n_eval, double* best,
 
 __global__ void snapshot_kernel(float* dst, const float* params, size_t np, const float* stats,
                                 size_t ns, const int* take) {
+    pdl_enter();
     if (!*take) return;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < np + ns;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -1379,6 +1399,21 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     const int ichunk = std::max(B, (chunk / B) * B);
     const size_t wsz = static_cast<size_t>(std::max(chunk, ichunk)) * mrow * sizeof(float);
     DevBuf ping(wsz), pong(wsz), t1(wsz), sk(wsz), ia(wsz), ib(wsz), io(wsz);
+    // tf32 planes of the teacher's working buffers (pre-split conv operands)
+    DevBuf plane_bufs[6];
+    const bool tplanes = gemm_presplit_ok(32);
+    if (tplanes) {
+        float* bufs[3] = {ping.f(), pong.f(), t1.f()};
+        for (int i = 0; i < 3; ++i) {
+            plane_bufs[2 * i].alloc(wsz);
+            plane_bufs[2 * i + 1].alloc(wsz);
+            act_planes[bufs[i]] = Planes2{plane_bufs[2 * i].f(), plane_bufs[2 * i + 1].f()};
+        }
+    }
+    struct PlaneReg {  // unregister when the buffers go away
+        std::map<const float*, Planes2>& m;
+        ~PlaneReg() { m.clear(); }
+    } plane_reg{act_planes};
     DevBuf correct(sizeof(int) * ts.size());
     int emax = 0;
     for (TaskState* s : ts) emax = std::max(emax, s->task.epochs);
@@ -1439,8 +1474,8 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             const float* sp = s.mstats.f();
             const size_t np = s.nparams, ns = s.nstats;
             P.raw([=](cudaStream_t s2) {
-                eval_decide_kernel<<<1, 1, 0, s2>>>(corr, neval, bestp, takep, accp, slotp, fl);
-                snapshot_kernel<<<64, 256, 0, s2>>>(snapp, pp, np, sp, ns, takep);
+                launch_k(eval_decide_kernel, dim3(1), dim3(1), 0, s2, corr, neval, bestp, takep, accp, slotp, fl);
+                launch_k(snapshot_kernel, dim3(64), dim3(256), 0, s2, snapp, pp, np, sp, ns, takep);
             });
         }
         if (opt.use_graphs) {
@@ -1735,6 +1770,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
 
 // ====================================================== kernel bench
 __global__ void fill_kernel(float* p, size_t n, float v) {
+    pdl_enter();
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
         p[i] = v * (1.0f + 0.001f * static_cast<float>(i % 97));
@@ -1760,7 +1796,7 @@ void Engine::bench_kernel(int which, int batch, int iters, double* ms, double* b
     DevBuf x(big * 4), y(big * 4), z(big * 4), w(static_cast<size_t>(c) * std::max(c, b.cin) * 9 * 4 + 64),
         v(static_cast<size_t>(c) * 64 * 4 + 4096), parts(static_cast<size_t>(4096) * 9 * c * 4 + 4096);
     for (DevBuf* d : {&x, &y, &z, &w, &v})
-        fill_kernel<<<1024, 256, 0, m.st>>>(d->f(), d->bytes / 4, 0.37f);
+        launch_k(fill_kernel, dim3(1024), dim3(256), 0, m.st, d->f(), d->bytes / 4, 0.37f);
     PBKD_LAUNCH_CHECK();
     Program P;
     double by = 0, fl = 0;

@@ -8,10 +8,19 @@
 // trees: deterministic run to run, equal to the reference within fp32
 // tolerance.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
 namespace pbkd_gpu {
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PBKD_PDL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 // ---------------------------------------------------------------- partition
 int rows_part_ctas(long long rows, int c) {
@@ -206,6 +215,7 @@ __device__ __forceinline__ DwPos dw_pos(const DwTile& t, int local) {
 // ---------------------------------------------------------- depthwise fwd
 // Warp = output row (image i, row oy) of the tile, lane = channel.
 __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restrict__ ops, int nd) {
+    pdl_enter();
     extern __shared__ float xs[];
     int local;
     const DwFwdOp& o = op_of(ops, nd, local);
@@ -262,7 +272,7 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
 }
 
 void launch_dw_fwd(const DwFwdOp* d, int nd, int ctas, cudaStream_t st) {
-    dw_fwd_kernel<<<ctas, kThreads, kDwTileBytes, st>>>(d, nd);
+    launch_k(dw_fwd_kernel, dim3(ctas), dim3(kThreads), kDwTileBytes, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
@@ -290,6 +300,7 @@ __device__ __forceinline__ void dw_lane_sum(float* red, const float* v, float* o
 // (oy, ox) order with zero terms skipped (ops.hpp:156-174), the weight-
 // gradient terms, the previous ReLU mask and batch-norm partial sums.
 __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restrict__ ops, int nd) {
+    pdl_enter();
     extern __shared__ float sm[];
     int local;
     const DwBwdOp& o = op_of(ops, nd, local);
@@ -371,13 +382,14 @@ void launch_dw_bwd(const DwBwdOp* d, int nd, int ctas, cudaStream_t st) {
         PBKD_CUDA(cudaFuncSetAttribute(dw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDwTileBytes));
         attr = true;
     }
-    dw_bwd_kernel<<<ctas, kThreads, 2 * kDwTileBytes, st>>>(d, nd);
+    launch_k(dw_bwd_kernel, dim3(ctas), dim3(kThreads), 2 * kDwTileBytes, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
 // ------------------------------------------- depthwise weight grad (unit 0)
 // model.cpp:570 skips the input gradient of the block's first layer.
 __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restrict__ ops, int nd) {
+    pdl_enter();
     extern __shared__ float sm[];
     int local;
     const DwGkOp& o = op_of(ops, nd, local);
@@ -420,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restric
 }
 
 void launch_dw_gk(const DwGkOp* d, int nd, int ctas, cudaStream_t st) {
-    dw_gk_kernel<<<ctas, kThreads, kDwTileBytes, st>>>(d, nd);
+    launch_k(dw_gk_kernel, dim3(ctas), dim3(kThreads), kDwTileBytes, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
@@ -452,6 +464,7 @@ __device__ __forceinline__ float col_sum(const float* __restrict__ part, int par
 }
 
 __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __restrict__ ops, int nd) {
+    pdl_enter();
     __shared__ float red[kColLanes][32];
     int local;
     const BnStatOp& o = op_of(ops, nd, local);
@@ -481,6 +494,7 @@ __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __res
 int ctas_reduce(const ReduceOp& o) { return std::max(1, ceil_div(o.width, kThreads)); }
 
 __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __restrict__ ops, int nd) {
+    pdl_enter();
     int local;
     const ReduceOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
@@ -501,17 +515,18 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __rest
 }
 
 void launch_reduce(const ReduceOp* d, int nd, int ctas, cudaStream_t st) {
-    reduce_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    launch_k(reduce_kernel, dim3(ctas), dim3(kThreads), 0, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
 void launch_bn_stat(const BnStatOp* d, int nd, int ctas, cudaStream_t st) {
-    bn_stat_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    launch_k(bn_stat_kernel, dim3(ctas), dim3(kThreads), 0, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------- loss + BN
 __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict__ ops, int nd) {
+    pdl_enter();
     extern __shared__ float red[];
     __shared__ float lred[kThreads];
     int local;
@@ -559,11 +574,12 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
 }
 
 void launch_loss(const LossOp* d, int nd, int ctas, cudaStream_t st) {
-    loss_kernel<<<ctas, kThreads, red_smem(0), st>>>(d, nd);
+    launch_k(loss_kernel, dim3(ctas), dim3(kThreads), red_smem(0), st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
 __global__ void __launch_bounds__(kThreads) bn_bwd_fin_kernel(const BnBwdFinOp* __restrict__ ops, int nd) {
+    pdl_enter();
     __shared__ float red[kColLanes][32];
     int local;
     const BnBwdFinOp& o = op_of(ops, nd, local);
@@ -589,7 +605,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_fin_kernel(const BnBwdFinOp* 
 }
 
 void launch_bn_bwd_fin(const BnBwdFinOp* d, int nd, int ctas, cudaStream_t st) {
-    bn_bwd_fin_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    launch_k(bn_bwd_fin_kernel, dim3(ctas), dim3(kThreads), 0, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
@@ -617,6 +633,7 @@ __device__ __forceinline__ BnBwdPar bn_bwd_par(const BnBwdApplyOp& o, int ch) {
 }
 
 __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApplyOp* __restrict__ ops, int nd) {
+    pdl_enter();
     int local;
     const BnBwdApplyOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
@@ -667,12 +684,13 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApply
 }
 
 void launch_bn_bwd_apply(const BnBwdApplyOp* d, int nd, int ctas, cudaStream_t st) {
-    bn_bwd_apply_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    launch_k(bn_bwd_apply_kernel, dim3(ctas), dim3(kThreads), 0, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
 // -------------------------------------------------------------------- SGD
 __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__ ops, int nd) {
+    pdl_enter();
     int local;
     const SgdOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
@@ -715,12 +733,13 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__
 }
 
 void launch_sgd(const SgdOp* d, int nd, int ctas, cudaStream_t st) {
-    sgd_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    launch_k(sgd_kernel, dim3(ctas), dim3(kThreads), 0, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- scatter
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const ScatterOp* __restrict__ ops, int nd) {
+    pdl_enter();
     int local;
     const ScatterOp& o = op_of(ops, nd, local);
     const long long step = static_cast<long long>(kThreads) * kScatterCtas;
@@ -755,7 +774,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const ScatterOp* __re
 }
 
 void launch_scatter(const ScatterOp* d, int nd, int ctas, cudaStream_t st) {
-    scatter_kernel<<<ctas, kThreads, 0, st>>>(d, nd);
+    launch_k(scatter_kernel, dim3(ctas), dim3(kThreads), 0, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 
@@ -763,6 +782,7 @@ void launch_scatter(const ScatterOp* d, int nd, int ctas, cudaStream_t st) {
 // tf32 hi / lo planes of x (RNE split, as the GEMM converters do it)
 __global__ void tf32_split_kernel(const float* __restrict__ x, long long n, float* __restrict__ hi,
                                   float* __restrict__ lo) {
+    pdl_enter();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const float v = x[i];
@@ -776,6 +796,7 @@ __global__ void tf32_split_kernel(const float* __restrict__ x, long long n, floa
 // layout [cout][kk][cin] (K index = tap * cin + j) plus its tf32 planes.
 __global__ void conv_weight_prep_kernel(const float* __restrict__ raw, int cout, int cin, int kk,
                                         float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo) {
+    pdl_enter();
     const long long n = static_cast<long long>(cout) * cin * kk;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -795,18 +816,19 @@ void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, float*
                              cudaStream_t st) {
     const long long n = static_cast<long long>(cout) * cin * kk;
     const int blocks = static_cast<int>(std::min<long long>(4096, (n + 255) / 256));
-    conv_weight_prep_kernel<<<std::max(1, blocks), 256, 0, st>>>(raw, cout, cin, kk, w, hi, lo);
+    launch_k(conv_weight_prep_kernel, dim3(std::max(1, blocks)), dim3(256), 0, st, raw, cout, cin, kk, w, hi, lo);
     PBKD_LAUNCH_CHECK();
 }
 
 void launch_tf32_split(const float* x, long long n, float* hi, float* lo, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>(4096, (n + 255) / 256));
-    tf32_split_kernel<<<std::max(1, blocks), 256, 0, st>>>(x, n, hi, lo);
+    launch_k(tf32_split_kernel, dim3(std::max(1, blocks)), dim3(256), 0, st, x, n, hi, lo);
     PBKD_LAUNCH_CHECK();
 }
 
 __global__ void gather_nhwc_kernel(const float* __restrict__ img, const int* __restrict__ idx, int n,
                                    int c, int h, int w, float* __restrict__ out) {
+    pdl_enter();
     const long long total = static_cast<long long>(n) * c * h * w;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -824,12 +846,13 @@ void launch_gather_nhwc(const float* images, const int* idx, int n, int c, int h
                         cudaStream_t st) {
     const long long total = static_cast<long long>(n) * c * h * w;
     const int blocks = static_cast<int>(std::min<long long>(4096, (total + 255) / 256));
-    gather_nhwc_kernel<<<std::max(1, blocks), 256, 0, st>>>(images, idx, n, c, h, w, out);
+    launch_k(gather_nhwc_kernel, dim3(std::max(1, blocks)), dim3(256), 0, st, images, idx, n, c, h, w, out);
     PBKD_LAUNCH_CHECK();
 }
 
 __global__ void bn_infer_prep_kernel(const float* gamma, const float* beta, const float* mm,
                                      const float* mv, int c, float* scale, float* shift) {
+    pdl_enter();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= c) return;
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(add(mv[j], 1e-5f)));
@@ -840,12 +863,13 @@ __global__ void bn_infer_prep_kernel(const float* gamma, const float* beta, cons
 
 void launch_bn_infer_prep(const float* gamma, const float* beta, const float* mm, const float* mv,
                           int c, float* scale, float* shift, cudaStream_t st) {
-    bn_infer_prep_kernel<<<ceil_div(c, 256), 256, 0, st>>>(gamma, beta, mm, mv, c, scale, shift);
+    launch_k(bn_infer_prep_kernel, dim3(ceil_div(c, 256)), dim3(256), 0, st, gamma, beta, mm, mv, c, scale, shift);
     PBKD_LAUNCH_CHECK();
 }
 
 __global__ void bn_infer_relu_kernel(const float* x, float* y, long long total, int c,
                                      const float* scale, const float* shift) {
+    pdl_enter();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int ch = static_cast<int>(i % c);
@@ -856,13 +880,14 @@ __global__ void bn_infer_relu_kernel(const float* x, float* y, long long total, 
 void launch_bn_infer_relu(const float* x, float* y, long long total, int c, const float* scale,
                           const float* shift, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>(4096, (total + 255) / 256));
-    bn_infer_relu_kernel<<<std::max(1, blocks), 256, 0, st>>>(x, y, total, c, scale, shift);
+    launch_k(bn_infer_relu_kernel, dim3(std::max(1, blocks)), dim3(256), 0, st, x, y, total, c, scale, shift);
     PBKD_LAUNCH_CHECK();
 }
 
 // one CTA per segment: fixed-order double sum of (s-t)^2
 __global__ void mse_segments_kernel(const float* s, const float* t, long long seg, long long total,
                                     double* out) {
+    pdl_enter();
     __shared__ double red[256];
     const long long b = static_cast<long long>(blockIdx.x) * seg;
     const long long e = min(total, b + seg);
@@ -882,7 +907,7 @@ __global__ void mse_segments_kernel(const float* s, const float* t, long long se
 
 void launch_mse_segments(const float* s, const float* t, long long seg, long long total, int nseg,
                          double* out, cudaStream_t st) {
-    mse_segments_kernel<<<nseg, 256, 0, st>>>(s, t, seg, total, out);
+    launch_k(mse_segments_kernel, dim3(nseg), dim3(256), 0, st, s, t, seg, total, out);
     PBKD_LAUNCH_CHECK();
 }
 
@@ -891,6 +916,7 @@ void launch_mse_segments(const float* s, const float* t, long long seg, long lon
 __global__ void classifier_kernel(const float* __restrict__ x, int hw, int c, const int* kinds,
                                   int nlayers, const float* dw, const float* db, int nout,
                                   const int* labels, int* correct) {
+    pdl_enter();
     extern __shared__ float vec[];  // 2 * max(c, nout) floats
     const int n = blockIdx.x;
     float* cur = vec;
@@ -944,7 +970,7 @@ void launch_classifier_count(const float* x, int n, int hw, int c, const int* ki
                              const float* dw, const float* db, int nout, const int* labels,
                              int* correct, cudaStream_t st) {
     const size_t smem = 2 * sizeof(float) * std::max(c, nout) + 64;
-    classifier_kernel<<<n, 128, smem, st>>>(x, hw, c, kinds, nlayers, dw, db, nout, labels, correct);
+    launch_k(classifier_kernel, dim3(n), dim3(128), smem, st, x, hw, c, kinds, nlayers, dw, db, nout, labels, correct);
     PBKD_LAUNCH_CHECK();
 }
 

@@ -155,6 +155,7 @@ __device__ __forceinline__ const Op& op_of_u(const Op* ops, int nd, int& local) 
 // per-row fp32 sums stay in registers.
 template <int BN>
 __global__ void __launch_bounds__(kThreadsG, 1) umma_gemm_kernel(const GemmOp* __restrict__ ops, int nd) {
+    pdl_enter();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bars[kStages];
     __shared__ uint32_t tmem_base_sh;
@@ -300,7 +301,7 @@ static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
                                        static_cast<int>(smem)));
         attr = true;
     }
-    umma_gemm_kernel<BN><<<ctas, kThreadsG, smem, st>>>(d, nd);
+    launch_k(umma_gemm_kernel<BN>, dim3(ctas), dim3(kThreadsG), smem, st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 

@@ -323,6 +323,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // predecessor results (failure flags, operands) only after this point
+    pdl_enter();
     // decode this CTA's tiles once (all threads in parallel: one global-load
     // latency instead of a dependent chain per tile per role)
     for (int i = tid; i < nd; i += kThreadsT) begins[i] = ops[i].cta_begin;
@@ -642,7 +644,8 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         PBKD_CUDA(cudaMalloc(&trace, 10 * 512 * sizeof(unsigned long long)));
     unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
     if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, 10 * 512 * sizeof(unsigned long long), st));
-    umma_tma_kernel<BN, PS><<<grid, kThreadsT, Cfg<BN, PS>::smem, st>>>(d, nd, total, tr);
+    launch_k(umma_tma_kernel<BN, PS>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(Cfg<BN, PS>::smem), st, d, nd,
+             total, tr);
     PBKD_LAUNCH_CHECK();
     static const int trace_from = [] {
         const char* e = std::getenv("PBKD_GEMM_TRACE");
