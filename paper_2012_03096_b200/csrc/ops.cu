@@ -251,14 +251,28 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
         if (nn >= o.n || yy >= o.ho) continue;
         const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
         const long long obase = ((static_cast<long long>(nn) * o.ho + yy) * o.wo) * o.c + c;
-#pragma unroll 2
+        const int rs = t.tw * kDwC;
+        float win[3][3];  // stride 1: 3x3 register window slid along x
+        if (s == 1) {
+#pragma unroll
+            for (int r = 0; r < 3; ++r) win[r][1] = base[r * rs], win[r][2] = base[r * rs + kDwC];
+        }
         for (int ox = 0; ox < o.wo; ++ox) {
-            const float* b = base + ox * s * kDwC;
+            if (s == 1) {
+#pragma unroll
+                for (int r = 0; r < 3; ++r) win[r][0] = win[r][1], win[r][1] = win[r][2], win[r][2] = base[r * rs + (ox + 2) * kDwC];
+            } else {
+                const float* b = base + ox * s * kDwC;
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) win[r][cc] = b[r * rs + cc * kDwC];
+            }
             float acc = 0.0f;  // 9-term serial sum in (ky, kx) order (ops.hpp:131-140)
 #pragma unroll
             for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
-                for (int kx = 0; kx < 3; ++kx) acc = add(acc, mul(b[(ky * t.tw + kx) * kDwC], wk[ky * 3 + kx]));
+                for (int kx = 0; kx < 3; ++kx) acc = add(acc, mul(win[ky][kx], wk[ky * 3 + kx]));
             const long long oi = obase + static_cast<long long>(ox) * o.c;
             if (o.y_hi) {  // tf32 planes for the pointwise GEMMs (3xTF32 operand split)
                 const float hv = __uint_as_float(tc_split_hi(acc));
@@ -319,8 +333,10 @@ __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restr
     dw_stage(gs, o.gy, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 - 1, -1, q.c0);
     dw_stage(xs, o.xp, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 - 1, -1, q.c0);
     __syncthreads();
-    // xs keeps the raw pre-BN p for the centre (xhat, mask); the relu(bn(p))
-    // view the weight gradient needs is formed per tap below
+    // xs -> relu(bn(p)), the dw layer's actual input (padding stays 0); the
+    // centre's raw p (xhat, mask) is re-read from global (L2)
+    dw_map(xs, t, o.n, o.h, o.wd, q.n0, q.y0 - 1, -1, [&](float v) { return relu(bn_train_apply(v, mean, inv, gam, bet)); });
+    __syncthreads();
 
     float acc[11];  // gk[9], sg, sgx
 #pragma unroll
@@ -332,35 +348,47 @@ __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restr
             const int nn = q.n0 + i, yy = q.y0 + y;
             if (nn >= o.n || yy >= o.h) continue;
             const long long grow = ((static_cast<long long>(nn) * o.h + yy) * o.wd) * o.c + c;
+            // 3x3 register windows over tile rows y..y+2 (= image rows yy-1..yy+1),
+            // columns x..x+2 (= image columns x-1..x+1), slid along x
+            const float* g0 = gs + ((i * t.tr + y) * t.tw) * kDwC + ch;
+            const float* x0 = xs + ((i * t.tr + y) * t.tw) * kDwC + ch;
+            const int rs = t.tw * kDwC;
+            float gw[3][3], xw[3][3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    gw[r][cc + 1] = g0[r * rs + cc * kDwC];
+                    xw[r][cc + 1] = x0[r * rs + cc * kDwC];
+                }
             for (int x = 0; x < o.wd; ++x) {
-                const int ctr = ((i * t.tr + y + 1) * t.tw + x + 1) * kDwC + ch;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    gw[r][0] = gw[r][1], gw[r][1] = gw[r][2], gw[r][2] = g0[r * rs + (x + 2) * kDwC];
+                    xw[r][0] = xw[r][1], xw[r][1] = xw[r][2], xw[r][2] = x0[r * rs + (x + 2) * kDwC];
+                }
+                // input gradient: outputs (oy, ox) = (yy+dy, x+dx) ascending, tap
+                // (1-dy, 1-dx), zero terms skipped (ops.hpp:156-174)
                 float gx = 0.0f;
 #pragma unroll
-                for (int dy = -1; dy <= 1; ++dy)
+                for (int r = 0; r < 3; ++r)
 #pragma unroll
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        const float gv = gs[ctr + (dy * t.tw + dx) * kDwC];
-                        if (gv != 0.0f) gx = add(gx, mul(gv, wk[(1 - dy) * 3 + (1 - dx)]));
+                    for (int cc = 0; cc < 3; ++cc) {
+                        const float gv = gw[r][cc];
+                        if (gv != 0.0f) gx = add(gx, mul(gv, wk[(2 - r) * 3 + (2 - cc)]));
                     }
-                const float gyc = gs[ctr];
+                const float gyc = gw[1][1];
                 if (gyc != 0.0f) {
 #pragma unroll
-                    for (int ky = 0; ky < 3; ++ky) {
-                        const int iy = yy + ky - 1;
+                    for (int r = 0; r < 3; ++r)
 #pragma unroll
-                        for (int kx = 0; kx < 3; ++kx) {
-                            const int ix = x + kx - 1;
-                            if (iy < 0 || iy >= o.h || ix < 0 || ix >= o.wd) continue;  // padded input is 0
-                            const float xin =
-                                relu(bn_train_apply(xs[ctr + ((ky - 1) * t.tw + kx - 1) * kDwC], mean, inv, gam, bet));
-                            acc[ky * 3 + kx] += gyc * xin;
-                        }
-                    }
+                        for (int cc = 0; cc < 3; ++cc) acc[r * 3 + cc] += gyc * xw[r][cc];
                 }
-                const float xh = mul(sub(xs[ctr], mean), inv);
+                const long long gi = grow + static_cast<long long>(x) * o.c;
+                const float xh = mul(sub(__ldg(o.xp + gi), mean), inv);
                 const float yv = add(mul(gam, xh), bet);
                 const float gm = yv > 0.0f ? add(0.0f, gx) : 0.0f;
-                o.gyprev[grow + static_cast<long long>(x) * o.c] = gm;
+                o.gyprev[gi] = gm;
                 acc[9] += gm;
                 acc[10] += gm * xh;
             }
@@ -488,30 +516,41 @@ __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __res
 }
 
 // --------------------------------------------------------- fixed-order sums
-// out[i] = sum over parts of part[p][i]: one column per thread, four
-// independent accumulators (p mod 4) combined as (a0+a1)+(a2+a3) -- the order
-// depends only on `parts`; the loads of four parts are in flight at once.
-int ctas_reduce(const ReduceOp& o) { return std::max(1, ceil_div(o.width, kThreads)); }
+// out[i] = sum over parts of part[p][i]: a CTA owns 32 columns; its 8 warps
+// stride over the parts (4 independent accumulators each), then the 8 warp
+// sums combine in fixed order -- the order depends only on `parts`, and the
+// dependent-load chain is parts/32 deep instead of parts.
+int ctas_reduce(const ReduceOp& o) { return std::max(1, ceil_div(o.width, 32)); }
 
 __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __restrict__ ops, int nd) {
     pdl_enter();
+    __shared__ float red[kThreads / 32][32];
     int local;
     const ReduceOp& o = op_of(ops, nd, local);
     if (is_failed(o.failed)) return;
-    const int col = local * kThreads + threadIdx.x;
-    if (col >= o.width) return;
-    const float* __restrict__ p = o.part + col;
-    const long long w = o.width;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int col = local * 32 + lane;
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-    int q = 0;
-    for (; q + 3 < o.parts; q += 4) {
-        a0 += __ldg(p + q * w);
-        a1 += __ldg(p + (q + 1) * w);
-        a2 += __ldg(p + (q + 2) * w);
-        a3 += __ldg(p + (q + 3) * w);
+    if (col < o.width) {
+        const float* __restrict__ p = o.part + col;
+        const long long wd = o.width;
+        int q = w;
+        for (; q + 24 < o.parts; q += 32) {
+            a0 += __ldg(p + q * wd);
+            a1 += __ldg(p + (q + 8) * wd);
+            a2 += __ldg(p + (q + 16) * wd);
+            a3 += __ldg(p + (q + 24) * wd);
+        }
+        for (; q < o.parts; q += 8) a0 += __ldg(p + q * wd);
     }
-    for (; q < o.parts; ++q) a0 += __ldg(p + q * w);
-    o.out[col] = (a0 + a1) + (a2 + a3);
+    red[w][lane] = (a0 + a1) + (a2 + a3);
+    __syncthreads();
+    if (w == 0 && col < o.width) {
+        float sacc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < kThreads / 32; ++i) sacc += red[i][lane];
+        o.out[col] = sacc;
+    }
 }
 
 void launch_reduce(const ReduceOp* d, int nd, int ctas, cudaStream_t st) {
