@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
     pdl_enter();
     extern __shared__ float xs[];
     int local;
-    const DwFwdOp& o = op_of(ops, nd, local);
+    const DwFwdOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const DwTile t = o.tile;
     const DwPos q = dw_pos(t, local);
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restr
     pdl_enter();
     extern __shared__ float sm[];
     int local;
-    const DwBwdOp& o = op_of(ops, nd, local);
+    const DwBwdOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const DwTile t = o.tile;
     const DwPos q = dw_pos(t, local);
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restric
     pdl_enter();
     extern __shared__ float sm[];
     int local;
-    const DwGkOp& o = op_of(ops, nd, local);
+    const DwGkOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const DwTile t = o.tile;
     const DwPos q = dw_pos(t, local);
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __res
     pdl_enter();
     __shared__ float red[kColLanes][32];
     int local;
-    const BnStatOp& o = op_of(ops, nd, local);
+    const BnStatOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const int ch = local * 32 + threadIdx.x % 32;
     const float sum = col_sum(o.part_sum, o.tiles, o.c, ch, red);
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __rest
     pdl_enter();
     __shared__ float red[kThreads / 32][32];
     int local;
-    const ReduceOp& o = op_of(ops, nd, local);
+    const ReduceOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int col = local * 32 + lane;
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
     extern __shared__ float red[];
     __shared__ float lred[kThreads];
     int local;
-    const LossOp& o = op_of(ops, nd, local);
+    const LossOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const Geo g = geo_of(o.c);
     const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_fin_kernel(const BnBwdFinOp* 
     pdl_enter();
     __shared__ float red[kColLanes][32];
     int local;
-    const BnBwdFinOp& o = op_of(ops, nd, local);
+    const BnBwdFinOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     if (o.loss_out && local == 0 && threadIdx.x < 32) {  // one warp, fixed-order tree
         double s = 0.0;
@@ -674,7 +674,7 @@ __device__ __forceinline__ BnBwdPar bn_bwd_par(const BnBwdApplyOp& o, int ch) {
 __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApplyOp* __restrict__ ops, int nd) {
     pdl_enter();
     int local;
-    const BnBwdApplyOp& o = op_of(ops, nd, local);
+    const BnBwdApplyOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const long long base = (static_cast<long long>(local) * kThreads + threadIdx.x) * 4;
     if (base >= o.total) return;
@@ -731,7 +731,7 @@ void launch_bn_bwd_apply(const BnBwdApplyOp* d, int nd, int ctas, cudaStream_t s
 __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__ ops, int nd) {
     pdl_enter();
     int local;
-    const SgdOp& o = op_of(ops, nd, local);
+    const SgdOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const long long base = (static_cast<long long>(local) * kThreads + threadIdx.x) * 4;
     if (base >= o.n) return;
@@ -780,7 +780,7 @@ void launch_sgd(const SgdOp* d, int nd, int ctas, cudaStream_t st) {
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const ScatterOp* __restrict__ ops, int nd) {
     pdl_enter();
     int local;
-    const ScatterOp& o = op_of(ops, nd, local);
+    const ScatterOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     const long long step = static_cast<long long>(kThreads) * kScatterCtas;
     if ((o.width % 4) == 0) {
         const int wv = o.width / 4;
