@@ -251,9 +251,15 @@ __global__ void __launch_bounds__(kThreadsG, 1) umma_gemm_kernel(const GemmOp* _
 
 // ------------------------------------------------------------------- host
 namespace {
+// N tile: 32 / 64 / 128.  (PBKD_BN64=0 folds the 64 class into the 128
+// launches: one launch per step phase fewer, measured 2% slower on VGG-16.)
 int bn_for(int n) {
+    static const bool bn64 = [] {
+        const char* e = std::getenv("PBKD_BN64");
+        return !(e && e[0] == '0');
+    }();
     if (n <= 32) return 32;
-    if (n <= 64) return 64;
+    if (n <= 64 && bn64) return 64;
     return 128;
 }
 }  // namespace
