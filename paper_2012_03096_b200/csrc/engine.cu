@@ -150,40 +150,46 @@ public:
         work_.push_back(w);
     }
     // tcgen05 GEMMs: one launch per kernel / N-tile class (the tile is a
-    // template parameter), all tasks of that class grouped in it
+    // template parameter), all tasks of that class grouped in it; several
+    // classes run as a parallel section (independent outputs)
     void gemm(std::vector<GemmOp> all) {
         std::vector<int> classes;
         for (const GemmOp& o : all) classes.push_back(gemm_bn_class(o));
         std::sort(classes.begin(), classes.end());
         classes.erase(std::unique(classes.begin(), classes.end()), classes.end());
-        for (int cls : classes) {
+        std::vector<Program*> dst(classes.size(), this);
+        if (classes.size() > 1) dst = par(static_cast<int>(classes.size()));
+        for (size_t ci = 0; ci < classes.size(); ++ci) {
             std::vector<GemmOp> ops;
             for (const GemmOp& o : all)
-                if (gemm_bn_class(o) == cls) ops.push_back(o);
-            if (ops.empty()) continue;
-            int total = 0;
-            for (GemmOp& o : ops) {
-                o.cta_begin = total;
-                total += std::max(1, ctas_gemm(o));
-            }
-            const size_t off = (host_.size() + 63) & ~size_t(63);
-            host_.resize(off + ops.size() * sizeof(GemmOp));
-            std::memcpy(host_.data() + off, ops.data(), ops.size() * sizeof(GemmOp));
-            const int nd = static_cast<int>(ops.size());
-            steps_.push_back([off, nd, total, cls](cudaStream_t st, const uint8_t* slab) {
-                launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, cls, st);
-            });
-            const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
-            names_.push_back(std::string("gemm_") + kind +
-                             (cls >= 2 * kGemmClassTma ? "_pre" : cls >= kGemmClassTma ? "_tma" : "_reg") +
-                             std::to_string(cls % kGemmClassTma));
-            KernelStat w;
-            for (const GemmOp& o : ops) {
-                const auto bf = op_work(o);
-                w.bytes += bf.first, w.flops += bf.second;
-            }
-            work_.push_back(w);
+                if (gemm_bn_class(o) == classes[ci]) ops.push_back(o);
+            dst[ci]->gemm_class(classes[ci], std::move(ops));
         }
+    }
+    void gemm_class(int cls, std::vector<GemmOp> ops) {
+        if (ops.empty()) return;
+        int total = 0;
+        for (GemmOp& o : ops) {
+            o.cta_begin = total;
+            total += std::max(1, ctas_gemm(o));
+        }
+        const size_t off = (host_.size() + 63) & ~size_t(63);
+        host_.resize(off + ops.size() * sizeof(GemmOp));
+        std::memcpy(host_.data() + off, ops.data(), ops.size() * sizeof(GemmOp));
+        const int nd = static_cast<int>(ops.size());
+        steps_.push_back([off, nd, total, cls](cudaStream_t st, const uint8_t* slab) {
+            launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, cls, st);
+        });
+        const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
+        names_.push_back(std::string("gemm_") + kind +
+                         (cls >= 2 * kGemmClassTma ? "_pre" : cls >= kGemmClassTma ? "_tma" : "_reg") +
+                         std::to_string(cls % kGemmClassTma));
+        KernelStat w;
+        for (const GemmOp& o : ops) {
+            const auto bf = op_work(o);
+            w.bytes += bf.first, w.flops += bf.second;
+        }
+        work_.push_back(w);
     }
     void raw(std::function<void(cudaStream_t)> f, const char* name = "raw", double bytes = 0.0) {
         steps_.push_back([f](cudaStream_t st, const uint8_t*) { f(st); });
@@ -192,10 +198,33 @@ public:
         w.bytes = bytes;
         work_.push_back(w);
     }
+    // Parallel section: n independent sub-programs (disjoint outputs).  In a
+    // captured graph sub 0 runs on the parent stream and sub i on a side
+    // stream (fork / join events), so they execute concurrently; eagerly they
+    // run in order.  The caller fills the returned programs.
+    std::vector<Program*> par(int n) {
+        auto ps = std::make_unique<ParStep>();
+        std::vector<Program*> out;
+        for (int i = 0; i < n; ++i) {
+            ps->subs.push_back(std::make_unique<Program>());
+            out.push_back(ps->subs.back().get());
+        }
+        ParStep* raw_ps = ps.get();
+        pars_.push_back(std::move(ps));
+        steps_.push_back([this, raw_ps](cudaStream_t st, const uint8_t*) { run_par(*raw_ps, st); });
+        names_.push_back("par");
+        work_.push_back(KernelStat{});
+        par_of_.resize(steps_.size(), nullptr);
+        par_of_.back() = raw_ps;
+        return out;
+    }
     void finalize(cudaStream_t st) {
         slab_.alloc(std::max<size_t>(host_.size(), 64));
         if (!host_.empty())
             PBKD_CUDA(cudaMemcpyAsync(slab_.p, host_.data(), host_.size(), cudaMemcpyHostToDevice, st));
+        for (auto& ps : pars_)
+            for (auto& sub : ps->subs)
+                if (!sub->finalized_) sub->finalize(st);
         PBKD_CUDA(cudaStreamSynchronize(st));
         finalized_ = true;
     }
@@ -204,18 +233,25 @@ public:
         for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
     }
     // Eager run with a CUDA event after every launch; adds each launch's
-    // device time and algorithmic work to prof[name].
+    // device time and algorithmic work to prof[name] (parallel sections are
+    // profiled launch by launch, in order).
     void run_profiled(cudaStream_t st, std::map<std::string, KernelStat>& prof) {
         if (!finalized_) finalize(st);
         std::vector<cudaEvent_t> ev(steps_.size() + 1);
         for (auto& e : ev) PBKD_CUDA(cudaEventCreate(&e));
         PBKD_CUDA(cudaEventRecord(ev[0], st));
+        par_of_.resize(steps_.size(), nullptr);
         for (size_t i = 0; i < steps_.size(); ++i) {
-            steps_[i](st, static_cast<const uint8_t*>(slab_.p));
+            if (par_of_[i]) {
+                for (auto& sub : par_of_[i]->subs) sub->run_profiled(st, prof);
+            } else {
+                steps_[i](st, static_cast<const uint8_t*>(slab_.p));
+            }
             PBKD_CUDA(cudaEventRecord(ev[i + 1], st));
         }
         PBKD_CUDA(cudaEventSynchronize(ev.back()));
         for (size_t i = 0; i < steps_.size(); ++i) {
+            if (par_of_[i]) continue;
             float ms = 0.0f;
             PBKD_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
             KernelStat& e = prof[names_[i]];
@@ -226,23 +262,72 @@ public:
         }
         for (auto& e : ev) cudaEventDestroy(e);
     }
-    void build_graph(cudaStream_t st) {
+    void build_graph(cudaStream_t st, const std::vector<cudaStream_t>* side = nullptr) {
         if (!finalized_) finalize(st);
         cudaGraph_t g;
+        set_side(side);
         PBKD_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
         PBKD_CUDA(cudaStreamEndCapture(st, &g));
+        set_side(nullptr);
+        for (cudaEvent_t e : cap_events_) cudaEventDestroy(e);
+        cap_events_.clear();
         PBKD_CUDA(cudaGraphInstantiate(&exec_, g, 0));
         PBKD_CUDA(cudaGraphDestroy(g));
     }
     void launch_graph(cudaStream_t st) { PBKD_CUDA(cudaGraphLaunch(exec_, st)); }
     bool has_graph() const { return exec_ != nullptr; }
-    size_t launches() const { return steps_.size(); }
+    size_t launches() const {
+        size_t n = 0;
+        for (size_t i = 0; i < steps_.size(); ++i) {
+            const ParStep* ps = i < par_of_.size() ? par_of_[i] : nullptr;
+            if (!ps) ++n;
+            else
+                for (auto& sub : ps->subs) n += sub->launches();
+        }
+        return n;
+    }
     ~Program() {
         if (exec_) cudaGraphExecDestroy(exec_);
     }
 
 private:
+    struct ParStep {
+        std::vector<std::unique_ptr<Program>> subs;
+    };
+    // side streams while capturing (null: eager, sub-programs in order)
+    void set_side(const std::vector<cudaStream_t>* side) {
+        side_ = side;
+        for (auto& ps : pars_)
+            for (auto& sub : ps->subs) sub->set_side(side);
+    }
+    void run_par(ParStep& ps, cudaStream_t st) {
+        if (!side_ || side_->empty() || ps.subs.size() < 2) {
+            for (auto& sub : ps.subs) sub->run(st);
+            return;
+        }
+        std::vector<cudaEvent_t> joins;
+        for (size_t i = 1; i < ps.subs.size(); ++i) {
+            cudaStream_t bs = (*side_)[(i - 1) % side_->size()];
+            cudaEvent_t fork, join;
+            PBKD_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+            PBKD_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+            cap_events_.push_back(fork), cap_events_.push_back(join);
+            PBKD_CUDA(cudaEventRecord(fork, st));
+            PBKD_CUDA(cudaStreamWaitEvent(bs, fork, 0));
+            ps.subs[i]->run_on(bs);
+            PBKD_CUDA(cudaEventRecord(join, bs));
+            joins.push_back(join);
+        }
+        ps.subs[0]->run_on(st);
+        for (cudaEvent_t j : joins) PBKD_CUDA(cudaStreamWaitEvent(st, j, 0));
+    }
+    void run_on(cudaStream_t st) {  // finalized already (capture time)
+        for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
+        for (auto& ps : pars_)
+            for (auto& sub : ps->subs)
+                for (cudaEvent_t e : sub->cap_events_) cap_events_.push_back(e);
+    }
     static std::string op_name(const char* mangled) {  // "N8pbkd_gpu7DwFwdOpE" -> "DwFwdOp"
         std::string m(mangled), out;
         size_t i = m.find("pbkd_gpu");
@@ -256,6 +341,10 @@ private:
     std::vector<std::function<void(cudaStream_t, const uint8_t*)>> steps_;
     std::vector<std::string> names_;
     std::vector<KernelStat> work_;
+    std::vector<std::unique_ptr<ParStep>> pars_;
+    std::vector<ParStep*> par_of_;  // step index -> parallel section (or null)
+    const std::vector<cudaStream_t>* side_ = nullptr;
+    std::vector<cudaEvent_t> cap_events_;
     bool finalized_ = false;
     cudaGraphExec_t exec_ = nullptr;
 };
@@ -452,11 +541,15 @@ struct Engine::Impl {
     PhaseTrace trace;
     void* pinned = nullptr;  // readback staging (grows as needed)
     size_t pinned_bytes = 0;
+    std::vector<cudaStream_t> side_streams;  // parallel sections of the epoch graphs
 
     explicit Impl(int device) : dev(device) {
         PBKD_CUDA(cudaSetDevice(dev));
         g_alloc_stream = st;
         PBKD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const char* ps = std::getenv("PBKD_SIDE_STREAMS");
+        side_streams.resize(ps ? std::max(0, std::atoi(ps)) : 4);
+        for (cudaStream_t& s2 : side_streams) PBKD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
         cudaMemPool_t pool;
         PBKD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
         uint64_t keep = ~uint64_t(0);
@@ -472,6 +565,7 @@ struct Engine::Impl {
             cudaStreamSynchronize(st);
             cudaStreamDestroy(st);
         }
+        for (cudaStream_t s2 : side_streams) cudaStreamDestroy(s2);
         if (pinned) cudaFreeHost(pinned);
         g_alloc_stream = nullptr;
     }
@@ -1058,17 +1152,23 @@ struct Engine::Impl {
             }
             auto red_ctas = ctas_reduce;
             P.grouped<BnBwdApplyOp>(launch_bn_bwd_apply, aps, [](const BnBwdApplyOp& o) { return ctas_elem(o.total); });
-            P.gemm(dg);
-            P.gemm(wg);
-            P.grouped<ReduceOp>(launch_reduce, wr, red_ctas);
+            // two independent branches: input gradient (dgrad -> dw backward
+            // -> its reductions) and pointwise weight gradient (wgrad ->
+            // split-K reduction); disjoint buffers, concurrent in the graph
+            std::vector<Program*> br = P.par(2);
+            Program& bx = *br[0];
+            Program& bw = *br[1];
+            bx.gemm(dg);
             if (u > 0) {
-                P.grouped<DwBwdOp>(launch_dw_bwd, dbs, ctas_dw_bwd);
-                P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
-                P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fins, [](const BnBwdFinOp& o) { return ctas_cols(o.c); });
+                bx.grouped<DwBwdOp>(launch_dw_bwd, dbs, ctas_dw_bwd);
+                bx.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
+                bx.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fins, [](const BnBwdFinOp& o) { return ctas_cols(o.c); });
             } else {
-                P.grouped<DwGkOp>(launch_dw_gk, gks, ctas_dw_gk);
-                P.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
+                bx.grouped<DwGkOp>(launch_dw_gk, gks, ctas_dw_gk);
+                bx.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
             }
+            bw.gemm(wg);
+            bw.grouped<ReduceOp>(launch_reduce, wr, red_ctas);
         }
         // ---- optimizer
         std::vector<SgdOp> sg;
@@ -1690,7 +1790,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             }
             if (opt.use_graphs) {
                 ep.pre->build_graph(st);
-                ep.post->build_graph(st);
+                ep.post->build_graph(st, &side_streams);
             }
             if (std::getenv("PBKD_PROFILE")) {  // one extra eager pass, timed per launch
                 std::map<std::string, KernelStat> pa, pb;

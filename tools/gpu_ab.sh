@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider --timeout=280 -x -k "gemm_kernels or pointwise or replay" > gpurun_out/pytest_gemm.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gemm.log
-PBKD_BN64=1 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_a.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout=400 -x > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+PBKD_SIDE_STREAMS=0 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_a.log 2>&1
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_b.log 2>&1
