@@ -1209,15 +1209,27 @@ struct Engine::Impl {
             P.raw([=](cudaStream_t s) { launch_gather_nhwc(img, idx, nc, in_c, in_h, in_w, ping, s); });
             float* cur = ping;
             float* nxt = pong;
+            // boundary j's rows are scattered while teacher block j+1 runs
+            // (both only read `cur`): a parallel section per boundary
             for (int j = 0; j <= kmax; ++j) {
-                if (j > 0) {
-                    teacher_block(P, j - 1, cur, nxt, nc, t1, sk);
-                    std::swap(cur, nxt);
-                }
                 std::vector<ScatterOp> sc;
                 for (const Sink& s : sinks)
                     if (s.boundary == j) sc.push_back(ScatterOp{cur, s.dst, s.pos + t0, nc, s.width, 0});
-                P.grouped<ScatterOp>(launch_scatter, sc, [](const ScatterOp&) { return kScatterCtas; });
+                auto scatter = [](Program& Q, std::vector<ScatterOp> ops) {
+                    Q.grouped<ScatterOp>(launch_scatter, std::move(ops), [](const ScatterOp&) { return kScatterCtas; });
+                };
+                if (j == kmax) {
+                    scatter(P, std::move(sc));
+                    break;
+                }
+                if (sc.empty()) {
+                    teacher_block(P, j, cur, nxt, nc, t1, sk);
+                } else {
+                    std::vector<Program*> br = P.par(2);
+                    teacher_block(*br[0], j, cur, nxt, nc, t1, sk);
+                    scatter(*br[1], std::move(sc));
+                }
+                std::swap(cur, nxt);
             }
         }
     }
@@ -1789,7 +1801,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 add_step(*ep.post, act, step, 0, ntrain, gs);
             }
             if (opt.use_graphs) {
-                ep.pre->build_graph(st);
+                ep.pre->build_graph(st, &side_streams);
                 ep.post->build_graph(st, &side_streams);
             }
             if (std::getenv("PBKD_PROFILE")) {  // one extra eager pass, timed per launch
