@@ -145,7 +145,7 @@ def run_reference(args):
     spec, classes, images, labels, tr, ev, blocks = workload(args.config, args.dataset_size, P)
     tw = O.teacher_init(spec, O.mix_seed(42, 0x7E11))
     threads = os.cpu_count() or 1
-    bsz = min(args.batch, 8)
+    bsz = args.batch  # same batch as the GPU arm: one optimizer step of every block
     seed_of = lambda k: O.mix_seed(42, k)  # noqa: E731
     for _ in range(args.warmup):
         cpu_reference_step(O, spec, tw, images, labels, tr, ev, blocks, bsz, seed_of, threads)
@@ -320,7 +320,7 @@ def main():
         O = OR.Oracle("ref" if kind == "reference" else "orc")
         tw = O.teacher_init(spec, teacher_seed)
         threads = os.cpu_count() or 1
-        bsz = 8
+        bsz = B
         T = cpu_reference_step(O, spec, tw, images, labels, tr, ev, blocks, bsz,
                                lambda k: P.mix_seed(42, k), threads)
         cpu = {"value": bsz / T, "unit": "samples/s", "cores": threads, "kind": kind,
