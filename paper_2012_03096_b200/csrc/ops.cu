@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restr
                     gw[r][cc + 1] = g0[r * rs + cc * kDwC];
                     xw[r][cc + 1] = x0[r * rs + cc * kDwC];
                 }
+            #pragma unroll 4
             for (int x = 0; x < o.wd; ++x) {
 #pragma unroll
                 for (int r = 0; r < 3; ++r) {
