@@ -23,9 +23,15 @@ bool pdl_enabled() {
 }
 
 // ---------------------------------------------------------------- partition
+// Row partition of the loss / BN-backward partial sums: ~16K elements per CTA
+// (per-CTA fixed costs amortised; fewer partial rows for the final sums).
 int rows_part_ctas(long long rows, int c) {
     const long long elems = rows * static_cast<long long>(c);
-    long long ctas = (elems + 4095) / 4096;
+    static const long long per_cta = [] {
+        const char* e = std::getenv("PBKD_ROWS_PER_CTA");
+        return e ? std::max(256LL, std::atoll(e)) : 16384LL;
+    }();
+    long long ctas = (elems + per_cta - 1) / per_cta;
     ctas = std::max<long long>(1, std::min<long long>(ctas, 1024));
     ctas = std::min<long long>(ctas, rows);
     const int per = rows_part_per(rows, static_cast<int>(ctas));
