@@ -1185,7 +1185,7 @@ struct Engine::Impl {
             o.failed = c.failed;
             sg.push_back(o);
         }
-        P.grouped<SgdOp>(launch_sgd, sg, [](const SgdOp& o) { return ctas_elem(o.n); });
+        P.grouped<SgdOp>(launch_sgd, sg, [](const SgdOp& o) { return ctas_sgd(o.n); });
     }
 
     // Teacher pass over `n` samples (dataset indices at d_idx), scattering

@@ -817,7 +817,7 @@ int pbkd_k_sgd(pbkd_ctx* ctx, float* w, const float* g, float* v, size_t n, floa
         if (m < 0.0f || m >= 1.0f) throw std::invalid_argument("sgd_step: momentum must be in [0,1)");
         SgdOp o{};
         o.w = w, o.v = v, o.g = g, o.n = static_cast<long long>(n), o.lr = lr, o.mom = m;
-        launch_one(ctx->eng->stream(), launch_sgd, o, ctas_elem(o.n));
+        launch_one(ctx->eng->stream(), launch_sgd, o, ctas_sgd(o.n));
     });
 }
 
@@ -832,7 +832,7 @@ int pbkd_sgd_host(float* w, const float* g, float* v, size_t n, float lr, float 
         PBKD_CUDA(cudaMemcpy(dv.p, v, n * 4, cudaMemcpyHostToDevice));
         SgdOp o{};
         o.w = dw.p, o.v = dv.p, o.g = dg.p, o.n = static_cast<long long>(n), o.lr = lr, o.mom = m;
-        launch_one(cudaStream_t(0), launch_sgd, o, ctas_elem(o.n));
+        launch_one(cudaStream_t(0), launch_sgd, o, ctas_sgd(o.n));
         PBKD_CUDA(cudaMemcpy(w, dw.p, n * 4, cudaMemcpyDeviceToHost));
         PBKD_CUDA(cudaMemcpy(v, dv.p, n * 4, cudaMemcpyDeviceToHost));
     });

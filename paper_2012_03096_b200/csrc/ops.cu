@@ -38,7 +38,6 @@ int rows_part_ctas(long long rows, int c) {
     return ceil_div(rows, per);
 }
 int rows_part_per(long long rows, int ctas) { return ceil_div(rows, ctas); }
-int ctas_elem(long long total) { return std::max(1, ceil_div(total, 256LL * 4)); }
 
 template <class Op>
 __device__ __forceinline__ const Op& op_of(const Op* ops, int nd, int& local) {
@@ -678,53 +677,76 @@ __device__ __forceinline__ BnBwdPar bn_bwd_par(const BnBwdApplyOp& o, int ch) {
     return {o.mean[ch], o.inv[ch], o.gamma[ch], o.beta[ch], o.sg[ch], o.sgx[ch]};
 }
 
+__device__ __forceinline__ float4 bn_bwd_quad(const BnBwdApplyOp& o, int ch, float4 p, float4 g) {
+    const float4 mn = __ldg(reinterpret_cast<const float4*>(o.mean + ch));
+    const float4 iv = __ldg(reinterpret_cast<const float4*>(o.inv + ch));
+    const float4 gm = __ldg(reinterpret_cast<const float4*>(o.gamma + ch));
+    const float4 bt = __ldg(reinterpret_cast<const float4*>(o.beta + ch));
+    const float4 s1 = __ldg(reinterpret_cast<const float4*>(o.sg + ch));
+    const float4 s2 = __ldg(reinterpret_cast<const float4*>(o.sgx + ch));
+    float4 r;
+    r.x = bn_bwd_one(o, {mn.x, iv.x, gm.x, bt.x, s1.x, s2.x}, p.x, g.x);
+    r.y = bn_bwd_one(o, {mn.y, iv.y, gm.y, bt.y, s1.y, s2.y}, p.y, g.y);
+    r.z = bn_bwd_one(o, {mn.z, iv.z, gm.z, bt.z, s1.z, s2.z}, p.z, g.z);
+    r.w = bn_bwd_one(o, {mn.w, iv.w, gm.w, bt.w, s1.w, s2.w}, p.w, g.w);
+    return r;
+}
+__device__ __forceinline__ void split_store4(float* hi, float* lo, long long i, float4 r) {
+    float4 h, l;
+    h.x = __uint_as_float(tc_split_hi(r.x)), l.x = __uint_as_float(tc_split_hi(__fsub_rn(r.x, h.x)));
+    h.y = __uint_as_float(tc_split_hi(r.y)), l.y = __uint_as_float(tc_split_hi(__fsub_rn(r.y, h.y)));
+    h.z = __uint_as_float(tc_split_hi(r.z)), l.z = __uint_as_float(tc_split_hi(__fsub_rn(r.z, h.z)));
+    h.w = __uint_as_float(tc_split_hi(r.w)), l.w = __uint_as_float(tc_split_hi(__fsub_rn(r.w, h.w)));
+    *reinterpret_cast<float4*>(hi + i) = h;
+    *reinterpret_cast<float4*>(lo + i) = l;
+}
+
+// kElemQuads float4 quads per thread (strided by the CTA: coalesced), all
+// loads issued before any store
+constexpr int kElemQuads = 4;
+int ctas_elem(long long total) { return std::max(1, ceil_div(total, 4LL * kThreads * kElemQuads)); }
+constexpr int kSgdQuads = 1;  // SGD: more CTAs beat deeper per-thread batches (measured)
+int ctas_sgd(long long n) { return std::max(1, ceil_div(n, 4LL * kThreads * kSgdQuads)); }
+
 __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApplyOp* __restrict__ ops, int nd) {
     pdl_enter();
     int local;
     const BnBwdApplyOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
-    const long long base = (static_cast<long long>(local) * kThreads + threadIdx.x) * 4;
-    if (base >= o.total) return;
     const float* tg = o.t ? o.t : o.gin;
-    if ((o.c & 3) == 0 && base + 4 <= o.total) {
-        const int ch = static_cast<int>(base % o.c);
-        const float4 p = __ldg(reinterpret_cast<const float4*>(o.p + base));
-        const float4 g = __ldg(reinterpret_cast<const float4*>(tg + base));
-        const float4 mn = __ldg(reinterpret_cast<const float4*>(o.mean + ch));
-        const float4 iv = __ldg(reinterpret_cast<const float4*>(o.inv + ch));
-        const float4 gm = __ldg(reinterpret_cast<const float4*>(o.gamma + ch));
-        const float4 bt = __ldg(reinterpret_cast<const float4*>(o.beta + ch));
-        const float4 s1 = __ldg(reinterpret_cast<const float4*>(o.sg + ch));
-        const float4 s2 = __ldg(reinterpret_cast<const float4*>(o.sgx + ch));
-        float4 r;
-        r.x = bn_bwd_one(o, {mn.x, iv.x, gm.x, bt.x, s1.x, s2.x}, p.x, g.x);
-        r.y = bn_bwd_one(o, {mn.y, iv.y, gm.y, bt.y, s1.y, s2.y}, p.y, g.y);
-        r.z = bn_bwd_one(o, {mn.z, iv.z, gm.z, bt.z, s1.z, s2.z}, p.z, g.z);
-        r.w = bn_bwd_one(o, {mn.w, iv.w, gm.w, bt.w, s1.w, s2.w}, p.w, g.w);
-        if (o.gout_hi) {
-            float4 h, l;
-            h.x = __uint_as_float(tc_split_hi(r.x)), l.x = __uint_as_float(tc_split_hi(__fsub_rn(r.x, h.x)));
-            h.y = __uint_as_float(tc_split_hi(r.y)), l.y = __uint_as_float(tc_split_hi(__fsub_rn(r.y, h.y)));
-            h.z = __uint_as_float(tc_split_hi(r.z)), l.z = __uint_as_float(tc_split_hi(__fsub_rn(r.z, h.z)));
-            h.w = __uint_as_float(tc_split_hi(r.w)), l.w = __uint_as_float(tc_split_hi(__fsub_rn(r.w, h.w)));
-            *reinterpret_cast<float4*>(o.gout_hi + base) = h;
-            *reinterpret_cast<float4*>(o.gout_lo + base) = l;
-        } else {
-            *reinterpret_cast<float4*>(o.gout + base) = r;
+    const long long cta0 = static_cast<long long>(local) * kThreads * kElemQuads * 4;
+    if ((o.c & 3) == 0 && cta0 + 4LL * kThreads * kElemQuads <= o.total) {
+        float4 p[kElemQuads], g[kElemQuads];
+#pragma unroll
+        for (int j = 0; j < kElemQuads; ++j) {
+            const long long i = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
+            p[j] = __ldg(reinterpret_cast<const float4*>(o.p + i));
+            g[j] = __ldg(reinterpret_cast<const float4*>(tg + i));
+        }
+#pragma unroll
+        for (int j = 0; j < kElemQuads; ++j) {
+            const long long i = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
+            const float4 r = bn_bwd_quad(o, static_cast<int>(i % o.c), p[j], g[j]);
+            if (o.gout_hi) split_store4(o.gout_hi, o.gout_lo, i, r);
+            else *reinterpret_cast<float4*>(o.gout + i) = r;
         }
         return;
     }
-    float pv[4], gv[4], rv[4];
-    const int cnt = static_cast<int>(min(4LL, o.total - base));
-    for (int q = 0; q < cnt; ++q) pv[q] = o.p[base + q], gv[q] = tg[base + q];
-    for (int q = 0; q < cnt; ++q) rv[q] = bn_bwd_one(o, bn_bwd_par(o, static_cast<int>((base + q) % o.c)), pv[q], gv[q]);
-    for (int q = 0; q < cnt; ++q) {
-        if (o.gout_hi) {
-            const float hv = __uint_as_float(tc_split_hi(rv[q]));
-            o.gout_hi[base + q] = hv;
-            o.gout_lo[base + q] = __uint_as_float(tc_split_hi(__fsub_rn(rv[q], hv)));
-        } else {
-            o.gout[base + q] = rv[q];
+    for (int j = 0; j < kElemQuads; ++j) {  // tail / odd channel counts
+        const long long base = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
+        if (base >= o.total) break;
+        float pv[4], gv[4], rv[4];
+        const int cnt = static_cast<int>(min(4LL, o.total - base));
+        for (int q = 0; q < cnt; ++q) pv[q] = o.p[base + q], gv[q] = tg[base + q];
+        for (int q = 0; q < cnt; ++q) rv[q] = bn_bwd_one(o, bn_bwd_par(o, static_cast<int>((base + q) % o.c)), pv[q], gv[q]);
+        for (int q = 0; q < cnt; ++q) {
+            if (o.gout_hi) {
+                const float hv = __uint_as_float(tc_split_hi(rv[q]));
+                o.gout_hi[base + q] = hv;
+                o.gout_lo[base + q] = __uint_as_float(tc_split_hi(__fsub_rn(rv[q], hv)));
+            } else {
+                o.gout[base + q] = rv[q];
+            }
         }
     }
 }
@@ -735,45 +757,50 @@ void launch_bn_bwd_apply(const BnBwdApplyOp* d, int nd, int ctas, cudaStream_t s
 }
 
 // -------------------------------------------------------------------- SGD
+__device__ __forceinline__ void sgd_quad(const SgdOp& o, long long i, float4 v, float4 g, float4 w) {
+    // v = m*v + g; w = w - lr*v   (ops.hpp:554-557, two roundings each)
+    float4 nv, nw;
+    nv.x = add(mul(o.mom, v.x), g.x), nv.y = add(mul(o.mom, v.y), g.y);
+    nv.z = add(mul(o.mom, v.z), g.z), nv.w = add(mul(o.mom, v.w), g.w);
+    nw.x = sub(w.x, mul(o.lr, nv.x)), nw.y = sub(w.y, mul(o.lr, nv.y));
+    nw.z = sub(w.z, mul(o.lr, nv.z)), nw.w = sub(w.w, mul(o.lr, nv.w));
+    *reinterpret_cast<float4*>(o.v + i) = nv;
+    *reinterpret_cast<float4*>(o.w + i) = nw;
+    if (o.w_hi) split_store4(o.w_hi, o.w_lo, i, nw);
+}
+
 __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__ ops, int nd) {
     pdl_enter();
     int local;
     const SgdOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
-    const long long base = (static_cast<long long>(local) * kThreads + threadIdx.x) * 4;
-    if (base >= o.n) return;
-    // v = m*v + g; w = w - lr*v   (ops.hpp:554-557, two roundings each)
-    if (base + 4 <= o.n) {  // flat parameter buffers are 16-byte aligned, n % 4 == 0
-        const float4 v = *reinterpret_cast<const float4*>(o.v + base);
-        const float4 g = *reinterpret_cast<const float4*>(o.g + base);
-        const float4 w = *reinterpret_cast<const float4*>(o.w + base);
-        float4 nv, nw;
-        nv.x = add(mul(o.mom, v.x), g.x), nv.y = add(mul(o.mom, v.y), g.y);
-        nv.z = add(mul(o.mom, v.z), g.z), nv.w = add(mul(o.mom, v.w), g.w);
-        nw.x = sub(w.x, mul(o.lr, nv.x)), nw.y = sub(w.y, mul(o.lr, nv.y));
-        nw.z = sub(w.z, mul(o.lr, nv.z)), nw.w = sub(w.w, mul(o.lr, nv.w));
-        *reinterpret_cast<float4*>(o.v + base) = nv;
-        *reinterpret_cast<float4*>(o.w + base) = nw;
-        if (o.w_hi) {
-            float4 h, l;
-            h.x = __uint_as_float(tc_split_hi(nw.x)), l.x = __uint_as_float(tc_split_hi(__fsub_rn(nw.x, h.x)));
-            h.y = __uint_as_float(tc_split_hi(nw.y)), l.y = __uint_as_float(tc_split_hi(__fsub_rn(nw.y, h.y)));
-            h.z = __uint_as_float(tc_split_hi(nw.z)), l.z = __uint_as_float(tc_split_hi(__fsub_rn(nw.z, h.z)));
-            h.w = __uint_as_float(tc_split_hi(nw.w)), l.w = __uint_as_float(tc_split_hi(__fsub_rn(nw.w, h.w)));
-            *reinterpret_cast<float4*>(o.w_hi + base) = h;
-            *reinterpret_cast<float4*>(o.w_lo + base) = l;
+    const long long cta0 = static_cast<long long>(local) * kThreads * kSgdQuads * 4;
+    if (cta0 + 4LL * kThreads * kSgdQuads <= o.n) {  // flat buffers: 16-byte aligned, n % 4 == 0
+        float4 v[kSgdQuads], g[kSgdQuads], w[kSgdQuads];
+#pragma unroll
+        for (int j = 0; j < kSgdQuads; ++j) {
+            const long long i = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
+            v[j] = *reinterpret_cast<const float4*>(o.v + i);
+            g[j] = __ldg(reinterpret_cast<const float4*>(o.g + i));
+            w[j] = *reinterpret_cast<const float4*>(o.w + i);
         }
+#pragma unroll
+        for (int j = 0; j < kSgdQuads; ++j)
+            sgd_quad(o, cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4, v[j], g[j], w[j]);
         return;
     }
-    for (long long i = base; i < o.n; ++i) {
-        const float v = add(mul(o.mom, o.v[i]), o.g[i]);
-        o.v[i] = v;
-        const float w = sub(o.w[i], mul(o.lr, v));
-        o.w[i] = w;
-        if (o.w_hi) {
-            const float hv = __uint_as_float(tc_split_hi(w));
-            o.w_hi[i] = hv;
-            o.w_lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(w, hv)));
+    for (int j = 0; j < kSgdQuads; ++j) {
+        const long long base = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
+        for (long long i = base; i < min(o.n, base + 4); ++i) {
+            const float vv = add(mul(o.mom, o.v[i]), o.g[i]);
+            o.v[i] = vv;
+            const float ww = sub(o.w[i], mul(o.lr, vv));
+            o.w[i] = ww;
+            if (o.w_hi) {
+                const float hv = __uint_as_float(tc_split_hi(ww));
+                o.w_hi[i] = hv;
+                o.w_lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(ww, hv)));
+            }
         }
     }
 }

@@ -257,7 +257,8 @@ void dw_fwd_finalize(DwFwdOp& o);
 void dw_bwd_finalize(DwBwdOp& o);
 void dw_gk_finalize(DwGkOp& o);
 int ctas_gemm(const GemmOp& o);
-int ctas_elem(long long total);
+int ctas_elem(long long total);  // bn_bwd_apply
+int ctas_sgd(long long n);
 int ctas_cols(int c);  // bn_stat / bn_bwd_fin CTAs per task
 
 // Non-grouped helpers used by evaluation / teacher / tests -----------------
