@@ -226,21 +226,27 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
             stores = 1;
         }
         if (epi == 1) {
-            // (column, quarter) pairs over the 8 warps; lane = row of the quarter
-            for (int pq = warp8; pq < 128; pq += 8) {
-                const int col = pq & 31, qq = pq >> 5;
-                const float v = lds32(cs_addr(cs, qq * 32 + lane, col));
-                float sv = v, sq = __fmul_rn(v, v);
+            // thread = (column, row quarter, sum | sum of squares), warp-uniform
+            // quarter and kind: the quarter's 32 rows summed serially in the
+            // xor-butterfly tree of gemm_epilogue (rows i, i+16 first, then
+            // +8, +4, +2, +1: identical bits, no shuffle latency chains)
+            const int col = et & 31, qq = (et >> 5) & 3, sqr = et >> 7;
+            float v[8];
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    sv = __fadd_rn(sv, __shfl_xor_sync(0xffffffffu, sv, off));
-                    sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, off));
+            for (int i = 0; i < 8; ++i) {
+                float x[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {  // rows i, i+16, i+8, i+24
+                    x[k] = lds32(cs_addr(cs, qq * 32 + i + (k & 1) * 16 + (k >> 1) * 8, col));
+                    if (sqr) x[k] = __fmul_rn(x[k], x[k]);
                 }
-                if (lane == 0) {
-                    red[0][qq][col] = sv;
-                    red[1][qq][col] = sq;
-                }
+                v[i] = __fadd_rn(__fadd_rn(x[0], x[1]), __fadd_rn(x[2], x[3]));
             }
+#pragma unroll
+            for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+                for (int i = 0; i < w; ++i) v[i] = __fadd_rn(v[i], v[i + w]);
+            red[sqr][qq][col] = v[0];
             named_bar(1, 256);
             if (et < 32) {
                 const int cg = n0 + pass * 32 + et;
@@ -295,6 +301,13 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     (void)trace;
 #endif
     if (threadIdx.x == 0) mark(5, 0);
+#ifdef PBKD_GEMM_TRACE_BUILD
+    if (trace != nullptr && threadIdx.x == 0 && blockIdx.x < 1024) {  // per-CTA start
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace[10 * 512 + blockIdx.x] = t;
+    }
+#endif
     const uint32_t sbase = smem_u32(smem_raw);
     const uint32_t pad = (1024u - (sbase & 1023u)) & 1023u;
     uint8_t* raw_ring = smem_raw + pad;  // stays a shared-space pointer
@@ -581,6 +594,17 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
 done:
     tc_fence_before();
     __syncthreads();
+#ifdef PBKD_GEMM_TRACE_BUILD
+    if (trace != nullptr && threadIdx.x == 0 && blockIdx.x < 1024) {  // per-CTA end and chunk count
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        trace[10 * 512 + 1024 + blockIdx.x] = t;
+        unsigned long long nc = 0;
+        for (int j = 0; j < ntiles; ++j)
+            if (tiles_sh[j].op >= 0) nc += tiles_sh[j].g.nchunks;
+        trace[10 * 512 + 2048 + blockIdx.x] = nc | (static_cast<unsigned long long>(ntiles) << 32);
+    }
+#endif
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::tmem_cols));
@@ -641,9 +665,9 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (trace_on) PBKD_CUDA(cudaStreamIsCapturing(st, &cap));
     if (trace_on && cap == cudaStreamCaptureStatusNone && !trace)
-        PBKD_CUDA(cudaMalloc(&trace, 10 * 512 * sizeof(unsigned long long)));
+        PBKD_CUDA(cudaMalloc(&trace, (10 * 512 + 3 * 1024) * sizeof(unsigned long long)));
     unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
-    if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, 10 * 512 * sizeof(unsigned long long), st));
+    if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, (10 * 512 + 3 * 1024) * sizeof(unsigned long long), st));
     launch_k(umma_tma_kernel<BN, PS>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(Cfg<BN, PS>::smem), st, d, nd,
              total, tr);
     PBKD_LAUNCH_CHECK();
@@ -653,14 +677,36 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     }();
     static int launch_no = 0;
     if (tr) ++launch_no;
-    if (tr && launch_no >= trace_from && launch_no < trace_from + 8) {  // diagnosis: CTA 0 timeline on stderr
-        std::vector<unsigned long long> h(10 * 512);
+    static const int trace_n = [] {
+        const char* e = std::getenv("PBKD_GEMM_TRACE_N");
+        return e ? std::atoi(e) : 8;
+    }();
+    if (tr && launch_no >= trace_from && launch_no < trace_from + trace_n) {  // diagnosis: CTA 0 timeline on stderr
+        std::vector<unsigned long long> h(10 * 512 + 3 * 1024);
         PBKD_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
         PBKD_CUDA(cudaStreamSynchronize(st));
         const unsigned long long t0 = h[5 * 512];
         auto rel = [&](int ev, int i) { return h[ev * 512 + i] ? static_cast<long long>(h[ev * 512 + i] - t0) : -1LL; };
         std::fprintf(stderr, "[gemm-trace] launch %d BN=%d grid=%d tiles=%d nd=%d setup=%lld ns\n", launch_no, BN, grid,
                      total, nd, rel(5, 1));
+        {  // per-CTA: start / end relative to the earliest start, chunks, tiles
+            unsigned long long s0 = ~0ull, e1 = 0;
+            for (int b = 0; b < grid && b < 1024; ++b) {
+                s0 = std::min(s0, h[5120 + b]);
+                e1 = std::max(e1, h[5120 + 1024 + b]);
+            }
+            std::fprintf(stderr, "[gemm-cta] launch %d BN=%d PS=%d grid=%d span %.2f us\n", launch_no, BN, PS ? 1 : 0,
+                         grid, (e1 - s0) * 1e-3);
+            std::vector<GemmOp> hop(static_cast<size_t>(nd));
+            PBKD_CUDA(cudaMemcpy(hop.data(), d, hop.size() * sizeof(GemmOp), cudaMemcpyDeviceToHost));
+            for (const GemmOp& o : hop)
+                std::fprintf(stderr, "[gemm-cta]   op M=%d N=%d K=%d ksplit=%d tiles=%dx%d epi=%d conv=%d\n", o.M, o.N,
+                             o.K, o.ksplit, o.tiles_m, o.tiles_n, o.epi, o.conv);
+            for (int b = 0; b < grid && b < 1024; ++b)
+                std::fprintf(stderr, "[gemm-cta]   cta %3d start %7.2f end %7.2f chunks %4llu tiles %llu\n", b,
+                             (h[5120 + b] - s0) * 1e-3, (h[5120 + 1024 + b] - s0) * 1e-3, h[5120 + 2048 + b] & 0xffffffffull,
+                             h[5120 + 2048 + b] >> 32);
+        }
         for (int i = 0; i < 512 && h[i]; ++i)
             std::fprintf(stderr, "[gemm-trace]   chunk %3d: tma %8lld raw_full %8lld op_empty %8lld A %8lld B %8lld fence %8lld mma %8lld drain %8lld\n",
                          i, rel(0, i), rel(6, i), rel(7, i), rel(8, i), rel(9, i), rel(1, i), rel(2, i), rel(3, i));
