@@ -87,6 +87,35 @@ __device__ __forceinline__ uint32_t tc_split_hi(float x) {
     return r & 0xFFFFE000u;
 }
 
+// Packed fp32x2 arithmetic (FFMA2: two lanes per instruction, each rounded
+// exactly like the scalar _rn op).  mul / add / sub are spelled as single
+// fma.rn.f32x2 with a -0 addend / a 1 or -1 multiplier; those constants are
+// loaded from memory (pk_consts) so that ptxas cannot simplify the fma back
+// into a mul + add pair and contract it with a neighbour.
+static __device__ __align__(16) float g_pk_consts[4] = {1.0f, -0.0f, -1.0f, 0.0f};  // per translation unit
+struct PkConsts {
+    float2 one, nz, mone, z;
+};
+__device__ __forceinline__ PkConsts pk_consts() {
+    float a, b, c, d;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(g_pk_consts));
+    return PkConsts{make_float2(a, a), make_float2(b, b), make_float2(c, c), make_float2(d, d)};
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+// rn(a * b) and rn(a + b), rn(a - b) per lane
+__device__ __forceinline__ float2 mul2(const PkConsts& k, float2 a, float2 b) { return fma2(a, b, k.nz); }
+__device__ __forceinline__ float2 add2(const PkConsts& k, float2 a, float2 b) { return fma2(a, k.one, b); }
+__device__ __forceinline__ float2 sub2(const PkConsts& k, float2 a, float2 b) { return fma2(b, k.mone, a); }
+
 // Which op of a grouped launch owns work item t (ops sorted by cta_begin,
 // ops[0].cta_begin == 0).  Must be called by all 32 lanes of a warp with the
 // same t: lane l reads ops[l].cta_begin, one ballot -- a single global-load

@@ -8,9 +8,13 @@
 // trees: deterministic run to run, equal to the reference within fp32
 // tolerance.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "ops.cuh"
+#include "tc.cuh"
 
 namespace pbkd_gpu {
 
@@ -21,6 +25,73 @@ bool pdl_enabled() {
     }();
     return on;
 }
+
+// ------------------------------------------------------------ CTA tracer
+// Diagnosis only (build with NVEXTRA=-DPBKD_GEMM_TRACE_BUILD, run with
+// PBKD_CTA_TRACE=<kernel name>): globaltimer stamps per CTA at 4 points,
+// summarised per launch on stderr.
+#ifdef PBKD_GEMM_TRACE_BUILD
+__device__ unsigned long long* g_cta_trace = nullptr;
+__device__ __forceinline__ void cta_mark(int ev) {
+    unsigned long long* tr = g_cta_trace;
+    if (threadIdx.x == 0 && tr != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[blockIdx.x * 4 + ev] = t;
+    }
+}
+template <class Launch>
+void traced(const char* name, int ctas, cudaStream_t st, Launch launch) {
+    static const char* want = std::getenv("PBKD_CTA_TRACE");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    PBKD_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (!want || std::strcmp(want, name) != 0 || cap != cudaStreamCaptureStatusNone) {
+        launch();
+        return;
+    }
+    unsigned long long* buf = nullptr;
+    PBKD_CUDA(cudaMalloc(&buf, static_cast<size_t>(ctas) * 4 * 8));
+    PBKD_CUDA(cudaMemsetAsync(buf, 0, static_cast<size_t>(ctas) * 4 * 8, st));
+    PBKD_CUDA(cudaMemcpyToSymbolAsync(g_cta_trace, &buf, sizeof(buf), 0, cudaMemcpyHostToDevice, st));
+    launch();
+    unsigned long long* none = nullptr;
+    PBKD_CUDA(cudaMemcpyToSymbolAsync(g_cta_trace, &none, sizeof(none), 0, cudaMemcpyHostToDevice, st));
+    std::vector<unsigned long long> h(static_cast<size_t>(ctas) * 4);
+    PBKD_CUDA(cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    PBKD_CUDA(cudaStreamSynchronize(st));
+    PBKD_CUDA(cudaFree(buf));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int b = 0; b < ctas; ++b)
+        if (h[b * 4]) t0 = std::min(t0, h[b * 4]), t1 = std::max(t1, h[b * 4 + 3]);
+    std::vector<double> ph[3];
+    for (int b = 0; b < ctas; ++b) {
+        if (!h[b * 4] || !h[b * 4 + 1] || !h[b * 4 + 2] || !h[b * 4 + 3]) continue;
+        for (int k = 0; k < 3; ++k) ph[k].push_back((h[b * 4 + k + 1] - h[b * 4 + k]) * 1e-3);
+    }
+    auto med = [](std::vector<double> v) {
+        if (v.empty()) return 0.0;
+        std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+        return v[v.size() / 2];
+    };
+    auto mx = [](const std::vector<double>& v) { return v.empty() ? 0.0 : *std::max_element(v.begin(), v.end()); };
+    static int no = 0;
+    std::fprintf(stderr, "[cta-trace] %s #%d ctas=%d span %.2f us | setup med %.2f max %.2f | stage med %.2f max %.2f | compute med %.2f max %.2f\n",
+                 name, no++, ctas, (t1 - t0) * 1e-3, med(ph[0]), mx(ph[0]), med(ph[1]), mx(ph[1]), med(ph[2]), mx(ph[2]));
+    // start-time histogram (waves)
+    std::vector<double> st0;
+    for (int b = 0; b < ctas; ++b)
+        if (h[b * 4]) st0.push_back((h[b * 4] - t0) * 1e-3);
+    std::sort(st0.begin(), st0.end());
+    std::fprintf(stderr, "[cta-trace]   starts: p10 %.2f p50 %.2f p90 %.2f max %.2f\n", st0[st0.size() / 10], st0[st0.size() / 2],
+                 st0[st0.size() * 9 / 10], st0.back());
+}
+#else
+__device__ __forceinline__ void cta_mark(int) {}
+template <class Launch>
+void traced(const char*, int, cudaStream_t, Launch launch) {
+    launch();
+}
+#endif
 
 // ---------------------------------------------------------------- partition
 // Row partition of the loss / BN-backward partial sums: ~16K elements per CTA
@@ -97,7 +168,15 @@ __device__ void cta_reduce_rows(float* red, const float* v, const Geo& g, int rr
 // consecutive words (conflict-free); global loads/stores are 128-byte rows.
 constexpr int kDwC = 32;             // channels per CTA
 constexpr int kDwLanes = kThreads / kDwC;
-constexpr int kDwTileBytes = 48 * 1024;  // per staged array
+// Shared-memory budget per staged array (PBKD_DW_TILE_KB, default 48; the
+// dw backward's reduction needs >= 12 KB).
+static int dw_tile_bytes() {
+    static const int b = [] {
+        const char* e = std::getenv("PBKD_DW_TILE_KB");
+        return std::max(12, std::min(96, e ? std::atoi(e) : 48)) * 1024;
+    }();
+    return b;
+}
 
 DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays) {
     DwTile t{};
@@ -112,7 +191,7 @@ DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays) {
     auto fp = [&](const DwTile& q) {
         return static_cast<long long>(q.ni) * ((q.th - 1) * stride + 3) * ((wo - 1) * stride + 3) * kDwC * 4;
     };
-    while (fp(t) > kDwTileBytes / std::max(1, arrays - 1) && (t.ni > 1 || t.th > 1)) {
+    while (fp(t) > dw_tile_bytes() / std::max(1, arrays - 1) && (t.ni > 1 || t.th > 1)) {
         if (t.ni > 1) t.ni = (t.ni + 1) / 2;
         else t.th = (t.th + 1) / 2;
     }
@@ -121,20 +200,40 @@ DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays) {
     t.tiles_y = ceil_div(ho, t.th);
     t.tiles = ceil_div(n, t.ni) * t.tiles_y;
     t.cslices = ceil_div(c, kDwC);
+    // x segments per output row so that the 16 packed row workers all have
+    // work on tiles with few rows (wide images)
+    t.xsh = 0;
+    while ((t.ni * t.th << t.xsh) < 16 && (2 << t.xsh) <= wo) ++t.xsh;
     return t;
 }
 static size_t dw_smem(const DwTile& t) { return static_cast<size_t>(t.ni) * t.tr * t.tw * kDwC * sizeof(float); }
 
-void dw_fwd_finalize(DwFwdOp& o) { o.tile = dw_tile(o.n, o.ho, o.wo, o.c, o.stride, 1); }
+// Tensor maps of the staged tiles (TMA path) are built here, so the tensor
+// pointers must be final before finalize.
+void dw_fwd_finalize(DwFwdOp& o) {
+    o.tile = dw_tile(o.n, o.ho, o.wo, o.c, o.stride, 1);
+    const DwTile& t = o.tile;
+    o.tma = encode_nhwc_box(&o.map_x, o.x, o.n, o.h, o.wd, o.c, kDwC, t.tw, t.tr, t.ni) ? 1 : 0;
+}
 void dw_bwd_finalize(DwBwdOp& o) {
     o.tile = dw_tile(o.n, o.h, o.wd, o.c, 1, 2);
     o.ctas = o.tile.tiles;
     o.rows_per = 0;
+    const DwTile& t = o.tile;
+    o.tma = encode_nhwc_box(&o.map_g, o.gy, o.n, o.h, o.wd, o.c, kDwC, t.tw, t.tr, t.ni) &&
+                    encode_nhwc_box(&o.map_x, o.xp, o.n, o.h, o.wd, o.c, kDwC, t.tw, t.tr, t.ni)
+                ? 1
+                : 0;
 }
 void dw_gk_finalize(DwGkOp& o) {
     o.tile = dw_tile(o.n, o.ho, o.wo, o.c, o.stride, 2);
     o.ctas = o.tile.tiles;
     o.rows_per = 0;
+    const DwTile& t = o.tile;
+    o.tma = encode_nhwc_box(&o.map_x, o.x, o.n, o.h, o.wd, o.c, kDwC, t.tw, t.tr, t.ni) &&
+                    encode_nhwc_box(&o.map_g, o.gy, o.n, o.ho, o.wo, o.c, kDwC, o.wo, t.th, t.ni)
+                ? 1
+                : 0;
 }
 int ctas_dw_fwd(const DwFwdOp& o) { return o.tile.tiles * o.tile.cslices; }
 int ctas_dw_bwd(const DwBwdOp& o) { return o.tile.tiles * o.tile.cslices; }
@@ -190,17 +289,47 @@ __device__ __forceinline__ void dw_stage(float* dst, const float* __restrict__ s
 
 // In-place prologue f on the staged in-range pixels (padding stays 0); the
 // caller synchronises before and after.  Warp = staged row, lane = channel.
+// Rows are walked without divisions (tile row counts are small).
 template <class F>
 __device__ __forceinline__ void dw_map(float* buf, const DwTile& t, int n, int h, int w, int n0, int iy0, int ix0,
                                        F f) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int R = warp; R < t.ni * t.tr; R += kThreads / 32) {
-        const int i = R / t.tr, rr = R - i * t.tr;
+    int i = 0, rr = warp;
+    while (rr >= t.tr) rr -= t.tr, ++i;
+    const int cb = max(0, -ix0), ce = min(t.tw, w - ix0);
+    for (; i < t.ni;) {
         const int iy = iy0 + rr;
-        if (n0 + i >= n || iy < 0 || iy >= h) continue;
-        float* row = buf + R * t.tw * kDwC + lane;
-        const int cb = max(0, -ix0), ce = min(t.tw, w - ix0);
-        for (int col = cb; col < ce; ++col) row[col * kDwC] = f(row[col * kDwC]);
+        if (n0 + i < n && iy >= 0 && iy < h) {
+            float* row = buf + (i * t.tr + rr) * t.tw * kDwC + lane;
+            for (int col = cb; col < ce; ++col) row[col * kDwC] = f(row[col * kDwC], lane);
+        }
+        rr += kThreads / 32;
+        while (rr >= t.tr) rr -= t.tr, ++i;
+    }
+}
+
+// Vectorised dw_map for 4-aligned channel counts: a warp pass covers 4 staged
+// pixels x 8 channel quads (512 contiguous bytes); f(v, k) maps channel
+// c0 + 4*quad + k.
+template <class F>
+__device__ __forceinline__ void dw_map4(float* buf, const DwTile& t, int n, int h, int w, int n0, int iy0, int ix0,
+                                        F f) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, quad = lane & 7, sub = lane >> 3;
+    int i = 0, rr = warp;
+    while (rr >= t.tr) rr -= t.tr, ++i;
+    const int cb = max(0, -ix0), ce = min(t.tw, w - ix0);
+    for (; i < t.ni;) {
+        const int iy = iy0 + rr;
+        if (n0 + i < n && iy >= 0 && iy < h) {
+            float4* row = reinterpret_cast<float4*>(buf) + (i * t.tr + rr) * t.tw * (kDwC / 4) + quad;
+            for (int col = cb + sub; col < ce; col += 4) {
+                float4 v = row[col * (kDwC / 4)];
+                v.x = f(v.x, 0), v.y = f(v.y, 1), v.z = f(v.z, 2), v.w = f(v.w, 3);
+                row[col * (kDwC / 4)] = v;
+            }
+        }
+        rr += kThreads / 32;
+        while (rr >= t.tr) rr -= t.tr, ++i;
     }
 }
 
@@ -217,86 +346,220 @@ __device__ __forceinline__ DwPos dw_pos(const DwTile& t, int local) {
     return q;
 }
 
+// Grouped-launch descriptor copied once into shared memory (16-byte words):
+// one global-load latency per CTA, then every field read is a shared-memory
+// broadcast.  Thread 0 also initialises the CTA's staging barrier.
+template <class Op>
+__device__ __forceinline__ int op_to_shared(const Op* __restrict__ ops, int nd, Op* sh, uint64_t* bar, int& local) {
+    static_assert(sizeof(Op) % 16 == 0, "descriptor copied in 16-byte words");
+    const int t = op_index(ops, nd, static_cast<int>(blockIdx.x));
+    const uint4* src = reinterpret_cast<const uint4*>(ops + t);
+    uint4* dst = reinterpret_cast<uint4*>(sh);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(Op) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+    if (threadIdx.x == 0) {
+        tc::mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    local = static_cast<int>(blockIdx.x) - sh->cta_begin;
+    return t;
+}
+
+// Train-mode BN + ReLU of the previous unit (ops.hpp:290-293, 380-385) for
+// the vectorised prologue: parameters of channels c0 + 4*quad + k.
+struct BnRelu4 {
+    float m[4], iv[4], g[4], b[4];
+    __device__ void load(const float* mean, const float* inv, const float* gam, const float* bet, int c0, int c) {
+        const int quad = threadIdx.x & 7;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ch = c0 + 4 * quad + k;
+            const bool ok = ch < c;
+            m[k] = ok ? mean[ch] : 0.0f, iv[k] = ok ? inv[ch] : 0.0f;
+            g[k] = ok && gam ? gam[ch] : 0.0f, b[k] = ok && bet ? bet[ch] : 0.0f;
+        }
+    }
+    __device__ __forceinline__ float train(float v, int k) const { return relu(bn_train_apply(v, m[k], iv[k], g[k], b[k])); }
+    __device__ __forceinline__ float infer(float v, int k) const { return relu(bn_infer_apply(v, m[k], iv[k])); }
+};
+
 // ---------------------------------------------------------- depthwise fwd
-// Warp = output row (image i, row oy) of the tile, lane = channel.
+// The x tile arrives by one 4-D TMA box (zero-filled halo / channel tail) or,
+// for channel counts TMA cannot address, by cp.async.  Warp = output row
+// (image i, row oy) of the tile, lane = channel; stride 1 slides a 3x3
+// register window along x (3 shared loads per output).
 __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restrict__ ops, int nd) {
     pdl_enter();
-    extern __shared__ float xs[];
+    cta_mark(0);
+    extern __shared__ __align__(128) float xs[];
+    __shared__ DwFwdOp osh;
+    __shared__ uint64_t bar;
     int local;
-    const DwFwdOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    const int oi = op_to_shared(ops, nd, &osh, &bar, local);
+    cta_mark(1);
+    const DwFwdOp& o = osh;
     if (is_failed(o.failed)) return;
     const DwTile t = o.tile;
     const DwPos q = dw_pos(t, local);
-    const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5, c = q.c0 + ch;
-    const bool cok = c < o.c;
-    float pa = 0, pb = 0, pc = 0, pd = 0;
-    if (o.pro != 0 && cok) {
-        pa = o.pa[c], pb = o.pb[c];
-        if (o.pro == 1) pc = o.pc[c], pd = o.pd[c];
+    const int n = o.n, h = o.h, w = o.wd, C = o.c, ho = o.ho, wo = o.wo, s = o.stride, pad = o.pad, pro = o.pro;
+    const int iy0 = q.y0 * s - pad;
+    const bool tma = o.tma != 0;
+    if (tma && threadIdx.x == 0) {
+        tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(t.ni * t.tr * t.tw * kDwC * 4));
+        tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, iy0, q.n0);
     }
-    const int pro = o.pro;
-    const int iy0 = q.y0 * o.stride - o.pad;
+    const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5, c = q.c0 + ch;
+    const bool cok = c < C;
     float wk[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) wk[k] = cok ? o.w[k * o.c + c] : 0.0f;
-    dw_stage(xs, o.x, t, o.n, o.h, o.wd, o.c, q.n0, iy0, -o.pad, q.c0);
-    __syncthreads();
-    if (pro == 1) {
-        dw_map(xs, t, o.n, o.h, o.wd, q.n0, iy0, -o.pad, [&](float v) { return relu(bn_train_apply(v, pa, pb, pc, pd)); });
+    for (int k = 0; k < 9; ++k) wk[k] = cok ? o.w[k * C + c] : 0.0f;
+    float* const yh = o.y_hi;
+    float* const yl = o.y_lo;
+    float* const yf = o.y;
+    if (tma) {
+        BnRelu4 p4;
+        if (pro != 0) p4.load(o.pa, o.pb, o.pc, o.pd, q.c0, C);
+        tc::mbar_wait(&bar, 0);
+        cta_mark(2);
+        if (pro != 0) {
+            if (pro == 1) dw_map4(xs, t, n, h, w, q.n0, iy0, -pad, [&](float v, int k) { return p4.train(v, k); });
+            else dw_map4(xs, t, n, h, w, q.n0, iy0, -pad, [&](float v, int k) { return p4.infer(v, k); });
+            __syncthreads();
+        }
+    } else {
+        float pa = 0, pb = 0, pc = 0, pd = 0;
+        if (pro != 0 && cok) {
+            pa = o.pa[c], pb = o.pb[c];
+            if (pro == 1) pc = o.pc[c], pd = o.pd[c];
+        }
+        dw_stage(xs, o.x, t, n, h, w, C, q.n0, iy0, -pad, q.c0);
         __syncthreads();
-    } else if (pro == 2) {
-        dw_map(xs, t, o.n, o.h, o.wd, q.n0, iy0, -o.pad, [&](float v) { return relu(bn_infer_apply(v, pa, pb)); });
-        __syncthreads();
+        if (pro == 1) {
+            dw_map(xs, t, n, h, w, q.n0, iy0, -pad, [&](float v, int) { return relu(bn_train_apply(v, pa, pb, pc, pd)); });
+            __syncthreads();
+        } else if (pro == 2) {
+            dw_map(xs, t, n, h, w, q.n0, iy0, -pad, [&](float v, int) { return relu(bn_infer_apply(v, pa, pb)); });
+            __syncthreads();
+        }
+    }
+    const int rs = t.tw * kDwC;
+    if (tma) {
+        // packed: lane = (channel pair p, half); row worker 2*warp + half
+        // walks output rows; two channels per FFMA2
+        const int p = ch & 15, c2 = q.c0 + 2 * p;
+        if (c2 >= C) return;
+        const PkConsts K = pk_consts();
+        float2 w2[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) w2[k] = *reinterpret_cast<const float2*>(o.w + k * C + c2);
+        const int rw = 2 * warp + (ch >> 4), xsh = t.xsh, seg = rw & ((1 << xsh) - 1);
+        const int sw = (wo + (1 << xsh) - 1) >> xsh, xb = seg * sw, xe = min(wo, xb + sw);
+        int i = 0, oy = rw >> xsh;
+        while (oy >= t.th) oy -= t.th, ++i;
+        for (; i < t.ni;) {
+            const int nn = q.n0 + i, yy = q.y0 + oy;
+            if (nn < n && yy < ho) {
+                const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + 2 * p;
+                long long off = ((static_cast<long long>(nn) * ho + yy) * wo + xb) * C + c2;
+                auto ld = [&](int r, int col) { return *reinterpret_cast<const float2*>(base + r * rs + col * kDwC); };
+                float2 win[3][3];
+                if (s == 1) {
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) win[r][1] = ld(r, xb), win[r][2] = ld(r, xb + 1);
+                }
+#pragma unroll 3
+                for (int ox = xb; ox < xe; ++ox, off += C) {
+                    if (s == 1) {
+#pragma unroll
+                        for (int r = 0; r < 3; ++r) win[r][0] = win[r][1], win[r][1] = win[r][2], win[r][2] = ld(r, ox + 2);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)
+#pragma unroll
+                            for (int cc = 0; cc < 3; ++cc) win[r][cc] = ld(r, ox * s + cc);
+                    }
+                    float2 acc = K.z;  // 9-term serial sum in (ky, kx) order, per lane
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                        for (int kx = 0; kx < 3; ++kx) acc = add2(K, acc, mul2(K, win[ky][kx], w2[ky * 3 + kx]));
+                    if (yh) {
+                        const float2 hv = make_float2(__uint_as_float(tc_split_hi(acc.x)), __uint_as_float(tc_split_hi(acc.y)));
+                        const float2 d = sub2(K, acc, hv);
+                        *reinterpret_cast<float2*>(yh + off) = hv;
+                        *reinterpret_cast<float2*>(yl + off) =
+                            make_float2(__uint_as_float(tc_split_hi(d.x)), __uint_as_float(tc_split_hi(d.y)));
+                    } else {
+                        *reinterpret_cast<float2*>(yf + off) = acc;
+                    }
+                }
+            }
+            oy += (2 * (kThreads / 32)) >> xsh;
+            while (oy >= t.th) oy -= t.th, ++i;
+        }
+        cta_mark(3);
+        return;
     }
     if (!cok) return;
-    const int s = o.stride;
-    for (int R = warp; R < t.ni * t.th; R += kThreads / 32) {
-        const int i = R / t.th, oy = R - i * t.th;
+    int i = 0, oy = warp;
+    while (oy >= t.th) oy -= t.th, ++i;
+    for (; i < t.ni;) {
         const int nn = q.n0 + i, yy = q.y0 + oy;
-        if (nn >= o.n || yy >= o.ho) continue;
-        const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
-        const long long obase = ((static_cast<long long>(nn) * o.ho + yy) * o.wo) * o.c + c;
-        const int rs = t.tw * kDwC;
-        float win[3][3];  // stride 1: 3x3 register window slid along x
-        if (s == 1) {
-#pragma unroll
-            for (int r = 0; r < 3; ++r) win[r][1] = base[r * rs], win[r][2] = base[r * rs + kDwC];
-        }
-        for (int ox = 0; ox < o.wo; ++ox) {
+        if (nn < n && yy < ho) {
+            const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
+            long long off = ((static_cast<long long>(nn) * ho + yy) * wo) * C + c;
+            float win[3][3];  // stride 1: 3x3 register window slid along x
             if (s == 1) {
 #pragma unroll
-                for (int r = 0; r < 3; ++r) win[r][0] = win[r][1], win[r][1] = win[r][2], win[r][2] = base[r * rs + (ox + 2) * kDwC];
-            } else {
-                const float* b = base + ox * s * kDwC;
-#pragma unroll
-                for (int r = 0; r < 3; ++r)
-#pragma unroll
-                    for (int cc = 0; cc < 3; ++cc) win[r][cc] = b[r * rs + cc * kDwC];
+                for (int r = 0; r < 3; ++r) win[r][1] = base[r * rs], win[r][2] = base[r * rs + kDwC];
             }
-            float acc = 0.0f;  // 9-term serial sum in (ky, kx) order (ops.hpp:131-140)
+#pragma unroll 2
+            for (int ox = 0; ox < wo; ++ox, off += C) {
+                if (s == 1) {
 #pragma unroll
-            for (int ky = 0; ky < 3; ++ky)
+                    for (int r = 0; r < 3; ++r)
+                        win[r][0] = win[r][1], win[r][1] = win[r][2], win[r][2] = base[r * rs + (ox + 2) * kDwC];
+                } else {
+                    const float* b = base + ox * s * kDwC;
 #pragma unroll
-                for (int kx = 0; kx < 3; ++kx) acc = add(acc, mul(win[ky][kx], wk[ky * 3 + kx]));
-            const long long oi = obase + static_cast<long long>(ox) * o.c;
-            if (o.y_hi) {  // tf32 planes for the pointwise GEMMs (3xTF32 operand split)
-                const float hv = __uint_as_float(tc_split_hi(acc));
-                o.y_hi[oi] = hv;
-                o.y_lo[oi] = __uint_as_float(tc_split_hi(__fsub_rn(acc, hv)));
-            } else {
-                o.y[oi] = acc;
+                    for (int r = 0; r < 3; ++r)
+#pragma unroll
+                        for (int cc = 0; cc < 3; ++cc) win[r][cc] = b[r * rs + cc * kDwC];
+                }
+                float acc = 0.0f;  // 9-term serial sum in (ky, kx) order (ops.hpp:131-140)
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                    for (int kx = 0; kx < 3; ++kx) acc = add(acc, mul(win[ky][kx], wk[ky * 3 + kx]));
+                if (yh) {  // tf32 planes for the pointwise GEMMs (3xTF32 operand split)
+                    const float hv = __uint_as_float(tc_split_hi(acc));
+                    yh[off] = hv;
+                    yl[off] = __uint_as_float(tc_split_hi(__fsub_rn(acc, hv)));
+                } else {
+                    yf[off] = acc;
+                }
             }
         }
+        oy += kThreads / 32;
+        while (oy >= t.th) oy -= t.th, ++i;
     }
+    cta_mark(3);
 }
 
 void launch_dw_fwd(const DwFwdOp* d, int nd, int ctas, cudaStream_t st) {
-    launch_k(dw_fwd_kernel, dim3(ctas), dim3(kThreads), kDwTileBytes, st, d, nd);
+    static bool attr = false;
+    if (!attr) {  // 48 KB dynamic + the static descriptor copy exceed the default
+        PBKD_CUDA(cudaFuncSetAttribute(dw_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_tile_bytes()));
+        attr = true;
+    }
+    traced("dw_fwd", ctas, st, [&] { launch_k(dw_fwd_kernel, dim3(ctas), dim3(kThreads), dw_tile_bytes(), st, d, nd); });
     PBKD_LAUNCH_CHECK();
 }
 
-// CTA-level fixed-order sum of per-thread values v[k] (k < nv) over the 8
-// pixel lanes; thread ch of the result gets out[k] for its channel.
+// CTA-level fixed-order sum of per-thread values over the row workers.
+// Scalar layout: thread (row worker = warp, channel = lane) holds v[k].
+// Packed layout: thread (row worker = 2*warp + lane/16, channels 2p, 2p+1
+// with p = lane%16) holds v2[k].  Thread ch < 32 gets out[k] for channel ch.
 template <int NV>
 __device__ __forceinline__ void dw_lane_sum(float* red, const float* v, float* out) {
     const int ch = threadIdx.x % kDwC, lane = threadIdx.x / kDwC;
@@ -312,6 +575,22 @@ __device__ __forceinline__ void dw_lane_sum(float* red, const float* v, float* o
         }
     }
 }
+template <int NV>
+__device__ __forceinline__ void dw_lane_sum2(float* red, const float2* v, float* out) {
+    const int lane = threadIdx.x & 31, rw = 2 * (threadIdx.x >> 5) + (lane >> 4), p = lane & 15;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) *reinterpret_cast<float2*>(red + (rw * NV + k) * kDwC + 2 * p) = v[k];
+    __syncthreads();
+    if (threadIdx.x < kDwC) {
+        const int ch = threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            float acc = 0.0f;
+            for (int l = 0; l < 2 * kDwLanes; ++l) acc += red[(l * NV + k) * kDwC + ch];
+            out[k] = acc;
+        }
+    }
+}
 
 // ------------------------------------------- depthwise bwd (unit > 0, s=1)
 // gy (dw output gradient) and the previous unit's activation relu(bn(p)) are
@@ -320,153 +599,368 @@ __device__ __forceinline__ void dw_lane_sum(float* red, const float* v, float* o
 // gradient terms, the previous ReLU mask and batch-norm partial sums.
 __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restrict__ ops, int nd) {
     pdl_enter();
-    extern __shared__ float sm[];
+    cta_mark(0);
+    extern __shared__ __align__(128) float sm[];
+    __shared__ DwBwdOp osh;
+    __shared__ uint64_t bar;
     int local;
-    const DwBwdOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    const int oi = op_to_shared(ops, nd, &osh, &bar, local);
+    cta_mark(1);
+    const DwBwdOp& o = osh;
     if (is_failed(o.failed)) return;
     const DwTile t = o.tile;
     const DwPos q = dw_pos(t, local);
+    const int n = o.n, h = o.h, w = o.wd, C = o.c;
+    const int tile_elems = t.ni * t.tr * t.tw * kDwC;
+    float* gs = sm;
+    float* xs = sm + tile_elems;
+    const bool tma = o.tma != 0;
+    if (tma && threadIdx.x == 0) {
+        tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(2 * tile_elems * 4));
+        tc::tma_load_4d(gs, &ops[oi].map_g, &bar, q.c0, -1, q.y0 - 1, q.n0);
+        tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -1, q.y0 - 1, q.n0);
+    }
     const int ch = threadIdx.x % kDwC, c = q.c0 + ch;
-    const bool cok = c < o.c;
+    const bool cok = c < C;
     float mean = 0, inv = 0, gam = 0, bet = 0;
     if (cok) mean = o.mean[c], inv = o.inv[c], gam = o.gamma[c], bet = o.beta[c];
-    float* gs = sm;
-    float* xs = sm + static_cast<size_t>(t.ni) * t.tr * t.tw * kDwC;
     float wk[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) wk[k] = cok ? o.w[k * o.c + c] : 0.0f;
-    dw_stage(gs, o.gy, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 - 1, -1, q.c0);
-    dw_stage(xs, o.xp, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 - 1, -1, q.c0);
-    __syncthreads();
-    // xs -> relu(bn(p)), the dw layer's actual input (padding stays 0); the
-    // centre's raw p (xhat, mask) is re-read from global (L2)
-    dw_map(xs, t, o.n, o.h, o.wd, q.n0, q.y0 - 1, -1, [&](float v) { return relu(bn_train_apply(v, mean, inv, gam, bet)); });
+    for (int k = 0; k < 9; ++k) wk[k] = cok ? o.w[k * C + c] : 0.0f;
+    const float* const xp = o.xp;
+    float* const gyprev = o.gyprev;
+    // TMA path: pass A reads the raw p centre from the staged tile, then xs
+    // is mapped to relu(bn(p)) (the dw layer's input) for pass B.  Scalar
+    // path: xs is mapped first and the raw centre is re-read from global.
+    if (tma) {
+        tc::mbar_wait(&bar, 0);
+        cta_mark(2);
+    } else {
+        dw_stage(gs, o.gy, t, n, h, w, C, q.n0, q.y0 - 1, -1, q.c0);
+        dw_stage(xs, xp, t, n, h, w, C, q.n0, q.y0 - 1, -1, q.c0);
+        __syncthreads();
+        dw_map(xs, t, n, h, w, q.n0, q.y0 - 1, -1, [&](float v, int) { return relu(bn_train_apply(v, mean, inv, gam, bet)); });
+    }
     __syncthreads();
 
+    if (tma) {
+        // packed: lane = (channel pair p, half); row worker 2*warp + half
+        // walks (row, x segment) items
+        const int p = ch & 15, c2 = q.c0 + 2 * p;
+        const int rs = t.tw * kDwC;
+        const bool pok = c2 < C;
+        float2 acc2[11];  // gk[9], sg, sgx
+#pragma unroll
+        for (int k = 0; k < 11; ++k) acc2[k] = make_float2(0.0f, 0.0f);
+        const PkConsts K = pk_consts();
+        const int rw = 2 * (threadIdx.x >> 5) + (ch >> 4), xsh = t.xsh, seg = rw & ((1 << xsh) - 1);
+        const int sw = (w + (1 << xsh) - 1) >> xsh, xb = seg * sw, xe = min(w, xb + sw);
+        // pass A: input gradient (outputs ascending, tap (1-dy, 1-dx),
+        // ops.hpp:156-174), previous ReLU mask, BN-backward partials
+        if (pok) {
+            float2 w2[9];
+            bool fin = true;  // finite weights: adding the skipped zero terms is exact
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                w2[k] = *reinterpret_cast<const float2*>(o.w + k * C + c2);
+                fin = fin && isfinite(w2[k].x) && isfinite(w2[k].y);
+            }
+            const float2 mean2 = *reinterpret_cast<const float2*>(o.mean + c2);
+            const float2 inv2 = *reinterpret_cast<const float2*>(o.inv + c2);
+            const float2 gam2 = *reinterpret_cast<const float2*>(o.gamma + c2);
+            const float2 bet2 = *reinterpret_cast<const float2*>(o.beta + c2);
+            int i = 0, y = rw >> xsh;
+            while (y >= t.th) y -= t.th, ++i;
+            for (; i < t.ni;) {
+                const int nn = q.n0 + i, yy = q.y0 + y;
+                if (nn < n && yy < h) {
+                    long long gi = ((static_cast<long long>(nn) * h + yy) * w + xb) * C + c2;
+                    const float* g0 = gs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
+                    const float* x0 = xs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
+                    auto ldg2 = [&](int r, int col) { return *reinterpret_cast<const float2*>(g0 + r * rs + col * kDwC); };
+                    float2 gw[3][3];
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) gw[r][1] = ldg2(r, xb), gw[r][2] = ldg2(r, xb + 1);
+                    for (int x = xb; x < xe; ++x, gi += C) {
+#pragma unroll
+                        for (int r = 0; r < 3; ++r) gw[r][0] = gw[r][1], gw[r][1] = gw[r][2], gw[r][2] = ldg2(r, x + 2);
+                        float2 gx = K.z;
+                        if (fin) {
+#pragma unroll
+                            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                                for (int cc = 0; cc < 3; ++cc) gx = add2(K, gx, mul2(K, gw[r][cc], w2[(2 - r) * 3 + (2 - cc)]));
+                        } else {  // zero terms skipped per lane (0 * inf would be NaN)
+#pragma unroll
+                            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                                for (int cc = 0; cc < 3; ++cc) {
+                                    const float2 gv = gw[r][cc], wv = w2[(2 - r) * 3 + (2 - cc)];
+                                    if (gv.x != 0.0f) gx.x = add(gx.x, mul(gv.x, wv.x));
+                                    if (gv.y != 0.0f) gx.y = add(gx.y, mul(gv.y, wv.y));
+                                }
+                        }
+                        const float2 xpc = *reinterpret_cast<const float2*>(x0 + rs + (x + 1) * kDwC);  // raw centre
+                        const float2 xh = mul2(K, sub2(K, xpc, mean2), inv2);
+                        const float2 yv = add2(K, mul2(K, gam2, xh), bet2);
+                        const float2 gz = add2(K, K.z, gx);
+                        const float2 gm = make_float2(yv.x > 0.0f ? gz.x : 0.0f, yv.y > 0.0f ? gz.y : 0.0f);
+                        *reinterpret_cast<float2*>(gyprev + gi) = gm;
+                        acc2[9] = add2(K, acc2[9], gm);
+                        acc2[10] = fma2(gm, xh, acc2[10]);
+                    }
+                }
+                y += (2 * (kThreads / 32)) >> xsh;
+                while (y >= t.th) y -= t.th, ++i;
+            }
+        }
+        __syncthreads();  // pass A read the raw tile
+        {
+            BnRelu4 p4;
+            p4.load(o.mean, o.inv, o.gamma, o.beta, q.c0, C);
+            dw_map4(xs, t, n, h, w, q.n0, q.y0 - 1, -1, [&](float v, int k) { return p4.train(v, k); });
+        }
+        __syncthreads();
+        // pass B: weight-gradient terms gy(centre) * relu(bn(p))(window)
+        if (pok) {
+            int i = 0, y = rw >> xsh;
+            while (y >= t.th) y -= t.th, ++i;
+            for (; i < t.ni;) {
+                const int nn = q.n0 + i, yy = q.y0 + y;
+                if (nn < n && yy < h) {
+                    const float* g0 = gs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
+                    const float* x0 = xs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
+                    auto ldx2 = [&](int r, int col) { return *reinterpret_cast<const float2*>(x0 + r * rs + col * kDwC); };
+                    float2 xw[3][3];
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) xw[r][1] = ldx2(r, xb), xw[r][2] = ldx2(r, xb + 1);
+                    for (int x = xb; x < xe; ++x) {
+#pragma unroll
+                        for (int r = 0; r < 3; ++r) xw[r][0] = xw[r][1], xw[r][1] = xw[r][2], xw[r][2] = ldx2(r, x + 2);
+                        const float2 gyc = *reinterpret_cast<const float2*>(g0 + rs + (x + 1) * kDwC);
+                        if (gyc.x != 0.0f || gyc.y != 0.0f) {
+#pragma unroll
+                            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                                for (int cc = 0; cc < 3; ++cc) acc2[r * 3 + cc] = fma2(gyc, xw[r][cc], acc2[r * 3 + cc]);
+                        }
+                    }
+                }
+                y += (2 * (kThreads / 32)) >> xsh;
+                while (y >= t.th) y -= t.th, ++i;
+            }
+        }
+        __syncthreads();  // staging buffers are reused for the reduction
+        float out[11];
+        dw_lane_sum2<11>(sm, acc2, out);
+        if (threadIdx.x < kDwC && cok) {
+            for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * C + c] = out[k];
+            o.part_sg[static_cast<long long>(q.tile) * C + c] = out[9];
+            o.part_sgx[static_cast<long long>(q.tile) * C + c] = out[10];
+        }
+        cta_mark(3);
+        return;
+    }
     float acc[11];  // gk[9], sg, sgx
 #pragma unroll
     for (int k = 0; k < 11; ++k) acc[k] = 0.0f;
     if (cok) {
-        const int warp = threadIdx.x >> 5;
-        for (int R = warp; R < t.ni * t.th; R += kThreads / 32) {
-            const int i = R / t.th, y = R - i * t.th;
+        const int warp = threadIdx.x >> 5, rs = t.tw * kDwC;
+        int i = 0, y = warp;
+        while (y >= t.th) y -= t.th, ++i;
+        for (; i < t.ni;) {
             const int nn = q.n0 + i, yy = q.y0 + y;
-            if (nn >= o.n || yy >= o.h) continue;
-            const long long grow = ((static_cast<long long>(nn) * o.h + yy) * o.wd) * o.c + c;
-            // 3x3 register windows over tile rows y..y+2 (= image rows yy-1..yy+1),
-            // columns x..x+2 (= image columns x-1..x+1), slid along x
-            const float* g0 = gs + ((i * t.tr + y) * t.tw) * kDwC + ch;
-            const float* x0 = xs + ((i * t.tr + y) * t.tw) * kDwC + ch;
-            const int rs = t.tw * kDwC;
-            float gw[3][3], xw[3][3];
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    gw[r][cc + 1] = g0[r * rs + cc * kDwC];
-                    xw[r][cc + 1] = x0[r * rs + cc * kDwC];
-                }
-            #pragma unroll 4
-            for (int x = 0; x < o.wd; ++x) {
-#pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    gw[r][0] = gw[r][1], gw[r][1] = gw[r][2], gw[r][2] = g0[r * rs + (x + 2) * kDwC];
-                    xw[r][0] = xw[r][1], xw[r][1] = xw[r][2], xw[r][2] = x0[r * rs + (x + 2) * kDwC];
-                }
-                // input gradient: outputs (oy, ox) = (yy+dy, x+dx) ascending, tap
-                // (1-dy, 1-dx), zero terms skipped (ops.hpp:156-174)
-                float gx = 0.0f;
+            if (nn < n && yy < h) {
+                long long gi = ((static_cast<long long>(nn) * h + yy) * w) * C + c;
+                // 3x3 register windows over tile rows y..y+2 (= image rows yy-1..yy+1),
+                // columns x..x+2 (= image columns x-1..x+1), slid along x
+                const float* g0 = gs + ((i * t.tr + y) * t.tw) * kDwC + ch;
+                const float* x0 = xs + ((i * t.tr + y) * t.tw) * kDwC + ch;
+                float gw[3][3], xw[3][3];
 #pragma unroll
                 for (int r = 0; r < 3; ++r)
 #pragma unroll
-                    for (int cc = 0; cc < 3; ++cc) {
-                        const float gv = gw[r][cc];
-                        if (gv != 0.0f) gx = add(gx, mul(gv, wk[(2 - r) * 3 + (2 - cc)]));
+                    for (int cc = 0; cc < 2; ++cc) {
+                        gw[r][cc + 1] = g0[r * rs + cc * kDwC];
+                        xw[r][cc + 1] = x0[r * rs + cc * kDwC];
                     }
-                const float gyc = gw[1][1];
-                if (gyc != 0.0f) {
+#pragma unroll 4
+                for (int x = 0; x < w; ++x, gi += C) {
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) {
+                        gw[r][0] = gw[r][1], gw[r][1] = gw[r][2], gw[r][2] = g0[r * rs + (x + 2) * kDwC];
+                        xw[r][0] = xw[r][1], xw[r][1] = xw[r][2], xw[r][2] = x0[r * rs + (x + 2) * kDwC];
+                    }
+                    // input gradient: outputs (oy, ox) = (yy+dy, x+dx) ascending, tap
+                    // (1-dy, 1-dx), zero terms skipped (ops.hpp:156-174)
+                    float gx = 0.0f;
 #pragma unroll
                     for (int r = 0; r < 3; ++r)
 #pragma unroll
-                        for (int cc = 0; cc < 3; ++cc) acc[r * 3 + cc] += gyc * xw[r][cc];
+                        for (int cc = 0; cc < 3; ++cc) {
+                            const float gv = gw[r][cc];
+                            if (gv != 0.0f) gx = add(gx, mul(gv, wk[(2 - r) * 3 + (2 - cc)]));
+                        }
+                    const float gyc = gw[1][1];
+                    if (gyc != 0.0f) {
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)
+#pragma unroll
+                            for (int cc = 0; cc < 3; ++cc) acc[r * 3 + cc] += gyc * xw[r][cc];
+                    }
+                    const float xh = mul(sub(__ldg(xp + gi), mean), inv);
+                    const float yv = add(mul(gam, xh), bet);
+                    const float gm = yv > 0.0f ? add(0.0f, gx) : 0.0f;
+                    gyprev[gi] = gm;
+                    acc[9] += gm;
+                    acc[10] += gm * xh;
                 }
-                const long long gi = grow + static_cast<long long>(x) * o.c;
-                const float xh = mul(sub(__ldg(o.xp + gi), mean), inv);
-                const float yv = add(mul(gam, xh), bet);
-                const float gm = yv > 0.0f ? add(0.0f, gx) : 0.0f;
-                o.gyprev[gi] = gm;
-                acc[9] += gm;
-                acc[10] += gm * xh;
             }
+            y += kThreads / 32;
+            while (y >= t.th) y -= t.th, ++i;
         }
     }
     __syncthreads();  // staging buffers are reused for the reduction
     float out[11];
     dw_lane_sum<11>(sm, acc, out);
     if (threadIdx.x < kDwC && cok) {
-        for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * o.c + c] = out[k];
-        o.part_sg[static_cast<long long>(q.tile) * o.c + c] = out[9];
-        o.part_sgx[static_cast<long long>(q.tile) * o.c + c] = out[10];
+        for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * C + c] = out[k];
+        o.part_sg[static_cast<long long>(q.tile) * C + c] = out[9];
+        o.part_sgx[static_cast<long long>(q.tile) * C + c] = out[10];
     }
+    cta_mark(3);
 }
 
 void launch_dw_bwd(const DwBwdOp* d, int nd, int ctas, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PBKD_CUDA(cudaFuncSetAttribute(dw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDwTileBytes));
+        PBKD_CUDA(cudaFuncSetAttribute(dw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * dw_tile_bytes()));
         attr = true;
     }
-    launch_k(dw_bwd_kernel, dim3(ctas), dim3(kThreads), 2 * kDwTileBytes, st, d, nd);
+    traced("dw_bwd", ctas, st, [&] { launch_k(dw_bwd_kernel, dim3(ctas), dim3(kThreads), 2 * dw_tile_bytes(), st, d, nd); });
     PBKD_LAUNCH_CHECK();
 }
 
 // ------------------------------------------- depthwise weight grad (unit 0)
-// model.cpp:570 skips the input gradient of the block's first layer.
+// model.cpp:570 skips the input gradient of the block's first layer.  With
+// TMA both the input tile (halo) and the output-gradient tile are staged.
 __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restrict__ ops, int nd) {
     pdl_enter();
-    extern __shared__ float sm[];
+    cta_mark(0);
+    extern __shared__ __align__(128) float sm[];
+    __shared__ DwGkOp osh;
+    __shared__ uint64_t bar;
     int local;
-    const DwGkOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    const int oi = op_to_shared(ops, nd, &osh, &bar, local);
+    cta_mark(1);
+    const DwGkOp& o = osh;
     if (is_failed(o.failed)) return;
     const DwTile t = o.tile;
     const DwPos q = dw_pos(t, local);
-    const int ch = threadIdx.x % kDwC, c = q.c0 + ch;
-    const bool cok = c < o.c;
+    const int n = o.n, h = o.h, w = o.wd, C = o.c, ho = o.ho, wo = o.wo, s = o.stride, pad = o.pad;
+    const int tile_elems = t.ni * t.tr * t.tw * kDwC;
     float* xs = sm;
-    dw_stage(xs, o.x, t, o.n, o.h, o.wd, o.c, q.n0, q.y0 * o.stride - o.pad, -o.pad, q.c0);
-    __syncthreads();
+    float* gs = sm + tile_elems;  // [ni][th][wo][32] (TMA path)
+    const bool tma = o.tma != 0;
+    if (tma && threadIdx.x == 0) {
+        tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>((tile_elems + t.ni * t.th * wo * kDwC) * 4));
+        tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, q.y0 * s - pad, q.n0);
+        tc::tma_load_4d(gs, &ops[oi].map_g, &bar, q.c0, 0, q.y0, q.n0);
+    }
+    const int ch = threadIdx.x % kDwC, c = q.c0 + ch;
+    const bool cok = c < C;
+    const float* const gy = o.gy;
+    if (tma) {
+        tc::mbar_wait(&bar, 0);
+        cta_mark(2);
+    } else {
+        dw_stage(xs, o.x, t, n, h, w, C, q.n0, q.y0 * s - pad, -pad, q.c0);
+        __syncthreads();
+    }
+    if (tma) {
+        // packed: lane = (channel pair p, half); row worker 2*warp + half
+        const int p = ch & 15, c2 = q.c0 + 2 * p;
+        float2 acc2[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc2[k] = make_float2(0.0f, 0.0f);
+        if (c2 < C) {
+            const int rw = 2 * (threadIdx.x >> 5) + (ch >> 4), xsh = t.xsh, seg = rw & ((1 << xsh) - 1);
+            const int sw = (wo + (1 << xsh) - 1) >> xsh, xb = seg * sw, xe = min(wo, xb + sw);
+            int i = 0, oy = rw >> xsh;
+            while (oy >= t.th) oy -= t.th, ++i;
+            for (; i < t.ni;) {
+                const int nn = q.n0 + i, yy = q.y0 + oy;
+                if (nn < n && yy < ho) {
+                    const float* gsr = gs + ((i * t.th + oy) * wo) * kDwC + 2 * p;
+                    const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + 2 * p;
+#pragma unroll 2
+                    for (int ox = xb; ox < xe; ++ox) {
+                        const float2 gv = *reinterpret_cast<const float2*>(gsr + ox * kDwC);
+                        if (gv.x == 0.0f && gv.y == 0.0f) continue;
+                        const float* b = base + ox * s * kDwC;
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+                            for (int kx = 0; kx < 3; ++kx)
+                                acc2[ky * 3 + kx] =
+                                    fma2(gv, *reinterpret_cast<const float2*>(b + (ky * t.tw + kx) * kDwC), acc2[ky * 3 + kx]);
+                    }
+                }
+                oy += (2 * (kThreads / 32)) >> xsh;
+                while (oy >= t.th) oy -= t.th, ++i;
+            }
+        }
+        __syncthreads();
+        float out[9];
+        dw_lane_sum2<9>(sm, acc2, out);
+        if (threadIdx.x < kDwC && cok)
+            for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * C + c] = out[k];
+        cta_mark(3);
+        return;
+    }
     float acc[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = 0.0f;
     if (cok) {
-        const int s = o.stride, warp = threadIdx.x >> 5;
-        for (int R = warp; R < t.ni * t.th; R += kThreads / 32) {
-            const int i = R / t.th, oy = R - i * t.th;
+        const int warp = threadIdx.x >> 5;
+        int i = 0, oy = warp;
+        while (oy >= t.th) oy -= t.th, ++i;
+        for (; i < t.ni;) {
             const int nn = q.n0 + i, yy = q.y0 + oy;
-            if (nn >= o.n || yy >= o.ho) continue;
-            const float* gyr = o.gy + ((static_cast<long long>(nn) * o.ho + yy) * o.wo) * o.c + c;
-            const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
+            if (nn < n && yy < ho) {
+                const float* gyr = gy + ((static_cast<long long>(nn) * ho + yy) * wo) * C + c;
+                const float* gsr = gs + ((i * t.th + oy) * wo) * kDwC + ch;
+                const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + ch;
 #pragma unroll 2
-            for (int ox = 0; ox < o.wo; ++ox) {
-                const float gv = __ldg(gyr + static_cast<long long>(ox) * o.c);
-                if (gv == 0.0f) continue;
-                const float* b = base + ox * s * kDwC;
+                for (int ox = 0; ox < wo; ++ox) {
+                    const float gv = tma ? gsr[ox * kDwC] : __ldg(gyr + static_cast<long long>(ox) * C);
+                    if (gv == 0.0f) continue;
+                    const float* b = base + ox * s * kDwC;
 #pragma unroll
-                for (int ky = 0; ky < 3; ++ky)
+                    for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
-                    for (int kx = 0; kx < 3; ++kx) acc[ky * 3 + kx] += gv * b[(ky * t.tw + kx) * kDwC];
+                        for (int kx = 0; kx < 3; ++kx) acc[ky * 3 + kx] += gv * b[(ky * t.tw + kx) * kDwC];
+                }
             }
+            oy += kThreads / 32;
+            while (oy >= t.th) oy -= t.th, ++i;
         }
     }
     __syncthreads();
     float out[9];
     dw_lane_sum<9>(sm, acc, out);
     if (threadIdx.x < kDwC && cok)
-        for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * o.c + c] = out[k];
+        for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * C + c] = out[k];
+    cta_mark(3);
 }
 
 void launch_dw_gk(const DwGkOp* d, int nd, int ctas, cudaStream_t st) {
-    launch_k(dw_gk_kernel, dim3(ctas), dim3(kThreads), kDwTileBytes, st, d, nd);
+    static bool attr = false;
+    if (!attr) {
+        PBKD_CUDA(cudaFuncSetAttribute(dw_gk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * dw_tile_bytes()));
+        attr = true;
+    }
+    traced("dw_gk", ctas, st, [&] { launch_k(dw_gk_kernel, dim3(ctas), dim3(kThreads), 2 * dw_tile_bytes(), st, d, nd); });
     PBKD_LAUNCH_CHECK();
 }
 

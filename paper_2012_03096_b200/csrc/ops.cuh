@@ -27,6 +27,7 @@ struct DwTile {
     int tiles_y, tiles; // row tiles per image group, spatial tiles
     int cslices;        // 32-channel slices
     int tr, tw;         // staged input rows / cols (halo included)
+    int xsh;            // log2 of the x segments per output row (packed kernels)
 };
 DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays);
 
@@ -46,6 +47,8 @@ struct DwFwdOp {
     const int* failed;
     int cta_begin;
     DwTile tile;  // set by dw_fwd_finalize
+    int tma;      // x tile staged by one 4-D TMA box (dw_fwd_finalize), else cp.async
+    CUtensorMap map_x;
 };
 
 // Depthwise 3x3 backward of a stride-1 unit u>0 (ops.hpp:149-178) fused with
@@ -66,6 +69,8 @@ struct DwBwdOp {
     const int* failed;
     int cta_begin;
     DwTile tile;
+    int tma;  // gy / xp tiles staged by 4-D TMA boxes (dw_bwd_finalize)
+    CUtensorMap map_g, map_x;
 };
 
 // Depthwise weight-gradient partials only (unit 0, any stride; model.cpp:570
@@ -79,6 +84,8 @@ struct DwGkOp {
     const int* failed;
     int cta_begin;
     DwTile tile;
+    int tma;  // x / gy tiles staged by 4-D TMA boxes (dw_gk_finalize)
+    CUtensorMap map_x, map_g;
 };
 
 // Sum `parts` rows of width `width` in fixed order into out (optionally
@@ -253,6 +260,10 @@ int ctas_reduce(const ReduceOp& o);
 int ctas_dw_bwd(const DwBwdOp& o);
 int ctas_dw_gk(const DwGkOp& o);
 // fill the tile geometry (and partial-row count `ctas` for bwd / gk)
+// 4-D map {C, W, H, N} over an NHWC fp32 tensor, box {bc, bw, bh, bn},
+// out-of-range elements zero filled (umma_tma.cu); false if TMA cannot
+// address it (16-byte alignment, C % 4, box limits).
+bool encode_nhwc_box(CUtensorMap* m, const float* base, int n, int h, int w, int c, int bc, int bw, int bh, int bn);
 void dw_fwd_finalize(DwFwdOp& o);
 void dw_bwd_finalize(DwBwdOp& o);
 void dw_gk_finalize(DwGkOp& o);

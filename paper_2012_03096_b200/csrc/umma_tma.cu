@@ -261,15 +261,6 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
     }
 }
 
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
-                                            int c3) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-        : "memory");
-}
-
 }  // namespace
 
 template <int BN, bool PS>
@@ -719,6 +710,27 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool encode_nhwc_box(CUtensorMap* m, const float* base, int n, int h, int w, int c, int bc, int bw, int bh, int bn) {
+    static const bool on = [] {
+        const char* e = std::getenv("PBKD_DW_TMA");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || base == nullptr || (reinterpret_cast<uintptr_t>(base) & 15) != 0 || c % 4 != 0 || n < 1 || h < 1 ||
+        w < 1 || bc < 1 || bw < 1 || bh < 1 || bn < 1 || bc > 256 || bw > 256 || bh > 256 || bn > 256 || (bc * 4) % 16 != 0)
+        return false;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w), static_cast<cuuint64_t>(h),
+                                static_cast<cuuint64_t>(n)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(c) * 4, static_cast<cuuint64_t>(w) * c * 4,
+                                   static_cast<cuuint64_t>(h) * w * c * 4};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(bc), static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh),
+                               static_cast<cuuint32_t>(bn)};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 
 // Implicit-im2col A operand of a teacher conv as a 4-D map over the NHWC
 // input {C, W, H, N}, box = one tap's 32 channels at the 128 output pixels
