@@ -38,10 +38,11 @@ bool pdl_enabled();
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Every CTA triggers its dependents on entry (a no-op without the launch
+// attribute): the next kernel's CTAs are scheduled once this grid's last
+// wave is resident, and run their static setup before pdl_wait.
 __device__ __forceinline__ void pdl_enter() {
-#ifdef PBKD_PDL_EARLY_TRIGGER
     pdl_trigger();
-#endif
     pdl_wait();
 }
 

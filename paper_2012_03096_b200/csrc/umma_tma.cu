@@ -327,10 +327,11 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // predecessor results (failure flags, operands) only after this point
-    pdl_enter();
     // decode this CTA's tiles once (all threads in parallel: one global-load
-    // latency instead of a dependent chain per tile per role)
+    // latency instead of a dependent chain per tile per role).  The op
+    // descriptors are static, so this runs before the programmatic-launch
+    // wait (overlapping the predecessor's tail); failure flags and operands
+    // are read only after it.
     for (int i = tid; i < nd; i += kThreadsT) begins[i] = ops[i].cta_begin;
     __syncthreads();
     const int ntiles = static_cast<int>(blockIdx.x) < total ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
@@ -344,10 +345,20 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
         }
         const GemmOp& o = ops[lo];
         TileInfo ti;
-        ti.op = op_failed(o) ? -1 : lo;
+        ti.op = lo;
         ti.g = tile_geo<BN>(o, t - begins[lo]);
         tiles_sh[j] = ti;
+        if (j == 0) {  // warm the first tile's tensor maps
+            if (o.a_presplit) prefetch_map(&o.map_ah), prefetch_map(&o.map_al);
+            else prefetch_map(&o.map_a);
+            if (o.b_presplit) prefetch_map(&o.map_bh), prefetch_map(&o.map_bl);
+            else prefetch_map(&o.map_b);
+        }
     }
+    // predecessor results (failure flags, operands) only after this point
+    pdl_enter();
+    for (int j = tid; j < ntiles; j += kThreadsT)
+        if (op_failed(ops[tiles_sh[j].op])) tiles_sh[j].op = -1;  // task predicated off (diverged)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
