@@ -13,6 +13,7 @@
 #include <cstring>
 #include <vector>
 
+#include "dw_tile.cuh"
 #include "ops.cuh"
 #include "tc.cuh"
 
@@ -166,14 +167,11 @@ __device__ void cta_reduce_rows(float* red, const float* v, const Geo& g, int rr
 // shared memory ([pixel][32], zero halo), then thread (channel = tid % 32,
 // pixel lane = tid / 32) walks the tile's output pixels.  Warps read 32
 // consecutive words (conflict-free); global loads/stores are 128-byte rows.
-constexpr int kDwC = 32;             // channels per CTA
-constexpr int kDwLanes = kThreads / kDwC;
-// Shared-memory budget per staged array (PBKD_DW_TILE_KB, default 48; the
-// dw backward's reduction needs >= 12 KB).
+// Shared-memory budget per staged array (PBKD_DW_TILE_KB, default 48).
 static int dw_tile_bytes() {
     static const int b = [] {
         const char* e = std::getenv("PBKD_DW_TILE_KB");
-        return std::max(12, std::min(96, e ? std::atoi(e) : 48)) * 1024;
+        return std::max(24, std::min(96, e ? std::atoi(e) : 48)) * 1024;
     }();
     return b;
 }
@@ -308,44 +306,6 @@ __device__ __forceinline__ void dw_map(float* buf, const DwTile& t, int n, int h
     }
 }
 
-// Vectorised dw_map for 4-aligned channel counts: a warp pass covers 4 staged
-// pixels x 8 channel quads (512 contiguous bytes); f(v, k) maps channel
-// c0 + 4*quad + k.
-template <class F>
-__device__ __forceinline__ void dw_map4(float* buf, const DwTile& t, int n, int h, int w, int n0, int iy0, int ix0,
-                                        F f) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, quad = lane & 7, sub = lane >> 3;
-    int i = 0, rr = warp;
-    while (rr >= t.tr) rr -= t.tr, ++i;
-    const int cb = max(0, -ix0), ce = min(t.tw, w - ix0);
-    for (; i < t.ni;) {
-        const int iy = iy0 + rr;
-        if (n0 + i < n && iy >= 0 && iy < h) {
-            float4* row = reinterpret_cast<float4*>(buf) + (i * t.tr + rr) * t.tw * (kDwC / 4) + quad;
-            for (int col = cb + sub; col < ce; col += 4) {
-                float4 v = row[col * (kDwC / 4)];
-                v.x = f(v.x, 0), v.y = f(v.y, 1), v.z = f(v.z, 2), v.w = f(v.w, 3);
-                row[col * (kDwC / 4)] = v;
-            }
-        }
-        rr += kThreads / 32;
-        while (rr >= t.tr) rr -= t.tr, ++i;
-    }
-}
-
-struct DwPos {
-    int n0, y0, c0, tile;
-};
-__device__ __forceinline__ DwPos dw_pos(const DwTile& t, int local) {
-    DwPos q;
-    const int cs = local % t.cslices;
-    q.tile = local / t.cslices;
-    q.n0 = (q.tile / t.tiles_y) * t.ni;
-    q.y0 = (q.tile % t.tiles_y) * t.th;
-    q.c0 = cs * kDwC;
-    return q;
-}
-
 // Grouped-launch descriptor copied once into shared memory (16-byte words):
 // one global-load latency per CTA, then every field read is a shared-memory
 // broadcast.  Thread 0 also initialises the CTA's staging barrier.
@@ -364,24 +324,6 @@ __device__ __forceinline__ int op_to_shared(const Op* __restrict__ ops, int nd, 
     local = static_cast<int>(blockIdx.x) - sh->cta_begin;
     return t;
 }
-
-// Train-mode BN + ReLU of the previous unit (ops.hpp:290-293, 380-385) for
-// the vectorised prologue: parameters of channels c0 + 4*quad + k.
-struct BnRelu4 {
-    float m[4], iv[4], g[4], b[4];
-    __device__ void load(const float* mean, const float* inv, const float* gam, const float* bet, int c0, int c) {
-        const int quad = threadIdx.x & 7;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int ch = c0 + 4 * quad + k;
-            const bool ok = ch < c;
-            m[k] = ok ? mean[ch] : 0.0f, iv[k] = ok ? inv[ch] : 0.0f;
-            g[k] = ok && gam ? gam[ch] : 0.0f, b[k] = ok && bet ? bet[ch] : 0.0f;
-        }
-    }
-    __device__ __forceinline__ float train(float v, int k) const { return relu(bn_train_apply(v, m[k], iv[k], g[k], b[k])); }
-    __device__ __forceinline__ float infer(float v, int k) const { return relu(bn_infer_apply(v, m[k], iv[k])); }
-};
 
 // ---------------------------------------------------------- depthwise fwd
 // The x tile arrives by one 4-D TMA box (zero-filled halo / channel tail) or,
@@ -417,15 +359,9 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
     float* const yl = o.y_lo;
     float* const yf = o.y;
     if (tma) {
-        BnRelu4 p4;
-        if (pro != 0) p4.load(o.pa, o.pb, o.pc, o.pd, q.c0, C);
-        tc::mbar_wait(&bar, 0);
-        cta_mark(2);
-        if (pro != 0) {
-            if (pro == 1) dw_map4(xs, t, n, h, w, q.n0, iy0, -pad, [&](float v, int k) { return p4.train(v, k); });
-            else dw_map4(xs, t, n, h, w, q.n0, iy0, -pad, [&](float v, int k) { return p4.infer(v, k); });
-            __syncthreads();
-        }
+        dw_fwd_tile(o, q, xs, [&] { tc::mbar_wait(&bar, 0); cta_mark(2); });
+        cta_mark(3);
+        return;
     } else {
         float pa = 0, pb = 0, pc = 0, pd = 0;
         if (pro != 0 && cok) {
@@ -443,63 +379,6 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
         }
     }
     const int rs = t.tw * kDwC;
-    if (tma) {
-        // packed: lane = (channel pair p, half); row worker 2*warp + half
-        // walks output rows; two channels per FFMA2
-        const int p = ch & 15, c2 = q.c0 + 2 * p;
-        if (c2 >= C) return;
-        const PkConsts K = pk_consts();
-        float2 w2[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) w2[k] = *reinterpret_cast<const float2*>(o.w + k * C + c2);
-        const int rw = 2 * warp + (ch >> 4), xsh = t.xsh, seg = rw & ((1 << xsh) - 1);
-        const int sw = (wo + (1 << xsh) - 1) >> xsh, xb = seg * sw, xe = min(wo, xb + sw);
-        int i = 0, oy = rw >> xsh;
-        while (oy >= t.th) oy -= t.th, ++i;
-        for (; i < t.ni;) {
-            const int nn = q.n0 + i, yy = q.y0 + oy;
-            if (nn < n && yy < ho) {
-                const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + 2 * p;
-                long long off = ((static_cast<long long>(nn) * ho + yy) * wo + xb) * C + c2;
-                auto ld = [&](int r, int col) { return *reinterpret_cast<const float2*>(base + r * rs + col * kDwC); };
-                float2 win[3][3];
-                if (s == 1) {
-#pragma unroll
-                    for (int r = 0; r < 3; ++r) win[r][1] = ld(r, xb), win[r][2] = ld(r, xb + 1);
-                }
-#pragma unroll 3
-                for (int ox = xb; ox < xe; ++ox, off += C) {
-                    if (s == 1) {
-#pragma unroll
-                        for (int r = 0; r < 3; ++r) win[r][0] = win[r][1], win[r][1] = win[r][2], win[r][2] = ld(r, ox + 2);
-                    } else {
-#pragma unroll
-                        for (int r = 0; r < 3; ++r)
-#pragma unroll
-                            for (int cc = 0; cc < 3; ++cc) win[r][cc] = ld(r, ox * s + cc);
-                    }
-                    float2 acc = K.z;  // 9-term serial sum in (ky, kx) order, per lane
-#pragma unroll
-                    for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-                        for (int kx = 0; kx < 3; ++kx) acc = add2(K, acc, mul2(K, win[ky][kx], w2[ky * 3 + kx]));
-                    if (yh) {
-                        const float2 hv = make_float2(__uint_as_float(tc_split_hi(acc.x)), __uint_as_float(tc_split_hi(acc.y)));
-                        const float2 d = sub2(K, acc, hv);
-                        *reinterpret_cast<float2*>(yh + off) = hv;
-                        *reinterpret_cast<float2*>(yl + off) =
-                            make_float2(__uint_as_float(tc_split_hi(d.x)), __uint_as_float(tc_split_hi(d.y)));
-                    } else {
-                        *reinterpret_cast<float2*>(yf + off) = acc;
-                    }
-                }
-            }
-            oy += (2 * (kThreads / 32)) >> xsh;
-            while (oy >= t.th) oy -= t.th, ++i;
-        }
-        cta_mark(3);
-        return;
-    }
     if (!cok) return;
     int i = 0, oy = warp;
     while (oy >= t.th) oy -= t.th, ++i;
@@ -575,23 +454,6 @@ __device__ __forceinline__ void dw_lane_sum(float* red, const float* v, float* o
         }
     }
 }
-template <int NV>
-__device__ __forceinline__ void dw_lane_sum2(float* red, const float2* v, float* out) {
-    const int lane = threadIdx.x & 31, rw = 2 * (threadIdx.x >> 5) + (lane >> 4), p = lane & 15;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) *reinterpret_cast<float2*>(red + (rw * NV + k) * kDwC + 2 * p) = v[k];
-    __syncthreads();
-    if (threadIdx.x < kDwC) {
-        const int ch = threadIdx.x;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            float acc = 0.0f;
-            for (int l = 0; l < 2 * kDwLanes; ++l) acc += red[(l * NV + k) * kDwC + ch];
-            out[k] = acc;
-        }
-    }
-}
-
 // ------------------------------------------- depthwise bwd (unit > 0, s=1)
 // gy (dw output gradient) and the previous unit's activation relu(bn(p)) are
 // staged with halos; per pixel: the input gradient gathered in ascending
@@ -644,120 +506,7 @@ __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restr
     __syncthreads();
 
     if (tma) {
-        // packed: lane = (channel pair p, half); row worker 2*warp + half
-        // walks (row, x segment) items
-        const int p = ch & 15, c2 = q.c0 + 2 * p;
-        const int rs = t.tw * kDwC;
-        const bool pok = c2 < C;
-        float2 acc2[11];  // gk[9], sg, sgx
-#pragma unroll
-        for (int k = 0; k < 11; ++k) acc2[k] = make_float2(0.0f, 0.0f);
-        const PkConsts K = pk_consts();
-        const int rw = 2 * (threadIdx.x >> 5) + (ch >> 4), xsh = t.xsh, seg = rw & ((1 << xsh) - 1);
-        const int sw = (w + (1 << xsh) - 1) >> xsh, xb = seg * sw, xe = min(w, xb + sw);
-        // pass A: input gradient (outputs ascending, tap (1-dy, 1-dx),
-        // ops.hpp:156-174), previous ReLU mask, BN-backward partials
-        if (pok) {
-            float2 w2[9];
-            bool fin = true;  // finite weights: adding the skipped zero terms is exact
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                w2[k] = *reinterpret_cast<const float2*>(o.w + k * C + c2);
-                fin = fin && isfinite(w2[k].x) && isfinite(w2[k].y);
-            }
-            const float2 mean2 = *reinterpret_cast<const float2*>(o.mean + c2);
-            const float2 inv2 = *reinterpret_cast<const float2*>(o.inv + c2);
-            const float2 gam2 = *reinterpret_cast<const float2*>(o.gamma + c2);
-            const float2 bet2 = *reinterpret_cast<const float2*>(o.beta + c2);
-            int i = 0, y = rw >> xsh;
-            while (y >= t.th) y -= t.th, ++i;
-            for (; i < t.ni;) {
-                const int nn = q.n0 + i, yy = q.y0 + y;
-                if (nn < n && yy < h) {
-                    long long gi = ((static_cast<long long>(nn) * h + yy) * w + xb) * C + c2;
-                    const float* g0 = gs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
-                    const float* x0 = xs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
-                    auto ldg2 = [&](int r, int col) { return *reinterpret_cast<const float2*>(g0 + r * rs + col * kDwC); };
-                    float2 gw[3][3];
-#pragma unroll
-                    for (int r = 0; r < 3; ++r) gw[r][1] = ldg2(r, xb), gw[r][2] = ldg2(r, xb + 1);
-                    for (int x = xb; x < xe; ++x, gi += C) {
-#pragma unroll
-                        for (int r = 0; r < 3; ++r) gw[r][0] = gw[r][1], gw[r][1] = gw[r][2], gw[r][2] = ldg2(r, x + 2);
-                        float2 gx = K.z;
-                        if (fin) {
-#pragma unroll
-                            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                                for (int cc = 0; cc < 3; ++cc) gx = add2(K, gx, mul2(K, gw[r][cc], w2[(2 - r) * 3 + (2 - cc)]));
-                        } else {  // zero terms skipped per lane (0 * inf would be NaN)
-#pragma unroll
-                            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                                for (int cc = 0; cc < 3; ++cc) {
-                                    const float2 gv = gw[r][cc], wv = w2[(2 - r) * 3 + (2 - cc)];
-                                    if (gv.x != 0.0f) gx.x = add(gx.x, mul(gv.x, wv.x));
-                                    if (gv.y != 0.0f) gx.y = add(gx.y, mul(gv.y, wv.y));
-                                }
-                        }
-                        const float2 xpc = *reinterpret_cast<const float2*>(x0 + rs + (x + 1) * kDwC);  // raw centre
-                        const float2 xh = mul2(K, sub2(K, xpc, mean2), inv2);
-                        const float2 yv = add2(K, mul2(K, gam2, xh), bet2);
-                        const float2 gz = add2(K, K.z, gx);
-                        const float2 gm = make_float2(yv.x > 0.0f ? gz.x : 0.0f, yv.y > 0.0f ? gz.y : 0.0f);
-                        *reinterpret_cast<float2*>(gyprev + gi) = gm;
-                        acc2[9] = add2(K, acc2[9], gm);
-                        acc2[10] = fma2(gm, xh, acc2[10]);
-                    }
-                }
-                y += (2 * (kThreads / 32)) >> xsh;
-                while (y >= t.th) y -= t.th, ++i;
-            }
-        }
-        __syncthreads();  // pass A read the raw tile
-        {
-            BnRelu4 p4;
-            p4.load(o.mean, o.inv, o.gamma, o.beta, q.c0, C);
-            dw_map4(xs, t, n, h, w, q.n0, q.y0 - 1, -1, [&](float v, int k) { return p4.train(v, k); });
-        }
-        __syncthreads();
-        // pass B: weight-gradient terms gy(centre) * relu(bn(p))(window)
-        if (pok) {
-            int i = 0, y = rw >> xsh;
-            while (y >= t.th) y -= t.th, ++i;
-            for (; i < t.ni;) {
-                const int nn = q.n0 + i, yy = q.y0 + y;
-                if (nn < n && yy < h) {
-                    const float* g0 = gs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
-                    const float* x0 = xs + ((i * t.tr + y) * t.tw) * kDwC + 2 * p;
-                    auto ldx2 = [&](int r, int col) { return *reinterpret_cast<const float2*>(x0 + r * rs + col * kDwC); };
-                    float2 xw[3][3];
-#pragma unroll
-                    for (int r = 0; r < 3; ++r) xw[r][1] = ldx2(r, xb), xw[r][2] = ldx2(r, xb + 1);
-                    for (int x = xb; x < xe; ++x) {
-#pragma unroll
-                        for (int r = 0; r < 3; ++r) xw[r][0] = xw[r][1], xw[r][1] = xw[r][2], xw[r][2] = ldx2(r, x + 2);
-                        const float2 gyc = *reinterpret_cast<const float2*>(g0 + rs + (x + 1) * kDwC);
-                        if (gyc.x != 0.0f || gyc.y != 0.0f) {
-#pragma unroll
-                            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                                for (int cc = 0; cc < 3; ++cc) acc2[r * 3 + cc] = fma2(gyc, xw[r][cc], acc2[r * 3 + cc]);
-                        }
-                    }
-                }
-                y += (2 * (kThreads / 32)) >> xsh;
-                while (y >= t.th) y -= t.th, ++i;
-            }
-        }
-        __syncthreads();  // staging buffers are reused for the reduction
-        float out[11];
-        dw_lane_sum2<11>(sm, acc2, out);
-        if (threadIdx.x < kDwC && cok) {
-            for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * C + c] = out[k];
-            o.part_sg[static_cast<long long>(q.tile) * C + c] = out[9];
-            o.part_sgx[static_cast<long long>(q.tile) * C + c] = out[10];
-        }
+        dw_bwd_tile(o, q, gs, xs, [] {});
         cta_mark(3);
         return;
     }
@@ -878,43 +627,7 @@ __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restric
         __syncthreads();
     }
     if (tma) {
-        // packed: lane = (channel pair p, half); row worker 2*warp + half
-        const int p = ch & 15, c2 = q.c0 + 2 * p;
-        float2 acc2[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) acc2[k] = make_float2(0.0f, 0.0f);
-        if (c2 < C) {
-            const int rw = 2 * (threadIdx.x >> 5) + (ch >> 4), xsh = t.xsh, seg = rw & ((1 << xsh) - 1);
-            const int sw = (wo + (1 << xsh) - 1) >> xsh, xb = seg * sw, xe = min(wo, xb + sw);
-            int i = 0, oy = rw >> xsh;
-            while (oy >= t.th) oy -= t.th, ++i;
-            for (; i < t.ni;) {
-                const int nn = q.n0 + i, yy = q.y0 + oy;
-                if (nn < n && yy < ho) {
-                    const float* gsr = gs + ((i * t.th + oy) * wo) * kDwC + 2 * p;
-                    const float* base = xs + ((i * t.tr + oy * s) * t.tw) * kDwC + 2 * p;
-#pragma unroll 2
-                    for (int ox = xb; ox < xe; ++ox) {
-                        const float2 gv = *reinterpret_cast<const float2*>(gsr + ox * kDwC);
-                        if (gv.x == 0.0f && gv.y == 0.0f) continue;
-                        const float* b = base + ox * s * kDwC;
-#pragma unroll
-                        for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-                            for (int kx = 0; kx < 3; ++kx)
-                                acc2[ky * 3 + kx] =
-                                    fma2(gv, *reinterpret_cast<const float2*>(b + (ky * t.tw + kx) * kDwC), acc2[ky * 3 + kx]);
-                    }
-                }
-                oy += (2 * (kThreads / 32)) >> xsh;
-                while (oy >= t.th) oy -= t.th, ++i;
-            }
-        }
-        __syncthreads();
-        float out[9];
-        dw_lane_sum2<9>(sm, acc2, out);
-        if (threadIdx.x < kDwC && cok)
-            for (int k = 0; k < 9; ++k) o.part_gk[(static_cast<long long>(q.tile) * 9 + k) * C + c] = out[k];
+        dw_gk_tile(o, q, xs, gs, sm, [] {});
         cta_mark(3);
         return;
     }
