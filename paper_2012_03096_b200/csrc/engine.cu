@@ -120,6 +120,35 @@ Work op_work(const GemmOp& o) {
     return {4.0 * (a + el(o.K, o.N) + el(o.M, o.N)), 2.0 * el(o.M, o.N, o.K)};
 }
 
+// Knockout profiling (diagnosis only): PBKD_KNOCKOUT=<name>[,<name>...] drops
+// those launch classes (op names as in the profile, or gemm_fwd / gemm_dgrad /
+// gemm_wgrad / gemm_conv) from the recorded programs and ignores the failure
+// flags, so the epoch time shows each class's critical-path contribution
+// (tools/gpu_knockout.sh).  Results are meaningless in this mode.
+const std::vector<std::string>& knockouts() {
+    static const std::vector<std::string> v = [] {
+        std::vector<std::string> out;
+        const char* e = std::getenv("PBKD_KNOCKOUT");
+        std::string cur;
+        for (const char* c = e ? e : "";; ++c) {
+            if (*c == ',' || *c == 0) {
+                if (!cur.empty()) out.push_back(cur);
+                cur.clear();
+                if (*c == 0) break;
+            } else {
+                cur += *c;
+            }
+        }
+        return out;
+    }();
+    return v;
+}
+bool knocked_out(const std::string& name) {
+    for (const std::string& k : knockouts())
+        if (name.rfind(k, 0) == 0) return true;
+    return false;
+}
+
 // ----------------------------------------------------------------- program
 // A recorded sequence of launches.  Grouped ops keep their descriptor arrays
 // in one device slab; the whole program can be captured into a CUDA graph.
@@ -128,7 +157,7 @@ public:
     template <class Op>
     void grouped(void (*launch)(const Op*, int, int, cudaStream_t), std::vector<Op> ops,
                  const std::function<int(const Op&)>& ctas) {
-        if (ops.empty()) return;
+        if (ops.empty() || knocked_out(op_name(typeid(Op).name()))) return;
         int total = 0;
         for (Op& o : ops) {
             o.cta_begin = total;
@@ -168,6 +197,8 @@ public:
     }
     void gemm_class(int cls, std::vector<GemmOp> ops) {
         if (ops.empty()) return;
+        if (knocked_out(std::string("gemm_") + (ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad")))
+            return;
         int total = 0;
         for (GemmOp& o : ops) {
             o.cta_begin = total;
@@ -886,7 +917,8 @@ struct Engine::Impl {
             const int n = std::min(B, ntrain - step * B);
             Ctx c{s, n, static_cast<long long>(n) * s->u[0].ho * s->u[0].wo,
                   s->in_stream.f() + static_cast<size_t>(step) * B * s->in_row,
-                  s->tgt_stream.f() + static_cast<size_t>(step) * B * s->out_row, s->failed.i(), gsteps[i]};
+                  s->tgt_stream.f() + static_cast<size_t>(step) * B * s->out_row,
+                  knockouts().empty() ? s->failed.i() : nullptr, gsteps[i]};
             cx.push_back(c);
         }
         // ---- forward
