@@ -178,10 +178,22 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
                                                 int& stores) {
     constexpr int HB = BN / 2;
     const int warp8 = et >> 5;
-    const int M = op.M, N = op.N, epi = op.epi;
+    // every descriptor field in registers up front: the global stores below
+    // could alias the descriptor, which would force a reload of each field
+    // after each store (a dependent L1/L2 round trip per element)
+    const int M = op.M, N = op.N, epi = op.epi, relu_on = op.relu;
+    const long long ldc = op.ldc;
+    const float* __restrict__ scale = op.scale;
+    const float* __restrict__ shift = op.shift;
+    const float* __restrict__ skip = op.skip;
+    float* __restrict__ c_hi = op.c_hi;
+    float* __restrict__ c_lo = op.c_lo;
+    float* __restrict__ part0 = op.part0;
+    float* __restrict__ part1 = op.part1;
+    const CUtensorMap* map_c = &op.map_c;
     const int m0 = tm * kBM, n0 = tn * BN;
     const int r = q * 32 + lane;
-    const bool xform = op.scale || op.skip || op.relu || op.c_hi;
+    const bool xform = scale || skip || relu_on || c_hi;
 #pragma unroll
     for (int pass = 0; pass < BN / 32; ++pass) {
         if (et == 0 && stores) tma_store_wait_read();  // staging block free again
@@ -199,29 +211,28 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
         if (xform) {  // thread = column (lane), rows strided by warp
             named_bar(1, 256);
             const int n = n0 + pass * 32 + lane;
-            const long long ldc = op.ldc;
             float sc = 1.0f, sh = 0.0f;
-            if (op.scale && n < N) sc = __ldg(op.scale + n), sh = __ldg(op.shift + n);
+            if (scale && n < N) sc = __ldg(scale + n), sh = __ldg(shift + n);
             for (int rr = warp8; rr < kBM; rr += 8) {
                 const int row = m0 + rr;
                 if (row >= M || n >= N) continue;
                 const uint32_t a = cs_addr(cs, rr, lane);
                 float x = lds32(a);
-                if (op.scale) x = bn_infer_apply(x, sc, sh);
-                if (op.skip) x = add(x, __ldg(op.skip + static_cast<long long>(row) * ldc + n));
-                if (op.relu) x = relu(x);
+                if (scale) x = bn_infer_apply(x, sc, sh);
+                if (skip) x = add(x, __ldg(skip + static_cast<long long>(row) * ldc + n));
+                if (relu_on) x = relu(x);
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
-                if (op.c_hi) {
+                if (c_hi) {
                     const float hv = __uint_as_float(tc_split_hi(x));
-                    op.c_hi[static_cast<long long>(row) * ldc + n] = hv;
-                    op.c_lo[static_cast<long long>(row) * ldc + n] = __uint_as_float(tc_split_hi(__fsub_rn(x, hv)));
+                    c_hi[static_cast<long long>(row) * ldc + n] = hv;
+                    c_lo[static_cast<long long>(row) * ldc + n] = __uint_as_float(tc_split_hi(__fsub_rn(x, hv)));
                 }
             }
         }
         fence_async_smem();
         named_bar(1, 256);
         if (et == 0) {
-            tma_store_3d(&op.map_c, cs, n0 + pass * 32, m0, epi == 2 ? split : 0);
+            tma_store_3d(map_c, cs, n0 + pass * 32, m0, epi == 2 ? split : 0);
             tma_store_commit();
             stores = 1;
         }
@@ -251,9 +262,9 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
             if (et < 32) {
                 const int cg = n0 + pass * 32 + et;
                 if (cg < N) {
-                    op.part0[static_cast<long long>(tm) * N + cg] =
+                    part0[static_cast<long long>(tm) * N + cg] =
                         __fadd_rn(__fadd_rn(red[0][0][et], red[0][1][et]), __fadd_rn(red[0][2][et], red[0][3][et]));
-                    op.part1[static_cast<long long>(tm) * N + cg] =
+                    part1[static_cast<long long>(tm) * N + cg] =
                         __fadd_rn(__fadd_rn(red[1][0][et], red[1][1][et]), __fadd_rn(red[1][2][et], red[1][3][et]));
                 }
             }
