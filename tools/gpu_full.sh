@@ -9,8 +9,10 @@ echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 echo "ref rc=$?" >> gpurun_out/bench_ref.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_bench.log 2>&1
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:umma_tma_kernel -c 448 --csv --log-file gpurun_out/traffic.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_traffic.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_bench.log
 for k in umma_tma_kernel dw_bwd_kernel dw_fwd_kernel bn_bwd_apply_kernel loss_kernel; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 40 -c 1 -o gpurun_out/full_$k python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_$k.log 2>&1
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:umma_tma_kernel -s 2 -c 1 -o gpurun_out/full_teacher_conv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_conv.log 2>&1
+bash tools/gpu_knockout.sh > /dev/null 2>&1
