@@ -507,6 +507,12 @@ struct TaskState {
     DevBuf params, grads, vel, mstats, snapshot;
     // streams
     DevBuf in_stream, tgt_stream, pos, eval_in;
+    // boundary-buffer mode (single GPU): teacher boundaries k-1 / k for all
+    // training samples in train order, read through the epoch order in pos
+    // (pos[slot] = train row); the streams above are not allocated then
+    const float* bx = nullptr;
+    const float* bt = nullptr;
+    int nsrc = 0;
     // workspace
     DevBuf d[kMaxUnits], p[kMaxUnits], gp, gd, gy;
     // tf32 hi / lo planes of the pointwise GEMM operands (3xTF32 split),
@@ -840,8 +846,8 @@ struct Engine::Impl {
     void init_task_device(TaskState& s, int B, int ho, int wo, const TBlockDev& tb, int ntrain, int neval,
                           long long total, int spe) {
         // streams and workspace
-        s.in_stream.alloc(static_cast<size_t>(ntrain) * s.in_row * sizeof(float));
-        s.tgt_stream.alloc(static_cast<size_t>(ntrain) * s.out_row * sizeof(float));
+        // in_stream / tgt_stream: allocated by run_group when the run needs
+        // them (sample-sharded teacher); pos: epoch positions or order
         s.pos.alloc(static_cast<size_t>(ntrain) * sizeof(int));
         s.eval_in.alloc(static_cast<size_t>(std::max(neval, 1)) * s.in_row * sizeof(float));
         const long long M = static_cast<long long>(B) * ho * wo;
@@ -909,16 +915,19 @@ struct Engine::Impl {
             const float* t;
             const int* failed;
             long long gstep;
+            const int* rows;  // boundary mode: batch slot -> train row
         };
         std::vector<Ctx> cx;
         for (size_t i = 0; i < act.size(); ++i) {
             TaskState* s = act[i];
             const int B = s->task.batch_size;
             const int n = std::min(B, ntrain - step * B);
+            const bool bm = s->bx != nullptr;
             Ctx c{s, n, static_cast<long long>(n) * s->u[0].ho * s->u[0].wo,
-                  s->in_stream.f() + static_cast<size_t>(step) * B * s->in_row,
-                  s->tgt_stream.f() + static_cast<size_t>(step) * B * s->out_row,
-                  knockouts().empty() ? s->failed.i() : nullptr, gsteps[i]};
+                  bm ? s->bx : s->in_stream.f() + static_cast<size_t>(step) * B * s->in_row,
+                  bm ? s->bt : s->tgt_stream.f() + static_cast<size_t>(step) * B * s->out_row,
+                  knockouts().empty() ? s->failed.i() : nullptr, gsteps[i],
+                  bm ? s->pos.i() + static_cast<size_t>(step) * B : nullptr};
             cx.push_back(c);
         }
         // ---- forward
@@ -943,6 +952,7 @@ struct Engine::Impl {
                 o.stride = d.stride;
                 o.pad = 1;
                 o.pro = u == 0 ? 0 : 1;
+                if (u == 0 && c.rows) o.rows = c.rows, o.nsrc = s.nsrc;
                 if (u > 0) {
                     o.pa = s.mean_u(u - 1);
                     o.pb = s.inv_u(u - 1);
@@ -1017,6 +1027,7 @@ struct Engine::Impl {
                 const size_t count = static_cast<size_t>(c.M) * cout;
                 o.kmse = (1.0f * 2.0f) / static_cast<float>(count);
                 o.failed = c.failed;
+                if (c.rows) o.trows = c.rows, o.srow = s.out_row;
                 ls.push_back(o);
                 BnBwdFinOp f{};
                 f.part_sg = s.psg.f();
@@ -1064,6 +1075,7 @@ struct Engine::Impl {
                 a.inv_m = 1.0f / static_cast<float>(c.M);
                 a.kmse = (1.0f * 2.0f) / static_cast<float>(static_cast<size_t>(c.M) * d.cout);
                 a.failed = c.failed;
+                if (a.t && c.rows) a.trows = c.rows, a.srow = s.out_row;
                 aps.push_back(a);
                 // dgrad: gd[m][j] = sum_o gp[m][o] W[o][j]
                 GemmOp g{};
@@ -1171,6 +1183,7 @@ struct Engine::Impl {
                     b.stride = d.stride;
                     b.pad = 1;
                     b.failed = c.failed;
+                    if (c.rows) b.rows = c.rows, b.nsrc = s.nsrc;
                     dw_gk_finalize(b);
                     gks.push_back(b);
                     ReduceOp kk{};
@@ -1229,6 +1242,35 @@ struct Engine::Impl {
         const int* pos;
         int width;
     };
+    // Boundary mode: the teacher writes every boundary 0..kmax of the samples
+    // at d_idx into bnd[j] (rows in d_idx order; bnd[0] = the NHWC images);
+    // students read them through their epoch order, so nothing is scattered.
+    // Block j's output planes alternate between the pong / ping plane pairs.
+    int bnd_row(int j) const {
+        if (j == 0) return net.in_c * net.in_h * net.in_w;
+        const TBlockDev& b = tblocks[static_cast<size_t>(j) - 1];
+        return b.cout * b.hout * b.wout;
+    }
+    void add_teacher_pass_bnd(Program& P, const int* d_idx, int n, int kmax, const std::vector<float*>& bnd,
+                              int chunk, const float* ping, const float* pong, float* t1, float* sk) {
+        const Planes2 pp = planes_for(ping), qp = planes_for(pong);
+        for (int t0 = 0; t0 < n; t0 += chunk) {
+            const int nc = std::min(chunk, n - t0);
+            const int* idx = d_idx + t0;
+            float* x0 = bnd[0] + static_cast<size_t>(t0) * bnd_row(0);
+            const float* img = images.f();
+            const int in_c = net.in_c, in_h = net.in_h, in_w = net.in_w;
+            P.raw([=](cudaStream_t s) { launch_gather_nhwc(img, idx, nc, in_c, in_h, in_w, x0, s); });
+            for (int j = 0; j < kmax; ++j) {
+                float* x = bnd[static_cast<size_t>(j)] + static_cast<size_t>(t0) * bnd_row(j);
+                float* y = bnd[static_cast<size_t>(j) + 1] + static_cast<size_t>(t0) * bnd_row(j + 1);
+                const Planes2 yp = (j % 2 == 0) ? qp : pp;
+                if (yp.hi) act_planes[y] = yp;
+                teacher_block(P, j, x, y, nc, t1, sk);
+            }
+        }
+    }
+
     void add_teacher_pass(Program& P, const int* d_idx, int n, const std::vector<Sink>& sinks,
                           int chunk, float* ping, float* pong, float* t1, float* sk) {
         int kmax = 0;
@@ -1562,6 +1604,41 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     int emax = 0;
     for (TaskState* s : ts) emax = std::max(emax, s->task.epochs);
 
+    // Boundary mode (one GPU, no sample-sharded teacher): every teacher
+    // boundary of the training split lives once in HBM in train order and
+    // the student kernels gather their batches through the epoch order (no
+    // per-epoch scatter into per-task streams).  PBKD_STREAMS=1 forces the
+    // stream + scatter path the sharded runs use.
+    const bool bnd_mode = opt.virtual_shards <= 1 && opt.global_blocks.empty() && [] {
+        const char* e = std::getenv("PBKD_STREAMS");
+        return !(e && e[0] == '1');
+    }();
+    int bkmax = 0;
+    for (TaskState* s : ts) bkmax = std::max(bkmax, s->k);
+    std::vector<DevBuf> bnd_bufs(bnd_mode ? static_cast<size_t>(bkmax) + 1 : 0);
+    std::vector<float*> bnd;
+    for (size_t j = 0; j < bnd_bufs.size(); ++j) {
+        bnd_bufs[j].alloc(static_cast<size_t>(ntrain) * bnd_row(static_cast<int>(j)) * sizeof(float));
+        bnd.push_back(bnd_bufs[j].f());
+    }
+    for (TaskState* s : ts) {
+        if (bnd_mode) {
+            s->bx = bnd[static_cast<size_t>(s->k) - 1];
+            s->bt = bnd[static_cast<size_t>(s->k)];
+            s->nsrc = ntrain;
+        } else {
+            s->bx = s->bt = nullptr;
+            s->in_stream.alloc(static_cast<size_t>(ntrain) * s->in_row * sizeof(float));
+            s->tgt_stream.alloc(static_cast<size_t>(ntrain) * s->out_row * sizeof(float));
+        }
+    }
+    struct BndReset {  // the task states outlive this group's boundary buffers
+        std::vector<TaskState*>& v;
+        ~BndReset() {
+            for (TaskState* s : v) s->bx = s->bt = nullptr;
+        }
+    } bnd_reset{ts};
+
     auto sinks_for = [&](bool identity) {
         std::vector<Sink> v;
         for (TaskState* s : ts) {
@@ -1652,12 +1729,17 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         }
         {
             Program P;
-            add_teacher_pass(P, d_train.i(), ntrain, sinks_for(true), chunk, ping.f(), pong.f(), t1.f(), sk.f());
+            if (bnd_mode)
+                add_teacher_pass_bnd(P, d_train.i(), ntrain, bkmax, bnd, chunk, ping.f(), pong.f(), t1.f(), sk.f());
+            else
+                add_teacher_pass(P, d_train.i(), ntrain, sinks_for(true), chunk, ping.f(), pong.f(), t1.f(), sk.f());
             for (TaskState* s : ts) {
+                const float* xin = bnd_mode ? s->bx : s->in_stream.f();
+                const float* tin = bnd_mode ? s->bt : s->tgt_stream.f();
                 for (int r0 = 0; r0 < ntrain; r0 += ichunk) {
                     const int nr = std::min(ichunk, ntrain - r0);
-                    add_student_infer(P, *s, s->in_stream.f() + static_cast<size_t>(r0) * s->in_row, nr, ia.f(), ib.f(), io.f());
-                    const float* tg = s->tgt_stream.f() + static_cast<size_t>(r0) * s->out_row;
+                    add_student_infer(P, *s, xin + static_cast<size_t>(r0) * s->in_row, nr, ia.f(), ib.f(), io.f());
+                    const float* tg = tin + static_cast<size_t>(r0) * s->out_row;
                     const float* so = io.f();
                     const long long seg = static_cast<long long>(B) * s->out_row;
                     const long long tot = static_cast<long long>(nr) * s->out_row;
@@ -1763,7 +1845,14 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             PBKD_CUDA(cudaEventRecord(t0, st));
             timed_started = true;
         }
-        const std::vector<std::vector<int>> pos_now = std::move(pos_next);
+        std::vector<std::vector<int>> pos_now = std::move(pos_next);
+        if (bnd_mode)  // epoch order: slot -> train row
+            for (size_t i = 0; i < ts.size(); ++i) {
+                if (key[i] == 0) continue;
+                std::vector<int> ord(pos_now[i].size());
+                for (size_t t = 0; t < ord.size(); ++t) ord[static_cast<size_t>(pos_now[i][t])] = static_cast<int>(t);
+                pos_now[i] = std::move(ord);
+            }
         for (size_t i = 0; i < ts.size(); ++i)
             if (key[i] > 0)
                 PBKD_CUDA(cudaMemcpyAsync(ts[i]->pos.p, pos_now[i].data(), pos_now[i].size() * sizeof(int),
@@ -1772,7 +1861,9 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         auto it = graphs.find(gkey);
         if (it == graphs.end()) {
             EpochProg ep{std::make_unique<Program>(), std::make_unique<Program>()};
-            if (!sharded) {
+            if (bnd_mode) {
+                add_teacher_pass_bnd(*ep.pre, d_train.i(), ntrain, bkmax, bnd, chunk, ping.f(), pong.f(), t1.f(), sk.f());
+            } else if (!sharded) {
                 std::vector<Sink> sinks;
                 for (size_t i = 0; i < ts.size(); ++i) {
                     if (key[i] == 0) continue;

@@ -120,6 +120,14 @@ __device__ __forceinline__ const Op& op_of(const Op* ops, int nd, int& local) {
 
 __device__ __forceinline__ bool is_failed(const int* f) { return f != nullptr && *f != 0; }
 
+// element i of a batch stored as a gather: sample i / srow is sample
+// rows[i / srow] of the source (srow elements per sample; a step's batch
+// has < 2^31 elements, so the division is 32-bit)
+__device__ __forceinline__ long long row_remap(const int* rows, long long srow, long long i) {
+    const unsigned smp = static_cast<unsigned>(i) / static_cast<unsigned>(srow);
+    return static_cast<long long>(__ldg(rows + smp)) * srow + (i - static_cast<long long>(smp) * srow);
+}
+
 // channel-group geometry shared by the row-partitioned kernels
 struct Geo {
     int V, G, RP;  // vector width, channel groups, rows processed in parallel
@@ -211,7 +219,8 @@ static size_t dw_smem(const DwTile& t) { return static_cast<size_t>(t.ni) * t.tr
 void dw_fwd_finalize(DwFwdOp& o) {
     o.tile = dw_tile(o.n, o.ho, o.wo, o.c, o.stride, 1);
     const DwTile& t = o.tile;
-    o.tma = encode_nhwc_box(&o.map_x, o.x, o.n, o.h, o.wd, o.c, kDwC, t.tw, t.tr, t.ni) ? 1 : 0;
+    const int nsrc = o.rows ? o.nsrc : o.n;  // gather: single-image boxes over all source images
+    o.tma = encode_nhwc_box(&o.map_x, o.x, nsrc, o.h, o.wd, o.c, kDwC, t.tw, t.tr, o.rows ? 1 : t.ni) ? 1 : 0;
 }
 void dw_bwd_finalize(DwBwdOp& o) {
     o.tile = dw_tile(o.n, o.h, o.wd, o.c, 1, 2);
@@ -228,7 +237,8 @@ void dw_gk_finalize(DwGkOp& o) {
     o.ctas = o.tile.tiles;
     o.rows_per = 0;
     const DwTile& t = o.tile;
-    o.tma = encode_nhwc_box(&o.map_x, o.x, o.n, o.h, o.wd, o.c, kDwC, t.tw, t.tr, t.ni) &&
+    const int nsrc = o.rows ? o.nsrc : o.n;
+    o.tma = encode_nhwc_box(&o.map_x, o.x, nsrc, o.h, o.wd, o.c, kDwC, t.tw, t.tr, o.rows ? 1 : t.ni) &&
                     encode_nhwc_box(&o.map_g, o.gy, o.n, o.ho, o.wo, o.c, kDwC, o.wo, t.th, t.ni)
                 ? 1
                 : 0;
@@ -255,7 +265,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // takes whole rows, lanes walk the row's 16-byte chunks (col*8 + q), so the
 // only index math per chunk is a shift and a mask.
 __device__ __forceinline__ void dw_stage(float* dst, const float* __restrict__ src, const DwTile& t, int n, int h,
-                                         int w, int c, int n0, int iy0, int ix0, int c0) {
+                                         int w, int c, int n0, int iy0, int ix0, int c0, const int* gather = nullptr) {
     const uint32_t sd = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rows = t.ni * t.tr;
@@ -264,7 +274,8 @@ __device__ __forceinline__ void dw_stage(float* dst, const float* __restrict__ s
         const int i = R / t.tr, rr = R - i * t.tr;
         const int nn = n0 + i, iy = iy0 + rr;
         const bool row_in = nn < n && iy >= 0 && iy < h;
-        const float* rowp = src + (static_cast<long long>(nn) * h + iy) * w * c;
+        const long long img = gather != nullptr && nn < n ? __ldg(gather + nn) : nn;
+        const float* rowp = src + (img * h + iy) * w * c;
         const uint32_t drow = sd + R * t.tw * kDwC * 4;
         if (vec) {
             for (int it = lane; it < t.tw * 8; it += 32) {
@@ -346,9 +357,19 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
     const int n = o.n, h = o.h, w = o.wd, C = o.c, ho = o.ho, wo = o.wo, s = o.stride, pad = o.pad, pro = o.pro;
     const int iy0 = q.y0 * s - pad;
     const bool tma = o.tma != 0;
-    if (tma && threadIdx.x == 0) {
-        tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(t.ni * t.tr * t.tw * kDwC * 4));
-        tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, iy0, q.n0);
+    if (tma && threadIdx.x < 32) {
+        if (o.rows == nullptr) {
+            if (threadIdx.x == 0) {
+                tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(t.ni * t.tr * t.tw * kDwC * 4));
+                tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, iy0, q.n0);
+            }
+        } else {  // gather: one single-image box per batch image, lanes in parallel
+            const int cnt = min(t.ni, n - q.n0), img_f = t.tr * t.tw * kDwC;
+            if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(cnt * img_f * 4));
+            __syncwarp();
+            for (int i = threadIdx.x; i < cnt; i += 32)
+                tc::tma_load_4d(xs + i * img_f, &ops[oi].map_x, &bar, q.c0, -pad, iy0, __ldg(o.rows + q.n0 + i));
+        }
     }
     const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5, c = q.c0 + ch;
     const bool cok = c < C;
@@ -368,7 +389,7 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
             pa = o.pa[c], pb = o.pb[c];
             if (pro == 1) pc = o.pc[c], pd = o.pd[c];
         }
-        dw_stage(xs, o.x, t, n, h, w, C, q.n0, iy0, -pad, q.c0);
+        dw_stage(xs, o.x, t, n, h, w, C, q.n0, iy0, -pad, q.c0, o.rows);
         __syncthreads();
         if (pro == 1) {
             dw_map(xs, t, n, h, w, q.n0, iy0, -pad, [&](float v, int) { return relu(bn_train_apply(v, pa, pb, pc, pd)); });
@@ -611,10 +632,23 @@ __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restric
     float* xs = sm;
     float* gs = sm + tile_elems;  // [ni][th][wo][32] (TMA path)
     const bool tma = o.tma != 0;
-    if (tma && threadIdx.x == 0) {
-        tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>((tile_elems + t.ni * t.th * wo * kDwC) * 4));
-        tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, q.y0 * s - pad, q.n0);
-        tc::tma_load_4d(gs, &ops[oi].map_g, &bar, q.c0, 0, q.y0, q.n0);
+    if (tma && threadIdx.x < 32) {
+        if (o.rows == nullptr) {
+            if (threadIdx.x == 0) {
+                tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>((tile_elems + t.ni * t.th * wo * kDwC) * 4));
+                tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, q.y0 * s - pad, q.n0);
+                tc::tma_load_4d(gs, &ops[oi].map_g, &bar, q.c0, 0, q.y0, q.n0);
+            }
+        } else {  // x gathered image by image (lanes in parallel), gy as one box
+            const int cnt = min(t.ni, n - q.n0), img_f = t.tr * t.tw * kDwC;
+            if (threadIdx.x == 0) {
+                tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>((cnt * img_f + t.ni * t.th * wo * kDwC) * 4));
+                tc::tma_load_4d(gs, &ops[oi].map_g, &bar, q.c0, 0, q.y0, q.n0);
+            }
+            __syncwarp();
+            for (int i = threadIdx.x; i < cnt; i += 32)
+                tc::tma_load_4d(xs + i * img_f, &ops[oi].map_x, &bar, q.c0, -pad, q.y0 * s - pad, __ldg(o.rows + q.n0 + i));
+        }
     }
     const int ch = threadIdx.x % kDwC, c = q.c0 + ch;
     const bool cok = c < C;
@@ -623,7 +657,7 @@ __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restric
         tc::mbar_wait(&bar, 0);
         cta_mark(2);
     } else {
-        dw_stage(xs, o.x, t, n, h, w, C, q.n0, q.y0 * s - pad, -pad, q.c0);
+        dw_stage(xs, o.x, t, n, h, w, C, q.n0, q.y0 * s - pad, -pad, q.c0, o.rows);
         __syncthreads();
     }
     if (tma) {
@@ -798,11 +832,10 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
         load_v(o.inv + c0, g.V, inv);
         load_v(o.gamma + c0, g.V, gam);
         load_v(o.beta + c0, g.V, bet);
-#pragma unroll 4
-        for (long long r = r0 + rr; r < r1; r += g.RP) {
+        auto body = [&](long long r, const float* tp) {
             float pv[4], tv[4];
             load_v(o.p + r * o.c + c0, g.V, pv);
-            load_v(o.t + r * o.c + c0, g.V, tv);
+            load_v(tp, g.V, tv);
             for (int q = 0; q < g.V; ++q) {
                 const float xh = mul(sub(pv[q], mean[q]), inv[q]);
                 const float y = add(mul(gam[q], xh), bet[q]);
@@ -812,6 +845,13 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
                 sg[q] += gy;
                 sgx[q] += gy * xh;
             }
+        };
+        if (o.trows == nullptr) {
+#pragma unroll 4
+            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + r * o.c + c0);
+        } else {  // targets gathered through the epoch order
+#pragma unroll 4
+            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + row_remap(o.trows, o.srow, r * o.c + c0));
         }
     }
     cta_reduce_rows(red, sg, g, rr, gg, lane_ok, o.c, o.part_sg + static_cast<long long>(local) * o.c);
@@ -928,7 +968,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApply
         for (int j = 0; j < kElemQuads; ++j) {
             const long long i = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
             p[j] = __ldg(reinterpret_cast<const float4*>(o.p + i));
-            g[j] = __ldg(reinterpret_cast<const float4*>(tg + i));
+            g[j] = __ldg(reinterpret_cast<const float4*>(tg + (o.trows ? row_remap(o.trows, o.srow, i) : i)));
         }
 #pragma unroll
         for (int j = 0; j < kElemQuads; ++j) {
@@ -944,7 +984,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApply
         if (base >= o.total) break;
         float pv[4], gv[4], rv[4];
         const int cnt = static_cast<int>(min(4LL, o.total - base));
-        for (int q = 0; q < cnt; ++q) pv[q] = o.p[base + q], gv[q] = tg[base + q];
+        for (int q = 0; q < cnt; ++q) pv[q] = o.p[base + q], gv[q] = tg[o.trows ? row_remap(o.trows, o.srow, base + q) : base + q];
         for (int q = 0; q < cnt; ++q) rv[q] = bn_bwd_one(o, bn_bwd_par(o, static_cast<int>((base + q) % o.c)), pv[q], gv[q]);
         for (int q = 0; q < cnt; ++q) {
             if (o.gout_hi) {

@@ -46,6 +46,10 @@ struct DwFwdOp {
     const float *pa, *pb, *pc, *pd;  // mean,inv,gamma,beta | scale,shift
     const int* failed;
     int cta_begin;
+    // optional gather: batch image i is image rows[i] of x (nsrc images), e.g.
+    // a teacher boundary buffer read in the task's epoch order
+    const int* rows;
+    int nsrc;
     DwTile tile;  // set by dw_fwd_finalize
     int tma;      // x tile staged by one 4-D TMA box (dw_fwd_finalize), else cp.async
     CUtensorMap map_x;
@@ -83,6 +87,8 @@ struct DwGkOp {
     int ctas, rows_per;  // ctas: partial rows (= spatial tiles, dw_gk_finalize)
     const int* failed;
     int cta_begin;
+    const int* rows;  // optional gather of x images (as DwFwdOp)
+    int nsrc;
     DwTile tile;
     int tma;  // x / gy tiles staged by 4-D TMA boxes (dw_gk_finalize)
     CUtensorMap map_x, map_g;
@@ -183,6 +189,8 @@ struct LossOp {
     float kmse;        // (scale*2)/count
     const int* failed;
     int cta_begin;
+    const int* trows;  // optional gather of t: sample i is sample trows[i] (srow elements each)
+    long long srow;
 };
 
 // Reduce batch-norm backward partials -> sum_g, sum_gx, parameter gradients
@@ -212,6 +220,8 @@ struct BnBwdApplyOp {
     float inv_m, kmse;
     const int* failed;
     int cta_begin;
+    const int* trows;  // optional gather of t (as LossOp)
+    long long srow;
 };
 
 // Momentum SGD over a task's flat parameter buffer (ops.hpp:545-558).
