@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <numeric>
 #include <sstream>
 
@@ -307,6 +308,27 @@ public:
         PBKD_CUDA(cudaGraphDestroy(g));
     }
     void launch_graph(cudaStream_t st) { PBKD_CUDA(cudaGraphLaunch(exec_, st)); }
+    // Eager run with the parallel sections on the side streams (fork / join
+    // events, as in a captured graph): for programs that run only once, where
+    // capturing and instantiating a graph would cost more than it saves.
+    void run_concurrent(cudaStream_t st, const std::vector<cudaStream_t>* side) {
+        if (!finalized_) finalize(st);
+        set_side(side);
+        for (auto& s : steps_) s(st, static_cast<const uint8_t*>(slab_.p));
+        set_side(nullptr);
+        // fork / join events of every nesting level (run_on also copies nested
+        // handles one level up: destroy each handle once); recorded events may
+        // be destroyed before they complete (released then)
+        std::set<cudaEvent_t> evs;
+        collect_events(evs);
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    }
+    void collect_events(std::set<cudaEvent_t>& evs) {
+        evs.insert(cap_events_.begin(), cap_events_.end());
+        cap_events_.clear();
+        for (auto& ps : pars_)
+            for (auto& sub : ps->subs) sub->collect_events(evs);
+    }
     bool has_graph() const { return exec_ != nullptr; }
     size_t launches() const {
         size_t n = 0;
@@ -1837,6 +1859,8 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         return out;
     };
     std::vector<std::vector<int>> pos_next = make_pos(1, epoch_key(1));
+    std::map<std::vector<int>, int> key_uses;  // epochs sharing each program key
+    for (int e = 1; e <= emax; ++e) key_uses[epoch_key(e)] += 1;
     for (int e = 1; e <= emax; ++e) {
         const std::vector<int> key = epoch_key(e);
         if (std::all_of(key.begin(), key.end(), [](int v) { return v == 0; })) break;
@@ -1923,7 +1947,9 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                     }
                 add_step(*ep.post, act, step, 0, ntrain, gs);
             }
-            if (opt.use_graphs) {
+            trace.mark("epoch: record programs");
+            // a graph pays off only for an epoch program that runs again
+            if (opt.use_graphs && key_uses[gkey] > 1) {
                 ep.pre->build_graph(st, &side_streams);
                 ep.post->build_graph(st, &side_streams);
             }
@@ -1943,7 +1969,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             if (pr->has_graph())
                 pr->launch_graph(st);
             else
-                pr->run(st);
+                pr->run_concurrent(st, &side_streams);
             if (pr == it->second.pre.get() && world > 1)  // boundary rows to their owners
                 comm->all_to_all_v(sendbuf.f(), send_off, send_cnt, recvbuf.f(), recv_off, recv_cnt, st);
             if (pr == it->second.pre.get()) PBKD_CUDA(cudaEventRecord(eT, st));
