@@ -1622,6 +1622,39 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         std::map<const float*, Planes2>& m;
         ~PlaneReg() { m.clear(); }
     } plane_reg{act_planes};
+    // Evaluations and the epoch-0 baseline run the tasks as parallel sections
+    // (one branch per stream: the main stream + the side streams); each branch
+    // has its own workspace (student scratch, teacher-suffix buffers and their
+    // planes), sized for the eval split (teacher suffix) or an inference chunk.
+    const int nbr = std::max(1, std::min(static_cast<int>(ts.size()), 1 + static_cast<int>(side_streams.size())));
+    const size_t esz = static_cast<size_t>(std::max(1, std::min(neval, ichunk))) * mrow * sizeof(float);
+    struct BranchWs {
+        DevBuf ia, ib, io, ping, pong, t1, sk, pl[6];
+    };
+    std::vector<BranchWs> bws(static_cast<size_t>(nbr));
+    for (size_t b = 0; b < bws.size(); ++b) {
+        BranchWs& w = bws[b];
+        if (b == 0) continue;  // branch 0 uses the group's own buffers
+        for (DevBuf* d : {&w.ia, &w.ib, &w.io}) d->alloc(wsz);
+        for (DevBuf* d : {&w.ping, &w.pong, &w.t1, &w.sk}) d->alloc(esz);
+        if (tplanes) {
+            float* bufs[3] = {w.ping.f(), w.pong.f(), w.t1.f()};
+            for (int i = 0; i < 3; ++i) {
+                w.pl[2 * i].alloc(esz);
+                w.pl[2 * i + 1].alloc(esz);
+                act_planes[bufs[i]] = Planes2{w.pl[2 * i].f(), w.pl[2 * i + 1].f()};
+            }
+        }
+    }
+    struct WsPtrs {
+        float *ia, *ib, *io, *ping, *pong, *t1, *sk;
+    };
+    auto branch_ws = [&](int b) {
+        if (b == 0) return WsPtrs{ia.f(), ib.f(), io.f(), ping.f(), pong.f(), t1.f(), sk.f()};
+        BranchWs& w = bws[static_cast<size_t>(b)];
+        return WsPtrs{w.ia.f(), w.ib.f(), w.io.f(), w.ping.f(), w.pong.f(), w.t1.f(), w.sk.f()};
+    };
+
     DevBuf correct(sizeof(int) * ts.size());
     int emax = 0;
     for (TaskState* s : ts) emax = std::max(emax, s->task.epochs);
@@ -1675,6 +1708,8 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     // eval_acc slot advances on the device), so each task set's program is
     // captured into a CUDA graph once and replayed.
     std::map<std::vector<TaskState*>, std::unique_ptr<Program>> eval_progs;
+    std::map<std::vector<TaskState*>, int> eval_uses;
+    std::vector<std::unique_ptr<Program>> eval_once;
     DevBuf eval_slots(sizeof(int) * ts.size());
     PBKD_CUDA(cudaMemsetAsync(eval_slots.p, 0, sizeof(int) * ts.size(), st));
     auto run_eval = [&](const std::vector<TaskState*>& which) {
@@ -1685,18 +1720,23 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             return;
         }
         auto prog = std::make_unique<Program>();
-        Program& P = *prog;
+        const int nb = std::min(nbr, static_cast<int>(which.size()));
+        std::vector<Program*> br = nb > 1 ? prog->par(nb) : std::vector<Program*>{prog.get()};
         for (size_t i = 0; i < which.size(); ++i) {
             TaskState& s = *which[i];
+            const int bi = static_cast<int>(i % static_cast<size_t>(nb));
+            Program& P = *br[static_cast<size_t>(bi)];
+            const WsPtrs W = branch_ws(bi);
             const size_t ti = static_cast<size_t>(std::find(ts.begin(), ts.end(), which[i]) - ts.begin());
             int* corr = correct.i() + ti;
-            for (int e0 = 0; e0 < neval; e0 += ichunk) {
-                const int ne = std::min(ichunk, neval - e0);
-                add_student_infer(P, s, s.eval_in.f() + static_cast<size_t>(e0) * s.in_row, ne, ia.f(), ib.f(), io.f());
-                float* cur = io.f();
+            const int ech = bi == 0 ? ichunk : std::max(1, std::min(neval, ichunk));
+            for (int e0 = 0; e0 < neval; e0 += ech) {
+                const int ne = std::min(ech, neval - e0);
+                add_student_infer(P, s, s.eval_in.f() + static_cast<size_t>(e0) * s.in_row, ne, W.ia, W.ib, W.io);
+                float* cur = W.io;
                 for (size_t j = static_cast<size_t>(s.k); j < tblocks.size(); ++j) {
-                    float* nxt = cur == ping.f() ? pong.f() : ping.f();
-                    teacher_block(P, static_cast<int>(j), cur, nxt, ne, t1.f(), sk.f());
+                    float* nxt = cur == W.ping ? W.pong : W.ping;
+                    teacher_block(P, static_cast<int>(j), cur, nxt, ne, W.t1, W.sk);
                     cur = nxt;
                 }
                 const int hw = cls_hw, cc = cls_in_c, nl = cls_layers, mw = cls_maxw;
@@ -1721,12 +1761,14 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 launch_k(snapshot_kernel, dim3(64), dim3(256), 0, s2, snapp, pp, np, sp, ns, takep);
             });
         }
-        if (opt.use_graphs) {
-            P.build_graph(st);
-            P.launch_graph(st);
+        // a graph pays off once the same evaluation repeats a few times
+        if (opt.use_graphs && ++eval_uses[which] >= 3) {
+            prog->build_graph(st, &side_streams);
+            prog->launch_graph(st);
             eval_progs.emplace(which, std::move(prog));
         } else {
-            P.run(st);
+            prog->run_concurrent(st, &side_streams);
+            eval_once.push_back(std::move(prog));  // its slab lives until the run ends
         }
     };
 
@@ -1755,22 +1797,28 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 add_teacher_pass_bnd(P, d_train.i(), ntrain, bkmax, bnd, chunk, ping.f(), pong.f(), t1.f(), sk.f());
             else
                 add_teacher_pass(P, d_train.i(), ntrain, sinks_for(true), chunk, ping.f(), pong.f(), t1.f(), sk.f());
-            for (TaskState* s : ts) {
+            const int nb = std::min(nbr, static_cast<int>(ts.size()));
+            std::vector<Program*> br = nb > 1 ? P.par(nb) : std::vector<Program*>{&P};
+            for (size_t ti = 0; ti < ts.size(); ++ti) {
+                TaskState* s = ts[ti];
+                const int bi = static_cast<int>(ti % static_cast<size_t>(nb));
+                Program& Q = *br[static_cast<size_t>(bi)];
+                const WsPtrs W = branch_ws(bi);
                 const float* xin = bnd_mode ? s->bx : s->in_stream.f();
                 const float* tin = bnd_mode ? s->bt : s->tgt_stream.f();
                 for (int r0 = 0; r0 < ntrain; r0 += ichunk) {
                     const int nr = std::min(ichunk, ntrain - r0);
-                    add_student_infer(P, *s, xin + static_cast<size_t>(r0) * s->in_row, nr, ia.f(), ib.f(), io.f());
+                    add_student_infer(Q, *s, xin + static_cast<size_t>(r0) * s->in_row, nr, W.ia, W.ib, W.io);
                     const float* tg = tin + static_cast<size_t>(r0) * s->out_row;
-                    const float* so = io.f();
+                    const float* so = W.io;
                     const long long seg = static_cast<long long>(B) * s->out_row;
                     const long long tot = static_cast<long long>(nr) * s->out_row;
                     const int nseg = ceil_div(nr, B);
                     double* outp = s->baseline.d() + r0 / B;
-                    P.raw([=](cudaStream_t s2) { launch_mse_segments(so, tg, seg, tot, nseg, outp, s2); });
+                    Q.raw([=](cudaStream_t s2) { launch_mse_segments(so, tg, seg, tot, nseg, outp, s2); });
                 }
             }
-            P.run(st);
+            P.run_concurrent(st, &side_streams);
         }
         trace.mark("group: epoch-0 baseline");
         run_eval(ts);
