@@ -434,7 +434,9 @@ struct TBlockDev {
     int mid_h = 0, mid_w = 0;
 };
 
-ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, cudaStream_t st) {
+// dev_w: the layer's weights already on the device ([cout][cin][kk], the
+// reference layout), e.g. inside the teacher's flat weight upload
+ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, const float* dev_w, cudaStream_t st) {
     ConvDev d;
     d.cin = conv.in_channels;
     d.cout = conv.out_channels;
@@ -444,11 +446,10 @@ ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, 
     const int kk = d.k * d.k;
     const size_t nw = static_cast<size_t>(d.cout) * kk * d.cin;
     {  // relayout [cout][cin][kk] -> [cout][kk][cin] and tf32 split on the device
-        DevBuf raw = upload(conv.weight.data, st);
         d.w.alloc(nw * sizeof(float));
         d.w_hi.alloc(nw * sizeof(float));
         d.w_lo.alloc(nw * sizeof(float));
-        launch_conv_weight_prep(raw.f(), d.cout, d.cin, kk, d.w.f(), d.w_hi.f(), d.w_lo.f(), st);
+        launch_conv_weight_prep(dev_w, d.cout, d.cin, kk, d.w.f(), d.w_hi.f(), d.w_lo.f(), st);
     }
     if (bn) {
         std::vector<float> sc(d.cout), sh(d.cout);
@@ -636,11 +637,33 @@ struct Engine::Impl {
         return m;
     }
 
-    void load_teacher(Network n_in) {
+    // flat: the weights in for_each_array order (host; pinned memory makes the
+    // single H2D copy asynchronous).  Null: taken from the network's tensors.
+    void load_teacher(Network n_in, const float* flat = nullptr, size_t nflat = 0) {
         PBKD_CUDA(cudaSetDevice(dev));
         g_alloc_stream = st;
         net = std::move(n_in);
-        const Network& n = net;
+        Network& n = net;
+        std::map<const pbkd::Tensor*, size_t> off;  // tensor -> offset in the flat array
+        size_t total = 0;
+        pbkd::for_each_array(n, [&](const std::string&, pbkd::Tensor& t) {
+            off[&t] = total;
+            total += t.data.size();
+        });
+        std::vector<float> packed;
+        if (flat == nullptr) {
+            packed.reserve(total);
+            pbkd::for_each_array(n, [&](const std::string&, pbkd::Tensor& t) {
+                packed.insert(packed.end(), t.data.begin(), t.data.end());
+            });
+            flat = packed.data();
+        } else if (nflat != total) {
+            throw std::invalid_argument("teacher weights: flat size does not match the network");
+        }
+        DevBuf dflat(std::max<size_t>(total, 1) * sizeof(float));
+        PBKD_CUDA(cudaMemcpyAsync(dflat.p, flat, total * sizeof(float), cudaMemcpyHostToDevice, st));
+        const float* dbase = dflat.f();
+        auto dev_of = [&](const pbkd::Tensor& t) { return dbase + off.at(&t); };
         tblocks.clear();
         int c = n.in_c, h = n.in_h, w = n.in_w;
         for (const Block& b : n.blocks) {
@@ -651,15 +674,14 @@ struct Engine::Impl {
             d.cout = b.out_channels;
             if (b.spec_kind == "residual3x3") {
                 d.kind = 1;
-                d.c1 = conv_upload(b.layers[0], &b.layers[1], st);
-                d.c2 = conv_upload(b.layers[3], &b.layers[4], st);
+                d.c1 = conv_upload(b.layers[0], &b.layers[1], dev_of(b.layers[0].weight), st);
+                d.c2 = conv_upload(b.layers[3], &b.layers[4], dev_of(b.layers[3].weight), st);
                 const pbkd::LayerParams& add = b.layers[5];
                 if (!add.weight.data.empty()) {
                     d.has_proj = true;
                     pbkd::LayerParams pl = pbkd::make_conv_layer(LayerKind::Conv1x1, add.in_channels,
                                                                  add.out_channels, 1, add.stride, 0);
-                    pl.weight = add.weight;
-                    d.proj = conv_upload(pl, nullptr, st);
+                    d.proj = conv_upload(pl, nullptr, dev_of(add.weight), st);
                 }
                 d.mid_h = (h + 2 * d.c1.pad - 3) / d.c1.stride + 1;
                 d.mid_w = (w + 2 * d.c1.pad - 3) / d.c1.stride + 1;
@@ -667,7 +689,7 @@ struct Engine::Impl {
                 d.wout = d.mid_w;
             } else {
                 d.kind = 0;
-                d.c1 = conv_upload(b.layers[0], &b.layers[1], st);
+                d.c1 = conv_upload(b.layers[0], &b.layers[1], dev_of(b.layers[0].weight), st);
                 d.hout = (h + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
                 d.wout = (w + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
             }
@@ -2197,6 +2219,7 @@ Engine::Engine(int device) : impl_(std::make_unique<Impl>(device)) {}
 Engine::~Engine() = default;
 void Engine::set_teacher(const Network& net) { impl_->load_teacher(net); }
 void Engine::set_teacher(Network&& net) { impl_->load_teacher(std::move(net)); }
+void Engine::set_teacher(Network&& net, const float* flat, size_t n) { impl_->load_teacher(std::move(net), flat, n); }
 const Network& Engine::teacher() const { return impl_->net; }
 bool Engine::has_teacher() const { return impl_->has_teacher; }
 void Engine::set_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {

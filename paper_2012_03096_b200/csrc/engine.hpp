@@ -90,6 +90,8 @@ public:
 
     void set_teacher(const pbkd::Network& net);
     void set_teacher(pbkd::Network&& net);
+    // flat: the same weights in for_each_array order (one H2D copy from it)
+    void set_teacher(pbkd::Network&& net, const float* flat, size_t n);
     const pbkd::Network& teacher() const;
     bool has_teacher() const;
     void set_dataset(const float* images, const int* labels, int count, int c, int h, int w,

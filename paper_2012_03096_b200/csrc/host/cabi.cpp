@@ -176,7 +176,7 @@ int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec, const float* w, size_t n)
             std::copy(w + at, w + at + t.data.size(), t.data.begin());
             at += t.data.size();
         });
-        ctx->eng->set_teacher(std::move(net));
+        ctx->eng->set_teacher(std::move(net), w, n);  // device copy straight from the caller's buffer
         ctx->spec = spec;
     });
 }
