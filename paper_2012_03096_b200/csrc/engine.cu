@@ -2045,6 +2045,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
             if (pr == it->second.pre.get()) PBKD_CUDA(cudaEventRecord(eT, st));
         }
         PBKD_CUDA(cudaEventRecord(e1, st));
+        trace.mark("epoch: launched (host)");
         for (size_t i = 0; i < ts.size(); ++i)  // epoch-local losses -> per-run history
             if (key[i] > 0)
                 PBKD_CUDA(cudaMemcpyAsync(ts[i]->step_loss.f() + gbase[i], ts[i]->epoch_loss.p,

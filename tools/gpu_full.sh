@@ -16,3 +16,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:umma_tma_kernel -s 2 -c 1 -o gpurun_out/full_teacher_conv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_conv.log 2>&1
 bash tools/gpu_knockout.sh > /dev/null 2>&1
+PBKD_TRACE=1 timeout 300 python tools/e2e_probe.py > gpurun_out/e2e_probe.log 2>&1
