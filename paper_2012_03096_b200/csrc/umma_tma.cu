@@ -672,7 +672,11 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         attr = true;
     }
     if (nd > kMaxOps) throw CudaError("umma_tma: too many ops in one launch");
-    const int grid = std::max({1, std::min(total, num_sms()), (total + kMaxTiles - 1) / kMaxTiles});
+    static const int grid_cap = [] {  // diagnosis (tools/gpu_gridcap.sh): cap the persistent grid
+        const char* e = std::getenv("PBKD_GEMM_GRID_MAX");
+        return e ? std::max(1, std::atoi(e)) : 1 << 30;
+    }();
+    const int grid = std::max({1, std::min({total, num_sms(), grid_cap}), (total + kMaxTiles - 1) / kMaxTiles});
     static const bool trace_on = std::getenv("PBKD_GEMM_TRACE") != nullptr;
     static unsigned long long* trace = nullptr;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
