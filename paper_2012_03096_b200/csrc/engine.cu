@@ -1098,7 +1098,6 @@ struct Engine::Impl {
             std::vector<ReduceOp> wr, kr;
             std::vector<DwBwdOp> dbs;
             std::vector<DwGkOp> gks;
-            std::vector<BnBwdFinOp> fins;
             for (Ctx& c : cx) {
                 TaskState& s = *c.s;
                 const UnitDims& d = s.u[u];
@@ -1202,17 +1201,22 @@ struct Engine::Impl {
                     kk.width = 9 * d.cin;
                     kk.failed = c.failed;
                     kr.push_back(kk);
-                    BnBwdFinOp f{};
-                    f.part_sg = s.psg.f();
-                    f.part_sgx = s.psgx.f();
-                    f.ctas = b.ctas;
-                    f.c = d.cin;
-                    f.sg = s.sg_u(u - 1);
-                    f.sgx = s.sgx_u(u - 1);
-                    f.ggamma = s.g_g(u - 1);
-                    f.gbeta = s.g_b(u - 1);
-                    f.failed = s.failed.i();
-                    fins.push_back(f);
+                    // previous unit's BN-backward sums (ops.hpp:343-344: ggamma =
+                    // sum(g * xhat), gbeta = sum(g)) in the same launch as the
+                    // weight-gradient reduction
+                    ReduceOp rg{};
+                    rg.part = s.psg.f();
+                    rg.out = s.sg_u(u - 1);
+                    rg.out2 = s.g_b(u - 1);
+                    rg.parts = b.ctas;
+                    rg.width = d.cin;
+                    rg.failed = c.failed;
+                    kr.push_back(rg);
+                    ReduceOp rx = rg;
+                    rx.part = s.psgx.f();
+                    rx.out = s.sgx_u(u - 1);
+                    rx.out2 = s.g_g(u - 1);
+                    kr.push_back(rx);
                 } else {
                     DwGkOp b{};
                     b.gy = s.gd.f();
@@ -1251,7 +1255,6 @@ struct Engine::Impl {
             if (u > 0) {
                 bx.grouped<DwBwdOp>(launch_dw_bwd, dbs, ctas_dw_bwd);
                 bx.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
-                bx.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fins, [](const BnBwdFinOp& o) { return ctas_cols(o.c); });
             } else {
                 bx.grouped<DwGkOp>(launch_dw_gk, gks, ctas_dw_gk);
                 bx.grouped<ReduceOp>(launch_reduce, kr, red_ctas);

@@ -797,6 +797,7 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __rest
 #pragma unroll
         for (int i = 0; i < kThreads / 32; ++i) sacc += red[i][lane];
         o.out[col] = sacc;
+        if (o.out2) o.out2[col] = sacc;
     }
 }
 

@@ -99,6 +99,7 @@ struct DwGkOp {
 struct ReduceOp {
     const float* part;
     float* out;
+    float* out2;  // optional second copy of the sums (e.g. sum_g -> sg and gbeta)
     int parts, width;
     int layout;  // 0: out[i] = sum ; 1: dw [9][c] -> out [9][c] (same)
     const int* failed;
