@@ -142,3 +142,32 @@ def test_virtual_shards_bitwise(orc, shards, share):
     for a, b in zip(base, shd):
         assert np.array_equal(a["step_losses"], b["step_losses"])
         assert np.array_equal(a["final_block"], b["final_block"])
+
+
+@pytest.mark.gpu
+def test_boundary_buffers_match_streams(orc, monkeypatch):
+    """Single-GPU boundary-buffer path (teacher boundaries stored once, student
+    batches gathered through the epoch order) against the per-task stream +
+    scatter path: identical bits, baseline and evaluations included."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from tests.conftest import spec_text
+    spec = spec_text("c1_small_vgg")
+    ctx = P.Context(0)
+    ctx.teacher_load(spec, orc.teacher_init(spec, 5))
+    img = np.random.default_rng(9).random((90, 3, 32, 32), dtype=np.float32)
+    lab = (np.arange(90) % 10).astype(np.int32)
+    ctx.dataset_load(img, lab)
+    tr, ev = orc.stratified_split(lab, 0.2, 4)
+    tasks = lambda: [P.make_task(k, epochs=2, eval_every=1, seed=P.mix_seed(3, k), batch_size=16)  # noqa: E731
+                     for k in (1, 2, 3, 4)]
+    monkeypatch.delenv("PBKD_STREAMS", raising=False)
+    bnd = ctx.run(tasks(), tr, ev)["results"]
+    monkeypatch.setenv("PBKD_STREAMS", "1")
+    stm = ctx.run(tasks(), tr, ev)["results"]
+    for a, b in zip(bnd, stm):
+        assert a["loss_history"] == b["loss_history"]
+        assert a["eval_history"] == b["eval_history"]
+        assert np.array_equal(a["block"], b["block"])
+        assert np.array_equal(a["final_block"], b["final_block"])
