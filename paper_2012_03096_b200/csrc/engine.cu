@@ -214,7 +214,9 @@ public:
         });
         const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
         names_.push_back(std::string("gemm_") + kind +
-                         (cls >= 2 * kGemmClassTma ? "_pre" : cls >= kGemmClassTma ? "_tma" : "_reg") +
+                         (cls % kGemmClassConv >= 2 * kGemmClassTma ? "_pre"
+                          : cls % kGemmClassConv >= kGemmClassTma   ? "_tma"
+                                                                    : "_reg") +
                          std::to_string(cls % kGemmClassTma));
         KernelStat w;
         for (const GemmOp& o : ops) {

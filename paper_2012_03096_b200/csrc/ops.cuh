@@ -157,6 +157,10 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo);
 void gemm_finalize(GemmOp& o);
 // Launch class of o: N tile (32/64/128), + kGemmClassTma for the TMA kernel.
 constexpr int kGemmClassTma = 1000;
+// + kGemmClassConv: teacher conv ops (TMA kernel specialised for convs: the
+// student kernels carry no im2col / transform code, the conv kernel no
+// batch-norm-partial / split-K epilogue)
+constexpr int kGemmClassConv = 4000;
 int gemm_bn_class(const GemmOp& o);
 bool gemm_tma_prepare(GemmOp& o);  // umma_tma.cu: tensor maps, false if ineligible
 // Whether GEMM operands with leading dimension `ld` (floats) will be consumed

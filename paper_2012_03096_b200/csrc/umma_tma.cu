@@ -172,7 +172,7 @@ __device__ __forceinline__ uint32_t cs_addr(uint32_t cs, int r, int col) {  // e
     return cs + r * 128 + ((((col >> 2) ^ (r & 7))) << 4) + (col & 3) * 4;
 }
 
-template <int BN>
+template <int BN, bool CONV>
 __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* acc, int tm, int tn, int split, int q,
                                                 int h, int lane, int et, float (*red)[4][32], uint32_t cs,
                                                 int& stores) {
@@ -193,7 +193,7 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
     const CUtensorMap* map_c = &op.map_c;
     const int m0 = tm * kBM, n0 = tn * BN;
     const int r = q * 32 + lane;
-    const bool xform = scale || skip || relu_on || c_hi;
+    const bool xform = CONV && (scale || skip || relu_on || c_hi);
 #pragma unroll
     for (int pass = 0; pass < BN / 32; ++pass) {
         if (et == 0 && stores) tma_store_wait_read();  // staging block free again
@@ -236,7 +236,7 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
             tma_store_commit();
             stores = 1;
         }
-        if (epi == 1) {
+        if (!CONV && epi == 1) {
             // thread = (column, row quarter, sum | sum of squares), warp-uniform
             // quarter and kind: the quarter's 32 rows summed serially in the
             // xor-butterfly tree of gemm_epilogue (rows i, i+16 first, then
@@ -274,7 +274,7 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
 
 }  // namespace
 
-template <int BN, bool PS>
+template <int BN, bool PS, bool CONV>
 __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total,
                                                                  unsigned long long* __restrict__ trace) {
     using C = Cfg<BN, PS>;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
             const int m0 = g.tm * kBM, n0 = g.tn * BN;
-            const bool conv = o.conv != 0, akm = o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            const bool conv = CONV && o.conv != 0, akm = o.a_kmajor != 0, bkm = o.b_kmajor != 0;
             int img = 0, y0 = 0;
             if (conv) {  // tiles cover whole output rows / images (gemm_tma_prepare)
                 const int hw = o.oh * o.ow;
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             const TileGeo g = tiles_sh[j].g;
             const int terms = o.tf32x3;
             // pre-split MN-major operands stay MN-major in shared memory
-            const bool amn = o.a_presplit && !o.conv && !o.a_kmajor, bmn = o.b_presplit && !o.b_kmajor;
+            const bool amn = o.a_presplit && !(CONV && o.conv) && !o.a_kmajor, bmn = o.b_presplit && !o.b_kmajor;
             const uint32_t idesc = instr_desc(BN, amn, bmn);
             for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                 const int s = it % S, a = it % C::A;
@@ -480,9 +480,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             const TileGeo g = tiles_sh[j].g;
             const int m0 = g.tm * kBM, n0 = g.tn * BN;
             const bool apre = o.a_presplit != 0, bpre = o.b_presplit != 0;
-            const bool akm = o.conv != 0 || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            const bool akm = (CONV && o.conv != 0) || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
             int img = 0, y0 = 0;
-            if (o.conv) {
+            if (CONV && o.conv) {
                 const int hw = o.oh * o.ow;
                 img = m0 / hw;
                 y0 = (m0 - img * hw) / o.ow * o.cstride - o.cpad;
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     uint8_t* os = op_ring + s * C::op_stage;
                     const int k = g.k0 + kc * kBK;
                     if (apre) {
-                        if (o.conv) {
+                        if (CONV && o.conv) {
                             const int tap = k / o.ic, c0 = k - tap * o.ic;
                             const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
                             tma_load_4d(os, &o.map_ah, &op_full[s], c0, kx - o.cpad, y0 + ky, img);
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
             const bool split3 = o.tf32x3 > 1;
-            const bool akm = o.conv != 0 || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            const bool akm = (CONV && o.conv != 0) || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
             for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                 const int r = it % R, s = it % S;
                 mbar_wait(&raw_full[r], (it / R) & 1);
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     if (warp == kEpiWarp0) mark(3, it);
                 }
             }
-            staged_epilogue<BN>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
+            staged_epilogue<BN, CONV>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
             if (warp == kEpiWarp0 && lane == 0) mark(4, j);
         }
     }
@@ -663,11 +663,11 @@ int num_sms() {
     return n;
 }
 
-template <int BN, bool PS>
+template <int BN, bool PS, bool CONV>
 void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN, PS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN, PS, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg<BN, PS>::smem));
         attr = true;
     }
@@ -685,7 +685,7 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         PBKD_CUDA(cudaMalloc(&trace, (10 * 512 + 3 * 1024) * sizeof(unsigned long long)));
     unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
     if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, (10 * 512 + 3 * 1024) * sizeof(unsigned long long), st));
-    launch_k(umma_tma_kernel<BN, PS>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(Cfg<BN, PS>::smem), st, d, nd,
+    launch_k(umma_tma_kernel<BN, PS, CONV>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(Cfg<BN, PS>::smem), st, d, nd,
              total, tr);
     PBKD_LAUNCH_CHECK();
     static const int trace_from = [] {
@@ -888,13 +888,21 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
 
 // bn: N tile, + kGemmClassTma when every op of the launch is fully pre-split
 void launch_gemm_tma(const GemmOp* d, int nd, int total, int bn, cudaStream_t st) {
-    switch (bn) {
-        case 32: launch_tma_t<32, false>(d, nd, total, st); break;
-        case 64: launch_tma_t<64, false>(d, nd, total, st); break;
-        case 128: launch_tma_t<128, false>(d, nd, total, st); break;
-        case kGemmClassTma + 32: launch_tma_t<32, true>(d, nd, total, st); break;
-        case kGemmClassTma + 64: launch_tma_t<64, true>(d, nd, total, st); break;
-        default: launch_tma_t<128, true>(d, nd, total, st); break;
+    const bool conv = bn >= kGemmClassConv;
+    bn %= kGemmClassConv;
+    switch (bn + (conv ? 10000 : 0)) {
+        case 32: launch_tma_t<32, false, false>(d, nd, total, st); break;
+        case 64: launch_tma_t<64, false, false>(d, nd, total, st); break;
+        case 128: launch_tma_t<128, false, false>(d, nd, total, st); break;
+        case kGemmClassTma + 32: launch_tma_t<32, true, false>(d, nd, total, st); break;
+        case kGemmClassTma + 64: launch_tma_t<64, true, false>(d, nd, total, st); break;
+        case kGemmClassTma + 128: launch_tma_t<128, true, false>(d, nd, total, st); break;
+        case 10000 + 32: launch_tma_t<32, false, true>(d, nd, total, st); break;
+        case 10000 + 64: launch_tma_t<64, false, true>(d, nd, total, st); break;
+        case 10000 + 128: launch_tma_t<128, false, true>(d, nd, total, st); break;
+        case 10000 + kGemmClassTma + 32: launch_tma_t<32, true, true>(d, nd, total, st); break;
+        case 10000 + kGemmClassTma + 64: launch_tma_t<64, true, true>(d, nd, total, st); break;
+        default: launch_tma_t<128, true, true>(d, nd, total, st); break;
     }
 }
 
