@@ -214,8 +214,8 @@ public:
         });
         const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
         names_.push_back(std::string("gemm_") + kind +
-                         (cls % kGemmClassConv >= 2 * kGemmClassTma ? "_pre"
-                          : cls % kGemmClassConv >= kGemmClassTma   ? "_tma"
+                         (cls % kGemmClassKind >= 2 * kGemmClassTma ? "_pre"
+                          : cls % kGemmClassKind >= kGemmClassTma   ? "_tma"
                                                                     : "_reg") +
                          std::to_string(cls % kGemmClassTma));
         KernelStat w;

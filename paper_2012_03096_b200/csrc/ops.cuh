@@ -157,10 +157,12 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo);
 void gemm_finalize(GemmOp& o);
 // Launch class of o: N tile (32/64/128), + kGemmClassTma for the TMA kernel.
 constexpr int kGemmClassTma = 1000;
-// + kGemmClassConv: teacher conv ops (TMA kernel specialised for convs: the
-// student kernels carry no im2col / transform code, the conv kernel no
-// batch-norm-partial / split-K epilogue)
-constexpr int kGemmClassConv = 4000;
+// TMA kernels are specialised per launch kind (class + kind * kGemmClassKind):
+// 0 plain store (dgrad, inference), 1 store + batch-norm partials (fwd),
+// 2 split-K partials (wgrad), 3 teacher conv (im2col + BN affine / skip /
+// ReLU / output planes); each kernel carries only its kind's code
+constexpr int kGemmClassKind = 10000;
+constexpr int kGemmKindConv = 3;
 int gemm_bn_class(const GemmOp& o);
 bool gemm_tma_prepare(GemmOp& o);  // umma_tma.cu: tensor maps, false if ineligible
 // Whether GEMM operands with leading dimension `ld` (floats) will be consumed
@@ -261,7 +263,7 @@ void launch_dw_gk(const DwGkOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_reduce(const ReduceOp* d_ops, int nd, int ctas, cudaStream_t st);
 // ctas: the ops' total tile count (sum of ctas_gemm); cls: gemm_bn_class
 void launch_gemm_bn(const GemmOp* d_ops, int nd, int ctas, int cls, cudaStream_t st);
-void launch_gemm_tma(const GemmOp* d_ops, int nd, int tiles, int bn, cudaStream_t st);
+void launch_gemm_tma(const GemmOp* d_ops, int nd, int tiles, int cls, cudaStream_t st);  // cls: gemm_bn_class
 void launch_bn_stat(const BnStatOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_loss(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_bn_bwd_fin(const BnBwdFinOp* d_ops, int nd, int ctas, cudaStream_t st);

@@ -295,8 +295,9 @@ void gemm_finalize(GemmOp& o) {
 int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
 // + kGemmClassTma: TMA kernel; + 2 kGemmClassTma: TMA kernel, both operands pre-split
 int gemm_bn_class(const GemmOp& o) {
-    return bn_for(o.N) + (o.tma ? kGemmClassTma : 0) + (o.tma && o.a_presplit && o.b_presplit ? kGemmClassTma : 0) +
-           (o.tma && o.conv ? kGemmClassConv : 0);
+    if (!o.tma) return bn_for(o.N);
+    const int kind = o.conv ? kGemmKindConv : o.epi;
+    return bn_for(o.N) + kGemmClassTma + (o.a_presplit && o.b_presplit ? kGemmClassTma : 0) + kind * kGemmClassKind;
 }
 
 template <int BN>
@@ -315,8 +316,8 @@ static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
 // All ops of one launch share the N tile and the kernel (the caller groups
 // ops by gemm_bn_class; narrower ops would pad their B rows with zeros).
 void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int cls, cudaStream_t st) {
-    if (cls % kGemmClassConv >= kGemmClassTma) {
-        launch_gemm_tma(d, nd, ctas, cls - kGemmClassTma, st);
+    if (cls % kGemmClassKind >= kGemmClassTma) {
+        launch_gemm_tma(d, nd, ctas, cls, st);
         return;
     }
     switch (bn_for(cls)) {

@@ -172,7 +172,7 @@ __device__ __forceinline__ uint32_t cs_addr(uint32_t cs, int r, int col) {  // e
     return cs + r * 128 + ((((col >> 2) ^ (r & 7))) << 4) + (col & 3) * 4;
 }
 
-template <int BN, bool CONV>
+template <int BN, int KIND>
 __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* acc, int tm, int tn, int split, int q,
                                                 int h, int lane, int et, float (*red)[4][32], uint32_t cs,
                                                 int& stores) {
@@ -193,7 +193,7 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
     const CUtensorMap* map_c = &op.map_c;
     const int m0 = tm * kBM, n0 = tn * BN;
     const int r = q * 32 + lane;
-    const bool xform = CONV && (scale || skip || relu_on || c_hi);
+    const bool xform = KIND == kGemmKindConv && (scale || skip || relu_on || c_hi);
 #pragma unroll
     for (int pass = 0; pass < BN / 32; ++pass) {
         if (et == 0 && stores) tma_store_wait_read();  // staging block free again
@@ -232,11 +232,11 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
         fence_async_smem();
         named_bar(1, 256);
         if (et == 0) {
-            tma_store_3d(map_c, cs, n0 + pass * 32, m0, epi == 2 ? split : 0);
+            tma_store_3d(map_c, cs, n0 + pass * 32, m0, KIND == 2 ? split : 0);
             tma_store_commit();
             stores = 1;
         }
-        if (!CONV && epi == 1) {
+        if (KIND == 1) {
             // thread = (column, row quarter, sum | sum of squares), warp-uniform
             // quarter and kind: the quarter's 32 rows summed serially in the
             // xor-butterfly tree of gemm_epilogue (rows i, i+16 first, then
@@ -274,10 +274,11 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
 
 }  // namespace
 
-template <int BN, bool PS, bool CONV>
+template <int BN, bool PS, int KIND>
 __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total,
                                                                  unsigned long long* __restrict__ trace) {
     using C = Cfg<BN, PS>;
+    constexpr bool CONV = KIND == kGemmKindConv;
     constexpr int R = C::R, S = C::S, HB = BN / 2;
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t raw_full[C::RB], raw_empty[C::RB], op_full[S], op_empty[S], acc_full[C::A], acc_empty[C::A];
@@ -596,7 +597,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     if (warp == kEpiWarp0) mark(3, it);
                 }
             }
-            staged_epilogue<BN, CONV>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
+            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
             if (warp == kEpiWarp0 && lane == 0) mark(4, j);
         }
     }
@@ -663,11 +664,11 @@ int num_sms() {
     return n;
 }
 
-template <int BN, bool PS, bool CONV>
+template <int BN, bool PS, int KIND>
 void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN, PS, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN, PS, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg<BN, PS>::smem));
         attr = true;
     }
@@ -685,7 +686,7 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         PBKD_CUDA(cudaMalloc(&trace, (10 * 512 + 3 * 1024) * sizeof(unsigned long long)));
     unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
     if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, (10 * 512 + 3 * 1024) * sizeof(unsigned long long), st));
-    launch_k(umma_tma_kernel<BN, PS, CONV>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(Cfg<BN, PS>::smem), st, d, nd,
+    launch_k(umma_tma_kernel<BN, PS, KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(Cfg<BN, PS>::smem), st, d, nd,
              total, tr);
     PBKD_LAUNCH_CHECK();
     static const int trace_from = [] {
@@ -886,23 +887,27 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
     }
 }
 
-// bn: N tile, + kGemmClassTma when every op of the launch is fully pre-split
-void launch_gemm_tma(const GemmOp* d, int nd, int total, int bn, cudaStream_t st) {
-    const bool conv = bn >= kGemmClassConv;
-    bn %= kGemmClassConv;
-    switch (bn + (conv ? 10000 : 0)) {
-        case 32: launch_tma_t<32, false, false>(d, nd, total, st); break;
-        case 64: launch_tma_t<64, false, false>(d, nd, total, st); break;
-        case 128: launch_tma_t<128, false, false>(d, nd, total, st); break;
-        case kGemmClassTma + 32: launch_tma_t<32, true, false>(d, nd, total, st); break;
-        case kGemmClassTma + 64: launch_tma_t<64, true, false>(d, nd, total, st); break;
-        case kGemmClassTma + 128: launch_tma_t<128, true, false>(d, nd, total, st); break;
-        case 10000 + 32: launch_tma_t<32, false, true>(d, nd, total, st); break;
-        case 10000 + 64: launch_tma_t<64, false, true>(d, nd, total, st); break;
-        case 10000 + 128: launch_tma_t<128, false, true>(d, nd, total, st); break;
-        case 10000 + kGemmClassTma + 32: launch_tma_t<32, true, true>(d, nd, total, st); break;
-        case 10000 + kGemmClassTma + 64: launch_tma_t<64, true, true>(d, nd, total, st); break;
-        default: launch_tma_t<128, true, true>(d, nd, total, st); break;
+
+template <int KIND>
+void launch_tma_kind(const GemmOp* d, int nd, int total, int cls, cudaStream_t st) {
+    switch (cls) {
+        case kGemmClassTma + 32: launch_tma_t<32, false, KIND>(d, nd, total, st); break;
+        case kGemmClassTma + 64: launch_tma_t<64, false, KIND>(d, nd, total, st); break;
+        case kGemmClassTma + 128: launch_tma_t<128, false, KIND>(d, nd, total, st); break;
+        case 2 * kGemmClassTma + 32: launch_tma_t<32, true, KIND>(d, nd, total, st); break;
+        case 2 * kGemmClassTma + 64: launch_tma_t<64, true, KIND>(d, nd, total, st); break;
+        default: launch_tma_t<128, true, KIND>(d, nd, total, st); break;
+    }
+}
+
+// cls: gemm_bn_class of every op of the launch (kind, pre-split, N tile)
+void launch_gemm_tma(const GemmOp* d, int nd, int total, int cls, cudaStream_t st) {
+    const int kind = cls / kGemmClassKind, rest = cls % kGemmClassKind;
+    switch (kind) {
+        case 0: launch_tma_kind<0>(d, nd, total, rest, st); break;
+        case 1: launch_tma_kind<1>(d, nd, total, rest, st); break;
+        case 2: launch_tma_kind<2>(d, nd, total, rest, st); break;
+        default: launch_tma_kind<kGemmKindConv>(d, nd, total, rest, st); break;
     }
 }
 
