@@ -184,6 +184,15 @@ static int dw_tile_bytes() {
     return b;
 }
 
+// per-array budget of the two-array kernels (dw backward, dw weight grad)
+static int dw_tile_bytes2() {
+    static const int b = [] {
+        const char* e = std::getenv("PBKD_DW_TILE2_KB");
+        return std::max(12, std::min(96, e ? std::atoi(e) : 48)) * 1024;
+    }();
+    return b;
+}
+
 DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays) {
     DwTile t{};
     const int target = 256;  // output pixels per CTA
@@ -197,7 +206,7 @@ DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays) {
     auto fp = [&](const DwTile& q) {
         return static_cast<long long>(q.ni) * ((q.th - 1) * stride + 3) * ((wo - 1) * stride + 3) * kDwC * 4;
     };
-    while (fp(t) > dw_tile_bytes() / std::max(1, arrays - 1) && (t.ni > 1 || t.th > 1)) {
+    while (fp(t) > (arrays >= 2 ? dw_tile_bytes2() : dw_tile_bytes()) && (t.ni > 1 || t.th > 1)) {
         if (t.ni > 1) t.ni = (t.ni + 1) / 2;
         else t.th = (t.th + 1) / 2;
     }
@@ -604,10 +613,10 @@ __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restr
 void launch_dw_bwd(const DwBwdOp* d, int nd, int ctas, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PBKD_CUDA(cudaFuncSetAttribute(dw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * dw_tile_bytes()));
+        PBKD_CUDA(cudaFuncSetAttribute(dw_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * dw_tile_bytes2()));
         attr = true;
     }
-    traced("dw_bwd", ctas, st, [&] { launch_k(dw_bwd_kernel, dim3(ctas), dim3(kThreads), 2 * dw_tile_bytes(), st, d, nd); });
+    traced("dw_bwd", ctas, st, [&] { launch_k(dw_bwd_kernel, dim3(ctas), dim3(kThreads), 2 * dw_tile_bytes2(), st, d, nd); });
     PBKD_LAUNCH_CHECK();
 }
 
@@ -704,10 +713,10 @@ __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restric
 void launch_dw_gk(const DwGkOp* d, int nd, int ctas, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PBKD_CUDA(cudaFuncSetAttribute(dw_gk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * dw_tile_bytes()));
+        PBKD_CUDA(cudaFuncSetAttribute(dw_gk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * dw_tile_bytes2()));
         attr = true;
     }
-    traced("dw_gk", ctas, st, [&] { launch_k(dw_gk_kernel, dim3(ctas), dim3(kThreads), 2 * dw_tile_bytes(), st, d, nd); });
+    traced("dw_gk", ctas, st, [&] { launch_k(dw_gk_kernel, dim3(ctas), dim3(kThreads), 2 * dw_tile_bytes2(), st, d, nd); });
     PBKD_LAUNCH_CHECK();
 }
 
