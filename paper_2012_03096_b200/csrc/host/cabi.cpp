@@ -105,7 +105,8 @@ double now_s(std::chrono::steady_clock::time_point t0) {
 
 // One-op launch helper for the kernel-level ABI.
 template <class Op>
-void launch_one(cudaStream_t st, void (*launch)(const Op*, int, int, cudaStream_t), Op op, int ctas) {
+void launch_one(cudaStream_t st, void (*launch)(const Op*, int, int, cudaStream_t), const Op& in, int ctas) {
+    Op op = in;
     op.cta_begin = 0;
     Op* d = nullptr;
     PBKD_CUDA(cudaMalloc(&d, sizeof(Op)));
