@@ -46,6 +46,7 @@ extern "C" {
 #define PBKD_ERR_LOGIC 4   /* std::logic_error */
 #define PBKD_ERR_CUDA 5    /* CUDA runtime failure */
 #define PBKD_ERR_OTHER 6
+#define PBKD_ERR_WEIGHTS 7 /* pbkd::WeightsError (unreadable / inconsistent weight file) */
 
 #define PBKD_RUN_STEP_ONLY 1 /* skip epoch-0 baseline and evaluations */
 #define PBKD_RUN_NO_GRAPH 2  /* launch eagerly instead of CUDA graphs */
@@ -111,6 +112,25 @@ int pbkd_spec_num_blocks(const char* spec_json, int* n);
 int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec_json, const float* weights, size_t n);
 int pbkd_teacher_init(pbkd_ctx* ctx, const char* spec_json, uint64_t seed); /* init_weights */
 int pbkd_teacher_weights(pbkd_ctx* ctx, float* out, size_t cap);
+
+/* ---- PBKD weight files (replaces weights_io.hpp save_weights /
+ * load_weights / load_into_network / rebuild_network_from_arrays /
+ * file_hash, weights_io.cpp:68-319; byte-identical files) ------------- */
+/* the loaded teacher, arrays in network traversal order */
+int pbkd_teacher_save_file(pbkd_ctx* ctx, const char* path);
+/* teacher of spec_json with its weights from a PBKD file (validated by name / shape) */
+int pbkd_teacher_load_file(pbkd_ctx* ctx, const char* spec_json, const char* path);
+/* network of spec_json (teacher weights `teacher`, n_teacher floats) with block
+ * `block_index` (1-based) replaced by a candidate of `kind` (pbkd_task.kind)
+ * whose weights are `block` (n_block floats, for_each_block_array order) */
+int pbkd_save_student_network(const char* spec_json, const float* teacher, size_t n_teacher, int block_index,
+                              int kind, const float* block, size_t n_block, const char* path);
+/* rebuild_network_from_arrays over a PBKD file against spec_json: per block 0 =
+ * teacher structure, 1 + kind = replacement candidate; the rebuilt network's
+ * arrays into out (cap floats, n_out written) */
+int pbkd_load_network_file(const char* spec_json, const char* path, int* block_kinds, int max_blocks, float* out,
+                           size_t cap, size_t* n_out);
+int pbkd_file_hash(const char* path, uint64_t* out);
 
 /* ---- dataset: images fp32 NCHW in [0,1], labels int -------------------- */
 int pbkd_dataset_load(pbkd_ctx* ctx, const float* images, const int* labels, int count, int c,

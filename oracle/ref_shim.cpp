@@ -20,6 +20,7 @@
 #include "pbkd/ops.hpp"
 #include "pbkd/replacement.hpp"
 #include "pbkd/scheduler.hpp"
+#include "pbkd/weights_io.hpp"
 
 using namespace pbkd;
 
@@ -410,6 +411,47 @@ int ref_train_replay_f64(const char* spec, const float* tw, const orc_dataset* d
         }
         flatten_block(student, final_w, cap);
     });
+}
+
+// PBKD weight files written / rebuilt by the reference (weights_io.cpp), for
+// byte-level comparison with the product's writer.  k = 0: the teacher as is;
+// else block k replaced by a candidate named like the teacher block (as
+// reassemble does, distill.cpp:319).
+__attribute__((visibility("default"))) int ref_save_network_file(const char* spec, uint64_t teacher_seed, int k, int kind, uint64_t cand_seed,
+                          const char* path) {
+    return guard([&] {
+        Network net = parse_model_spec(spec, "spec");
+        init_weights(net, teacher_seed);
+        if (k > 0) {
+            Block& tb = net.blocks.at(static_cast<size_t>(k) - 1);
+            Block nb = build_candidate(static_cast<CandidateKind>(kind), tb.in_channels, tb.out_channels, tb.stride,
+                                       cand_seed)
+                           .block;
+            nb.name = tb.name;
+            tb = std::move(nb);
+        }
+        save_weights(path, arrays_from_network(net));
+    });
+}
+
+// rebuild_network_from_arrays of a file against spec: network_weight_hash of
+// the result and each block's spec_kind (0 teacher structure, 1 + candidate)
+__attribute__((visibility("default"))) int ref_rebuild_network_file(const char* spec, const char* path, uint64_t* hash, int* kinds, int max_blocks) {
+    return guard([&] {
+        const Network teacher = parse_model_spec(spec, "spec");
+        const Network net = rebuild_network_from_arrays(teacher, load_weights(path), path);
+        *hash = network_weight_hash(net);
+        for (size_t i = 0; i < net.blocks.size() && static_cast<int>(i) < max_blocks; ++i) {
+            int kd = 0;
+            for (int c = 0; c < 4; ++c)
+                if (net.blocks[i].spec_kind == candidate_kind_name(static_cast<CandidateKind>(c))) kd = 1 + c;
+            kinds[i] = kd;
+        }
+    });
+}
+
+__attribute__((visibility("default"))) int ref_file_hash(const char* path, uint64_t* out) {
+    return guard([&] { *out = file_hash(path); });
 }
 
 }  // extern "C"

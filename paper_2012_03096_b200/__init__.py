@@ -22,8 +22,12 @@ LIB_PATH = os.path.join(HERE, "libpbkd_b200.so")
 KINDS = {"two_layer": 0, "three_layer": 1, "two_layer_skip": 2, "three_layer_skip": 3}
 POLICIES = {"round_robin": 0, "wfd": 1, "work_stealing": 2}
 RUN_STEP_ONLY, RUN_NO_GRAPH, RUN_PROFILE = 1, 2, 4
+class WeightsError(RuntimeError):
+    """pbkd::WeightsError: unreadable or inconsistent PBKD weight file."""
+
+
 ERR_KINDS = {1: ValueError, 2: ValueError, 3: IndexError, 4: RuntimeError, 5: RuntimeError,
-             6: RuntimeError}
+             6: RuntimeError, 7: WeightsError}
 
 
 class Task(C.Structure):
@@ -128,6 +132,13 @@ def lib() -> C.CDLL:
             "pbkd_k_pw_bwd": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int]),
             "pbkd_k_sgd": (C.c_int, [vp, vp, vp, vp, C.c_size_t, C.c_float, C.c_float]),
             "pbkd_sgd_host": (C.c_int, [vp, vp, vp, C.c_size_t, C.c_float, C.c_float]),
+            "pbkd_teacher_save_file": (C.c_int, [vp, C.c_char_p]),
+            "pbkd_teacher_load_file": (C.c_int, [vp, C.c_char_p, C.c_char_p]),
+            "pbkd_save_student_network": (C.c_int, [C.c_char_p, vp, C.c_size_t, C.c_int, C.c_int, vp,
+                                                    C.c_size_t, C.c_char_p]),
+            "pbkd_load_network_file": (C.c_int, [C.c_char_p, C.c_char_p, vp, C.c_int, vp, C.c_size_t,
+                                                 C.POINTER(C.c_size_t)]),
+            "pbkd_file_hash": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -245,6 +256,34 @@ def exchange_plan(blocks, owners, in_row, out_row, world, n_train, src, dst, sha
     return cnt.value, oi, ot, sbd
 
 
+def save_student_network(spec, teacher_weights, block_index, kind, block_weights, path):
+    """Network of `spec` with block `block_index` replaced by a candidate of
+    `kind` holding `block_weights` (e.g. a run result's "block"), as a PBKD file."""
+    tw, bw = _f32(teacher_weights), _f32(block_weights)
+    check(lib().pbkd_save_student_network(spec.encode(), _ptr(tw), tw.size, block_index, kind, _ptr(bw),
+                                          bw.size, os.fsencode(path)))
+
+
+def load_network_file(spec, path, cap=None):
+    """rebuild_network_from_arrays over a PBKD file: (per-block kind, 0 = teacher
+    structure / 1 + candidate kind, flat arrays of the rebuilt network)."""
+    nb = spec_num_blocks(spec)
+    kinds = np.zeros(nb, np.int32)
+    cap = cap or 4 * spec_num_floats(spec) + 1024
+    out = np.zeros(cap, np.float32)
+    n = C.c_size_t()
+    check(lib().pbkd_load_network_file(spec.encode(), os.fsencode(path), _ptr(kinds), nb, _ptr(out), cap,
+                                       C.byref(n)))
+    return kinds, out[:n.value].copy()
+
+
+def file_hash(path):
+    """FNV-1a 64 of the file bytes (weights_io.cpp file_hash)."""
+    h = C.c_uint64()
+    check(lib().pbkd_file_hash(os.fsencode(path), C.byref(h)))
+    return h.value
+
+
 def spec_num_floats(spec):
     n = C.c_size_t()
     check(lib().pbkd_spec_num_floats(spec.encode(), C.byref(n)))
@@ -287,6 +326,14 @@ class Context:
         out = np.zeros(n, np.float32)
         check(lib().pbkd_teacher_weights(self.h, _ptr(out), n))
         return out
+
+    def teacher_save_file(self, path):
+        """The loaded teacher as a PBKD weight file (weights_io.cpp:68-99 layout)."""
+        check(lib().pbkd_teacher_save_file(self.h, os.fsencode(path)))
+
+    def teacher_load_file(self, spec: str, path):
+        """Teacher of `spec` with its weights from a PBKD file (load_into_network)."""
+        check(lib().pbkd_teacher_load_file(self.h, spec.encode(), os.fsencode(path)))
 
     def dataset_load(self, images, labels, classes=10):
         img, lab = _f32(images), _i32(labels)

@@ -14,6 +14,7 @@
 #include "../ops.cuh"
 #include "pbkd/dataset.hpp"
 #include "pbkd/replacement.hpp"
+#include "pbkd/weights_io.hpp"
 #include "pbkd/scheduler.hpp"
 
 using namespace pbkd_gpu;
@@ -42,6 +43,8 @@ int guard(F&& f) {
         return 0;
     } catch (const pbkd::ShapeError& e) {
         g_err = e.what(), g_kind = PBKD_ERR_SHAPE;
+    } catch (const pbkd::WeightsError& e) {
+        g_err = e.what(), g_kind = PBKD_ERR_WEIGHTS;
     } catch (const pbkd_gpu::CudaError& e) {
         g_err = e.what(), g_kind = PBKD_ERR_CUDA;
     } catch (const std::out_of_range& e) {
@@ -201,6 +204,73 @@ int pbkd_teacher_weights(pbkd_ctx* ctx, float* out, size_t cap) {
             at += t.data.size();
         });
     });
+}
+
+int pbkd_teacher_save_file(pbkd_ctx* ctx, const char* path) {
+    return guard([&] { pbkd::save_weights(path, pbkd::arrays_from_network(ctx->eng->teacher())); });
+}
+
+int pbkd_teacher_load_file(pbkd_ctx* ctx, const char* spec, const char* path) {
+    return guard([&] {
+        pbkd::Network net = spec_net(spec);
+        pbkd::load_into_network(net, pbkd::load_weights(path), path);
+        ctx->eng->set_teacher(std::move(net));
+        ctx->spec = spec;
+    });
+}
+
+int pbkd_save_student_network(const char* spec, const float* teacher, size_t n_teacher, int block_index, int kind,
+                              const float* block, size_t n_block, const char* path) {
+    return guard([&] {
+        pbkd::Network net = spec_net(spec);
+        if (n_teacher != net_floats(net)) throw std::invalid_argument("teacher weights: wrong float count");
+        size_t at = 0;
+        pbkd::for_each_array(net, [&](const std::string&, pbkd::Tensor& t) {
+            std::copy(teacher + at, teacher + at + t.data.size(), t.data.begin());
+            at += t.data.size();
+        });
+        if (block_index < 1 || block_index > static_cast<int>(net.blocks.size()))
+            throw std::out_of_range("save_student_network: block index out of range");
+        pbkd::Block& tb = net.blocks[static_cast<size_t>(block_index) - 1];
+        pbkd::Block sb = pbkd::build_candidate(static_cast<pbkd::CandidateKind>(kind), tb.in_channels,
+                                               tb.out_channels, tb.stride, 0).block;
+        sb.name = tb.name;
+        size_t bn = 0;
+        pbkd::for_each_block_array(sb, [&](const std::string&, pbkd::Tensor& t) { bn += t.data.size(); });
+        if (bn != n_block) throw std::invalid_argument("save_student_network: wrong block float count");
+        at = 0;
+        pbkd::for_each_block_array(sb, [&](const std::string&, pbkd::Tensor& t) {
+            std::copy(block + at, block + at + t.data.size(), t.data.begin());
+            at += t.data.size();
+        });
+        tb = std::move(sb);
+        pbkd::save_weights(path, pbkd::arrays_from_network(net));
+    });
+}
+
+int pbkd_load_network_file(const char* spec, const char* path, int* block_kinds, int max_blocks, float* out,
+                           size_t cap, size_t* n_out) {
+    return guard([&] {
+        const pbkd::Network teacher = spec_net(spec);
+        const pbkd::Network net = pbkd::rebuild_network_from_arrays(teacher, pbkd::load_weights(path), path);
+        for (size_t i = 0; i < net.blocks.size() && static_cast<int>(i) < max_blocks; ++i) {
+            int k = 0;
+            for (int c = 0; c < 4; ++c)
+                if (net.blocks[i].spec_kind == pbkd::candidate_kind_name(static_cast<pbkd::CandidateKind>(c))) k = 1 + c;
+            block_kinds[i] = k;
+        }
+        size_t at = 0;
+        pbkd::for_each_array(const_cast<pbkd::Network&>(net), [&](const std::string&, pbkd::Tensor& t) {
+            if (at + t.data.size() > cap) throw std::length_error("buffer too small");
+            std::copy(t.data.begin(), t.data.end(), out + at);
+            at += t.data.size();
+        });
+        *n_out = at;
+    });
+}
+
+int pbkd_file_hash(const char* path, uint64_t* out) {
+    return guard([&] { *out = pbkd::file_hash(path); });
 }
 
 int pbkd_dataset_load(pbkd_ctx* ctx, const float* img, const int* lab, int count, int c, int h, int w,
