@@ -728,34 +728,50 @@ static size_t red_smem(int) { return static_cast<size_t>(kThreads) * 4 * sizeof(
 constexpr int kColLanes = kThreads / 32;
 int ctas_cols(int c) { return ceil_div(c, 32); }
 
-__device__ __forceinline__ float col_sum(const float* __restrict__ part, int parts, int c, int ch,
-                                         float (*red)[32]) {
+// Column sums of two [parts][c] partial arrays at once (a CTA owns 32
+// columns; its 8 warps stride over the parts with 8 loads of each array in
+// flight per round, then combine in fixed order): one dependent round trip
+// per 64 parts instead of one per 32 parts and array.
+__device__ __forceinline__ void col_sum2(const float* __restrict__ pa, const float* __restrict__ pb, int parts, int c,
+                                         int ch, float (*red)[2][32], float& sa, float& sb) {
     const int lane = threadIdx.x / 32, col = threadIdx.x % 32;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float a[4] = {0.0f, 0.0f, 0.0f, 0.0f}, b[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     if (ch < c) {
         int p = lane;
-        for (; p + 3 * kColLanes < parts; p += 4 * kColLanes)
+        for (; p + 7 * kColLanes < parts; p += 8 * kColLanes) {
+            float va[8], vb[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] += __ldg(part + static_cast<long long>(p + u * kColLanes) * c + ch);
-        for (; p < parts; p += kColLanes) acc[0] += __ldg(part + static_cast<long long>(p) * c + ch);
+            for (int u = 0; u < 8; ++u) {
+                const long long off = static_cast<long long>(p + u * kColLanes) * c + ch;
+                va[u] = __ldg(pa + off);
+                vb[u] = __ldg(pb + off);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u & 3] += va[u], b[u & 3] += vb[u];
+        }
+        for (; p < parts; p += kColLanes) {
+            const long long off = static_cast<long long>(p) * c + ch;
+            a[0] += __ldg(pa + off);
+            b[0] += __ldg(pb + off);
+        }
     }
-    red[lane][col] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    red[lane][0][col] = (a[0] + a[1]) + (a[2] + a[3]);
+    red[lane][1][col] = (b[0] + b[1]) + (b[2] + b[3]);
     __syncthreads();
-    float s = 0.0f;
-    for (int l = 0; l < kColLanes; ++l) s += red[l][col];
+    sa = sb = 0.0f;
+    for (int l = 0; l < kColLanes; ++l) sa += red[l][0][col], sb += red[l][1][col];
     __syncthreads();
-    return s;
 }
 
 __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __restrict__ ops, int nd) {
     pdl_enter();
-    __shared__ float red[kColLanes][32];
+    __shared__ float red[kColLanes][2][32];
     int local;
     const BnStatOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
     const int ch = local * 32 + threadIdx.x % 32;
-    const float sum = col_sum(o.part_sum, o.tiles, o.c, ch, red);
-    const float sq = col_sum(o.part_sq, o.tiles, o.c, ch, red);
+    float sum, sq;
+    col_sum2(o.part_sum, o.part_sq, o.tiles, o.c, ch, red, sum, sq);
     if (threadIdx.x >= 32 || ch >= o.c) return;
     const float fm = static_cast<float>(o.m);
     const float mean = __fdiv_rn(sum, fm);
@@ -882,7 +898,7 @@ void launch_loss(const LossOp* d, int nd, int ctas, cudaStream_t st) {
 
 __global__ void __launch_bounds__(kThreads) bn_bwd_fin_kernel(const BnBwdFinOp* __restrict__ ops, int nd) {
     pdl_enter();
-    __shared__ float red[kColLanes][32];
+    __shared__ float red[kColLanes][2][32];
     int local;
     const BnBwdFinOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
@@ -897,8 +913,8 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_fin_kernel(const BnBwdFinOp* 
         }
     }
     const int ch = local * 32 + threadIdx.x % 32;
-    const float a = col_sum(o.part_sg, o.ctas, o.c, ch, red);
-    const float b = col_sum(o.part_sgx, o.ctas, o.c, ch, red);
+    float a, b;
+    col_sum2(o.part_sg, o.part_sgx, o.ctas, o.c, ch, red, a, b);
     if (threadIdx.x >= 32 || ch >= o.c) return;
     o.sg[ch] = a;
     o.sgx[ch] = b;
