@@ -1,5 +1,6 @@
 // engine.cu -- per-GPU distillation engine (see engine.hpp).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cctype>
@@ -1300,22 +1301,38 @@ struct Engine::Impl {
         const TBlockDev& b = tblocks[static_cast<size_t>(j) - 1];
         return b.cout * b.hout * b.wout;
     }
+    // A teacher lane: the activation buffers one chain of teacher blocks
+    // uses (their registered tf32 planes; t1 / sk: residual-block scratch).
+    struct TLane {
+        const float *ping, *pong;
+        float *t1, *sk;
+    };
+    // Several lanes split the samples and run as a parallel section: a conv
+    // of one lane fills the last-wave tail of the other lane's conv.
     void add_teacher_pass_bnd(Program& P, const int* d_idx, int n, int kmax, const std::vector<float*>& bnd,
-                              int chunk, const float* ping, const float* pong, float* t1, float* sk) {
-        const Planes2 pp = planes_for(ping), qp = planes_for(pong);
-        for (int t0 = 0; t0 < n; t0 += chunk) {
-            const int nc = std::min(chunk, n - t0);
-            const int* idx = d_idx + t0;
-            float* x0 = bnd[0] + static_cast<size_t>(t0) * bnd_row(0);
-            const float* img = images.f();
-            const int in_c = net.in_c, in_h = net.in_h, in_w = net.in_w;
-            P.raw([=](cudaStream_t s) { launch_gather_nhwc(img, idx, nc, in_c, in_h, in_w, x0, s); });
-            for (int j = 0; j < kmax; ++j) {
-                float* x = bnd[static_cast<size_t>(j)] + static_cast<size_t>(t0) * bnd_row(j);
-                float* y = bnd[static_cast<size_t>(j) + 1] + static_cast<size_t>(t0) * bnd_row(j + 1);
-                const Planes2 yp = (j % 2 == 0) ? qp : pp;
-                if (yp.hi) act_planes[y] = yp;
-                teacher_block(P, j, x, y, nc, t1, sk);
+                              int chunk, const std::vector<TLane>& lanes) {
+        const int L = std::max(1, std::min(static_cast<int>(lanes.size()), n));
+        std::vector<Program*> br = L > 1 ? P.par(L) : std::vector<Program*>{&P};
+        for (int l = 0; l < L; ++l) {
+            Program& Q = *br[static_cast<size_t>(l)];
+            const TLane& ln = lanes[static_cast<size_t>(l)];
+            const Planes2 pp = planes_for(ln.ping), qp = planes_for(ln.pong);
+            const int b0 = static_cast<int>(static_cast<long long>(n) * l / L);
+            const int b1 = static_cast<int>(static_cast<long long>(n) * (l + 1) / L);
+            for (int t0 = b0; t0 < b1; t0 += chunk) {
+                const int nc = std::min(chunk, b1 - t0);
+                const int* idx = d_idx + t0;
+                float* x0 = bnd[0] + static_cast<size_t>(t0) * bnd_row(0);
+                const float* img = images.f();
+                const int in_c = net.in_c, in_h = net.in_h, in_w = net.in_w;
+                Q.raw([=](cudaStream_t s) { launch_gather_nhwc(img, idx, nc, in_c, in_h, in_w, x0, s); });
+                for (int j = 0; j < kmax; ++j) {
+                    float* x = bnd[static_cast<size_t>(j)] + static_cast<size_t>(t0) * bnd_row(j);
+                    float* y = bnd[static_cast<size_t>(j) + 1] + static_cast<size_t>(t0) * bnd_row(j + 1);
+                    const Planes2 yp = (j % 2 == 0) ? qp : pp;
+                    if (yp.hi) act_planes[y] = yp;
+                    teacher_block(Q, j, x, y, nc, ln.t1, ln.sk);
+                }
             }
         }
     }
@@ -1682,6 +1699,22 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         return WsPtrs{w.ia.f(), w.ib.f(), w.io.f(), w.ping.f(), w.pong.f(), w.t1.f(), w.sk.f()};
     };
 
+    // teacher lanes of the training-split pass (PBKD_TEACHER_LANES, default 2):
+    // lane 0 uses the group's buffers, the others their own planes / scratch
+    const int nlanes = [&] {
+        const char* e = std::getenv("PBKD_TEACHER_LANES");
+        return std::max(1, std::min(4, e ? std::atoi(e) : 2));
+    }();
+    const size_t lsz = static_cast<size_t>(std::max(1, std::min(chunk, ceil_div(ntrain, nlanes)))) * mrow * sizeof(float);
+    std::vector<std::array<DevBuf, 10>> lane_bufs(static_cast<size_t>(nlanes - 1));
+    std::vector<TLane> tlanes{TLane{ping.f(), pong.f(), t1.f(), sk.f()}};
+    for (auto& lb : lane_bufs) {
+        for (DevBuf& d : lb) d.alloc(lsz);  // ping, pong, t1, sk + planes of ping / pong / t1
+        if (tplanes)
+            for (int i = 0; i < 3; ++i) act_planes[lb[static_cast<size_t>(i)].f()] = Planes2{lb[4 + 2 * i].f(), lb[5 + 2 * i].f()};
+        tlanes.push_back(TLane{lb[0].f(), lb[1].f(), lb[2].f(), lb[3].f()});
+    }
+
     DevBuf correct(sizeof(int) * ts.size());
     int emax = 0;
     for (TaskState* s : ts) emax = std::max(emax, s->task.epochs);
@@ -1821,7 +1854,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         {
             Program P;
             if (bnd_mode)
-                add_teacher_pass_bnd(P, d_train.i(), ntrain, bkmax, bnd, chunk, ping.f(), pong.f(), t1.f(), sk.f());
+                add_teacher_pass_bnd(P, d_train.i(), ntrain, bkmax, bnd, chunk, tlanes);
             else
                 add_teacher_pass(P, d_train.i(), ntrain, sinks_for(true), chunk, ping.f(), pong.f(), t1.f(), sk.f());
             const int nb = std::min(nbr, static_cast<int>(ts.size()));
@@ -1961,7 +1994,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         if (it == graphs.end()) {
             EpochProg ep{std::make_unique<Program>(), std::make_unique<Program>()};
             if (bnd_mode) {
-                add_teacher_pass_bnd(*ep.pre, d_train.i(), ntrain, bkmax, bnd, chunk, ping.f(), pong.f(), t1.f(), sk.f());
+                add_teacher_pass_bnd(*ep.pre, d_train.i(), ntrain, bkmax, bnd, chunk, tlanes);
             } else if (!sharded) {
                 std::vector<Sink> sinks;
                 for (size_t i = 0; i < ts.size(); ++i) {
