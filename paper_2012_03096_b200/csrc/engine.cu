@@ -1432,9 +1432,12 @@ struct Engine::Impl {
 
     std::vector<TaskOutcome> run(const std::vector<DistillTask>& tasks, const std::vector<int>& train_idx,
                                  const std::vector<int>& eval_idx, const RunOptions& opt);
+    // prepare(): finishes the tasks' host candidate init and their device
+    // state (idempotent); run_group calls it as late as it can so the host RNG
+    // overlaps the first teacher pass on the GPU
     void run_group(std::vector<TaskState*>& ts, const std::vector<int>& train_idx,
                    const std::vector<int>& eval_idx, const RunOptions& opt, DevBuf& d_train,
-                   DevBuf& d_eval, DevBuf& d_iota);
+                   DevBuf& d_eval, DevBuf& d_iota, const std::function<void()>& prepare);
 };
 
 // =============================================================== run ======
@@ -1463,13 +1466,25 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
         states.push_back(std::make_unique<TaskState>());
         task_dims(*states.back(), t);
     }
-    {  // candidate inits (host RNG, bit-exact) for all tasks in parallel
-        std::vector<std::thread> pool;
-        for (auto& sp : states) pool.emplace_back([p = sp.get()] { init_task_host(*p); });
-        for (std::thread& th : pool) th.join();
-    }
-    for (size_t i = 0; i < tasks.size(); ++i) init_task(*states[i], tasks[i], ntrain, neval);
-    trace.mark("run: init tasks");
+    // candidate inits (host RNG, bit-exact) for all tasks in parallel, in the
+    // background: the first teacher pass runs on the GPU meanwhile
+    struct Pool {
+        std::vector<std::thread> th;
+        ~Pool() {
+            for (std::thread& t : th)
+                if (t.joinable()) t.join();
+        }
+    } pool;
+    for (auto& sp : states) pool.th.emplace_back([p = sp.get()] { init_task_host(*p); });
+    bool prepared = false;
+    const std::function<void()> prepare = [&] {
+        if (prepared) return;
+        for (std::thread& t : pool.th) t.join();
+        trace.mark("run: candidate init (host, overlapped)");
+        for (size_t i = 0; i < tasks.size(); ++i) init_task(*states[i], tasks[i], ntrain, neval);
+        prepared = true;
+        trace.mark("run: init tasks");
+    };
     DevBuf d_train = upload(train_idx, st), d_eval = upload(eval_idx, st);
     std::vector<int> iota(static_cast<size_t>(std::max(ntrain, neval)));
     std::iota(iota.begin(), iota.end(), 0);
@@ -1481,7 +1496,8 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
     if ((opt.virtual_shards > 1 || !opt.global_blocks.empty()) && groups.size() != 1)
         throw SpecError("sharded teacher runs need exactly one task group per rank (same batch size and "
                         "candidate depth); every rank must own at least one block");
-    for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota);
+    for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota, prepare);
+    prepare();
 
     trace.mark("run: groups done");
     // ---- read back and assemble train_block results: every task's arrays
@@ -1641,7 +1657,7 @@ __global__ void snapshot_kernel(float* dst, const float* params, size_t np, cons
 
 void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>& train_idx,
                              const std::vector<int>& eval_idx, const RunOptions& opt, DevBuf& d_train,
-                             DevBuf& d_eval, DevBuf& d_iota) {
+                             DevBuf& d_eval, DevBuf& d_iota, const std::function<void()>& prepare) {
     const int ntrain = static_cast<int>(train_idx.size());
     const int neval = static_cast<int>(eval_idx.size());
     const int B = ts[0]->task.batch_size;
@@ -1736,6 +1752,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         bnd_bufs[j].alloc(static_cast<size_t>(ntrain) * bnd_row(static_cast<int>(j)) * sizeof(float));
         bnd.push_back(bnd_bufs[j].f());
     }
+    if (!bnd_mode) prepare();  // per-task streams are sized from the task state
     for (TaskState* s : ts) {
         if (bnd_mode) {
             s->bx = bnd[static_cast<size_t>(s->k) - 1];
@@ -1844,6 +1861,12 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
 
     // ---- epoch 0: baseline losses and first evaluation
     if (opt.baseline_and_eval) {
+        if (bnd_mode) {  // the training split's teacher pass needs no task state: launch it first
+            Program P0;
+            add_teacher_pass_bnd(P0, d_train.i(), ntrain, bkmax, bnd, chunk, tlanes);
+            P0.run_concurrent(st, &side_streams);
+        }
+        prepare();
         {  // eval-split prefix activations (once per run)
             Program P;
             std::vector<Sink> sk_eval;
@@ -1853,9 +1876,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         }
         {
             Program P;
-            if (bnd_mode)
-                add_teacher_pass_bnd(P, d_train.i(), ntrain, bkmax, bnd, chunk, tlanes);
-            else
+            if (!bnd_mode)
                 add_teacher_pass(P, d_train.i(), ntrain, sinks_for(true), chunk, ping.f(), pong.f(), t1.f(), sk.f());
             const int nb = std::min(nbr, static_cast<int>(ts.size()));
             std::vector<Program*> br = nb > 1 ? P.par(nb) : std::vector<Program*>{&P};
@@ -1886,6 +1907,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     }
 
     // ---- training epochs
+    prepare();
     struct EpochProg {
         std::unique_ptr<Program> pre, post;  // teacher (+pack) | (scatter +) student steps
     };
