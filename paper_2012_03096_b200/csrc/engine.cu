@@ -1559,24 +1559,27 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
         std::vector<double> base(bp, bp + spe);
         const double best = *reinterpret_cast<const double*>(hb + rb[si].best);
         const float* fp = reinterpret_cast<const float*>(hb + rb[si].fin);
-        std::vector<float> fin(fp, fp + s.nparams + s.nstats);
         const float* sp = reinterpret_cast<const float*>(hb + rb[si].snap);
-        std::vector<float> snap(sp, sp + s.nparams + s.nstats);
-        auto to_ref_order = [&](const std::vector<float>& flat) {
-            std::vector<float> o;
+        // engine layout (dw tap-major, 16-byte padded segments) -> the
+        // reference's for_each_block_array order, written in place
+        auto to_ref_order = [&](const float* flat) {
+            size_t n = 0;
+            for (int u = 0; u < s.units; ++u) n += static_cast<size_t>(s.u[u].cin) * (9 + s.u[u].cout) + 4 * s.u[u].cout;
+            std::vector<float> o(n);
+            float* w = o.data();
             for (int u = 0; u < s.units; ++u) {
                 const int ci = s.u[u].cin, co = s.u[u].cout;
                 for (int c = 0; c < ci; ++c)
-                    for (int tap = 0; tap < 9; ++tap) o.push_back(flat[s.off_dw[u] + static_cast<size_t>(tap) * ci + c]);
-                o.insert(o.end(), flat.begin() + s.off_pw[u], flat.begin() + s.off_pw[u] + static_cast<size_t>(co) * ci);
-                o.insert(o.end(), flat.begin() + s.off_g[u], flat.begin() + s.off_g[u] + co);
-                o.insert(o.end(), flat.begin() + s.off_b[u], flat.begin() + s.off_b[u] + co);
+                    for (int tap = 0; tap < 9; ++tap) *w++ = flat[s.off_dw[u] + static_cast<size_t>(tap) * ci + c];
+                w = std::copy(flat + s.off_pw[u], flat + s.off_pw[u] + static_cast<size_t>(co) * ci, w);
+                w = std::copy(flat + s.off_g[u], flat + s.off_g[u] + co, w);
+                w = std::copy(flat + s.off_b[u], flat + s.off_b[u] + co, w);
                 const size_t st0 = s.nparams + static_cast<size_t>(u) * 2 * co;
-                o.insert(o.end(), flat.begin() + st0, flat.begin() + st0 + 2 * co);
+                w = std::copy(flat + st0, flat + st0 + 2 * co, w);
             }
             return o;
         };
-        r.final_block = to_ref_order(fin);
+        r.final_block = to_ref_order(fp);
         r.step_losses = losses;
         if (opt.baseline_and_eval) {
             // distill.cpp:166-192: mean over batches of float batch losses
@@ -1617,7 +1620,7 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
         }
         if (opt.baseline_and_eval) {
             r.best_eval = best;
-            r.best_block = to_ref_order(snap);
+            r.best_block = to_ref_order(sp);
         }
         r.wall_time_s = timing.epoch_ms_total * 1e-3;
         out.push_back(std::move(r));
