@@ -1543,10 +1543,11 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
         cp(rb[i].snap, s.snapshot.p, (s.nparams + s.nstats) * sizeof(float));
     }
     PBKD_CUDA(cudaStreamSynchronize(st));
-    std::vector<TaskOutcome> out;
-    for (size_t si = 0; si < states.size(); ++si) {
+    // per-task result assembly from the pinned buffer, tasks in parallel
+    std::vector<TaskOutcome> out(states.size());
+    auto assemble = [&](size_t si) {
         TaskState& s = *states[si];
-        TaskOutcome r;
+        TaskOutcome& r = out[si];
         r.block_index = s.k;
         r.kind = pbkd::candidate_kind_name(s.task.kind);
         const int B = s.task.batch_size;
@@ -1623,7 +1624,22 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
             r.best_block = to_ref_order(sp);
         }
         r.wall_time_s = timing.epoch_ms_total * 1e-3;
-        out.push_back(std::move(r));
+    };
+    {
+        std::vector<std::exception_ptr> err(states.size());
+        auto guarded = [&](size_t si) {
+            try {
+                assemble(si);
+            } catch (...) {
+                err[si] = std::current_exception();
+            }
+        };
+        std::vector<std::thread> th;
+        for (size_t si = 1; si < states.size(); ++si) th.emplace_back(guarded, si);
+        if (!states.empty()) guarded(0);
+        for (std::thread& t : th) t.join();
+        for (const std::exception_ptr& e : err)
+            if (e) std::rethrow_exception(e);
     }
     trace.mark("run: readback");
     return out;
