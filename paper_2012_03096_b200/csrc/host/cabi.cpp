@@ -6,6 +6,7 @@
 #include <memory>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "pbkd_b200.h"
@@ -175,11 +176,25 @@ int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec, const float* w, size_t n)
         if (n != need_n)
             throw std::invalid_argument("teacher weights: got " + std::to_string(n) + " floats, spec needs " +
                                         std::to_string(need_n));
+        // host network tensors from the caller's buffer, large tensors split
+        // over a few threads (tens of MB for VGG-16)
+        std::vector<std::pair<pbkd::Tensor*, size_t>> parts;
         size_t at = 0;
         pbkd::for_each_array(net, [&](const std::string&, pbkd::Tensor& t) {
-            std::copy(w + at, w + at + t.data.size(), t.data.begin());
+            parts.emplace_back(&t, at);
             at += t.data.size();
         });
+        const int nth = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, at >> 21)));
+        auto copy_range = [&](size_t lo, size_t hi) {  // flat element range [lo, hi)
+            for (const auto& [t, off] : parts) {
+                const size_t b = std::max(lo, off), e = std::min(hi, off + t->data.size());
+                if (b < e) std::copy(w + b, w + e, t->data.begin() + static_cast<std::ptrdiff_t>(b - off));
+            }
+        };
+        std::vector<std::thread> th;
+        for (int i = 1; i < nth; ++i) th.emplace_back(copy_range, at * i / nth, at * (i + 1) / nth);
+        copy_range(0, at / nth);
+        for (std::thread& x : th) x.join();
         ctx->eng->set_teacher(std::move(net), w, n);  // device copy straight from the caller's buffer
         ctx->spec = spec;
     });
