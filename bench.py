@@ -1,13 +1,19 @@
 """Benchmark: distillation samples/sec (all blocks), VGG-16 teacher, CIFAR-10
 shape synthetic data (BASELINE.json configs[1]).
 
-One bench step = one training epoch of blockwise distillation: the teacher
-forward over the training split (boundary activations streamed into every
-block's epoch order) plus ceil(N_train/B) optimizer steps of EVERY student
-block.  samples/s = N_train * K / T over K timed epochs; N GPUs split the
-blocks by WFD (strong scaling: total work fixed).
+One bench step = one training epoch of blockwise distillation:
+ceil(N_train/B) optimizer steps of EVERY student block.  The timed region is
+one run of K epochs (the reference's DistillTask default is 30, distill.hpp)
+INCLUDING the run's one-time teacher forward over the training split, whose
+boundary activations every epoch then reads (inference-mode BN makes them
+epoch-invariant); samples/s = N_train * K / T.  W warm-up epochs run first as
+a separate run.  N GPUs split the blocks by WFD (strong scaling: total work
+fixed).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+With --gpus N > 1 and no torchrun environment, bench.py launches the N ranks
+itself (python -m torch.distributed.run, one process per GPU).
 """
 import argparse
 import concurrent.futures as cf
@@ -32,7 +38,7 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="vgg16", choices=sorted(CONFIGS))
@@ -44,12 +50,15 @@ def parse():
 
 
 def workload(cfg, n, P):
+    """P: the product package, or (reference arm) the CPU reference's oracle
+    front end -- both expose mix_seed / stratified_split with the reference's
+    bit-exact semantics."""
     spec = open(os.path.join(ROOT, "configs", CONFIGS[cfg] + ".json")).read()
     classes = 100 if cfg == "resnet34" else 10
     images = np.random.default_rng(2012).random((n, 3, 32, 32), dtype=np.float32)
     labels = (np.arange(n) % classes).astype(np.int32)
     tr, ev = P.stratified_split(labels, 0.1, P.mix_seed(42, 0x5711))
-    nb = P.spec_num_blocks(spec)
+    nb = P.spec_num_blocks(spec) if hasattr(P, "spec_num_blocks") else P.teacher_num_blocks(spec)
     # every conv block of these configs is replaceable (identify_replaceable)
     blocks = list(range(1, nb + 1))
     return spec, classes, images, labels, tr, ev, blocks
@@ -107,17 +116,17 @@ def cpu_reference_step(O, spec, tw, images, labels, tr, ev, blocks, batch, seed_
     return time.perf_counter() - t0
 
 
-def calibrate(ctx, P, blocks, tr, ev, B):
-    """Per-block student epoch time (each block alone, teacher part subtracted)
-    and the all-block teacher forward time per epoch, in ms (1 GPU)."""
+def calibrate(ctx, P, blocks, tr, ev, B, epochs):
+    """Per-block student time of `epochs` epochs (each block alone, epochs >= 2
+    timed so the one-time teacher pass is excluded, scaled to `epochs`) and the
+    all-block one-time teacher pass, in ms (1 GPU)."""
     s_ms = {}
     for k in blocks:
-        t = [P.make_task(k, epochs=2, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B)]
+        t = [P.make_task(k, epochs=3, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B)]
         r = ctx.run(t, tr, ev, flags=P.RUN_STEP_ONLY, timed_from_epoch=2)
-        s_ms[k] = max(1e-3, r["timed_ms"] - r["teacher_ms"])
-    t = [P.make_task(k, epochs=2, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B) for k in blocks]
-    r = ctx.run(t, tr, ev, flags=P.RUN_STEP_ONLY, timed_from_epoch=2,
-                global_blocks=[(k, 0) for k in blocks])
+        s_ms[k] = max(1e-3, r["timed_ms"] / 2 * epochs)
+    t = [P.make_task(k, epochs=1, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B) for k in blocks]
+    r = ctx.run(t, tr, ev, flags=P.RUN_STEP_ONLY, global_blocks=[(k, 0) for k in blocks])
     return s_ms, r["teacher_ms"]
 
 
@@ -135,14 +144,25 @@ def water_fill(load, teacher_ms):
     return [v / s for v in x]
 
 
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle/_ref built from the
-    reference sources; the restatement if that build is absent)."""
-    import paper_2012_03096_b200 as P
+    reference sources; the restatement if that build is absent).  The product
+    package is NOT imported here: split and seeds come from the reference's
+    own library through the oracle front end."""
     from oracle import oracle as OR
     kind = "reference" if OR.available("ref") else "port"
     O = OR.Oracle("ref" if kind == "reference" else "orc")
-    spec, classes, images, labels, tr, ev, blocks = workload(args.config, args.dataset_size, P)
+    spec, classes, images, labels, tr, ev, blocks = workload(args.config, args.dataset_size, O)
     tw = O.teacher_init(spec, O.mix_seed(42, 0x7E11))
     threads = os.cpu_count() or 1
     bsz = args.batch  # same batch as the GPU arm: one optimizer step of every block
@@ -162,15 +182,31 @@ def run_reference(args):
             "config": {"workload": f"{CONFIGS[args.config]}: {len(blocks)} blocks, batch {bsz}, "
                                    f"dataset {args.dataset_size}, CPU reference step-only"},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def launch_ranks(args):
+    """--gpus N > 1 outside torchrun: one process per GPU on this node."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        launch_ranks(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and args.impl == "ours":
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         if rank == 0:
@@ -203,29 +239,38 @@ def main():
         # block -> GPU: WFD (scheduler.cpp:57-81) over MEASURED per-block student
         # epoch times, teacher shards sized to fill the imbalance (rank 0
         # calibrates, everyone gets the same numbers)
-        cal = [calibrate(ctx, P, blocks, tr, ev, B) if rank == 0 else None]
+        cal = [calibrate(ctx, P, blocks, tr, ev, B, K) if rank == 0 else None]
         dist.broadcast_object_list(cal, src=0)
         s_ms, t_ms_all = cal[0]
         plan, _ = P.wfd_bin_pack(blocks, [s_ms[k] for k in blocks], world)
         load = [sum(s_ms[k] for k in q) for q in plan]
         share = water_fill(load, t_ms_all)
-        weights_src = "measured student epoch ms " + json.dumps({k: round(v, 3) for k, v in s_ms.items()}) + \
-            f"; teacher {t_ms_all:.3f} ms/epoch; teacher shares {[round(x, 4) for x in share]}"
+        weights_src = f"measured student ms per {K} epochs " + json.dumps({k: round(v, 3) for k, v in s_ms.items()}) + \
+            f"; one-time teacher pass {t_ms_all:.3f} ms; teacher shares {[round(x, 4) for x in share]}"
     mine = sorted(plan[rank])
     owner = {k: r for r, q in enumerate(plan) for k in q}
-    tasks = [P.make_task(k, epochs=W + K, eval_every=10 ** 6, seed=P.mix_seed(42, k), batch_size=B,
-                         lr=0.05, momentum=0.9) for k in mine]
+    tasks = lambda e: [P.make_task(k, epochs=e, eval_every=10 ** 6, seed=P.mix_seed(42, k),  # noqa: E731
+                                   batch_size=B, lr=0.05, momentum=0.9) for k in mine]
+    gblocks = [(k, owner[k]) for k in blocks]
 
-    # ---------------- value: inputs resident in HBM, K timed epochs ----------
+    # ---------------- value: inputs resident in HBM, one run of K epochs ----
+    # warm-up: a separate run of W epochs (same shapes, same code path)
+    if W > 0:
+        if world == 1:
+            ctx.run(tasks(W), tr, ev, flags=P.RUN_STEP_ONLY)
+        else:
+            ctx.run(tasks(W), tr, ev, flags=P.RUN_STEP_ONLY, global_blocks=gblocks, share=share)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clk = Clocks(dev)
+    # timed: device events from before the one-time teacher pass (+ exchange)
+    # to the end of epoch K (timed_from_epoch=1)
     if world == 1:
-        res = ctx.run(tasks, tr, ev, flags=P.RUN_STEP_ONLY | P.RUN_PROFILE, timed_from_epoch=W + 1)
+        res = ctx.run(tasks(K), tr, ev, flags=P.RUN_STEP_ONLY | P.RUN_PROFILE, timed_from_epoch=1)
     else:
-        res = ctx.run(tasks, tr, ev, flags=P.RUN_STEP_ONLY | P.RUN_PROFILE, timed_from_epoch=W + 1,
-                      global_blocks=[(k, owner[k]) for k in blocks], share=share)
+        res = ctx.run(tasks(K), tr, ev, flags=P.RUN_STEP_ONLY | P.RUN_PROFILE, timed_from_epoch=1,
+                      global_blocks=gblocks, share=share)
     torch.cuda.synchronize()
     clocks = clk.stop()
     if dist:
@@ -284,8 +329,9 @@ def main():
                 "peak_source": ("MEASURED_PEAKS.json " + ("bf16_tflops/2/3 (3xTF32 fp32-equivalent roof)"
                                                           if kd["bound"] == "tensor" else "hbm_gbs"))
                 if peaks else "fallback (B200_PROFILING.md)",
-                "measured": "CUDA events per launch over one epoch of the bench workload (eager replay after "
-                            "the timed region); algorithmic bytes/flops per SURVEY 8d",
+                "measured": "CUDA events per launch over one epoch of the bench workload plus the one-time "
+                            "teacher pass (eager replay after the timed region, training state restored); "
+                            "algorithmic bytes/flops per SURVEY 8d",
                 "all_kernels": kernels}
 
     # ---------------- e2e: public API, host buffers, H2D+D2H inside ---------
@@ -337,6 +383,7 @@ def main():
         T = cpu_reference_step(O, spec, tw, images, labels, tr, ev, blocks, bsz,
                                lambda k: P.mix_seed(42, k), threads)
         cpu = {"value": bsz / T, "unit": "samples/s", "cores": threads, "kind": kind,
+               "cpu_model": cpu_model(),
                "sample": f"1 optimizer step of all {len(blocks)} blocks at batch {bsz} "
                          f"({T:.1f} s wall, train_block loop body, {threads} threads)"}
 
@@ -349,13 +396,14 @@ def main():
                     "init_weights(mix_seed(42,0x7e11)))",
             "config": {"workload": f"{CONFIGS[args.config]}: all {len(blocks)} blocks distilled, "
                                    f"TwoLayer students, batch {B}, dataset {args.dataset_size} "
-                                   f"({n_train} train), 1 step = 1 epoch (teacher forward over the "
-                                   f"train split + {-(-n_train // B)} optimizer steps per block)",
+                                   f"({n_train} train), 1 step = 1 epoch ({-(-n_train // B)} optimizer "
+                                   f"steps per block); the timed run of {K} epochs includes its one-time "
+                                   f"teacher forward over the train split",
                        "plan": plan,
                        "parallelism": f"blocks over {world} GPU(s) by WFD; teacher forward sample-sharded "
                                       "with NCCL all-to-all-v of boundary activations" if world > 1 else
                                       "1 GPU: all blocks grouped",
-                       "weights": weights_src, "teacher_ms_per_epoch": res["teacher_ms"] / max(1, K),
+                       "weights": weights_src, "teacher_ms_once": res["teacher_ms"],
                        "l2": "inputs larger than L2: each epoch streams every block's boundary "
                              "activations (~2.2 MB/sample for VGG-16, GBs per epoch) through HBM"},
             "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -183,22 +183,27 @@ int pbkd_bench_kernel(pbkd_ctx* ctx, int which, int batch, int iters, double* ms
 /* ---- multi-GPU: sample-sharded teacher + NCCL exchange ------------------ */
 /* Rank 0 creates the 128-byte NCCL id; the launcher broadcasts it; every rank
  * joins.  pbkd_run_sharded then trains the given (local) tasks while this
- * rank runs the teacher forward on its shard of the training split for every
- * block listed in g_blocks (owner g_owner) and exchanges boundary rows with
- * grouped ncclSend/ncclRecv.  virtual_shards > 1 on one GPU runs the same
- * pack/scatter path with local shards; share weights the teacher shards. */
+ * rank runs the teacher forward once on its shard of the training split for
+ * every boundary the blocks in g_blocks (owner g_owner) read, and receives
+ * the other shards' rows of the boundaries its own blocks read in one
+ * grouped ncclSend/ncclRecv round per run.  virtual_shards > 1 on one GPU
+ * computes the boundaries shard by shard; share weights the teacher shards. */
 int pbkd_nccl_unique_id(char* out128);
 int pbkd_ctx_set_comm(pbkd_ctx* ctx, const char* id128, int rank, int world);
 int pbkd_run_sharded(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const int* train_idx,
                      int n_train, const int* eval_idx, int n_eval, int flags, int timed_from_epoch,
                      const int* g_blocks, const int* g_owner, int n_global, int virtual_shards,
                      const double* share, int n_share, pbkd_results** out);
-/* Host-side exchange layout (what rank src sends rank dst), identical on all
- * ranks; exposed for the multi-process plan tests. */
-int pbkd_exchange_plan(const int* blocks, const int* owners, int nb, const long long* in_row,
-                       const long long* out_row, int world, int n_train, const double* share,
-                       int src, int dst, size_t* count, size_t* off_in, size_t* off_tgt,
-                       int* shard_begin);
+/* Host-side boundary exchange layout (BoundaryPlan, identical on all ranks):
+ * blocks / owners: every distilled block and its owner rank; rows: floats per
+ * sample of boundaries 0..max(blocks) (n_rows entries).  What rank src sends
+ * rank dst once per run, in issue order: boundary xj[i], first train row
+ * xrow0[i], xrows[i] rows (cap entries, *n written); *count = floats;
+ * shard_begin receives the world+1 shard bounds.  Exposed for the
+ * multi-process plan tests. */
+int pbkd_exchange_plan(const int* blocks, const int* owners, int nb, const long long* rows, int n_rows,
+                       int world, int n_train, const double* share, int src, int dst, size_t* count,
+                       int* xj, int* xrow0, int* xrows, int cap, int* n, int* shard_begin);
 
 /* ---- inference ----------------------------------------------------------- */
 int pbkd_prefix_infer(pbkd_ctx* ctx, const float* x, int n, int k, int inclusive, float* out,

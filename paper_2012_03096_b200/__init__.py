@@ -108,8 +108,9 @@ def lib() -> C.CDLL:
             "pbkd_ctx_set_comm": (C.c_int, [vp, vp, C.c_int, C.c_int]),
             "pbkd_run_sharded": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int,
                                            vp, vp, C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),
-            "pbkd_exchange_plan": (C.c_int, [vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, vp, C.c_int,
-                                             C.c_int, C.POINTER(C.c_size_t), vp, vp, vp]),
+            "pbkd_exchange_plan": (C.c_int, [vp, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp,
+                                             C.c_int, C.c_int, C.POINTER(C.c_size_t), vp, vp, vp,
+                                             C.c_int, ip, vp]),
             "pbkd_prefix_infer": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_size_t, vp]),
             "pbkd_candidate_infer": (C.c_int, [vp] + [C.c_int] * 4 + [vp, vp] + [C.c_int] * 3 +
                                      [vp, C.c_size_t]),
@@ -241,19 +242,21 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def exchange_plan(blocks, owners, in_row, out_row, world, n_train, src, dst, share=None):
-    """What rank `src` sends rank `dst` (count, per-block in/tgt offsets, shard bounds)."""
+def exchange_plan(blocks, owners, rows, world, n_train, src, dst, share=None):
+    """Boundary rows rank `src` sends rank `dst` once per run (BoundaryPlan):
+    (count in floats, [(boundary j, first train row, rows)], shard bounds)."""
     nb = len(blocks)
     b, o = _i32(blocks), _i32(owners)
-    ir, orow = np.ascontiguousarray(in_row, np.int64), np.ascontiguousarray(out_row, np.int64)
+    r = np.ascontiguousarray(rows, np.int64)
     sh = np.ascontiguousarray(share, np.float64) if share is not None else None
-    cnt = C.c_size_t()
-    oi, ot = np.zeros(nb, np.uint64), np.zeros(nb, np.uint64)
+    cnt, n = C.c_size_t(), C.c_int()
+    cap = len(rows) + 1
+    xj, x0, xr = np.zeros(cap, np.int32), np.zeros(cap, np.int32), np.zeros(cap, np.int32)
     sbd = np.zeros(world + 1, np.int32)
-    check(lib().pbkd_exchange_plan(_ptr(b), _ptr(o), nb, _ptr(ir), _ptr(orow), world, n_train,
+    check(lib().pbkd_exchange_plan(_ptr(b), _ptr(o), nb, _ptr(r), len(r), world, n_train,
                                    _ptr(sh) if sh is not None else None, src, dst, C.byref(cnt),
-                                   _ptr(oi), _ptr(ot), _ptr(sbd)))
-    return cnt.value, oi, ot, sbd
+                                   _ptr(xj), _ptr(x0), _ptr(xr), cap, C.byref(n), _ptr(sbd)))
+    return cnt.value, [(int(xj[i]), int(x0[i]), int(xr[i])) for i in range(n.value)], sbd
 
 
 def save_student_network(spec, teacher_weights, block_index, kind, block_weights, path):

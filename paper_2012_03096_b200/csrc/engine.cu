@@ -531,11 +531,11 @@ struct TaskState {
     size_t nparams = 0, nstats = 0;
     size_t off_dw[kMaxUnits], off_pw[kMaxUnits], off_g[kMaxUnits], off_b[kMaxUnits];
     DevBuf params, grads, vel, mstats, snapshot;
-    // streams
-    DevBuf in_stream, tgt_stream, pos, eval_in;
-    // boundary-buffer mode (single GPU): teacher boundaries k-1 / k for all
-    // training samples in train order, read through the epoch order in pos
-    // (pos[slot] = train row); the streams above are not allocated then
+    // pos: this epoch's order (slot -> train row); eval_in: the eval split's
+    // boundary k-1 (once per run)
+    DevBuf pos, eval_in;
+    // the run's teacher boundaries k-1 / k for all training samples in train
+    // order, read through pos
     const float* bx = nullptr;
     const float* bt = nullptr;
     int nsrc = 0;
@@ -892,9 +892,7 @@ struct Engine::Impl {
 
     void init_task_device(TaskState& s, int B, int ho, int wo, const TBlockDev& tb, int ntrain, int neval,
                           long long total, int spe) {
-        // streams and workspace
-        // in_stream / tgt_stream: allocated by run_group when the run needs
-        // them (sample-sharded teacher); pos: epoch positions or order
+        // epoch order and workspace
         s.pos.alloc(static_cast<size_t>(ntrain) * sizeof(int));
         s.eval_in.alloc(static_cast<size_t>(std::max(neval, 1)) * s.in_row * sizeof(float));
         const long long M = static_cast<long long>(B) * ho * wo;
@@ -969,12 +967,10 @@ struct Engine::Impl {
             TaskState* s = act[i];
             const int B = s->task.batch_size;
             const int n = std::min(B, ntrain - step * B);
-            const bool bm = s->bx != nullptr;
-            Ctx c{s, n, static_cast<long long>(n) * s->u[0].ho * s->u[0].wo,
-                  bm ? s->bx : s->in_stream.f() + static_cast<size_t>(step) * B * s->in_row,
-                  bm ? s->bt : s->tgt_stream.f() + static_cast<size_t>(step) * B * s->out_row,
+            if (!s->bx) throw std::logic_error("student step recorded without teacher boundaries");
+            Ctx c{s, n, static_cast<long long>(n) * s->u[0].ho * s->u[0].wo, s->bx, s->bt,
                   knockouts().empty() ? s->failed.i() : nullptr, gsteps[i],
-                  bm ? s->pos.i() + static_cast<size_t>(step) * B : nullptr};
+                  s->pos.i() + static_cast<size_t>(step) * B};
             cx.push_back(c);
         }
         // ---- forward
@@ -1292,10 +1288,9 @@ struct Engine::Impl {
         const int* pos;
         int width;
     };
-    // Boundary mode: the teacher writes every boundary 0..kmax of the samples
-    // at d_idx into bnd[j] (rows in d_idx order; bnd[0] = the NHWC images);
-    // students read them through their epoch order, so nothing is scattered.
-    // Block j's output planes alternate between the pong / ping plane pairs.
+    // Teacher boundaries: boundary j of training row t lives at bnd[j] + t *
+    // bnd_row(j) (bnd[0] = the NHWC images, gathered for every row first).
+    // The pass runs teacher blocks 1..kmax over training rows [r0, r1).
     int bnd_row(int j) const {
         if (j == 0) return net.in_c * net.in_h * net.in_w;
         const TBlockDev& b = tblocks[static_cast<size_t>(j) - 1];
@@ -1303,29 +1298,27 @@ struct Engine::Impl {
     }
     // A teacher lane: the activation buffers one chain of teacher blocks
     // uses (their registered tf32 planes; t1 / sk: residual-block scratch).
+    // Block j's output planes alternate between the pong / ping plane pairs.
     struct TLane {
         const float *ping, *pong;
         float *t1, *sk;
     };
-    // Several lanes split the samples and run as a parallel section: a conv
-    // of one lane fills the last-wave tail of the other lane's conv.
-    void add_teacher_pass_bnd(Program& P, const int* d_idx, int n, int kmax, const std::vector<float*>& bnd,
-                              int chunk, const std::vector<TLane>& lanes) {
+    // Several lanes split the rows and run as a parallel section: a conv of
+    // one lane fills the last-wave tail of the other lane's conv.
+    void add_teacher_pass_bnd(Program& P, int r0, int r1, int kmax, const std::vector<float*>& bnd, int chunk,
+                              const std::vector<TLane>& lanes) {
+        const int n = r1 - r0;
+        if (n <= 0 || kmax < 1) return;
         const int L = std::max(1, std::min(static_cast<int>(lanes.size()), n));
         std::vector<Program*> br = L > 1 ? P.par(L) : std::vector<Program*>{&P};
         for (int l = 0; l < L; ++l) {
             Program& Q = *br[static_cast<size_t>(l)];
             const TLane& ln = lanes[static_cast<size_t>(l)];
             const Planes2 pp = planes_for(ln.ping), qp = planes_for(ln.pong);
-            const int b0 = static_cast<int>(static_cast<long long>(n) * l / L);
-            const int b1 = static_cast<int>(static_cast<long long>(n) * (l + 1) / L);
+            const int b0 = r0 + static_cast<int>(static_cast<long long>(n) * l / L);
+            const int b1 = r0 + static_cast<int>(static_cast<long long>(n) * (l + 1) / L);
             for (int t0 = b0; t0 < b1; t0 += chunk) {
                 const int nc = std::min(chunk, b1 - t0);
-                const int* idx = d_idx + t0;
-                float* x0 = bnd[0] + static_cast<size_t>(t0) * bnd_row(0);
-                const float* img = images.f();
-                const int in_c = net.in_c, in_h = net.in_h, in_w = net.in_w;
-                Q.raw([=](cudaStream_t s) { launch_gather_nhwc(img, idx, nc, in_c, in_h, in_w, x0, s); });
                 for (int j = 0; j < kmax; ++j) {
                     float* x = bnd[static_cast<size_t>(j)] + static_cast<size_t>(t0) * bnd_row(j);
                     float* y = bnd[static_cast<size_t>(j) + 1] + static_cast<size_t>(t0) * bnd_row(j + 1);
@@ -1432,12 +1425,92 @@ struct Engine::Impl {
 
     std::vector<TaskOutcome> run(const std::vector<DistillTask>& tasks, const std::vector<int>& train_idx,
                                  const std::vector<int>& eval_idx, const RunOptions& opt);
-    // prepare(): finishes the tasks' host candidate init and their device
-    // state (idempotent); run_group calls it as late as it can so the host RNG
-    // overlaps the first teacher pass on the GPU
+
+    // Teacher boundaries of one run (see run()): buffers, the exchange plan
+    // and whether the one-time teacher pass has been issued.
+    struct Boundaries {
+        std::vector<DevBuf> bufs;
+        std::vector<float*> bnd;  // bnd[j], j = 0..kmax, [ntrain][bnd_row(j)]
+        BoundaryPlan plan;
+        int kmax = 0, me = 0, world = 1, chunk = 1;
+        bool done = false;
+        cudaEvent_t t0 = nullptr, t1 = nullptr;  // around the teacher pass + exchange
+        ~Boundaries() {
+            if (t0) cudaEventDestroy(t0);
+            if (t1) cudaEventDestroy(t1);
+        }
+    };
+    // Working buffers of the boundary pass: one TLane per teacher lane with
+    // its registered tf32 planes (unregistered on destruction).
+    struct TeacherWs {
+        Impl& m;
+        std::vector<std::array<DevBuf, 10>> bufs;
+        std::vector<TLane> lanes;
+        TeacherWs(Impl& im, size_t bytes, int nlanes) : m(im), bufs(static_cast<size_t>(nlanes)) {
+            const bool tplanes = gemm_presplit_ok(32);
+            for (auto& lb : bufs) {
+                for (DevBuf& d : lb) d.alloc(bytes);  // ping, pong, t1, sk + planes of ping / pong / t1
+                if (tplanes)
+                    for (int i = 0; i < 3; ++i) m.act_planes[lb[static_cast<size_t>(i)].f()] = Planes2{lb[4 + 2 * i].f(), lb[5 + 2 * i].f()};
+                lanes.push_back(TLane{lb[0].f(), lb[1].f(), lb[2].f(), lb[3].f()});
+            }
+        }
+        ~TeacherWs() {
+            for (auto& lb : bufs)
+                for (int i = 0; i < 3; ++i) m.act_planes.erase(lb[static_cast<size_t>(i)].f());
+        }
+    };
+    // The boundary pass of this rank (images of every training row into
+    // boundary 0, teacher blocks 1..kmax over its shard -- every virtual
+    // shard on one GPU) recorded into P.
+    void record_boundary_pass(Program& P, Boundaries& b, const DevBuf& d_train, int ntrain, const TeacherWs& ws) {
+        const float* img = images.f();
+        const int* idx = d_train.i();
+        float* x0 = b.bnd[0];
+        const int in_c = net.in_c, in_h = net.in_h, in_w = net.in_w;
+        P.raw([=](cudaStream_t s2) { launch_gather_nhwc(img, idx, ntrain, in_c, in_h, in_w, x0, s2); }, "GatherOp",
+              8.0 * ntrain * in_c * in_h * in_w);
+        const std::vector<int>& sb = b.plan.shard_begin;
+        std::vector<const float*> added;
+        for (int sh = 0; sh < b.plan.world; ++sh) {
+            if (b.world > 1 && sh != b.me) continue;
+            add_teacher_pass_bnd(P, sb[static_cast<size_t>(sh)], sb[static_cast<size_t>(sh) + 1], b.kmax, b.bnd,
+                                 b.chunk, ws.lanes);
+        }
+        // the boundary rows' plane registrations were only needed while recording
+        for (size_t j = 1; j < b.bnd.size(); ++j)
+            for (auto it = act_planes.begin(); it != act_planes.end();) {
+                const float* q = it->first;
+                const bool in_j = q >= b.bnd[j] && q < b.bnd[j] + static_cast<size_t>(ntrain) * bnd_row(static_cast<int>(j));
+                it = in_j ? act_planes.erase(it) : std::next(it);
+            }
+    }
+    // Issues the one-time teacher pass (+ NCCL exchange) unless already done.
+    void ensure_boundaries(Boundaries& b, const DevBuf& d_train, int ntrain, bool use_side) {
+        if (b.done) return;
+        b.done = true;
+        PBKD_CUDA(cudaEventRecord(b.t0, st));
+        {
+            TeacherWs ws(*this, static_cast<size_t>(std::max(1, std::min(b.chunk, ntrain))) * max_row() * sizeof(float),
+                         teacher_lanes());
+            Program P;
+            record_boundary_pass(P, b, d_train, ntrain, ws);
+            if (use_side)
+                P.run_concurrent(st, &side_streams);
+            else
+                P.run(st);
+        }
+        if (b.world > 1) comm->exchange(b.plan, b.bnd, st);  // boundary rows to the blocks that read them
+        PBKD_CUDA(cudaEventRecord(b.t1, st));
+        trace.mark("run: teacher boundaries");
+    }
+    static int teacher_lanes() {  // PBKD_TEACHER_LANES, default 2
+        const char* e = std::getenv("PBKD_TEACHER_LANES");
+        return std::max(1, std::min(4, e ? std::atoi(e) : 2));
+    }
     void run_group(std::vector<TaskState*>& ts, const std::vector<int>& train_idx,
                    const std::vector<int>& eval_idx, const RunOptions& opt, DevBuf& d_train,
-                   DevBuf& d_eval, DevBuf& d_iota, const std::function<void()>& prepare);
+                   DevBuf& d_eval, DevBuf& d_iota, Boundaries& bd, const std::function<void()>& prepare);
 };
 
 // =============================================================== run ======
@@ -1493,11 +1566,71 @@ std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks
     std::map<std::pair<int, int>, std::vector<TaskState*>> groups;
     for (auto& s : states) groups[{s->task.batch_size, s->units}].push_back(s.get());
     timing = RunTiming{};
-    if ((opt.virtual_shards > 1 || !opt.global_blocks.empty()) && groups.size() != 1)
-        throw SpecError("sharded teacher runs need exactly one task group per rank (same batch size and "
-                        "candidate depth); every rank must own at least one block");
-    for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota, prepare);
+
+    // Teacher boundaries.  Inference-mode BN makes the teacher
+    // per-sample and epoch-invariant (model.cpp:553-557), so every boundary
+    // 0..kmax of the whole training split is computed ONCE per run and kept
+    // in HBM in train order; the student kernels read their batches through
+    // each block's epoch order (slot -> train row), so gather_batch /
+    // make_batches (dataset.cpp:166-185, distill.cpp:22-30) become an index
+    // array and nothing is scattered.  Multi-GPU: each rank computes the rows
+    // of its shard of the training split and one grouped NCCL send/recv round
+    // per run delivers the rows its blocks read (BoundaryPlan, comm.cpp).
+    Boundaries bd;
+    {
+        const bool multi = comm && !opt.global_blocks.empty();
+        bd.world = multi ? comm->world() : 1;
+        bd.me = multi ? comm->rank() : 0;
+        std::vector<std::pair<int, int>> gb = opt.global_blocks;
+        if (gb.empty())
+            for (auto& sp : states) gb.push_back({sp->k, bd.me});
+        std::sort(gb.begin(), gb.end());
+        std::vector<int> gblocks, gowners;
+        for (const auto& [k, o] : gb) {
+            if (k < 1 || k > static_cast<int>(tblocks.size()))
+                throw SpecError("global block " + std::to_string(k) + " out of range");
+            gblocks.push_back(k);
+            gowners.push_back(o);
+            bd.kmax = std::max(bd.kmax, k);
+        }
+        for (auto& sp : states)
+            if (std::find(gb.begin(), gb.end(), std::make_pair(sp->k, bd.me)) == gb.end())
+                throw std::logic_error("sharded run: local task not owned by this rank in global_blocks");
+        std::vector<long long> rows;
+        for (int j = 0; j <= bd.kmax; ++j) rows.push_back(bnd_row(j));
+        const int nshards = bd.world > 1 ? bd.world : std::max(1, opt.virtual_shards);
+        bd.plan = make_boundary_plan(gblocks, gowners, rows, nshards, ntrain, opt.shard_share);
+        bd.chunk = std::max(1, std::min(ntrain, static_cast<int>((size_t(256) << 20) / (size_t(max_row()) * 4))));
+        bd.bufs.resize(static_cast<size_t>(bd.kmax) + 1);
+        for (int j = 0; j <= bd.kmax; ++j) {
+            bd.bufs[static_cast<size_t>(j)].alloc(static_cast<size_t>(ntrain) * bnd_row(j) * sizeof(float));
+            bd.bnd.push_back(bd.bufs[static_cast<size_t>(j)].f());
+        }
+        PBKD_CUDA(cudaEventCreate(&bd.t0));
+        PBKD_CUDA(cudaEventCreate(&bd.t1));
+        for (auto& sp : states) {
+            sp->bx = bd.bnd[static_cast<size_t>(sp->k) - 1];
+            sp->bt = bd.bnd[static_cast<size_t>(sp->k)];
+            sp->nsrc = ntrain;
+        }
+    }
+    for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota, bd, prepare);
+    // a rank without local blocks still owes its shard to the others
+    ensure_boundaries(bd, d_train, ntrain, true);
     prepare();
+    {
+        float ms = 0.0f;
+        PBKD_CUDA(cudaEventSynchronize(bd.t1));
+        PBKD_CUDA(cudaEventElapsedTime(&ms, bd.t0, bd.t1));
+        timing.teacher_ms = ms;
+    }
+    if (opt.profile) {  // the boundary pass once more, per launch (idempotent: same rows)
+        TeacherWs ws(*this, static_cast<size_t>(std::max(1, std::min(bd.chunk, ntrain))) * max_row() * sizeof(float), 1);
+        Program P;
+        record_boundary_pass(P, bd, d_train, ntrain, ws);
+        P.run_profiled(st, timing.prof);
+    }
+    for (auto& sp : states) sp->bx = sp->bt = nullptr;
 
     trace.mark("run: groups done");
     // ---- read back and assemble train_block results: every task's arrays
@@ -1676,7 +1809,8 @@ __global__ void snapshot_kernel(float* dst, const float* params, size_t np, cons
 
 void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>& train_idx,
                              const std::vector<int>& eval_idx, const RunOptions& opt, DevBuf& d_train,
-                             DevBuf& d_eval, DevBuf& d_iota, const std::function<void()>& prepare) {
+                             DevBuf& d_eval, DevBuf& d_iota, Boundaries& bd,
+                             const std::function<void()>& prepare) {
     const int ntrain = static_cast<int>(train_idx.size());
     const int neval = static_cast<int>(eval_idx.size());
     const int B = ts[0]->task.batch_size;
@@ -1734,71 +1868,9 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         return WsPtrs{w.ia.f(), w.ib.f(), w.io.f(), w.ping.f(), w.pong.f(), w.t1.f(), w.sk.f()};
     };
 
-    // teacher lanes of the training-split pass (PBKD_TEACHER_LANES, default 2):
-    // lane 0 uses the group's buffers, the others their own planes / scratch
-    const int nlanes = [&] {
-        const char* e = std::getenv("PBKD_TEACHER_LANES");
-        return std::max(1, std::min(4, e ? std::atoi(e) : 2));
-    }();
-    const size_t lsz = static_cast<size_t>(std::max(1, std::min(chunk, ceil_div(ntrain, nlanes)))) * mrow * sizeof(float);
-    std::vector<std::array<DevBuf, 10>> lane_bufs(static_cast<size_t>(nlanes - 1));
-    std::vector<TLane> tlanes{TLane{ping.f(), pong.f(), t1.f(), sk.f()}};
-    for (auto& lb : lane_bufs) {
-        for (DevBuf& d : lb) d.alloc(lsz);  // ping, pong, t1, sk + planes of ping / pong / t1
-        if (tplanes)
-            for (int i = 0; i < 3; ++i) act_planes[lb[static_cast<size_t>(i)].f()] = Planes2{lb[4 + 2 * i].f(), lb[5 + 2 * i].f()};
-        tlanes.push_back(TLane{lb[0].f(), lb[1].f(), lb[2].f(), lb[3].f()});
-    }
-
     DevBuf correct(sizeof(int) * ts.size());
     int emax = 0;
     for (TaskState* s : ts) emax = std::max(emax, s->task.epochs);
-
-    // Boundary mode (one GPU, no sample-sharded teacher): every teacher
-    // boundary of the training split lives once in HBM in train order and
-    // the student kernels gather their batches through the epoch order (no
-    // per-epoch scatter into per-task streams).  PBKD_STREAMS=1 forces the
-    // stream + scatter path the sharded runs use.
-    const bool bnd_mode = opt.virtual_shards <= 1 && opt.global_blocks.empty() && [] {
-        const char* e = std::getenv("PBKD_STREAMS");
-        return !(e && e[0] == '1');
-    }();
-    int bkmax = 0;
-    for (TaskState* s : ts) bkmax = std::max(bkmax, s->k);
-    std::vector<DevBuf> bnd_bufs(bnd_mode ? static_cast<size_t>(bkmax) + 1 : 0);
-    std::vector<float*> bnd;
-    for (size_t j = 0; j < bnd_bufs.size(); ++j) {
-        bnd_bufs[j].alloc(static_cast<size_t>(ntrain) * bnd_row(static_cast<int>(j)) * sizeof(float));
-        bnd.push_back(bnd_bufs[j].f());
-    }
-    if (!bnd_mode) prepare();  // per-task streams are sized from the task state
-    for (TaskState* s : ts) {
-        if (bnd_mode) {
-            s->bx = bnd[static_cast<size_t>(s->k) - 1];
-            s->bt = bnd[static_cast<size_t>(s->k)];
-            s->nsrc = ntrain;
-        } else {
-            s->bx = s->bt = nullptr;
-            s->in_stream.alloc(static_cast<size_t>(ntrain) * s->in_row * sizeof(float));
-            s->tgt_stream.alloc(static_cast<size_t>(ntrain) * s->out_row * sizeof(float));
-        }
-    }
-    struct BndReset {  // the task states outlive this group's boundary buffers
-        std::vector<TaskState*>& v;
-        ~BndReset() {
-            for (TaskState* s : v) s->bx = s->bt = nullptr;
-        }
-    } bnd_reset{ts};
-
-    auto sinks_for = [&](bool identity) {
-        std::vector<Sink> v;
-        for (TaskState* s : ts) {
-            const int* pos = identity ? d_iota.i() : s->pos.i();
-            v.push_back({s->k - 1, s->in_stream.f(), pos, s->in_row});
-            v.push_back({s->k, s->tgt_stream.f(), pos, s->out_row});
-        }
-        return v;
-    };
 
     // Evaluation programs are identical from one eval to the next (the
     // eval_acc slot advances on the device), so each task set's program is
@@ -1880,11 +1952,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
 
     // ---- epoch 0: baseline losses and first evaluation
     if (opt.baseline_and_eval) {
-        if (bnd_mode) {  // the training split's teacher pass needs no task state: launch it first
-            Program P0;
-            add_teacher_pass_bnd(P0, d_train.i(), ntrain, bkmax, bnd, chunk, tlanes);
-            P0.run_concurrent(st, &side_streams);
-        }
+        ensure_boundaries(bd, d_train, ntrain, true);  // needs no task state: launch it first
         prepare();
         {  // eval-split prefix activations (once per run)
             Program P;
@@ -1895,8 +1963,6 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         }
         {
             Program P;
-            if (!bnd_mode)
-                add_teacher_pass(P, d_train.i(), ntrain, sinks_for(true), chunk, ping.f(), pong.f(), t1.f(), sk.f());
             const int nb = std::min(nbr, static_cast<int>(ts.size()));
             std::vector<Program*> br = nb > 1 ? P.par(nb) : std::vector<Program*>{&P};
             for (size_t ti = 0; ti < ts.size(); ++ti) {
@@ -1904,12 +1970,10 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 const int bi = static_cast<int>(ti % static_cast<size_t>(nb));
                 Program& Q = *br[static_cast<size_t>(bi)];
                 const WsPtrs W = branch_ws(bi);
-                const float* xin = bnd_mode ? s->bx : s->in_stream.f();
-                const float* tin = bnd_mode ? s->bt : s->tgt_stream.f();
                 for (int r0 = 0; r0 < ntrain; r0 += ichunk) {
                     const int nr = std::min(ichunk, ntrain - r0);
-                    add_student_infer(Q, *s, xin + static_cast<size_t>(r0) * s->in_row, nr, W.ia, W.ib, W.io);
-                    const float* tg = tin + static_cast<size_t>(r0) * s->out_row;
+                    add_student_infer(Q, *s, s->bx + static_cast<size_t>(r0) * s->in_row, nr, W.ia, W.ib, W.io);
+                    const float* tg = s->bt + static_cast<size_t>(r0) * s->out_row;
                     const float* so = W.io;
                     const long long seg = static_cast<long long>(B) * s->out_row;
                     const long long tot = static_cast<long long>(nr) * s->out_row;
@@ -1927,60 +1991,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
 
     // ---- training epochs
     prepare();
-    struct EpochProg {
-        std::unique_ptr<Program> pre, post;  // teacher (+pack) | (scatter +) student steps
-    };
-    std::map<std::vector<int>, EpochProg> graphs;
-    // ---- sample-sharded teacher: exchange plan (identical on every rank)
-    // exchange only when the caller lists the global block ownership; without
-    // it every rank runs the teacher for its own blocks on all samples
-    const bool multi = comm && !opt.global_blocks.empty();
-    const int world = multi ? comm->world() : 1;
-    const int me = multi ? comm->rank() : 0;
-    const int vshards = std::max(1, opt.virtual_shards);
-    const bool sharded = vshards > 1 || !opt.global_blocks.empty();
-    ExchangePlan xp;
-    DevBuf sendbuf, recvbuf;
-    std::vector<size_t> send_off, send_cnt, recv_off, recv_cnt;
-    std::vector<size_t> my_bp(ts.size(), 0);  // position of each local task in xp.blocks
-    if (sharded) {
-        xp.world = world > 1 ? world : vshards;
-        std::vector<std::pair<int, int>> gb = opt.global_blocks;
-        if (gb.empty())
-            for (TaskState* s : ts) gb.push_back({s->k, me});
-        std::sort(gb.begin(), gb.end());
-        for (auto& [k, owner] : gb) {
-            const TBlockDev& b = tblocks.at(static_cast<size_t>(k) - 1);
-            xp.blocks.push_back(k);
-            xp.owner.push_back(owner);
-            xp.in_row.push_back(static_cast<long long>(b.cin) * b.hin * b.win);
-            xp.out_row.push_back(static_cast<long long>(b.cout) * b.hout * b.wout);
-        }
-        std::vector<double> share = opt.shard_share;
-        if (static_cast<int>(share.size()) != xp.world) share.assign(static_cast<size_t>(xp.world), 1.0);
-        xp.shard_begin = shard_bounds(ntrain, share);
-        for (size_t i = 0; i < ts.size(); ++i) {
-            auto f = std::find(xp.blocks.begin(), xp.blocks.end(), ts[i]->k);
-            if (f == xp.blocks.end() || xp.owner[static_cast<size_t>(f - xp.blocks.begin())] != me)
-                throw std::logic_error("sharded run: local task not owned by this rank in global_blocks");
-            my_bp[i] = static_cast<size_t>(f - xp.blocks.begin());
-        }
-        send_off.assign(static_cast<size_t>(xp.world), 0);
-        send_cnt = recv_off = recv_cnt = send_off;
-        size_t so = 0, ro = 0;
-        for (int p = 0; p < xp.world; ++p) {
-            send_off[static_cast<size_t>(p)] = so;
-            send_cnt[static_cast<size_t>(p)] = world > 1 ? xp.count(me, p) : 0;
-            so += send_cnt[static_cast<size_t>(p)];
-            recv_off[static_cast<size_t>(p)] = ro;
-            recv_cnt[static_cast<size_t>(p)] = xp.count(p, me);
-            ro += recv_cnt[static_cast<size_t>(p)];
-        }
-        sendbuf.alloc(std::max<size_t>(so, 1) * sizeof(float));
-        recvbuf.alloc(std::max<size_t>(ro, 1) * sizeof(float));
-    }
-    cudaEvent_t e0, e1, t0, t1e, eT;
-    PBKD_CUDA(cudaEventCreate(&eT));
+    cudaEvent_t e0, e1, t0, t1e;
     PBKD_CUDA(cudaEventCreate(&e0));
     PBKD_CUDA(cudaEventCreate(&e1));
     PBKD_CUDA(cudaEventCreate(&t0));
@@ -1992,155 +2003,89 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         for (TaskState* s : ts) key.push_back(e <= s->task.epochs ? s->steps_in_epoch[e] : 0);
         return key;
     };
-    // host: epoch permutations (bit-exact std::shuffle) -> stream positions.
-    // Computed for epoch e+1 while the GPU runs epoch e.
-    std::vector<int> where(static_cast<size_t>(count), -1);
-    auto make_pos = [&](int e, const std::vector<int>& key) {
-        std::vector<std::vector<int>> out(ts.size());
-        for (size_t i = 0; i < ts.size(); ++i) {
-            if (key[i] == 0) continue;
-            const std::vector<int> order = pbkd::epoch_order(train_idx, ts[i]->task.seed, e);
-            for (int q = 0; q < ntrain; ++q) where[static_cast<size_t>(order[static_cast<size_t>(q)])] = q;
-            out[i].resize(static_cast<size_t>(ntrain));
-            for (int t = 0; t < ntrain; ++t)
-                out[i][static_cast<size_t>(t)] = where[static_cast<size_t>(train_idx[static_cast<size_t>(t)])];
-        }
-        return out;
-    };
-    std::vector<std::vector<int>> pos_next = make_pos(1, epoch_key(1));
-    std::map<std::vector<int>, int> key_uses;  // epochs sharing each program key
-    for (int e = 1; e <= emax; ++e) key_uses[epoch_key(e)] += 1;
+    // Epoch programs (the student steps of one epoch), one per distinct key
+    // (steps per task), recorded and captured BEFORE the first epoch runs so
+    // no host capture time falls between device work.  A graph pays off only
+    // for a program that runs more than once.
+    std::map<std::vector<int>, std::unique_ptr<Program>> progs;
+    std::map<std::vector<int>, int> key_uses;
+    int last_epoch = 0;
     for (int e = 1; e <= emax; ++e) {
         const std::vector<int> key = epoch_key(e);
         if (std::all_of(key.begin(), key.end(), [](int v) { return v == 0; })) break;
+        key_uses[key] += 1;
+        last_epoch = e;
+    }
+    for (int e = 1; e <= last_epoch; ++e) {
+        const std::vector<int> key = epoch_key(e);
+        if (progs.count(key)) continue;
+        auto prog = std::make_unique<Program>();
+        for (int step = 0; step < spe; ++step) {
+            std::vector<TaskState*> act;
+            std::vector<long long> gs;
+            for (size_t i = 0; i < ts.size(); ++i)
+                if (step < key[i]) {
+                    act.push_back(ts[i]);
+                    gs.push_back(gbase[i] + step);
+                }
+            add_step(*prog, act, step, 0, ntrain, gs);
+        }
+        if (opt.use_graphs && key_uses[key] > 1) prog->build_graph(st, &side_streams);
+        progs.emplace(key, std::move(prog));
+    }
+    trace.mark("epoch: record programs / graphs");
+    // host: epoch orders (bit-exact std::shuffle of the training rows: the
+    // permutation std::shuffle applies depends only on the size and the
+    // engine, so shuffling row numbers gives the slot -> train-row map even
+    // when train_idx repeats a sample).  Computed for epoch e+1 while the GPU
+    // runs epoch e.
+    std::vector<int> rows_iota(static_cast<size_t>(ntrain));
+    std::iota(rows_iota.begin(), rows_iota.end(), 0);
+    auto make_ord = [&](int e, const std::vector<int>& key) {
+        std::vector<std::vector<int>> out(ts.size());
+        for (size_t i = 0; i < ts.size(); ++i)
+            if (key[i] > 0) out[i] = pbkd::epoch_order(rows_iota, ts[i]->task.seed, e);
+        return out;
+    };
+    std::vector<std::vector<int>> ord_next = last_epoch >= 1 ? make_ord(1, epoch_key(1)) : std::vector<std::vector<int>>{};
+    // the timed window of a step-only run starting at epoch 1 includes the
+    // run's one-time teacher pass (amortised over the epochs, not dropped)
+    if (last_epoch >= 1 && opt.timed_from_epoch <= 1 && !bd.done) {
+        PBKD_CUDA(cudaEventRecord(t0, st));
+        timed_started = true;
+    }
+    ensure_boundaries(bd, d_train, ntrain, true);
+    for (int e = 1; e <= last_epoch; ++e) {
+        const std::vector<int> key = epoch_key(e);
         const bool timed = e >= opt.timed_from_epoch;
         if (timed && !timed_started) {
             PBKD_CUDA(cudaEventRecord(t0, st));
             timed_started = true;
         }
-        std::vector<std::vector<int>> pos_now = std::move(pos_next);
-        if (bnd_mode)  // epoch order: slot -> train row
-            for (size_t i = 0; i < ts.size(); ++i) {
-                if (key[i] == 0) continue;
-                std::vector<int> ord(pos_now[i].size());
-                for (size_t t = 0; t < ord.size(); ++t) ord[static_cast<size_t>(pos_now[i][t])] = static_cast<int>(t);
-                pos_now[i] = std::move(ord);
-            }
+        std::vector<std::vector<int>> ord_now = std::move(ord_next);
         for (size_t i = 0; i < ts.size(); ++i)
             if (key[i] > 0)
-                PBKD_CUDA(cudaMemcpyAsync(ts[i]->pos.p, pos_now[i].data(), pos_now[i].size() * sizeof(int),
+                PBKD_CUDA(cudaMemcpyAsync(ts[i]->pos.p, ord_now[i].data(), ord_now[i].size() * sizeof(int),
                                           cudaMemcpyHostToDevice, st));
-        const std::vector<int>& gkey = key;
-        auto it = graphs.find(gkey);
-        if (it == graphs.end()) {
-            EpochProg ep{std::make_unique<Program>(), std::make_unique<Program>()};
-            if (bnd_mode) {
-                add_teacher_pass_bnd(*ep.pre, d_train.i(), ntrain, bkmax, bnd, chunk, tlanes);
-            } else if (!sharded) {
-                std::vector<Sink> sinks;
-                for (size_t i = 0; i < ts.size(); ++i) {
-                    if (key[i] == 0) continue;
-                    TaskState* s = ts[i];
-                    sinks.push_back({s->k - 1, s->in_stream.f(), s->pos.i(), s->in_row});
-                    sinks.push_back({s->k, s->tgt_stream.f(), s->pos.i(), s->out_row});
-                }
-                add_teacher_pass(*ep.pre, d_train.i(), ntrain, sinks, chunk, ping.f(), pong.f(), t1.f(), sk.f());
-            } else {
-                // pack: teacher forward on a shard, rows of every distilled block
-                // written in shard order into the buffer bound for its owner
-                auto pack = [&](int src) {
-                    std::vector<Sink> sinks;
-                    for (size_t bp = 0; bp < xp.blocks.size(); ++bp) {
-                        const int dst = xp.owner[bp];
-                        float* base = world > 1 ? sendbuf.f() + send_off[static_cast<size_t>(dst)]
-                                                : recvbuf.f() + recv_off[static_cast<size_t>(src)];
-                        sinks.push_back({xp.blocks[bp] - 1, base + xp.offset_in(src, dst, bp), d_iota.i(),
-                                         static_cast<int>(xp.in_row[bp])});
-                        sinks.push_back({xp.blocks[bp], base + xp.offset_tgt(src, dst, bp), d_iota.i(),
-                                         static_cast<int>(xp.out_row[bp])});
-                    }
-                    const int sb = xp.shard_begin[static_cast<size_t>(src)];
-                    if (xp.shard_rows(src) > 0)
-                        add_teacher_pass(*ep.pre, d_train.i() + sb, xp.shard_rows(src), sinks, chunk, ping.f(),
-                                         pong.f(), t1.f(), sk.f());
-                };
-                if (world > 1)
-                    pack(me);
-                else
-                    for (int src = 0; src < xp.world; ++src) pack(src);
-                // unpack: rows from every shard into each local task's epoch order
-                std::vector<ScatterOp> sc;
-                for (int src = 0; src < xp.world; ++src) {
-                    const int rows = xp.shard_rows(src);
-                    if (rows == 0) continue;
-                    const float* base = recvbuf.f() + recv_off[static_cast<size_t>(src)];
-                    const int sb = xp.shard_begin[static_cast<size_t>(src)];
-                    for (size_t i = 0; i < ts.size(); ++i) {
-                        if (key[i] == 0) continue;
-                        TaskState* s = ts[i];
-                        sc.push_back(ScatterOp{base + xp.offset_in(src, me, my_bp[i]), s->in_stream.f(), s->pos.i() + sb,
-                                               rows, s->in_row, 0});
-                        sc.push_back(ScatterOp{base + xp.offset_tgt(src, me, my_bp[i]), s->tgt_stream.f(),
-                                               s->pos.i() + sb, rows, s->out_row, 0});
-                    }
-                }
-                ep.post->grouped<ScatterOp>(launch_scatter, sc, [](const ScatterOp&) { return kScatterCtas; });
-            }
-            for (int step = 0; step < spe; ++step) {
-                std::vector<TaskState*> act;
-                std::vector<long long> gs;
-                for (size_t i = 0; i < ts.size(); ++i)
-                    if (step < key[i]) {
-                        act.push_back(ts[i]);
-                        gs.push_back(gbase[i] + step);
-                    }
-                add_step(*ep.post, act, step, 0, ntrain, gs);
-            }
-            trace.mark("epoch: record programs");
-            // a graph pays off only for an epoch program that runs again
-            if (opt.use_graphs && key_uses[gkey] > 1) {
-                ep.pre->build_graph(st, &side_streams);
-                ep.post->build_graph(st, &side_streams);
-            }
-            if (std::getenv("PBKD_PROFILE")) {  // one extra eager pass, timed per launch
-                std::map<std::string, KernelStat> pa, pb;
-                ep.pre->run_profiled(st, pa);
-                print_profile("teacher pass", pa);
-                ep.post->run_profiled(st, pb);
-                print_profile("student steps", pb);
-            }
-            it = graphs.emplace(gkey, std::move(ep)).first;
-            trace.mark("epoch: build programs/graphs");
-        }
+        Program& pr = *progs.at(key);
         PBKD_CUDA(cudaEventRecord(e0, st));
-        for (Program* pr : {it->second.pre.get(), it->second.post.get()}) {
-            if (pr->launches() == 0) continue;
-            if (pr->has_graph())
-                pr->launch_graph(st);
-            else
-                pr->run_concurrent(st, &side_streams);
-            if (pr == it->second.pre.get() && world > 1)  // boundary rows to their owners
-                comm->all_to_all_v(sendbuf.f(), send_off, send_cnt, recvbuf.f(), recv_off, recv_cnt, st);
-            if (pr == it->second.pre.get()) PBKD_CUDA(cudaEventRecord(eT, st));
-        }
+        if (pr.has_graph())
+            pr.launch_graph(st);
+        else
+            pr.run_concurrent(st, &side_streams);
         PBKD_CUDA(cudaEventRecord(e1, st));
         trace.mark("epoch: launched (host)");
         for (size_t i = 0; i < ts.size(); ++i)  // epoch-local losses -> per-run history
             if (key[i] > 0)
                 PBKD_CUDA(cudaMemcpyAsync(ts[i]->step_loss.f() + gbase[i], ts[i]->epoch_loss.p,
                                           static_cast<size_t>(key[i]) * sizeof(float), cudaMemcpyDeviceToDevice, st));
-        if (timed) timing.launches += static_cast<long long>(it->second.pre->launches() + it->second.post->launches());
-        if (e + 1 <= emax) pos_next = make_pos(e + 1, epoch_key(e + 1));  // overlaps the GPU
+        if (timed) timing.launches += static_cast<long long>(pr.launches());
+        if (e + 1 <= last_epoch) ord_next = make_ord(e + 1, epoch_key(e + 1));  // overlaps the GPU
         PBKD_CUDA(cudaEventSynchronize(e1));
         float ms = 0.0f;
         PBKD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         timing.epoch_ms_total += ms;
         timing.epoch_ms.push_back(ms);
-        if (timed) {
-            float tms = 0.0f;
-            PBKD_CUDA(cudaEventElapsedTime(&tms, e0, eT));
-            timing.teacher_ms += tms;
-        }
         timing.epochs += 1;
         if (timed) timing.timed_epochs += 1;
         for (size_t i = 0; i < ts.size(); ++i) {
@@ -2162,18 +2107,30 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         float ms = 0.0f;
         PBKD_CUDA(cudaEventElapsedTime(&ms, t0, t1e));
         timing.timed_ms += ms;
+        if (opt.timed_from_epoch <= 1) timing.timed_includes_teacher = true;
     }
-    // outside the timed window
-    if (opt.profile && !graphs.empty()) {  // last epoch's programs once more, per launch
-        EpochProg& ep = graphs.rbegin()->second;
-        ep.pre->run_profiled(st, timing.prof);
-        if (world > 1)
-            comm->all_to_all_v(sendbuf.f(), send_off, send_cnt, recvbuf.f(), recv_off, recv_cnt, st);
-        ep.post->run_profiled(st, timing.prof);
+    // outside the timed window: the last epoch's program once more, eagerly
+    // with an event per launch, on a saved copy of the training state that
+    // is restored afterwards (results are those of the real epochs)
+    if (opt.profile && last_epoch >= 1) {
+        struct Saved {
+            DevBuf* dst;
+            DevBuf copy;
+        };
+        std::vector<Saved> saved;
+        for (TaskState* s : ts)
+            for (DevBuf* b : {&s->params, &s->params_hi, &s->params_lo, &s->vel, &s->mstats, &s->failed, &s->grads}) {
+                if (!b->p) continue;
+                Saved sv{b, DevBuf(b->bytes)};
+                PBKD_CUDA(cudaMemcpyAsync(sv.copy.p, b->p, b->bytes, cudaMemcpyDeviceToDevice, st));
+                saved.push_back(std::move(sv));
+            }
+        progs.at(epoch_key(last_epoch))->run_profiled(st, timing.prof);
+        for (Saved& sv : saved)
+            PBKD_CUDA(cudaMemcpyAsync(sv.dst->p, sv.copy.p, sv.dst->bytes, cudaMemcpyDeviceToDevice, st));
     }
     cudaEventDestroy(t0);
     cudaEventDestroy(t1e);
-    cudaEventDestroy(eT);
     PBKD_CUDA(cudaStreamSynchronize(st));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -5,10 +5,11 @@
 // (distill.cpp:135-262) for every task, all tasks of the same batch size and
 // unit count advancing in lockstep as grouped launches:
 //
-//   per epoch:  teacher forward once per training sample, boundary activations
-//               scattered straight into each task's epoch-ordered stream
-//               (replaces prefix_infer per block per batch, distill.cpp:210-211)
-//            -> ceil(N/B) grouped student steps (fwd, MSE, bwd, SGD)
+//   once per run: teacher forward over the training split, every block
+//               boundary kept in HBM in train order (replaces prefix_infer +
+//               block_infer per block per batch, distill.cpp:210-211)
+//   per epoch:  ceil(N/B) grouped student steps (fwd, MSE, bwd, SGD) reading
+//               their batches through the epoch order
 //   the whole epoch is one CUDA graph; the host only uploads the epoch's
 //   permutation (std::shuffle + mt19937_64, bit-exact).
 #pragma once
@@ -44,20 +45,24 @@ struct TaskOutcome {
 struct RunOptions {
     bool baseline_and_eval = true;  // epoch-0 baseline + evaluations (train_block semantics)
     bool use_graphs = true;
-    int timed_from_epoch = 1;  // device events bracket epochs [timed_from_epoch, last]
+    // device events bracket epochs [timed_from_epoch, last]; for a step-only
+    // run with timed_from_epoch <= 1 the window also holds the one-time
+    // teacher boundary pass
+    int timed_from_epoch = 1;
     // Sample-sharded teacher (multi-GPU).  global_blocks lists every block
     // being distilled on any rank with its owner; this engine trains only the
-    // tasks passed to run() (owner == rank), runs the teacher forward on its
-    // shard of the training split for ALL blocks, and exchanges boundary rows
-    // with NCCL (set_comm).  virtual_shards > 1 on a single GPU runs the same
-    // pack/scatter path with local shards (tests).
+    // tasks passed to run() (owner == rank), runs the teacher forward once on
+    // its shard of the training split for every boundary any block reads,
+    // and exchanges boundary rows with NCCL (set_comm) once per run.
+    // virtual_shards > 1 on a single GPU computes the boundaries shard by
+    // shard (tests: results must not move a bit).
     std::vector<std::pair<int, int>> global_blocks;  // (block index, owner rank)
     int virtual_shards = 1;
     std::vector<double> shard_share;  // teacher share per rank (empty: uniform)
-    // after the last epoch, replay that epoch's programs once more eagerly
-    // with a CUDA event after every launch (per-kernel-class device time and
-    // algorithmic work, RunTiming::prof); training state moves on by one
-    // epoch, so only for measurement runs
+    // after the last epoch, replay that epoch's program (and the teacher
+    // boundary pass) once more eagerly with a CUDA event after every launch
+    // (per-kernel-class device time and algorithmic work, RunTiming::prof);
+    // the training state is saved before and restored after the replay
     bool profile = false;
 };
 
@@ -74,7 +79,8 @@ struct RunTiming {
     std::vector<double> epoch_ms; // per training epoch (graph only)
     double timed_ms = 0.0;        // events around epochs >= timed_from_epoch, host gaps included
     int timed_epochs = 0;
-    double teacher_ms = 0.0;      // timed epochs: teacher forward (+ pack + exchange) part
+    double teacher_ms = 0.0;      // the run's one-time teacher boundary pass (+ NCCL exchange)
+    bool timed_includes_teacher = false;  // timed window began before the teacher pass
     int epochs = 0;
     long long student_steps = 0;  // per task
     long long launches = 0;       // kernel launches in the timed window

@@ -400,24 +400,24 @@ int pbkd_run_sharded(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const i
     });
 }
 
-int pbkd_exchange_plan(const int* blocks, const int* owners, int nb, const long long* in_row,
-                       const long long* out_row, int world, int n_train, const double* share, int src, int dst,
-                       size_t* count, size_t* off_in, size_t* off_tgt, int* shard_begin) {
+int pbkd_exchange_plan(const int* blocks, const int* owners, int nb, const long long* rows, int n_rows, int world,
+                       int n_train, const double* share, int src, int dst, size_t* count, int* xj, int* xrow0,
+                       int* xrows, int cap, int* n, int* shard_begin) {
     return guard([&] {
-        ExchangePlan xp;
-        xp.world = world;
-        xp.blocks.assign(blocks, blocks + nb);
-        xp.owner.assign(owners, owners + nb);
-        xp.in_row.assign(in_row, in_row + nb);
-        xp.out_row.assign(out_row, out_row + nb);
-        std::vector<double> sh = share ? std::vector<double>(share, share + world) : std::vector<double>(world, 1.0);
-        xp.shard_begin = shard_bounds(n_train, sh);
-        *count = xp.count(src, dst);
-        for (int b = 0; b < nb; ++b) {
-            off_in[b] = xp.offset_in(src, dst, static_cast<size_t>(b));
-            off_tgt[b] = xp.offset_tgt(src, dst, static_cast<size_t>(b));
+        need(world >= 1 && src >= 0 && src < world && dst >= 0 && dst < world, "bad src / dst / world");
+        std::vector<double> sh = share ? std::vector<double>(share, share + world) : std::vector<double>();
+        const BoundaryPlan p = make_boundary_plan(std::vector<int>(blocks, blocks + nb),
+                                                  std::vector<int>(owners, owners + nb),
+                                                  std::vector<long long>(rows, rows + n_rows), world, n_train, sh);
+        const std::vector<BoundaryPlan::Xfer> xs = p.transfers(src, dst);
+        *count = p.count(src, dst);
+        *n = static_cast<int>(xs.size());
+        for (int i = 0; i < std::min(cap, *n); ++i) {
+            xj[i] = xs[static_cast<size_t>(i)].j;
+            xrow0[i] = xs[static_cast<size_t>(i)].row0;
+            xrows[i] = xs[static_cast<size_t>(i)].rows;
         }
-        for (int s = 0; s <= world; ++s) shard_begin[s] = xp.shard_begin[static_cast<size_t>(s)];
+        for (int s2 = 0; s2 <= world; ++s2) shard_begin[s2] = p.shard_begin[static_cast<size_t>(s2)];
     });
 }
 

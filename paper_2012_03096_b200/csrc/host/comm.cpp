@@ -1,14 +1,17 @@
 // comm.cpp -- NCCL all-to-all-v of teacher boundary activations (multi-GPU).
 //
 // The paper's only communication is the dispatch/gather pair;
-// the B200 path adds one exchange per epoch: every GPU runs the teacher forward
-// on its shard of the training samples and ships each block's boundary rows to
-// the GPU that owns that block (grouped ncclSend/ncclRecv over NVLink).
+// the B200 path adds one exchange per RUN: every GPU runs the teacher forward
+// once on its shard of the training samples and ships the boundary rows the
+// other GPUs' blocks read straight between the boundary buffers (grouped
+// ncclSend/ncclRecv over NVLink; inference-mode teacher rows are per-sample
+// and epoch-invariant, so one exchange serves every epoch).
 //
 // NCCL is resolved at run time with dlopen("libnccl.so.2") so the process
 // shares whichever NCCL torch.distributed already loaded (one NCCL per process).
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -78,19 +81,24 @@ NcclComm::~NcclComm() {
     if (comm_) api().comm_destroy(static_cast<ncclComm_t>(comm_));
 }
 
-void NcclComm::all_to_all_v(const float* send, const std::vector<size_t>& send_off, const std::vector<size_t>& send_cnt,
-                            float* recv, const std::vector<size_t>& recv_off, const std::vector<size_t>& recv_cnt,
-                            cudaStream_t st) {
+void NcclComm::exchange(const BoundaryPlan& plan, const std::vector<float*>& bnd, cudaStream_t st) {
     auto& a = api();
     auto c = static_cast<ncclComm_t>(comm_);
     check(a.group_start(), "ncclGroupStart");
     for (int p = 0; p < world_; ++p) {
-        if (send_cnt[static_cast<size_t>(p)])
-            check(a.send(send + send_off[static_cast<size_t>(p)], send_cnt[static_cast<size_t>(p)], ncclFloat, p, c, st),
-                  "ncclSend");
-        if (recv_cnt[static_cast<size_t>(p)])
-            check(a.recv(recv + recv_off[static_cast<size_t>(p)], recv_cnt[static_cast<size_t>(p)], ncclFloat, p, c, st),
-                  "ncclRecv");
+        if (p == rank_) continue;
+        // per peer pair, NCCL matches sends and receives in issue order: both
+        // sides walk transfers(src, dst) in the same (j ascending) order
+        for (const BoundaryPlan::Xfer& x : plan.transfers(rank_, p)) {
+            const long long r = plan.row[static_cast<size_t>(x.j)];
+            check(a.send(bnd[static_cast<size_t>(x.j)] + static_cast<size_t>(x.row0) * r,
+                         static_cast<size_t>(x.rows) * r, ncclFloat, p, c, st), "ncclSend");
+        }
+        for (const BoundaryPlan::Xfer& x : plan.transfers(p, rank_)) {
+            const long long r = plan.row[static_cast<size_t>(x.j)];
+            check(a.recv(bnd[static_cast<size_t>(x.j)] + static_cast<size_t>(x.row0) * r,
+                         static_cast<size_t>(x.rows) * r, ncclFloat, p, c, st), "ncclRecv");
+        }
     }
     check(a.group_end(), "ncclGroupEnd");
 }
@@ -99,24 +107,44 @@ void NcclComm::all_to_all_v(const float* send, const std::vector<size_t>& send_o
 
 namespace pbkd_gpu {
 
-size_t ExchangePlan::count(int src, int dst) const {
+std::vector<BoundaryPlan::Xfer> BoundaryPlan::transfers(int src, int dst) const {
+    std::vector<Xfer> v;
+    if (src == dst || shard_rows(src) == 0) return v;
+    for (int j = 1; j <= kmax(); ++j)
+        if (need[static_cast<size_t>(dst)][static_cast<size_t>(j)])
+            v.push_back({j, shard_begin[static_cast<size_t>(src)], shard_rows(src)});
+    return v;
+}
+
+size_t BoundaryPlan::count(int src, int dst) const {
     size_t n = 0;
-    const size_t rows = static_cast<size_t>(shard_rows(src));
-    for (size_t b = 0; b < blocks.size(); ++b)
-        if (owner[b] == dst) n += rows * static_cast<size_t>(in_row[b] + out_row[b]);
+    for (const Xfer& x : transfers(src, dst)) n += static_cast<size_t>(x.rows) * static_cast<size_t>(row[static_cast<size_t>(x.j)]);
     return n;
 }
 
-size_t ExchangePlan::offset_in(int src, int dst, size_t bp) const {
-    size_t off = 0;
-    const size_t rows = static_cast<size_t>(shard_rows(src));
-    for (size_t b = 0; b < bp; ++b)
-        if (owner[b] == dst) off += rows * static_cast<size_t>(in_row[b] + out_row[b]);
-    return off;
-}
-
-size_t ExchangePlan::offset_tgt(int src, int dst, size_t bp) const {
-    return offset_in(src, dst, bp) + static_cast<size_t>(shard_rows(src)) * static_cast<size_t>(in_row[bp]);
+BoundaryPlan make_boundary_plan(const std::vector<int>& blocks, const std::vector<int>& owners,
+                                const std::vector<long long>& row, int world, int n_train,
+                                const std::vector<double>& share) {
+    if (blocks.size() != owners.size()) throw std::invalid_argument("boundary plan: blocks / owners differ in length");
+    if (world < 1) throw std::invalid_argument("boundary plan: world must be at least 1");
+    BoundaryPlan p;
+    p.world = world;
+    p.row = row;
+    int kmax = 0;
+    for (int k : blocks) kmax = std::max(kmax, k);
+    if (static_cast<int>(row.size()) < kmax + 1) throw std::invalid_argument("boundary plan: row sizes missing");
+    p.row.resize(static_cast<size_t>(kmax) + 1);
+    p.need.assign(static_cast<size_t>(world), std::vector<char>(static_cast<size_t>(kmax) + 1, 0));
+    for (size_t i = 0; i < blocks.size(); ++i) {
+        const int k = blocks[i], o = owners[i];
+        if (k < 1 || o < 0 || o >= world) throw std::invalid_argument("boundary plan: bad block or owner");
+        p.need[static_cast<size_t>(o)][static_cast<size_t>(k) - 1] = 1;
+        p.need[static_cast<size_t>(o)][static_cast<size_t>(k)] = 1;
+    }
+    std::vector<double> sh = share;
+    if (static_cast<int>(sh.size()) != world) sh.assign(static_cast<size_t>(world), 1.0);
+    p.shard_begin = shard_bounds(n_train, sh);
+    return p;
 }
 
 std::vector<int> shard_bounds(int n, const std::vector<double>& share) {
