@@ -320,17 +320,28 @@ class Oracle:
                       C.byref(acc)))
         return acc.value
 
-    def train_block(self, spec, tw, images, labels, train_idx, eval_idx, task, n_block_floats):
+    def train_block(self, spec, tw, images, labels, train_idx, eval_idx, task, n_block_floats,
+                    with_f64=False):
+        """with_f64 (orc only): also "loss_history64", every entry's batch MSEs
+        summed in fp64 over the same outputs."""
         ds = self._ds(images, labels)
         sp = self._split(train_idx, eval_idx)
         res = Result()
         bw = np.zeros(max(n_block_floats, 1), np.float32)
-        f = self.fn("train_block", C.c_int, [C.c_char_p, F32P, C.POINTER(Dataset),
-                                              C.POINTER(Split), C.POINTER(Task),
-                                              C.POINTER(Result), F32P, C.c_size_t])
-        self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), C.byref(ds),
-                      C.byref(sp), C.byref(task), C.byref(res), bw, bw.size))
-        return {
+        h64 = np.zeros(256, np.float64)
+        if with_f64:
+            f = self.fn("train_block_f64", C.c_int, [C.c_char_p, F32P, C.POINTER(Dataset),
+                                                      C.POINTER(Split), C.POINTER(Task),
+                                                      C.POINTER(Result), F32P, C.c_size_t, F64P])
+            self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), C.byref(ds),
+                          C.byref(sp), C.byref(task), C.byref(res), bw, bw.size, h64))
+        else:
+            f = self.fn("train_block", C.c_int, [C.c_char_p, F32P, C.POINTER(Dataset),
+                                                  C.POINTER(Split), C.POINTER(Task),
+                                                  C.POINTER(Result), F32P, C.c_size_t])
+            self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), C.byref(ds),
+                          C.byref(sp), C.byref(task), C.byref(res), bw, bw.size))
+        return {"loss_history64": h64[:res.n_loss].tolist(),
             "loss_history": [res.loss_history[i] for i in range(res.n_loss)],
             "eval_history": [(res.eval_epoch[i], res.eval_acc[i]) for i in range(res.n_eval)],
             "final_local_loss": res.final_local_loss, "best_eval": res.best_eval,
@@ -351,3 +362,59 @@ class Oracle:
         self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), C.byref(ds),
                       C.byref(sp), C.byref(task), n_steps, losses, l64, fw, fw.size))
         return (losses, fw, l64) if with_f64 else (losses, fw)
+
+    def train_replay_multi(self, spec, tw, images, labels, train_idx, eval_idx, tasks, n_steps,
+                           n_floats, ck_steps=(), threads=None):
+        """Grouped replay (orc only): every task's per-step float losses and
+        fp64 losses [n_tasks, n_steps], and per task a [len(ck_steps), nf]
+        array of student weights after each checkpoint step."""
+        ds = self._ds(images, labels)
+        sp = self._split(train_idx, eval_idx)
+        nt = len(tasks)
+        ck = np.ascontiguousarray(sorted(ck_steps) or [n_steps], np.int32)
+        off = np.zeros(nt + 1, np.uint64)
+        for i, nf in enumerate(n_floats):
+            off[i + 1] = off[i] + nf * len(ck)
+        buf = np.zeros(max(int(off[-1]), 1), np.float32)
+        losses = np.zeros((nt, n_steps), np.float32)
+        l64 = np.zeros((nt, n_steps), np.float64)
+        arr = (Task * nt)(*tasks)
+        f = self.fn("train_replay_multi", C.c_int,
+                    [C.c_char_p, F32P, C.POINTER(Dataset), C.POINTER(Split), C.POINTER(Task), C.c_int,
+                     C.c_int, I32P, C.c_int, C.c_int, F32P, F64P, F32P,
+                     np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")])
+        self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), C.byref(ds), C.byref(sp), arr,
+                      nt, n_steps, ck, len(ck), threads or os.cpu_count() or 1, losses, l64, buf, off))
+        snaps = [buf[int(off[i]):int(off[i + 1])].reshape(len(ck), n_floats[i]) for i in range(nt)]
+        return losses, l64, snaps
+
+    def run_parallel(self, spec, tw, images, labels, train_idx, eval_idx, tasks, plan, n_floats,
+                     policy=0):
+        """run_parallel (runtime.cpp:124-243); results in ascending block order,
+        n_floats per result in that order."""
+        ds = self._ds(images, labels)
+        sp = self._split(train_idx, eval_idx)
+        nt = len(tasks)
+        ids = np.ascontiguousarray([i for q in plan for i in q], np.int32)
+        counts = np.ascontiguousarray([len(q) for q in plan], np.int32)
+        off = np.zeros(nt + 1, np.uint64)
+        for i, nf in enumerate(n_floats):
+            off[i + 1] = off[i] + nf
+        buf = np.zeros(max(int(off[-1]), 1), np.float32)
+        res = (Result * nt)()
+        arr = (Task * nt)(*tasks)
+        f = self.fn("run_parallel", C.c_int,
+                    [C.c_char_p, F32P, C.POINTER(Dataset), C.POINTER(Split), C.POINTER(Task), C.c_int,
+                     I32P, I32P, C.c_int, C.c_int, C.POINTER(Result), F32P,
+                     np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")])
+        self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), C.byref(ds), C.byref(sp), arr, nt,
+                      ids, counts, len(plan), policy, res, buf, off))
+        out = []
+        for i in range(nt):
+            r = res[i]
+            out.append({"loss_history": [r.loss_history[q] for q in range(r.n_loss)],
+                        "eval_history": [(r.eval_epoch[q], r.eval_acc[q]) for q in range(r.n_eval)],
+                        "final_local_loss": r.final_local_loss, "best_eval": r.best_eval,
+                        "failed": bool(r.failed), "failure": r.failure.decode(),
+                        "block": buf[int(off[i]):int(off[i + 1])].copy()})
+        return out

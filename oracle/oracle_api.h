@@ -140,6 +140,11 @@ int ORC(eval_with_student)(const char* spec, const float* tw, const orc_dataset*
 /* train_block (distill.cpp:135-262); block_w receives the best snapshot */
 int ORC(train_block)(const char* spec, const float* tw, const orc_dataset* d, const orc_split* s,
                      const orc_task* t, orc_result* r, float* block_w, size_t cap);
+/* train_block plus hist64[n_loss]: each loss_history entry recomputed with
+ * every batch's MSE summed in fp64 over the same outputs (restatement only). */
+int ORC(train_block_f64)(const char* spec, const float* tw, const orc_dataset* d,
+                         const orc_split* s, const orc_task* t, orc_result* r, float* block_w,
+                         size_t cap, double* hist64);
 /* Step-loop replay through the public block API (test_distill.cpp:93-118
  * pattern): n_steps optimizer steps of the train_block loop (epoch shuffles,
  * batches, max_steps ignored), no baseline/eval.  step_loss[n_steps] gets each
@@ -154,6 +159,29 @@ int ORC(train_replay)(const char* spec, const float* tw, const orc_dataset* d,
 int ORC(train_replay_f64)(const char* spec, const float* tw, const orc_dataset* d,
                           const orc_split* s, const orc_task* t, int n_steps, float* step_loss,
                           double* step_loss64, float* final_w, size_t cap);
+
+/* The bench workload restated on the CPU: n_tasks blocks trained side by side
+ * for n_steps optimizer steps each (the train_replay step loop).  The teacher
+ * boundaries are computed ONCE per training sample (inference-mode BN is
+ * per-sample, model.cpp:553-557, so prefix_infer/block_infer of a batch equals
+ * the per-sample results stacked -- bit for bit) on `threads` host threads,
+ * then each task runs on its own thread.  step_loss / step_loss64 are
+ * [n_tasks][n_steps]; ck_steps (ascending, each in 1..n_steps) selects the
+ * steps after which the student arrays are stored: task i's snapshot c lands
+ * at ck_w + w_off[i] + c * (w_off[i+1]-w_off[i]) / n_ck.  Restatement only. */
+int ORC(train_replay_multi)(const char* spec, const float* tw, const orc_dataset* d,
+                            const orc_split* s, const orc_task* tasks, int n_tasks, int n_steps,
+                            const int* ck_steps, int n_ck, int threads, float* step_loss,
+                            double* step_loss64, float* ck_w, const size_t* w_off);
+
+/* run_parallel (runtime.cpp:124-243): plan = per-worker task-id lists
+ * (plan_ids concatenated, plan_counts[w] ids each), policy = SchedulePolicy
+ * ordinal.  results[i] / block_w + w_off[i] receive the i-th result of the
+ * gather (ascending block index), best snapshot included. */
+int ORC(run_parallel)(const char* spec, const float* tw, const orc_dataset* d, const orc_split* s,
+                      const orc_task* tasks, int n_tasks, const int* plan_ids,
+                      const int* plan_counts, int workers, int policy, orc_result* results,
+                      float* block_w, const size_t* w_off);
 
 #pragma GCC visibility pop
 #ifdef __cplusplus

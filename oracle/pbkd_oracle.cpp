@@ -17,6 +17,9 @@
 #include "oracle_api.h"
 
 #include <algorithm>
+#include <array>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -899,6 +902,29 @@ void validate(const orc_task* t, const Net& net) {  // distill.cpp:86-100
     if (t->loss_mode != 0) throw std::invalid_argument("oracle restates LocalOnly mode only");
 }
 
+// Runs f(i) for i in [0, n) on up to `threads` host threads (dynamic
+// assignment; results must not depend on which thread runs which i).
+void parallel_for(int n, int threads, const std::function<void(int)>& f) {
+    std::atomic<int> next{0};
+    std::string err;
+    std::atomic<bool> bad{false};
+    auto body = [&] {
+        for (int i; (i = next.fetch_add(1)) < n && !bad;) {
+            try {
+                f(i);
+            } catch (const std::exception& e) {
+                if (!bad.exchange(true)) err = e.what();
+            }
+        }
+    };
+    const int nt = std::max(1, std::min(threads, n));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(body);
+    body();
+    for (std::thread& t : pool) t.join();
+    if (bad) throw std::runtime_error(err);
+}
+
 T4 wrap(const float* p, int n, int c, int h, int w) {
     T4 t(n, c, h, w);
     std::copy(p, p + t.d.size(), t.d.begin());
@@ -1189,6 +1215,19 @@ int orc_eval_with_student(const char* spec, const float* tw, const orc_dataset* 
 
 int orc_train_block(const char* spec, const float* tw, const orc_dataset* dd, const orc_split* s,
                     const orc_task* t, orc_result* r, float* block_w, size_t cap) {
+    return orc_train_block_f64(spec, tw, dd, s, t, r, block_w, cap, nullptr);
+}
+
+int orc_train_block_f64(const char* spec, const float* tw, const orc_dataset* dd, const orc_split* s,
+                        const orc_task* t, orc_result* r, float* block_w, size_t cap, double* hist64) {
+    auto mse64 = [](const T4& a, const T4& b) {
+        double acc = 0.0;
+        for (size_t q = 0; q < a.d.size(); ++q) {
+            const double df = static_cast<double>(a.d[q]) - static_cast<double>(b.d[q]);
+            acc += df * df;
+        }
+        return acc / static_cast<double>(a.d.size());
+    };
     return guard([&] {  // distill.cpp:135-262 (LocalOnly)
         Net net = load_net(spec, tw);
         validate(t, net);
@@ -1214,14 +1253,16 @@ int orc_train_block(const char* spec, const float* tw, const orc_dataset* dd, co
             }
         };
         {  // epoch-0 baseline, inference mode, unshuffled (distill.cpp:166-192)
-            double sum = 0.0;
+            double sum = 0.0, sum64 = 0.0;
             const auto bs = batches_of(train, t->batch_size);
             for (const auto& b : bs) {
                 const T4 a = prefix(net, gather(d, b), k, false);
                 const T4 tt = block_infer(tb, a);
                 const T4 so = block_infer(student, a);
                 sum += static_cast<double>(mse(so.d.data(), tt.d.data(), so.d.size()));
+                if (hist64) sum64 += mse64(so, tt);
             }
+            if (hist64) hist64[r->n_loss] = sum64 / static_cast<double>(bs.size());
             r->loss_history[r->n_loss++] = sum / static_cast<double>(bs.size());
             r->final_local_loss = sum / static_cast<double>(bs.size());
         }
@@ -1232,7 +1273,7 @@ int orc_train_block(const char* spec, const float* tw, const orc_dataset* dd, co
             std::vector<int> order = train;
             std::mt19937_64 rng(splitmix(t->seed, static_cast<uint64_t>(epoch)));
             std::shuffle(order.begin(), order.end(), rng);
-            double sum = 0.0;
+            double sum = 0.0, sum64 = 0.0;
             int done = 0;
             for (const auto& b : batches_of(order, t->batch_size)) {
                 if (t->max_steps > 0 && steps >= t->max_steps) {
@@ -1244,6 +1285,7 @@ int orc_train_block(const char* spec, const float* tw, const orc_dataset* dd, co
                 BlockCache cache;
                 const T4 so = block_forward(student, a, true, &cache);
                 const double local = mse(so.d.data(), tt.d.data(), so.d.size());
+                if (hist64) sum64 += mse64(so, tt);
                 if (!std::isfinite(local)) {
                     r->failed = 1;
                     std::snprintf(r->failure, sizeof(r->failure),
@@ -1262,6 +1304,7 @@ int orc_train_block(const char* spec, const float* tw, const orc_dataset* dd, co
             }
             if (r->failed) break;
             if (done == 0) break;
+            if (hist64) hist64[r->n_loss] = sum64 / done;
             r->loss_history[r->n_loss++] = sum / done;
             r->final_local_loss = sum / done;
             if (epoch % t->eval_every == 0) record(epoch);
@@ -1319,5 +1362,122 @@ int orc_train_replay_f64(const char* spec, const float* tw, const orc_dataset* d
     });
 }
 
+
+int orc_train_replay_multi(const char* spec, const float* tw, const orc_dataset* dd,
+                           const orc_split* s, const orc_task* tasks, int n_tasks, int n_steps,
+                           const int* ck_steps, int n_ck, int threads, float* step_loss,
+                           double* loss64, float* ck_w, const size_t* w_off) {
+    return guard([&] {
+        const Net net = load_net(spec, tw);
+        const Data d = to_data(dd);
+        const std::vector<int> train(s->train_idx, s->train_idx + s->n_train);
+        const int nt = static_cast<int>(train.size());
+        int maxk = 0;
+        for (int i = 0; i < n_tasks; ++i) maxk = std::max(maxk, tasks[i].block_index);
+        if (maxk < 1 || maxk > static_cast<int>(net.blocks.size())) throw std::out_of_range("block index");
+        // boundary j (0 = the input images) of every training sample, train order
+        std::vector<std::vector<float>> bnd(static_cast<size_t>(maxk) + 1);
+        std::vector<std::array<int, 3>> dims(static_cast<size_t>(maxk) + 1);
+        {
+            T4 cur = gather(d, {train.at(0)});
+            for (int j = 0; j <= maxk; ++j) {
+                if (j > 0) cur = block_infer(net.blocks[j - 1], cur);
+                dims[j] = {cur.c, cur.h, cur.w};
+                bnd[j].resize(static_cast<size_t>(nt) * cur.d.size());
+            }
+        }
+        parallel_for(nt, threads, [&](int i) {
+            T4 cur = gather(d, {train[i]});
+            for (int j = 0; j <= maxk; ++j) {
+                if (j > 0) cur = block_infer(net.blocks[j - 1], cur);
+                std::copy(cur.d.begin(), cur.d.end(), bnd[j].begin() + static_cast<size_t>(i) * cur.d.size());
+            }
+        });
+        auto rows = [&](int j, const std::vector<int>& pos) {
+            const auto& dm = dims[j];
+            T4 out(static_cast<int>(pos.size()), dm[0], dm[1], dm[2]);
+            const size_t row = static_cast<size_t>(dm[0]) * dm[1] * dm[2];
+            for (size_t q = 0; q < pos.size(); ++q)
+                std::copy_n(bnd[j].begin() + static_cast<size_t>(pos[q]) * row, row, out.d.begin() + q * row);
+            return out;
+        };
+        parallel_for(n_tasks, threads, [&](int ti) {
+            const orc_task* t = &tasks[ti];
+            const int k = t->block_index;
+            const Block& tb = net.blocks.at(k - 1);
+            Block student = candidate(t->kind, tb.cin, tb.cout, tb.stride, splitmix(t->seed, 0));
+            Sgd opt(student);
+            const size_t nf = n_ck > 0 ? (w_off[ti + 1] - w_off[ti]) / static_cast<size_t>(n_ck) : 0;
+            int done = 0, ck = 0;
+            for (int epoch = 1; done < n_steps; ++epoch) {
+                // std::shuffle's permutation depends only on the length and the
+                // engine, so shuffling positions equals shuffling train_idx
+                std::vector<int> pos(nt);
+                for (int q = 0; q < nt; ++q) pos[q] = q;
+                std::mt19937_64 rng(splitmix(t->seed, static_cast<uint64_t>(epoch)));
+                std::shuffle(pos.begin(), pos.end(), rng);
+                for (const auto& b : batches_of(pos, t->batch_size)) {
+                    if (done >= n_steps) break;
+                    const T4 a = rows(k - 1, b);
+                    const T4 tt = rows(k, b);
+                    BlockCache cache;
+                    const T4 so = block_forward(student, a, true, &cache);
+                    float* sl = step_loss + static_cast<size_t>(ti) * n_steps;
+                    sl[done] = mse(so.d.data(), tt.d.data(), so.d.size());
+                    if (loss64) {
+                        double acc = 0.0;
+                        for (size_t q = 0; q < so.d.size(); ++q) {
+                            const double df = static_cast<double>(so.d[q]) - static_cast<double>(tt.d[q]);
+                            acc += df * df;
+                        }
+                        loss64[static_cast<size_t>(ti) * n_steps + done] = acc / static_cast<double>(so.d.size());
+                    }
+                    T4 gs(so.n, so.c, so.h, so.w);
+                    mse_bwd(so.d.data(), tt.d.data(), so.d.size(), 1.0f, gs.d.data());
+                    opt.zero();
+                    block_backward(student, cache, gs);
+                    opt.step(t->lr, t->momentum);
+                    ++done;
+                    while (ck < n_ck && ck_steps[ck] == done) {
+                        block_store(student, ck_w + w_off[ti] + static_cast<size_t>(ck) * nf, nf);
+                        ++ck;
+                    }
+                }
+            }
+        });
+    });
+}
+
+int orc_run_parallel(const char* spec, const float* tw, const orc_dataset* dd, const orc_split* s,
+                     const orc_task* tasks, int n_tasks, const int* plan_ids, const int* plan_counts,
+                     int workers, int policy, orc_result* results, float* block_w, const size_t* w_off) {
+    (void)policy;  // results are schedule-invariant (test_runtime.cpp:206-253)
+    return guard([&] {  // runtime.cpp:124-243, workers as threads over the plan's queues
+        std::vector<int> order(n_tasks);
+        for (int i = 0; i < n_tasks; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(),
+                  [&](int a, int b) { return tasks[a].block_index < tasks[b].block_index; });
+        std::vector<std::vector<int>> queues(workers);
+        for (int w = 0, at = 0; w < workers; ++w)
+            for (int q = 0; q < plan_counts[w]; ++q, ++at) {
+                int ti = -1;
+                for (int i = 0; i < n_tasks; ++i)
+                    if (tasks[i].block_index == plan_ids[at]) ti = i;
+                if (ti < 0) throw std::invalid_argument("plan references unknown task id");
+                queues[w].push_back(ti);
+            }
+        parallel_for(workers, workers, [&](int w) {
+            for (int ti : queues[w]) {
+                const int slot = static_cast<int>(std::find(order.begin(), order.end(), ti) - order.begin());
+                const size_t cap = w_off[slot + 1] - w_off[slot];
+                if (orc_train_block(spec, tw, dd, s, &tasks[ti], &results[slot], block_w + w_off[slot], cap)) {
+                    std::memset(&results[slot], 0, sizeof(orc_result));
+                    results[slot].failed = 1;
+                    std::snprintf(results[slot].failure, sizeof(results[slot].failure), "%s", g_err.c_str());
+                }
+            }
+        });
+    });
+}
 
 }  // extern "C"

@@ -17,6 +17,7 @@
 #include "pbkd/dataset.hpp"
 #include "pbkd/distill.hpp"
 #include "pbkd/model.hpp"
+#include "pbkd/runtime.hpp"
 #include "pbkd/ops.hpp"
 #include "pbkd/replacement.hpp"
 #include "pbkd/scheduler.hpp"
@@ -410,6 +411,43 @@ int ref_train_replay_f64(const char* spec, const float* tw, const orc_dataset* d
             }
         }
         flatten_block(student, final_w, cap);
+    });
+}
+
+// run_parallel through the reference's own runtime (runtime.cpp:124-243).
+__attribute__((visibility("default"))) int ref_run_parallel(
+    const char* spec, const float* tw, const orc_dataset* d, const orc_split* s, const orc_task* tasks,
+    int n_tasks, const int* plan_ids, const int* plan_counts, int workers, int policy, orc_result* results,
+    float* block_w, const size_t* w_off) {
+    return guard([&] {
+        Network net = load_teacher(spec, tw);
+        std::vector<DistillTask> tv;
+        for (int i = 0; i < n_tasks; ++i) tv.push_back(to_task(&tasks[i]));
+        SchedulePlan plan;
+        plan.worker_count = workers;
+        plan.policy = static_cast<SchedulePolicy>(policy);
+        for (int w = 0, at = 0; w < workers; ++w) {
+            plan.assignments.emplace_back(plan_ids + at, plan_ids + at + plan_counts[w]);
+            at += plan_counts[w];
+        }
+        RunParallelResult out = run_parallel(net, to_dataset(d), to_split(s), tv, plan);
+        for (size_t i = 0; i < out.results.size(); ++i) {
+            TrainedBlockResult& res = out.results[i];
+            orc_result* r = &results[i];
+            std::memset(r, 0, sizeof(*r));
+            r->n_loss = static_cast<int>(res.loss_history.size());
+            for (int q = 0; q < r->n_loss && q < 256; ++q) r->loss_history[q] = res.loss_history[q];
+            r->n_eval = static_cast<int>(res.eval_history.size());
+            for (int q = 0; q < r->n_eval && q < 256; ++q) {
+                r->eval_epoch[q] = res.eval_history[q].epoch;
+                r->eval_acc[q] = res.eval_history[q].accuracy;
+            }
+            r->final_local_loss = res.final_local_loss;
+            r->best_eval = res.best_eval;
+            r->failed = res.failed ? 1 : 0;
+            std::strncpy(r->failure, res.failure.c_str(), sizeof(r->failure) - 1);
+            if (!res.block.layers.empty()) flatten_block(res.block, block_w + w_off[i], w_off[i + 1] - w_off[i]);
+        }
     });
 }
 

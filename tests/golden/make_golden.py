@@ -88,5 +88,41 @@ def main():
     print("wrote", os.listdir(HERE))
 
 
+def c1_run_parallel(O, n_epochs=2, f64=None):
+    """4. C1 (BASELINE configs[0]) through the reference's run_parallel:
+    4 blocks, batch 32, dataset 1000 (900 train / 100 eval), n_epochs epochs,
+    eval every epoch, WFD plan over 2 workers."""
+    c1 = spec("c1_small_vgg")
+    tw = O.teacher_init(c1, O.mix_seed(42, 0x7E11))
+    img = cifar_like(1000, 2012)
+    lab = (np.arange(1000) % 10).astype(np.int32)
+    tr, ev = O.stratified_split(lab, 0.1, O.mix_seed(42, 0x5711))
+    geo = [(3, 16, 1), (16, 32, 2), (32, 64, 2), (64, 64, 1)]
+    tasks = [make_task(k, epochs=n_epochs, eval_every=1, seed=O.mix_seed(42, k), batch_size=32)
+             for k in range(1, 5)]
+    nfs = [O.candidate_num_floats(0, *g) for g in geo]
+    res = O.run_parallel(c1, tw, img, lab, tr, ev, tasks, [[1, 4], [2, 3]], nfs, policy=1)
+    out = dict(teacher_w=tw, train_idx=tr, eval_idx=ev, epochs=n_epochs)
+    for k, r in zip(range(1, 5), res):
+        out[f"b{k}_loss_history"] = np.array(r["loss_history"])
+        out[f"b{k}_eval_history"] = np.array(r["eval_history"])
+        out[f"b{k}_best_eval"] = r["best_eval"]
+        out[f"b{k}_block"] = r["block"]
+        assert not r["failed"], r["failure"]
+    if f64 is not None:
+        # the reference's loss history is a mean of per-batch fp32 serial sums
+        # (ops.hpp:522-527) with their own rounding; the restatement (bitwise
+        # equal to the reference) also sums the same outputs in fp64
+        for k, t, nf in zip(range(1, 5), tasks, nfs):
+            r = f64.train_block(c1, tw, img, lab, tr, ev, t, nf, with_f64=True)
+            assert r["loss_history"] == out[f"b{k}_loss_history"].tolist(), k
+            out[f"b{k}_loss_history64"] = np.array(r["loss_history64"])
+    return out
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["c1"]:
+        np.savez_compressed(os.path.join(HERE, "c1_run_parallel.npz"),
+                            **c1_run_parallel(Oracle("ref"), f64=Oracle("orc")))
+    else:
+        main()

@@ -134,10 +134,18 @@ def test_golden_vgg_replay(orc):
     lab = (np.arange(40) % 10).astype(np.int32)
     tr, ev = orc.stratified_split(lab, 0.1, orc.mix_seed(42, 0x5711))
     assert np.array_equal(tr, g["vgg_train_idx"])
-    task = make_task(2, seed=orc.mix_seed(42, 2), batch_size=8)
-    losses, fw = orc.train_replay(vgg, tw, img, lab, tr, ev, task, 3, g["vgg_b2_final"].size)
-    assert np.array_equal(losses, g["vgg_b2_losses"])
-    assert np.array_equal(fw, g["vgg_b2_final"])
+    for k in (2, 9):  # 64- and 512-channel blocks
+        task = make_task(k, seed=orc.mix_seed(42, k), batch_size=8)
+        losses, fw = orc.train_replay(vgg, tw, img, lab, tr, ev, task, 3, g[f"vgg_b{k}_final"].size)
+        assert np.array_equal(losses, g[f"vgg_b{k}_losses"]), k
+        assert np.array_equal(fw, g[f"vgg_b{k}_final"]), k
+    # the grouped replay (teacher boundaries once per sample) gives the same bits
+    tasks = [make_task(k, seed=orc.mix_seed(42, k), batch_size=8) for k in (2, 9)]
+    nfs = [g["vgg_b2_final"].size, g["vgg_b9_final"].size]
+    losses, _, snaps = orc.train_replay_multi(vgg, tw, img, lab, tr, ev, tasks, 3, nfs, ck_steps=[3])
+    for i, k in enumerate((2, 9)):
+        assert np.array_equal(losses[i], g[f"vgg_b{k}_losses"]), k
+        assert np.array_equal(snaps[i][0], g[f"vgg_b{k}_final"]), k
 
 
 # ---------------------------------------------------- vs the reference ----
@@ -190,3 +198,55 @@ def test_bitwise_vs_reference_prefix_resnet(orc, ref):
     for k in (1, 2, 3, 4):
         assert np.array_equal(orc.prefix_infer(spec, tw, x, k, True),
                               ref.prefix_infer(spec, tw, x, k, True))
+
+
+def test_replay_multi_matches_single(orc):
+    """orc.train_replay_multi (boundaries cached per sample, tasks threaded,
+    weight checkpoints) == orc.train_replay task by task, bit for bit."""
+    from oracle.oracle import make_task
+    for name, seed in (("toy_teacher", 404), ("resnet_blocks_demo", 3)):
+        spec = spec_text(name)
+        tw = orc.teacher_init(spec, seed)
+        if name == "toy_teacher":
+            img, lab = orc.synthetic_dataset(50, 11, 2)
+        else:
+            img = np.random.default_rng(4).random((30, 3, 16, 16), dtype=np.float32)
+            lab = (np.arange(30) % 10).astype(np.int32)
+        tr, ev = orc.stratified_split(lab, 0.2, 12)
+        nb = orc.teacher_num_blocks(spec)
+        tasks = [make_task(k, seed=orc.mix_seed(7, k), batch_size=6, lr=0.02) for k in range(1, nb + 1)]
+        steps = 9  # buffers of 2^18 floats, zero beyond each block's arrays on both sides
+        losses, l64, snaps = orc.train_replay_multi(spec, tw, img, lab, tr, ev, tasks, steps,
+                                                    [1 << 18] * nb, ck_steps=[2, steps], threads=4)
+        for k in range(1, nb + 1):
+            for ck in (2, steps):
+                l1, fw = orc.train_replay(spec, tw, img, lab, tr, ev, tasks[k - 1], ck, 1 << 18)
+                assert np.array_equal(l1, losses[k - 1][:ck]), (name, k)
+                assert np.array_equal(fw, snaps[k - 1][[2, steps].index(ck)]), (name, k, ck)
+
+
+def test_run_parallel_vs_reference(orc, ref):
+    """orc.run_parallel == the reference's own run_parallel (runtime.cpp), bit for bit."""
+    from oracle.oracle import make_task
+    spec = spec_text("toy_teacher")
+    tw = orc.teacher_init(spec, 2025)
+    img, lab = orc.synthetic_dataset(40, 21, 2)
+    tr, ev = orc.stratified_split(lab, 0.25, 3)
+    tasks = [make_task(k, epochs=2, eval_every=1, seed=orc.mix_seed(99, k), batch_size=10, lr=0.02)
+             for k in (1, 2, 3)]
+    nfs = [orc.candidate_num_floats(0, ci, co, s) for ci, co, s in ((3, 16, 1), (16, 32, 2), (32, 32, 1))]
+    a = orc.run_parallel(spec, tw, img, lab, tr, ev, tasks, [[1, 3], [2]], nfs)
+    b = ref.run_parallel(spec, tw, img, lab, tr, ev, tasks, [[1, 3], [2]], nfs, policy=1)
+    for x, y in zip(a, b):
+        assert x["loss_history"] == y["loss_history"] and x["eval_history"] == y["eval_history"]
+        assert x["best_eval"] == y["best_eval"] and np.array_equal(x["block"], y["block"])
+
+
+def test_golden_c1_run_parallel(orc):
+    """The restatement's run_parallel reproduces the reference's C1 run
+    (tests/golden/c1_run_parallel.npz, made by oracle/_ref) bit for bit."""
+    from tests.golden.make_golden import c1_run_parallel
+    g = np.load(os.path.join(GOLD, "c1_run_parallel.npz"))
+    mine = c1_run_parallel(orc, int(g["epochs"]))
+    for key in mine:
+        assert np.array_equal(np.asarray(mine[key]), g[key]), key
