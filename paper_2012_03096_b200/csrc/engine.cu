@@ -783,6 +783,11 @@ struct Engine::Impl {
         if (t.lambda_local < 0) throw SpecError("lambda_local must be non-negative");
         if (t.threshold < 0.0 || t.threshold > 1.0) throw SpecError("threshold must lie in [0,1]");
         if (t.max_steps < 0) throw SpecError("max_steps must be non-negative");
+        // SgdState::step -> ops::sgd_step (ops.hpp:545-548) rejects these on the
+        // first step; train_block propagates it (run_parallel: failed result)
+        if (!(t.lr > 0.0f)) throw std::invalid_argument("sgd_step: lr must be > 0");
+        if (t.momentum < 0.0f || t.momentum >= 1.0f)
+            throw std::invalid_argument("sgd_step: momentum must be in [0,1)");
         const std::vector<int> ok = pbkd::identify_replaceable(net);
         if (!std::binary_search(ok.begin(), ok.end(), t.block_index))
             throw SpecError("block " + std::to_string(t.block_index) + " of '" + net.name +
