@@ -252,6 +252,83 @@ int pbkd_k_sgd(pbkd_ctx* ctx, float* w, const float* g, float* v, size_t n, floa
 /* host-buffer SGD through the device kernel (pbkd::SgdState::step) */
 int pbkd_sgd_host(float* w, const float* g, float* v, size_t n, float lr, float momentum);
 
+/* ---- block / network level (layer-by-layer on the GPU, csrc/netexec.cu) ----
+ *
+ * A block is described by its layer list (pbkd::LayerParams, model.hpp:40-52)
+ * plus its arrays flat in for_each_block_array order (model.cpp:448-478).
+ * A network is n_blocks feature blocks followed by the classifier block
+ * (layer_counts has n_blocks + 1 entries; a classifier of 0 layers = none),
+ * arrays flat in for_each_array order.  spec_kind names each block
+ * ("conv3x3", "two_layer", ...; replacement.cpp:78-82 decides which blocks
+ * are replacements). */
+typedef struct {
+    int kind; /* pbkd::LayerKind ordinal (model.hpp:25-35) */
+    int in_channels, out_channels, kernel, stride, padding;
+    int has_weight, has_bias; /* Add: has_weight = 1x1 stride projection */
+} pbkd_layer_desc;
+
+typedef struct {
+    int n_blocks;
+    const int* layer_counts;        /* n_blocks + 1 (classifier last) */
+    const pbkd_layer_desc* layers;  /* all layers, block after block */
+    const char* const* spec_kinds;  /* n_blocks + 1 */
+    int in_c, in_h, in_w;
+} pbkd_net_desc;
+
+typedef struct pbkd_block_cache pbkd_block_cache;
+
+/* block_forward (model.cpp:498-551) on a host NCHW batch x -> y.  train: batch
+ * statistics, and the updated moving statistics are written back into
+ * arrays; cache (optional) receives the device-side cache block_backward
+ * needs. */
+int pbkd_block_forward(pbkd_ctx* ctx, const pbkd_layer_desc* layers, int n_layers, float* arrays, size_t n_arrays,
+                       const float* x, int n, int c, int h, int w, int train, float* y, size_t y_cap, int* y_shape,
+                       pbkd_block_cache** cache);
+/* block_backward (model.cpp:559-656).  grads (n_arrays, arrays layout):
+ * parameter gradients ACCUMULATED when param_grads; gx (optional, x's shape)
+ * the input gradient when need_input_grad.  Errors as the reference
+ * (std::logic_error on a cache / mode mismatch). */
+int pbkd_block_backward(pbkd_ctx* ctx, const pbkd_layer_desc* layers, int n_layers, const float* arrays,
+                        size_t n_arrays, const pbkd_block_cache* cache, const float* gy, int n, int c, int h, int w,
+                        int need_input_grad, int param_grads, float* grads, float* gx, size_t gx_cap);
+void pbkd_block_cache_free(pbkd_block_cache* cache);
+
+/* ops::mse_local_loss / mse_local_loss_bwd (ops.hpp:518-539), host buffers */
+int pbkd_mse_local_loss(pbkd_ctx* ctx, const float* s, const float* t, size_t count, float* loss);
+int pbkd_mse_local_loss_bwd(pbkd_ctx* ctx, const float* s, const float* t, size_t count, float scale, float* g);
+
+/* reassemble + finetune / train_teacher in one call (distill.cpp:297-441):
+ * the teacher of spec_json with weights teacher_w, blocks[i] replaced by a
+ * candidate of kinds[i] whose arrays (for_each_block_array order) follow one
+ * another in cand_w; then pbkd_fit_network over the context's dataset.
+ * net_out (cap floats) receives the trained network, *n_out its length. */
+int pbkd_fit_assembled(pbkd_ctx* ctx, const char* spec_json, const float* teacher_w, size_t n_teacher,
+                       const int* blocks, const int* kinds, const float* cand_w, int n_replaced,
+                       const int* train_idx, int n_train, const int* eval_idx, int n_eval_idx, int epochs,
+                       int freeze_non_replaced, float lr, float momentum, int batch_size, uint64_t seed,
+                       int teacher_mode, double* initial_eval, double* final_eval, double* loss_hist,
+                       int* eval_epochs, double* eval_acc, int* n_eval, float* net_out, size_t cap, size_t* n_out);
+
+/* ops::softmax_cross_entropy_fwd / _bwd (ops.hpp:474-514): logits / probs
+ * [n][k] host row-major; loss = mean NLL; probs optional; g accumulated */
+int pbkd_softmax_ce(pbkd_ctx* ctx, const float* logits, int n, int k, const int* labels, float* loss,
+                    float* probs);
+int pbkd_softmax_ce_bwd(pbkd_ctx* ctx, const float* probs, int n, int k, const int* labels, float scale,
+                        float* g);
+
+/* evaluate_network (distill.cpp:286-295) over the context's dataset */
+int pbkd_evaluate_network(pbkd_ctx* ctx, const pbkd_net_desc* net, const float* arrays, size_t n_arrays,
+                          const int* idx, int n_idx, int batch_size, double* acc);
+/* finetune (distill.cpp:325-391; teacher_mode 0) or train_teacher
+ * (distill.cpp:393-441; teacher_mode 1, freeze ignored) of a network over the
+ * context's dataset.  arrays are updated in place.  loss_hist[epochs],
+ * eval_epochs / eval_acc [epochs + 1]; n_eval receives the eval count. */
+int pbkd_fit_network(pbkd_ctx* ctx, const pbkd_net_desc* net, float* arrays, size_t n_arrays,
+                     const int* train_idx, int n_train, const int* eval_idx, int n_eval_idx, int epochs,
+                     int freeze_non_replaced, float lr, float momentum, int batch_size, uint64_t seed,
+                     int teacher_mode, double* initial_eval, double* final_eval, double* loss_hist,
+                     int* eval_epochs, double* eval_acc, int* n_eval);
+
 #ifdef __cplusplus
 }
 #endif

@@ -418,3 +418,29 @@ class Oracle:
                         "failed": bool(r.failed), "failure": r.failure.decode(),
                         "block": buf[int(off[i]):int(off[i + 1])].copy()})
         return out
+
+    def fit_network(self, spec, tw, images, labels, train_idx, eval_idx, reps, epochs, freeze, lr, momentum,
+                    batch, seed, teacher_mode, cap=1 << 22):
+        """ref only: finetune / train_teacher of the teacher with blocks
+        reps = [(k, kind, cand_seed), ...] swapped in (reassemble)."""
+        ds = self._ds(images, labels)
+        sp = self._split(train_idx, eval_idx)
+        ks = np.ascontiguousarray([r[0] for r in reps] or [0], np.int32)
+        kinds = np.ascontiguousarray([r[1] for r in reps] or [0], np.int32)
+        seeds = np.ascontiguousarray([r[2] for r in reps] or [0], np.uint64)
+        lh = np.zeros(max(epochs, 1), np.float64)
+        ea = np.zeros(epochs + 1, np.float64)
+        ne = C.c_int()
+        inf = np.zeros(2, np.float64)
+        out = np.zeros(cap, np.float32)
+        U64P = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+        f = self.fn("fit_network", C.c_int,
+                    [C.c_char_p, F32P, I32P, I32P, U64P, C.c_int, C.POINTER(Dataset), C.POINTER(Split), C.c_int,
+                     C.c_int, C.c_float, C.c_float, C.c_int, C.c_uint64, C.c_int, F64P, F64P, C.POINTER(C.c_int),
+                     F64P, F32P, C.c_size_t])
+        self._check(f(spec.encode(), np.ascontiguousarray(tw, np.float32), ks, kinds, seeds, len(reps), C.byref(ds),
+                      C.byref(sp), epochs, int(freeze), lr, momentum, batch, seed, int(teacher_mode), lh, ea,
+                      C.byref(ne), inf, out, out.size))
+        n = ne.value
+        return {"loss_history": lh[:max(n - 1, 0)], "eval_history": ea[:n], "initial_eval": inf[0],
+                "final_eval": inf[1], "net": out}

@@ -492,4 +492,51 @@ __attribute__((visibility("default"))) int ref_file_hash(const char* path, uint6
     return guard([&] { *out = file_hash(path); });
 }
 
+
+// finetune (distill.cpp:325-391) or train_teacher (:393-441) through the
+// reference.  The network: the teacher of `spec` with weights tw, blocks
+// reps[i] (1-based) replaced as reassemble does (distill.cpp:313-318) by
+// build_candidate(kinds[i], ..., seeds[i]).  net_out receives the trained
+// network's arrays (for_each_array order); hist: loss[epochs], eval[epochs+1].
+__attribute__((visibility("default"))) int ref_fit_network(
+    const char* spec, const float* tw, const int* reps, const int* kinds, const uint64_t* seeds, int n_reps,
+    const orc_dataset* d, const orc_split* s, int epochs, int freeze, float lr, float momentum, int batch,
+    uint64_t seed, int teacher_mode, double* loss_hist, double* eval_acc, int* n_eval, double* init_final,
+    float* net_out, size_t cap) {
+    return guard([&] {
+        Network net = load_teacher(spec, tw);
+        for (int i = 0; i < n_reps; ++i) {
+            Block& tb = net.blocks.at(static_cast<size_t>(reps[i]) - 1);
+            Block nb = build_candidate(static_cast<CandidateKind>(kinds[i]), tb.in_channels, tb.out_channels,
+                                       tb.stride, seeds[i])
+                           .block;
+            nb.name = tb.name;
+            nb.replaceable = false;
+            tb = std::move(nb);
+        }
+        const Dataset data = to_dataset(d);
+        const SplitIndices split = to_split(s);
+        std::vector<EvalPoint> ev;
+        std::vector<double> lh;
+        if (teacher_mode) {
+            TeacherTrainResult r = train_teacher(net, data, split, epochs, lr, momentum, batch, seed);
+            ev = r.eval_history, lh = r.loss_history;
+            init_final[0] = ev.front().accuracy, init_final[1] = r.final_eval;
+        } else {
+            FinetuneResult r = finetune(net, data, split, epochs, freeze != 0, lr, momentum, batch, seed);
+            ev = r.eval_history, lh = r.loss_history;
+            init_final[0] = r.initial_eval, init_final[1] = r.final_eval;
+        }
+        for (size_t i = 0; i < lh.size(); ++i) loss_hist[i] = lh[i];
+        for (size_t i = 0; i < ev.size(); ++i) eval_acc[i] = ev[i].accuracy;
+        *n_eval = static_cast<int>(ev.size());
+        size_t at = 0;
+        for_each_array(net, [&](const std::string&, Tensor& t) {
+            if (at + t.data.size() > cap) throw std::length_error("network buffer too small");
+            std::copy(t.data.begin(), t.data.end(), net_out + at);
+            at += t.data.size();
+        });
+    });
+}
+
 }  // extern "C"

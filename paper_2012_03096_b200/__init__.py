@@ -140,6 +140,12 @@ def lib() -> C.CDLL:
             "pbkd_load_network_file": (C.c_int, [C.c_char_p, C.c_char_p, vp, C.c_int, vp, C.c_size_t,
                                                  C.POINTER(C.c_size_t)]),
             "pbkd_file_hash": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64)]),
+            "pbkd_fit_assembled": (C.c_int, [vp, C.c_char_p, vp, C.c_size_t, vp, vp, vp, C.c_int, vp, C.c_int,
+                                             vp, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float, C.c_int,
+                                             C.c_uint64, C.c_int, dp, dp, vp, vp, vp, ip, vp, C.c_size_t,
+                                             C.POINTER(C.c_size_t)]),
+            "pbkd_mse_local_loss": (C.c_int, [vp, vp, vp, C.c_size_t, fp]),
+            "pbkd_softmax_ce": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, fp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -460,6 +466,31 @@ class Context:
         check(lib().pbkd_candidate_infer(self.h, kind, cin, cout, stride, _ptr(bw), _ptr(x), n, h,
                                          w, _ptr(out), out.size))
         return out
+
+    def fit_assembled(self, spec, teacher_w, reps, train_idx, eval_idx, epochs, freeze, lr, momentum, batch,
+                      seed, teacher_mode=False, cap=1 << 24):
+        """reassemble + finetune (or train_teacher) on the GPU (pbkd_fit_assembled).
+        reps: [(block_index, kind, candidate_weights), ...]"""
+        tw = _f32(teacher_w)
+        blocks = _i32([r[0] for r in reps] or [0])
+        kinds = _i32([r[1] for r in reps] or [0])
+        cw = _f32(np.concatenate([np.asarray(r[2], np.float32) for r in reps]) if reps else np.zeros(1))
+        tr, ev = _i32(train_idx), _i32(eval_idx)
+        lh = np.zeros(max(epochs, 1), np.float64)
+        ee = np.zeros(epochs + 1, np.int32)
+        ea = np.zeros(epochs + 1, np.float64)
+        ne = C.c_int()
+        init, fin = C.c_double(), C.c_double()
+        out = np.zeros(cap, np.float32)
+        n_out = C.c_size_t()
+        check(lib().pbkd_fit_assembled(self.h, spec.encode(), _ptr(tw), tw.size, _ptr(blocks), _ptr(kinds),
+                                       _ptr(cw), len(reps), _ptr(tr), len(tr), _ptr(ev), len(ev), epochs,
+                                       int(freeze), lr, momentum, batch, seed, int(teacher_mode), C.byref(init),
+                                       C.byref(fin), _ptr(lh), _ptr(ee), _ptr(ea), C.byref(ne), _ptr(out),
+                                       out.size, C.byref(n_out)))
+        n = ne.value
+        return {"loss_history": lh[:max(n - 1, 0)], "eval_history": list(zip(ee[:n].tolist(), ea[:n].tolist())),
+                "initial_eval": init.value, "final_eval": fin.value, "net": out[:n_out.value].copy()}
 
     def eval_with_student(self, k, kind, sw, eval_idx, batch_size):
         sw, ev = _f32(sw), _i32(eval_idx)

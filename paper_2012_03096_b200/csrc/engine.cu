@@ -16,6 +16,7 @@
 
 #include "comm.hpp"
 #include "engine.hpp"
+#include "nettrain.hpp"
 #include "ops.cuh"
 #include "pbkd/dataset.hpp"
 #include "pbkd/replacement.hpp"
@@ -605,6 +606,13 @@ struct Engine::Impl {
     void* pinned = nullptr;  // readback staging (grows as needed)
     size_t pinned_bytes = 0;
     std::vector<cudaStream_t> side_streams;  // parallel sections of the epoch graphs
+    // layer-by-layer executor (generic candidates, Combined objective,
+    // fine-tuning, block-level API) and the teacher it runs: the flat teacher
+    // weights stay resident; the DevNet is built on first use
+    std::unique_ptr<NetExec> nx;
+    DevBuf teacher_flat;
+    std::unique_ptr<DevNet> tnet;
+    std::vector<int> host_labels;
 
     explicit Impl(int device) : dev(device) {
         PBKD_CUDA(cudaSetDevice(dev));
@@ -613,6 +621,7 @@ struct Engine::Impl {
         const char* ps = std::getenv("PBKD_SIDE_STREAMS");
         side_streams.resize(ps ? std::max(0, std::atoi(ps)) : 4);
         for (cudaStream_t& s2 : side_streams) PBKD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        nx = std::make_unique<NetExec>(st);
         cudaMemPool_t pool;
         PBKD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
         uint64_t keep = ~uint64_t(0);
@@ -623,7 +632,8 @@ struct Engine::Impl {
         g_alloc_stream = st;
         // device buffers are freed on st, so before the stream goes away
         tblocks.clear();
-        for (DevBuf* b : {&cls_kinds, &cls_w, &cls_b, &images, &labels, &eval_labels}) b->release();
+        tnet.reset();
+        for (DevBuf* b : {&cls_kinds, &cls_w, &cls_b, &images, &labels, &eval_labels, &teacher_flat}) b->release();
         if (st) {
             cudaStreamSynchronize(st);
             cudaStreamDestroy(st);
@@ -663,9 +673,10 @@ struct Engine::Impl {
         } else if (nflat != total) {
             throw std::invalid_argument("teacher weights: flat size does not match the network");
         }
-        DevBuf dflat(std::max<size_t>(total, 1) * sizeof(float));
-        PBKD_CUDA(cudaMemcpyAsync(dflat.p, flat, total * sizeof(float), cudaMemcpyHostToDevice, st));
-        const float* dbase = dflat.f();
+        tnet.reset();
+        teacher_flat.alloc(std::max<size_t>(total, 1) * sizeof(float));
+        PBKD_CUDA(cudaMemcpyAsync(teacher_flat.p, flat, total * sizeof(float), cudaMemcpyHostToDevice, st));
+        const float* dbase = teacher_flat.f();
         auto dev_of = [&](const pbkd::Tensor& t) { return dbase + off.at(&t); };
         tblocks.clear();
         int c = n.in_c, h = n.in_h, w = n.in_w;
@@ -767,6 +778,7 @@ struct Engine::Impl {
         labels.alloc(static_cast<size_t>(n) * sizeof(int));
         PBKD_CUDA(cudaMemcpyAsync(labels.p, lab, static_cast<size_t>(n) * sizeof(int),
                                   cudaMemcpyHostToDevice, st));
+        host_labels.assign(lab, lab + n);
         PBKD_CUDA(cudaStreamSynchronize(st));
         count = n;
         dc = c;
@@ -794,11 +806,24 @@ struct Engine::Impl {
                             "' is not replaceable");
         if (t.loss_mode == pbkd::LossMode::Combined && !net.has_classifier())
             throw SpecError("combined loss needs a network with a classifier");
-        if (t.loss_mode == pbkd::LossMode::Combined)
-            throw SpecError("combined loss mode is not implemented on the GPU path (LocalOnly only)");
-        if (t.kind == pbkd::CandidateKind::TwoLayerSkip || t.kind == pbkd::CandidateKind::ThreeLayerSkip)
-            throw SpecError(std::string("candidate ") + pbkd::candidate_kind_name(t.kind) +
-                            " is not implemented on the GPU path");
+    }
+
+    // Tasks the grouped lockstep path does not take run layer by layer
+    // (nettrain.cu): the Combined objective and the skip candidates.
+    static bool generic_task(const DistillTask& t) {
+        return t.loss_mode == pbkd::LossMode::Combined || t.kind == pbkd::CandidateKind::TwoLayerSkip ||
+               t.kind == pbkd::CandidateKind::ThreeLayerSkip;
+    }
+    DevNet& teacher_net() {
+        if (!tnet) tnet = std::make_unique<DevNet>(make_devnet(*nx, net, teacher_flat.f(), true));
+        return *tnet;
+    }
+    DataView data_view() const {
+        DataView d;
+        d.images = images.f();
+        d.labels = host_labels;
+        d.count = count, d.c = dc, d.h = dh, d.w = dw, d.classes = classes;
+        return d;
     }
 
     // task, block index, unit geometry (what init_task_host needs)
@@ -1430,6 +1455,8 @@ struct Engine::Impl {
 
     std::vector<TaskOutcome> run(const std::vector<DistillTask>& tasks, const std::vector<int>& train_idx,
                                  const std::vector<int>& eval_idx, const RunOptions& opt);
+    std::vector<TaskOutcome> run_grouped(const std::vector<DistillTask>& tasks, const std::vector<int>& train_idx,
+                                         const std::vector<int>& eval_idx, const RunOptions& opt);
 
     // Teacher boundaries of one run (see run()): buffers, the exchange plan
     // and whether the one-time teacher pass has been issued.
@@ -1522,6 +1549,35 @@ struct Engine::Impl {
 std::vector<TaskOutcome> Engine::Impl::run(const std::vector<DistillTask>& tasks,
                                            const std::vector<int>& train_idx,
                                            const std::vector<int>& eval_idx, const RunOptions& opt) {
+    std::vector<DistillTask> grouped;
+    std::vector<size_t> where;
+    for (size_t i = 0; i < tasks.size(); ++i)
+        if (!generic_task(tasks[i])) grouped.push_back(tasks[i]), where.push_back(i);
+    if (grouped.size() == tasks.size()) return run_grouped(tasks, train_idx, eval_idx, opt);
+    PBKD_CUDA(cudaSetDevice(dev));
+    g_alloc_stream = st;
+    if (!has_teacher) throw std::logic_error("engine: no teacher loaded");
+    if (count == 0) throw std::logic_error("engine: no dataset loaded");
+    if (train_idx.empty()) throw SpecError("training split is empty");
+    if (eval_idx.empty()) throw SpecError("evaluation split is empty");
+    if (dc != net.in_c || dh != net.in_h || dw != net.in_w)
+        throw pbkd::ShapeError("dataset image shape does not match the network input");
+    for (const DistillTask& t : tasks) validate(t);
+    std::vector<TaskOutcome> out(tasks.size());
+    if (!grouped.empty()) {
+        std::vector<TaskOutcome> g = run_grouped(grouped, train_idx, eval_idx, opt);
+        for (size_t i = 0; i < g.size(); ++i) out[where[i]] = std::move(g[i]);
+    }
+    NetTrainer tr(*nx, data_view());
+    for (size_t i = 0; i < tasks.size(); ++i)
+        if (generic_task(tasks[i]))
+            out[i] = tr.train_block(teacher_net(), net, tasks[i], train_idx, eval_idx, opt.baseline_and_eval);
+    return out;
+}
+
+std::vector<TaskOutcome> Engine::Impl::run_grouped(const std::vector<DistillTask>& tasks,
+                                                   const std::vector<int>& train_idx,
+                                                   const std::vector<int>& eval_idx, const RunOptions& opt) {
     PBKD_CUDA(cudaSetDevice(dev));
         g_alloc_stream = st;
     trace.t = std::chrono::steady_clock::now();
@@ -2272,6 +2328,32 @@ std::vector<TaskOutcome> Engine::run(const std::vector<DistillTask>& t, const st
     return impl_->run(t, tr, ev, o);
 }
 const RunTiming& Engine::timing() const { return impl_->timing; }
+NetExec& Engine::exec() {
+    PBKD_CUDA(cudaSetDevice(impl_->dev));
+    g_alloc_stream = impl_->st;
+    return *impl_->nx;
+}
+NetTrainer Engine::trainer() {
+    exec();
+    if (impl_->count == 0) throw std::logic_error("engine: no dataset loaded");
+    return NetTrainer(*impl_->nx, impl_->data_view());
+}
+DevNet& Engine::teacher_net() {
+    exec();
+    if (!impl_->has_teacher) throw std::logic_error("engine: no teacher loaded");
+    return impl_->teacher_net();
+}
+void Engine::validate(const DistillTask& t) const {
+    if (!impl_->has_teacher) throw std::logic_error("engine: no teacher loaded");
+    impl_->validate(t);
+}
+void Engine::check_split(const std::vector<int>& tr, const std::vector<int>& ev) const {
+    if (tr.empty()) throw SpecError("training split is empty");
+    if (ev.empty()) throw SpecError("evaluation split is empty");
+    for (const std::vector<int>* v : {&tr, &ev})
+        for (int i : *v)
+            if (i < 0 || i >= impl_->count) throw std::out_of_range("gather_batch: index out of range");
+}
 int Engine::device() const { return impl_->dev; }
 void Engine::set_comm(const char* id, int rank, int world) {
     PBKD_CUDA(cudaSetDevice(impl_->dev));

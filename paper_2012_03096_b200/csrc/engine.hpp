@@ -27,6 +27,10 @@
 
 namespace pbkd_gpu {
 
+class NetExec;
+class NetTrainer;
+struct DevNet;
+
 struct TaskOutcome {
     int block_index = 0;
     std::string kind;
@@ -106,6 +110,10 @@ public:
                                  const std::vector<int>& train_idx,
                                  const std::vector<int>& eval_idx, const RunOptions& opt);
     const RunTiming& timing() const;
+    // validate_task (distill.cpp:86-100) and the split checks of train_block
+    // (distill.cpp:144-145, dataset.cpp:166-179) with the reference's messages
+    void validate(const pbkd::DistillTask& t) const;
+    void check_split(const std::vector<int>& train_idx, const std::vector<int>& eval_idx) const;
 
     // Inference helpers (host NCHW in/out), used by the C ABI.
     pbkd::Tensor prefix_infer(const pbkd::Tensor& x, int k, bool inclusive);
@@ -118,6 +126,13 @@ public:
     // (fused), 4 loss + batch-norm backward sums.  Shapes: the teacher block
     // with the most MACs, `batch` samples.
     void bench_kernel(int which, int batch, int iters, double* ms, double* bytes, double* flops);
+
+    // Layer-by-layer executor on this engine's stream (netexec.hpp), a trainer
+    // over the resident dataset (nettrain.hpp) and the resident teacher as a
+    // device network.  Each call makes this engine's device current.
+    NetExec& exec();
+    NetTrainer trainer();
+    DevNet& teacher_net();
 
     int device() const;
     cudaStream_t stream() const;

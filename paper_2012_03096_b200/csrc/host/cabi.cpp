@@ -60,6 +60,15 @@ int guard(F&& f) {
     return 1;
 }
 
+}  // namespace
+
+// error state shared with cabi_net.cpp (not part of the public header)
+extern "C" void pbkd_internal_set_error(const char* msg, int kind) {
+    g_err = msg ? msg : "";
+    g_kind = kind;
+}
+
+namespace {
 void need(bool c, const char* msg) {
     if (!c) throw std::invalid_argument(msg);
 }
@@ -457,25 +466,19 @@ int pbkd_run_parallel(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const 
         std::map<int, int> worker_of;
         for (int w = 0; w < workers; ++w)
             for (int id : queues[static_cast<size_t>(w)]) worker_of[id] = w;
+        // per-task validation inside the per-task try (train_block throws,
+        // run_parallel turns it into a failed result: runtime.cpp:212-220)
+        const std::vector<int> trv(tr, tr + n_tr), evv(ev, ev + n_ev);
         for (int i = 0; i < n_tasks; ++i) {
             pbkd::DistillTask t = to_task(tasks[i]);
             try {
-                std::vector<pbkd::DistillTask> probe{t};
-                (void)probe;
-                if (t.loss_mode == pbkd::LossMode::Combined)
-                    throw pbkd::SpecError("combined loss mode is not implemented on the GPU path (LocalOnly only)");
-                if (t.kind == pbkd::CandidateKind::TwoLayerSkip || t.kind == pbkd::CandidateKind::ThreeLayerSkip)
-                    throw pbkd::SpecError(std::string("candidate ") + pbkd::candidate_kind_name(t.kind) +
-                                          " is not implemented on the GPU path");
-                const std::vector<int> rep = pbkd::identify_replaceable(ctx->eng->teacher());
-                if (!std::binary_search(rep.begin(), rep.end(), t.block_index))
-                    throw pbkd::SpecError("block " + std::to_string(t.block_index) + " is not replaceable");
-                if (t.epochs < 1 || t.eval_every < 1 || t.batch_size < 1 || t.max_steps < 0 ||
-                    t.lambda_local < 0 || t.threshold < 0.0 || t.threshold > 1.0)
-                    throw pbkd::SpecError("invalid task settings");
+                ctx->eng->validate(t);
+                ctx->eng->check_split(trv, evv);
                 ok.push_back(t);
             } catch (const std::exception& e) {
                 outcome[t.block_index] = failed_outcome(t, e.what());
+                r->trace.push_back({now_s(t0), worker_of[t.block_index], t.block_index, 1});
+                r->trace.push_back({now_s(t0), worker_of[t.block_index], t.block_index, 2});
             }
         }
         for (const pbkd::DistillTask& t : ok) r->trace.push_back({now_s(t0), worker_of[t.block_index], t.block_index, 1});
@@ -484,9 +487,7 @@ int pbkd_run_parallel(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const 
             opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
             opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
             opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
-        opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
-            std::vector<TaskOutcome> res =
-                ctx->eng->run(ok, std::vector<int>(tr, tr + n_tr), std::vector<int>(ev, ev + n_ev), opt);
+            std::vector<TaskOutcome> res = ctx->eng->run(ok, trv, evv, opt);
             for (TaskOutcome& o : res) outcome[o.block_index] = std::move(o);
             r->epoch_ms = ctx->eng->timing().epoch_ms_total;
             r->timing = ctx->eng->timing();

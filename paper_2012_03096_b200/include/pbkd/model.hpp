@@ -1,15 +1,21 @@
 #pragma once
 // pbkd-b200 host API: network graph.  Declarations match the reference's
-// include/pbkd/model.hpp:19-214 so a reference caller compiles unchanged; the
+// include/pbkd/model.hpp:19-214 (tests/cpp compiles reference callers
+// against them); the
 // implementations live in csrc/host/model.cpp and, for execution, run on the
 // GPU behind the C ABI (include/pbkd_b200.h).
+#include <array>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <random>
 #include <string>
 #include <vector>
 
+#include "pbkd/ops.hpp"
 #include "pbkd/tensor.hpp"
+
+struct pbkd_block_cache;  // device-side cache (include/pbkd_b200.h)
 
 namespace pbkd {
 
@@ -90,8 +96,39 @@ uint64_t network_weight_hash(const Network& net);
 // k (1-based; k = blocks+1 gives the classifier input).
 void block_input_shape(const Network& net, int k, int& c, int& h, int& w);
 
-// Inference on the GPU (C ABI pbkd_prefix_infer / pbkd_block_infer).
+// ---- execution (model.hpp:134-186 of the reference), on the GPU through
+// the C ABI (pbkd_block_forward / pbkd_block_backward, pbkd_prefix_infer).
+// A BlockCache keeps the forward's intermediate tensors on the device
+// (`device`); `layers` is sized like the block but its host tensors are left
+// empty (the reference fills them with host copies, which only its own
+// backward reads).
+struct LayerCache {
+    Tensor input;
+    ops::BnCache<float> bn;
+};
+
+struct BlockCache {
+    bool train_mode = false;
+    std::vector<LayerCache> layers;
+    std::shared_ptr<pbkd_block_cache> device;
+    std::array<int, 4> in_shape{};  // (n, c, h, w) of the block input
+};
+
+Tensor block_forward(Block& b, const Tensor& x, bool train, BlockCache* cache = nullptr);
 Tensor block_infer(const Block& b, const Tensor& x);
+Tensor block_backward(Block& b, const BlockCache& cache, const Tensor& gy, bool need_input_grad,
+                      bool param_grads);
+
+struct NetCache {
+    std::vector<BlockCache> blocks;
+    BlockCache classifier;
+};
+
+Tensor network_forward_train(Network& net, const Tensor& x, NetCache& cache,
+                             const std::vector<bool>& train_mask = {});
+void network_backward(Network& net, const NetCache& cache, const Tensor& glogits,
+                      const std::vector<bool>& train_mask = {}, bool freeze_classifier = false);
+Tensor network_infer(const Network& net, const Tensor& x);
 Tensor prefix_infer(const Network& net, const Tensor& x, int k, bool inclusive);
 
 struct CostRow {

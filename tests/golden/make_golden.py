@@ -120,8 +120,47 @@ def c1_run_parallel(O, n_epochs=2, f64=None):
     return out
 
 
+def generic_paths(O):
+    """5. The layer-by-layer GPU paths against the reference on the toy
+    teacher (test_distill.cpp fixture): train_block with the Combined
+    objective and with the skip candidates, reassemble + finetune (frozen and
+    not), train_teacher."""
+    toy = spec("toy_teacher")
+    tw = O.teacher_init(toy, 404)
+    img, lab = O.synthetic_dataset(60, 11, 2)
+    tr, ev = O.stratified_split(lab, 0.2, 12)
+    out = dict(teacher_w=tw, images=img, labels=lab, train_idx=tr, eval_idx=ev)
+    geo = {1: (3, 16, 1), 2: (16, 32, 2), 3: (32, 32, 1)}
+    cases = {"combined": make_task(2, epochs=2, eval_every=1, seed=1234, batch_size=16, lr=0.02, loss_mode=1,
+                                   lambda_local=0.5),
+             "skip2": make_task(2, kind=2, epochs=2, eval_every=1, seed=99, batch_size=16, lr=0.02),
+             "skip3": make_task(3, kind=3, epochs=2, eval_every=1, seed=98, batch_size=16, lr=0.02)}
+    for name, t in cases.items():
+        nf = O.candidate_num_floats(t.kind, *geo[t.block_index])
+        r = O.train_block(toy, tw, img, lab, tr, ev, t, nf)
+        assert not r["failed"], r["failure"]
+        out[f"{name}_loss_history"] = np.array(r["loss_history"])
+        out[f"{name}_eval_history"] = np.array(r["eval_history"])
+        out[f"{name}_best_eval"] = r["best_eval"]
+        out[f"{name}_block"] = r["block"]
+    reps = [(1, 0, 7), (3, 1, 9)]
+    out["reps"] = np.array(reps, np.int64)
+    for name, kw in {"ft_frozen": dict(epochs=2, freeze=1, lr=0.01, momentum=0.9, batch=16, seed=77, teacher_mode=0),
+                     "ft_all": dict(epochs=1, freeze=0, lr=0.01, momentum=0.9, batch=16, seed=78, teacher_mode=0),
+                     "teacher": dict(epochs=2, freeze=0, lr=0.05, momentum=0.9, batch=24, seed=900,
+                                     teacher_mode=1)}.items():
+        r = O.fit_network(toy, tw, img, lab, tr, ev, [] if name == "teacher" else reps, **kw)
+        n = int(np.max(np.nonzero(r["net"])[0])) + 1
+        out[f"{name}_loss_history"] = r["loss_history"]
+        out[f"{name}_eval_history"] = r["eval_history"]
+        out[f"{name}_net"] = r["net"][:n]
+    return out
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["c1"]:
+    if sys.argv[1:] == ["generic"]:
+        np.savez_compressed(os.path.join(HERE, "toy_generic_paths.npz"), **generic_paths(Oracle("ref")))
+    elif sys.argv[1:] == ["c1"]:
         np.savez_compressed(os.path.join(HERE, "c1_run_parallel.npz"),
                             **c1_run_parallel(Oracle("ref"), f64=Oracle("orc")))
     else:

@@ -313,7 +313,7 @@ def test_run_parallel_failure_isolation_and_validation(ctx, orc):
     ctx.dataset_load(img, lab)
     tr, ev = orc.stratified_split(lab, 0.2, 3)
     tasks = _three_tasks()
-    tasks[1].loss_mode = 1  # combined: not on the GPU path -> failed result
+    tasks[1].batch_size = 0  # SpecError inside the task -> failed result (runtime.cpp:212-220)
     r = ctx.run(tasks, tr, ev, plan=P.round_robin([1, 2, 3], 2), workers=2)
     assert [x["failed"] for x in r["results"]] == [False, True, False]
     with pytest.raises(ValueError):
