@@ -395,6 +395,12 @@ double evaluate_with_student_block(const Network& teacher, int block_index, cons
         swapped.blocks[static_cast<size_t>(block_index) - 1] = student;
         return evaluate_locked(swapped, data, eval_idx, batch_size);
     }
+    const Block& tb = teacher.blocks[static_cast<size_t>(block_index) - 1];
+    if (student.in_channels != tb.in_channels || student.out_channels != tb.out_channels ||
+        student.stride != tb.stride)
+        throw ShapeError("student block (" + std::to_string(student.in_channels) + "->" +
+                         std::to_string(student.out_channels) + ", stride " + std::to_string(student.stride) +
+                         ") does not match teacher block " + std::to_string(block_index));
     pbkd_ctx* ctx = bind(teacher, &data);
     const std::vector<float> w = flat_of(student);
     double acc = 0.0;
@@ -414,6 +420,9 @@ Tensor prefix_infer(const Network& net, const Tensor& x, int k, bool inclusive) 
     if (k < 1 || k > count)
         throw std::out_of_range("prefix_infer: k=" + std::to_string(k) + " out of range [1," +
                                 std::to_string(count) + "]");
+    if (x.c != net.in_c || x.h != net.in_h || x.w != net.in_w)
+        throw ShapeError("prefix_infer: input " + x.shape_str() + " does not match the network input (" +
+                         std::to_string(net.in_c) + "," + std::to_string(net.in_h) + "," + std::to_string(net.in_w) + ")");
     const int take = inclusive ? k : k - 1;
     if (take == 0) return x;
     pbkd_ctx* ctx = bind(net, nullptr);
