@@ -200,6 +200,12 @@ public:
     }
     void gemm_class(int cls, std::vector<GemmOp> ops) {
         if (ops.empty()) return;
+        // Longest-processing-time order: a persistent CTA takes tiles t,
+        // t+grid, ... of the launch, so ops whose tiles carry the most K
+        // chunks go first and start at t=0 on distinct CTAs instead of
+        // landing last behind the short tiles (the launch's critical path).
+        // Tile results do not depend on which CTA computes them.
+        std::stable_sort(ops.begin(), ops.end(), [](const GemmOp& a, const GemmOp& b) { return a.kchunk > b.kchunk; });
         if (knocked_out(std::string("gemm_") + (ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad")))
             return;
         int total = 0;
