@@ -104,6 +104,12 @@ const char* pbkd_version(void);
 /* ---- context (one GPU) ------------------------------------------------- */
 int pbkd_ctx_create(int device, pbkd_ctx** out);
 void pbkd_ctx_destroy(pbkd_ctx* ctx);
+/* A context over a GPU list: one engine per device, one
+ * in-process NCCL clique (ncclCommInitAll).  pbkd_run_parallel then places
+ * worker w on devices[w % n] with a host thread per GPU (runtime.cpp:226-233);
+ * teacher / dataset loads go to every device.  Devices must be distinct. */
+int pbkd_ctx_create_multi(const int* devices, int n, pbkd_ctx** out);
+int pbkd_ctx_device_count(const pbkd_ctx* ctx, int* n);
 int pbkd_device_count(int* n);
 
 /* ---- teacher: model spec JSON (reference schema, model.cpp:225-344) ---- */

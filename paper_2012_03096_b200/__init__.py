@@ -145,6 +145,8 @@ def lib() -> C.CDLL:
                                              C.c_uint64, C.c_int, dp, dp, vp, vp, vp, ip, vp, C.c_size_t,
                                              C.POINTER(C.c_size_t)]),
             "pbkd_mse_local_loss": (C.c_int, [vp, vp, vp, C.c_size_t, fp]),
+            "pbkd_ctx_create_multi": (C.c_int, [vp, C.c_int, C.POINTER(vp)]),
+            "pbkd_ctx_device_count": (C.c_int, [vp, ip]),
             "pbkd_softmax_ce": (C.c_int, [vp, vp, C.c_int, C.c_int, vp, fp, vp]),
         }
         for name, (res, args) in sig.items():
@@ -307,11 +309,17 @@ def spec_num_blocks(spec):
 
 # ----------------------------------------------------------------- context --
 class Context:
-    """One GPU (pbkd_ctx)."""
+    """One GPU (pbkd_ctx), or -- devices=[...] -- a context over a GPU list
+    (pbkd_ctx_create_multi: one engine per GPU, one in-process NCCL clique;
+    run() with a plan spreads the workers over the GPUs)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices=None):
         self.h = C.c_void_p()
-        check(lib().pbkd_ctx_create(device, C.byref(self.h)))
+        if devices is None:
+            check(lib().pbkd_ctx_create(device, C.byref(self.h)))
+        else:
+            d = _i32(list(devices))
+            check(lib().pbkd_ctx_create_multi(_ptr(d), len(d), C.byref(self.h)))
 
     def close(self):
         if self.h:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <memory>
 #include <vector>
 
 namespace pbkd_gpu {
@@ -15,6 +16,9 @@ struct BoundaryPlan;
 class NcclComm {
 public:
     NcclComm(const char* id128, int rank, int world);
+    // one process driving several GPUs: a clique over `devices`
+    // (ncclCommInitAll), rank i on devices[i]
+    static std::vector<std::unique_ptr<NcclComm>> clique(const std::vector<int>& devices);
     ~NcclComm();
     NcclComm(const NcclComm&) = delete;
     NcclComm& operator=(const NcclComm&) = delete;
@@ -26,6 +30,7 @@ public:
     void exchange(const BoundaryPlan& plan, const std::vector<float*>& bnd, cudaStream_t st);
 
 private:
+    NcclComm(void* comm, int rank, int world) : comm_(comm), rank_(rank), world_(world) {}
     void* comm_ = nullptr;
     int rank_ = 0, world_ = 1;
 };

@@ -2367,6 +2367,11 @@ void Engine::set_comm(const char* id, int rank, int world) {
     impl_->comm.reset();
     if (world > 1) impl_->comm = std::make_unique<NcclComm>(id, rank, world);
 }
+void Engine::set_comm(std::unique_ptr<NcclComm> c) {
+    PBKD_CUDA(cudaSetDevice(impl_->dev));
+    g_alloc_stream = impl_->st;
+    impl_->comm = std::move(c);
+}
 int Engine::comm_rank() const { return impl_->comm ? impl_->comm->rank() : 0; }
 int Engine::comm_world() const { return impl_->comm ? impl_->comm->world() : 1; }
 cudaStream_t Engine::stream() const { return impl_->st; }

@@ -28,6 +28,7 @@
 namespace pbkd_gpu {
 
 class NetExec;
+class NcclComm;
 class NetTrainer;
 struct DevNet;
 
@@ -138,6 +139,7 @@ public:
     cudaStream_t stream() const;
     // join an NCCL communicator (id from nccl_unique_id on rank 0)
     void set_comm(const char* nccl_id128, int rank, int world);
+    void set_comm(std::unique_ptr<NcclComm> comm);  // a member of an in-process clique
     int comm_rank() const;
     int comm_world() const;
 

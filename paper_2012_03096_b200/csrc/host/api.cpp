@@ -41,10 +41,27 @@ struct Shared {
     pbkd_ctx* ctx = nullptr;
     uint64_t teacher_hash = 0;
     uint64_t data_hash = 0;
+    // PBKD_DEVICES="0,1,..." (or, unset, every visible GPU when there is more
+    // than one): a context over that GPU list, so run_parallel's workers map
+    // onto GPUs (runtime.cpp:226-233); else PBKD_DEVICE (default 0)
     pbkd_ctx* get() {
         if (!ctx) {
-            const char* dev = std::getenv("PBKD_DEVICE");
-            check(pbkd_ctx_create(dev ? std::atoi(dev) : 0, &ctx));
+            std::vector<int> devs;
+            if (const char* list = std::getenv("PBKD_DEVICES")) {
+                std::stringstream ss(list);
+                for (std::string tok; std::getline(ss, tok, ',');)
+                    if (!tok.empty()) devs.push_back(std::atoi(tok.c_str()));
+            } else if (!std::getenv("PBKD_DEVICE")) {
+                int n = 0;
+                if (pbkd_device_count(&n) == 0 && n > 1)
+                    for (int i = 0; i < n; ++i) devs.push_back(i);
+            }
+            if (!devs.empty()) {
+                check(pbkd_ctx_create_multi(devs.data(), static_cast<int>(devs.size()), &ctx));
+            } else {
+                const char* dev = std::getenv("PBKD_DEVICE");
+                check(pbkd_ctx_create(dev ? std::atoi(dev) : 0, &ctx));
+            }
         }
         return ctx;
     }

@@ -1,6 +1,7 @@
 // cabi.cu -- extern "C" boundary (include/pbkd_b200.h) over the engine.
 #include <algorithm>
 #include <chrono>
+#include <deque>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -10,6 +11,7 @@
 #include <vector>
 
 #include "pbkd_b200.h"
+#include "ctx.hpp"
 #include "../comm.hpp"
 #include "../engine.hpp"
 #include "../ops.cuh"
@@ -20,10 +22,7 @@
 
 using namespace pbkd_gpu;
 
-struct pbkd_ctx {
-    std::unique_ptr<Engine> eng;
-    std::string spec;
-};
+
 
 struct pbkd_results {
     RunTiming timing;
@@ -165,6 +164,33 @@ int pbkd_ctx_create(int device, pbkd_ctx** out) {
     });
 }
 
+int pbkd_ctx_create_multi(const int* devices, int n, pbkd_ctx** out) {
+    return guard([&] {
+        need(n >= 1 && devices != nullptr, "device list is empty");
+        std::vector<int> devs(devices, devices + n);
+        for (size_t i = 0; i < devs.size(); ++i)
+            for (size_t j = 0; j < i; ++j)
+                if (devs[i] == devs[j]) throw std::invalid_argument("device list repeats device " + std::to_string(devs[i]));
+        auto c = std::make_unique<pbkd_ctx>();
+        c->eng = std::make_unique<Engine>(devs[0]);
+        for (size_t i = 1; i < devs.size(); ++i) c->peers.push_back(std::make_unique<Engine>(devs[i]));
+        // one NCCL clique over the list (ncclCommInitAll); a one-GPU list
+        // still gets a one-rank communicator, so the exchange path is the same
+        auto comms = NcclComm::clique(devs);
+        const auto engs = c->engines();
+        for (size_t i = 0; i < engs.size(); ++i) engs[i]->set_comm(std::move(comms[i]));
+        c->multi = true;
+        *out = c.release();
+    });
+}
+
+int pbkd_ctx_device_count(const pbkd_ctx* ctx, int* n) {
+    return guard([&] {
+        need(ctx != nullptr, "null context");
+        *n = static_cast<int>(ctx->engines().size());
+    });
+}
+
 void pbkd_ctx_destroy(pbkd_ctx* ctx) { delete ctx; }
 
 int pbkd_spec_num_floats(const char* spec, size_t* n) {
@@ -204,6 +230,7 @@ int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec, const float* w, size_t n)
         for (int i = 1; i < nth; ++i) th.emplace_back(copy_range, at * i / nth, at * (i + 1) / nth);
         copy_range(0, at / nth);
         for (std::thread& x : th) x.join();
+        for (auto& p : ctx->peers) p->set_teacher(pbkd::Network(net), w, n);
         ctx->eng->set_teacher(std::move(net), w, n);  // device copy straight from the caller's buffer
         ctx->spec = spec;
     });
@@ -213,6 +240,7 @@ int pbkd_teacher_init(pbkd_ctx* ctx, const char* spec, uint64_t seed) {
     return guard([&] {
         pbkd::Network net = spec_net(spec);
         pbkd::init_weights(net, seed);
+        for (auto& p : ctx->peers) p->set_teacher(net);
         ctx->eng->set_teacher(std::move(net));
         ctx->spec = spec;
     });
@@ -238,6 +266,7 @@ int pbkd_teacher_load_file(pbkd_ctx* ctx, const char* spec, const char* path) {
     return guard([&] {
         pbkd::Network net = spec_net(spec);
         pbkd::load_into_network(net, pbkd::load_weights(path), path);
+        for (auto& p : ctx->peers) p->set_teacher(net);
         ctx->eng->set_teacher(std::move(net));
         ctx->spec = spec;
     });
@@ -301,7 +330,7 @@ int pbkd_dataset_load(pbkd_ctx* ctx, const float* img, const int* lab, int count
                       int classes) {
     return guard([&] {
         need(count > 0 && c > 0 && h > 0 && w > 0, "dataset dims must be positive");
-        ctx->eng->set_dataset(img, lab, count, c, h, w, classes, false);
+        for (Engine* e : ctx->engines()) e->set_dataset(img, lab, count, c, h, w, classes, false);
     });
 }
 
@@ -482,17 +511,88 @@ int pbkd_run_parallel(pbkd_ctx* ctx, const pbkd_task* tasks, int n_tasks, const 
             }
         }
         for (const pbkd::DistillTask& t : ok) r->trace.push_back({now_s(t0), worker_of[t.block_index], t.block_index, 1});
-        if (!ok.empty()) {
-            RunOptions opt;
-            opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
-            opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
-            opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
+        RunOptions opt;
+        opt.baseline_and_eval = (flags & PBKD_RUN_STEP_ONLY) == 0;
+        opt.use_graphs = (flags & PBKD_RUN_NO_GRAPH) == 0;
+        opt.profile = (flags & PBKD_RUN_PROFILE) != 0;
+        if (!ok.empty() && !ctx->multi) {
+            // a single-GPU context: every worker's tasks train on this GPU,
+            // grouped (results do not depend on the grouping)
             std::vector<TaskOutcome> res = ctx->eng->run(ok, trv, evv, opt);
             for (TaskOutcome& o : res) outcome[o.block_index] = std::move(o);
             r->epoch_ms = ctx->eng->timing().epoch_ms_total;
             r->timing = ctx->eng->timing();
+            for (const pbkd::DistillTask& t : ok)
+                r->trace.push_back({now_s(t0), worker_of[t.block_index], t.block_index, 2});
+        } else if (!ok.empty()) {
+            // a context over a GPU list: worker w runs on GPU w % G, one host
+            // thread per GPU (runtime.cpp:226-233); the GPUs share the teacher
+            // forward (sample shards) and exchange boundary rows once over the
+            // NCCL clique; every block trains on its own GPU with no
+            // cross-block synchronisation
+            const std::vector<Engine*> engs = ctx->engines();
+            const int G = static_cast<int>(engs.size());
+            std::map<int, pbkd::DistillTask> task_of;
+            for (const pbkd::DistillTask& t : ok) task_of[t.block_index] = t;
+            std::vector<std::deque<int>> gq(static_cast<size_t>(G));
+            for (int w = 0; w < workers; ++w)
+                for (int id : queues[static_cast<size_t>(w)])
+                    if (task_of.count(id)) gq[static_cast<size_t>(w % G)].push_back(id);
+            if (policy == static_cast<int>(pbkd::SchedulePolicy::WorkStealing)) {
+                // runtime.cpp:178-206 at dispatch granularity: an idle GPU takes
+                // the tail of the queue with the most remaining teacher MACs
+                std::vector<int> ids;
+                for (const auto& kv : task_of) ids.push_back(kv.first);
+                const auto wts = pbkd::mac_proxy_weights(ctx->eng->teacher(), ids);
+                std::map<int, double> wt;
+                for (const pbkd::TaskWeight& x : wts) wt[x.task_id] = x.weight;
+                for (int g = 0; g < G; ++g) {
+                    if (!gq[static_cast<size_t>(g)].empty()) continue;
+                    int victim = -1;
+                    double most = 0.0;
+                    for (int v = 0; v < G; ++v) {
+                        if (gq[static_cast<size_t>(v)].size() < 2) continue;
+                        double sum = 0.0;
+                        for (int id : gq[static_cast<size_t>(v)]) sum += wt[id];
+                        if (sum > most) most = sum, victim = v;
+                    }
+                    if (victim < 0) break;
+                    const int id = gq[static_cast<size_t>(victim)].back();
+                    gq[static_cast<size_t>(victim)].pop_back();
+                    gq[static_cast<size_t>(g)].push_back(id);
+                    worker_of[id] = g;
+                    r->trace.push_back({now_s(t0), g, id, 3});
+                }
+            }
+            std::vector<std::pair<int, int>> global;
+            for (int g = 0; g < G; ++g)
+                for (int id : gq[static_cast<size_t>(g)]) global.push_back({id, g});
+            std::vector<std::vector<TaskOutcome>> res(static_cast<size_t>(G));
+            std::vector<std::string> err(static_cast<size_t>(G));
+            std::vector<std::thread> th;
+            for (int g = 0; g < G; ++g)
+                th.emplace_back([&, g] {
+                    try {
+                        std::vector<pbkd::DistillTask> mine;
+                        for (int id : gq[static_cast<size_t>(g)]) mine.push_back(task_of[id]);
+                        RunOptions o = opt;
+                        o.global_blocks = global;
+                        res[static_cast<size_t>(g)] = engs[static_cast<size_t>(g)]->run(mine, trv, evv, o);
+                    } catch (const std::exception& e) {
+                        err[static_cast<size_t>(g)] = e.what();
+                    }
+                });
+            for (std::thread& x : th) x.join();
+            for (int g = 0; g < G; ++g)
+                if (!err[static_cast<size_t>(g)].empty())
+                    throw std::runtime_error("GPU " + std::to_string(g) + ": " + err[static_cast<size_t>(g)]);
+            for (auto& v : res)
+                for (TaskOutcome& o : v) outcome[o.block_index] = std::move(o);
+            r->timing = ctx->eng->timing();
+            for (Engine* e : engs) r->epoch_ms = std::max(r->epoch_ms, e->timing().epoch_ms_total);
+            for (const pbkd::DistillTask& t : ok)
+                r->trace.push_back({now_s(t0), worker_of[t.block_index], t.block_index, 2});
         }
-        for (const pbkd::DistillTask& t : ok) r->trace.push_back({now_s(t0), worker_of[t.block_index], t.block_index, 2});
         // sync point 2: gather in task-id order
         for (auto& kv : outcome) r->res.push_back(std::move(kv.second));
         r->trace.push_back({now_s(t0), 0, -1, 4});

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "pbkd_b200.h"
+#include "ctx.hpp"
 #include "../common.cuh"
 #include "../engine.hpp"
 #include "../netexec.hpp"
@@ -19,10 +20,7 @@
 using namespace pbkd_gpu;
 using pbkd::LayerKind;
 
-struct pbkd_ctx {  // layout shared with cabi.cpp
-    std::unique_ptr<Engine> eng;
-    std::string spec;
-};
+
 
 struct pbkd_block_cache {
     BlockCacheDev c;

@@ -27,6 +27,7 @@ struct NcclApi {
     void* h = nullptr;
     ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
     ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -42,6 +43,7 @@ struct NcclApi {
         get_unique_id = reinterpret_cast<decltype(get_unique_id)>(sym("ncclGetUniqueId"));
         comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(sym("ncclCommInitRank"));
         comm_destroy = reinterpret_cast<decltype(comm_destroy)>(sym("ncclCommDestroy"));
+        comm_init_all = reinterpret_cast<decltype(comm_init_all)>(sym("ncclCommInitAll"));
         send = reinterpret_cast<decltype(send)>(sym("ncclSend"));
         recv = reinterpret_cast<decltype(recv)>(sym("ncclRecv"));
         group_start = reinterpret_cast<decltype(group_start)>(sym("ncclGroupStart"));
@@ -75,6 +77,17 @@ NcclComm::NcclComm(const char* id128, int rank, int world) : rank_(rank), world_
     ncclComm_t c = nullptr;
     check(api().comm_init_rank(&c, world, id, rank), "ncclCommInitRank");
     comm_ = c;
+}
+
+std::vector<std::unique_ptr<NcclComm>> NcclComm::clique(const std::vector<int>& devices) {
+    auto& a = api();
+    if (!a.comm_init_all) throw std::runtime_error("NCCL: ncclCommInitAll not available");
+    std::vector<ncclComm_t> c(devices.size(), nullptr);
+    check(a.comm_init_all(c.data(), static_cast<int>(devices.size()), devices.data()), "ncclCommInitAll");
+    std::vector<std::unique_ptr<NcclComm>> out;
+    for (size_t i = 0; i < c.size(); ++i)
+        out.emplace_back(new NcclComm(c[i], static_cast<int>(i), static_cast<int>(c.size())));
+    return out;
 }
 
 NcclComm::~NcclComm() {

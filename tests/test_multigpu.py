@@ -146,3 +146,40 @@ def test_virtual_shards_bitwise(orc, shards, share):
     for a, b in zip(base, shd):
         assert np.array_equal(a["step_losses"], b["step_losses"])
         assert np.array_equal(a["final_block"], b["final_block"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", ["round_robin", "wfd", "work_stealing"])
+def test_context_over_gpu_list_run_parallel(orc, policy):
+    """A context over a GPU list (pbkd_ctx_create_multi: one engine per GPU,
+    one in-process NCCL clique, a host thread per GPU).  On this one-GPU box
+    the list is [0]: a one-rank communicator, so the teacher boundaries still
+    go through the NCCL exchange (self send/recv), and run_parallel with 2
+    workers and evaluations must give the single-GPU context's bits."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from tests.conftest import spec_text
+    spec = spec_text("toy_teacher")
+    tw = orc.teacher_init(spec, 2025)
+    img, lab = orc.synthetic_dataset(40, 21, 2)
+    tr, ev = orc.stratified_split(lab, 0.25, 3)
+    tasks = lambda: [P.make_task(k, epochs=2, eval_every=1, seed=P.mix_seed(99, k), batch_size=10, lr=0.02)  # noqa: E731
+                     for k in (1, 2, 3)]
+    plan = [[1, 2, 3], []] if policy == "work_stealing" else P.round_robin([1, 2, 3], 2)
+    one = P.Context(0)
+    one.teacher_load(spec, tw)
+    one.dataset_load(img, lab)
+    base = one.run(tasks(), tr, ev, plan=plan, workers=2, policy=policy)
+    one.close()
+    multi = P.Context(devices=[0])
+    multi.teacher_load(spec, tw)
+    multi.dataset_load(img, lab)
+    got = multi.run(tasks(), tr, ev, plan=plan, workers=2, policy=policy)
+    assert [x["block_index"] for x in got["results"]] == [1, 2, 3]
+    for a, b in zip(base["results"], got["results"]):
+        assert not b["failed"], b["failure"]
+        assert np.array_equal(a["block"], b["block"]) and np.array_equal(a["final_block"], b["final_block"])
+        assert a["loss_history"] == b["loss_history"] and a["eval_history"] == b["eval_history"]
+    kinds = [e[3] for e in got["trace"]]
+    assert kinds.count(0) == 3 and kinds.count(1) == 3 and kinds.count(2) == 3 and kinds.count(4) == 1
