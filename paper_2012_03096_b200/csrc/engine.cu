@@ -436,12 +436,14 @@ struct ConvDev {
 };
 
 struct TBlockDev {
-    int kind = 0;  // 0 conv (3x3 or 1x1), 1 residual
+    int kind = 0;  // 0 conv (3x3 or 1x1), 1 residual, 2 bottleneck, 3 stem (7x7 conv + max pool)
     int cin = 0, hin = 0, win = 0, cout = 0, hout = 0, wout = 0;
-    ConvDev c1, c2;
+    int stride = 1;  // the block's stride (the student candidate's)
+    ConvDev c1, c2, c3;
     bool has_proj = false;
     ConvDev proj;  // 1x1 stride projection, no affine
     int mid_h = 0, mid_w = 0;
+    long long scratch = 0;  // largest intermediate tensor per sample (floats)
 };
 
 // dev_w: the layer's weights already on the device ([cout][cin][kk], the
@@ -650,10 +652,10 @@ struct Engine::Impl {
     }
 
     int max_row() const {
-        int m = net.in_c * net.in_h * net.in_w;
-        for (const TBlockDev& b : tblocks) m = std::max(m, b.cout * b.hout * b.wout);
-        for (const TBlockDev& b : tblocks) m = std::max(m, b.cout * b.mid_h * b.mid_w);
-        return m;
+        long long m = static_cast<long long>(net.in_c) * net.in_h * net.in_w;
+        for (const TBlockDev& b : tblocks) m = std::max<long long>(m, static_cast<long long>(b.cout) * b.hout * b.wout);
+        for (const TBlockDev& b : tblocks) m = std::max(m, b.scratch);
+        return static_cast<int>(m);
     }
 
     // flat: the weights in for_each_array order (host; pinned memory makes the
@@ -692,7 +694,33 @@ struct Engine::Impl {
             d.hin = h;
             d.win = w;
             d.cout = b.out_channels;
-            if (b.spec_kind == "residual3x3") {
+            if (b.spec_kind == "bottleneck") {  // SURVEY 8f-4 (model.cpp build_bottleneck)
+                d.kind = 2;
+                d.c1 = conv_upload(b.layers[0], &b.layers[1], dev_of(b.layers[0].weight), st);
+                d.c2 = conv_upload(b.layers[3], &b.layers[4], dev_of(b.layers[3].weight), st);
+                d.c3 = conv_upload(b.layers[6], &b.layers[7], dev_of(b.layers[6].weight), st);
+                const pbkd::LayerParams& add = b.layers[8];
+                if (!add.weight.data.empty()) {
+                    d.has_proj = true;
+                    pbkd::LayerParams pl = pbkd::make_conv_layer(LayerKind::Conv1x1, add.in_channels,
+                                                                 add.out_channels, 1, add.stride, 0);
+                    d.proj = conv_upload(pl, nullptr, dev_of(add.weight), st);
+                }
+                d.stride = d.c2.stride;
+                d.hout = (h + 2 * d.c2.pad - 3) / d.c2.stride + 1;
+                d.wout = (w + 2 * d.c2.pad - 3) / d.c2.stride + 1;
+                d.mid_h = d.hout, d.mid_w = d.wout;
+                d.scratch = static_cast<long long>(d.c1.cout) * h * w;  // the 1x1 reduce at input resolution
+            } else if (b.spec_kind == "stem7x7") {
+                d.kind = 3;
+                d.c1 = conv_upload(b.layers[0], &b.layers[1], dev_of(b.layers[0].weight), st);
+                d.stride = d.c1.stride;
+                d.mid_h = (h + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
+                d.mid_w = (w + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
+                d.hout = (d.mid_h + 2 - 3) / 2 + 1;  // max pool 3x3 / 2, pad 1
+                d.wout = (d.mid_w + 2 - 3) / 2 + 1;
+                d.scratch = static_cast<long long>(d.cout) * d.mid_h * d.mid_w;
+            } else if (b.spec_kind == "residual3x3") {
                 d.kind = 1;
                 d.c1 = conv_upload(b.layers[0], &b.layers[1], dev_of(b.layers[0].weight), st);
                 d.c2 = conv_upload(b.layers[3], &b.layers[4], dev_of(b.layers[3].weight), st);
@@ -707,11 +735,14 @@ struct Engine::Impl {
                 d.mid_w = (w + 2 * d.c1.pad - 3) / d.c1.stride + 1;
                 d.hout = d.mid_h;
                 d.wout = d.mid_w;
+                d.stride = d.c1.stride;
+                d.scratch = static_cast<long long>(d.cout) * d.mid_h * d.mid_w;
             } else {
                 d.kind = 0;
                 d.c1 = conv_upload(b.layers[0], &b.layers[1], dev_of(b.layers[0].weight), st);
                 d.hout = (h + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
                 d.wout = (w + 2 * d.c1.pad - d.c1.k) / d.c1.stride + 1;
+                d.stride = d.c1.stride;
             }
             c = d.cout;
             h = d.hout;
@@ -763,6 +794,23 @@ struct Engine::Impl {
         const Planes2 xp = planes_for(x), yp = planes_for(y), tp = planes_for(t1);
         if (b.kind == 0) {
             P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, y, true, nullptr, true, xp, yp)});
+            return;
+        }
+        if (b.kind == 2) {  // bottleneck: t1 = reduce(x), sk = 3x3(t1), y = expand(sk) + skip
+            P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true, xp, tp)});
+            P.gemm({conv_gemm(b.c2, t1, n, b.hin, b.win, sk, true, nullptr, true, tp)});
+            const float* skip = x;
+            if (b.has_proj) {  // the projection lands in y; the expand conv adds it element-wise in place
+                P.gemm({conv_gemm(b.proj, x, n, b.hin, b.win, y, false, nullptr, false, xp)});
+                skip = y;
+            }
+            P.gemm({conv_gemm(b.c3, sk, n, b.hout, b.wout, y, true, skip, true, {}, yp)});
+            return;
+        }
+        if (b.kind == 3) {  // stem: conv7x7 + BN + ReLU into t1, 3x3/2 max pool into y
+            P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true, xp)});
+            const int c = b.cout, mh = b.mid_h, mw = b.mid_w;
+            P.raw([=](cudaStream_t s2) { launch_maxpool3x3(t1, y, yp.hi, yp.lo, n, mh, mw, c, s2); }, "MaxPoolOp");
             return;
         }
         P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true, xp, tp)});
@@ -838,9 +886,9 @@ struct Engine::Impl {
         s.k = t.block_index;
         const TBlockDev& tb = tblocks[static_cast<size_t>(s.k) - 1];
         s.units = (t.kind == pbkd::CandidateKind::ThreeLayer) ? 3 : 2;
-        const int ho = (tb.hin - 1) / tb.c1.stride + 1, wo = (tb.win - 1) / tb.c1.stride + 1;
+        const int ho = (tb.hin - 1) / tb.stride + 1, wo = (tb.win - 1) / tb.stride + 1;
         for (int u = 0; u < s.units; ++u)
-            s.u[u] = u == 0 ? UnitDims{tb.cin, tb.hin, tb.win, tb.cout, ho, wo, tb.c1.stride}
+            s.u[u] = u == 0 ? UnitDims{tb.cin, tb.hin, tb.win, tb.cout, ho, wo, tb.stride}
                             : UnitDims{tb.cout, ho, wo, tb.cout, ho, wo, 1};
     }
 

@@ -79,7 +79,8 @@ std::string spec_json_of(const Network& net) {
     doc["input_shape"] = {net.in_c, net.in_h, net.in_w};
     json blocks = json::array();
     for (const Block& b : net.blocks) {
-        if (b.spec_kind != "conv3x3" && b.spec_kind != "conv1x1" && b.spec_kind != "residual3x3")
+        if (b.spec_kind != "conv3x3" && b.spec_kind != "conv1x1" && b.spec_kind != "residual3x3" &&
+            b.spec_kind != "bottleneck" && b.spec_kind != "stem7x7")
             throw SpecError("block '" + b.name + "' of kind '" + b.spec_kind +
                             "' cannot be uploaded as a teacher block");
         blocks.push_back({{"name", b.name}, {"kind", b.spec_kind}, {"out_channels", b.out_channels},

@@ -54,12 +54,14 @@ int guard(F&& f) {
 }
 
 pbkd::LayerParams layer_of(const pbkd_layer_desc& d) {
-    if (d.kind < 0 || d.kind > static_cast<int>(LayerKind::Add)) throw pbkd::SpecError("layer kind out of range");
+    if (d.kind < 0 || d.kind > static_cast<int>(LayerKind::MaxPool3x3)) throw pbkd::SpecError("layer kind out of range");
     const auto kind = static_cast<LayerKind>(d.kind);
     switch (kind) {
         case LayerKind::Conv3x3:
         case LayerKind::Conv1x1:
+        case LayerKind::Conv7x7:
             return pbkd::make_conv_layer(kind, d.in_channels, d.out_channels, d.kernel, d.stride, d.padding);
+        case LayerKind::MaxPool3x3: return pbkd::make_maxpool_layer(d.in_channels);
         case LayerKind::DepthwiseConv3x3:
             return pbkd::make_conv_layer(kind, d.in_channels, d.in_channels, 3, d.stride, d.padding);
         case LayerKind::PointwiseConv:

@@ -397,18 +397,22 @@ __global__ void k_take_samples(const float* src, const int* pos, float* out, int
 // rows rr, rr+RP, ... over its V channels; thread 0 sums the 256 lanes
 __global__ void k_loss_parts(const float* s, const float* t, int rows, int c, int per, float* part) {
     __shared__ float lred[256];
-    const int V = (c % 4 == 0) ? 4 : 1, G = c / V, RP = max(1, 256 / G);
-    const int rr = threadIdx.x / G, gg = threadIdx.x % G;
+    const int V = (c % 4 == 0) ? 4 : 1;
     const long long r0 = static_cast<long long>(blockIdx.x) * per;
     const long long r1 = min(static_cast<long long>(rows), r0 + per);
     float lsum = 0.0f;
-    if (rr < RP) {
-        const int c0 = gg * V;
-        for (long long r = r0 + rr; r < r1; r += RP)
-            for (int q = 0; q < V; ++q) {
-                const float d = sub(s[r * c + c0 + q], t[r * c + c0 + q]);
-                lsum += d * d;
-            }
+    for (int cb = 0; cb < c; cb += 256 * V) {  // loss_kernel's channel passes
+        const int cw = min(256 * V, c - cb);
+        const int G = cw / V, RP = max(1, 256 / G);
+        const int rr = threadIdx.x / G, gg = threadIdx.x % G;
+        if (rr < RP) {
+            const int c0 = cb + gg * V;
+            for (long long r = r0 + rr; r < r1; r += RP)
+                for (int q = 0; q < V; ++q) {
+                    const float d = sub(s[r * c + c0 + q], t[r * c + c0 + q]);
+                    lsum += d * d;
+                }
+        }
     }
     lred[threadIdx.x] = lsum;
     __syncthreads();
@@ -527,6 +531,7 @@ DevBlock NetExec::make_block(const pbkd::Block& b, const float* src, bool src_on
         switch (lp.kind) {  // for_each_block_array order
             case LayerKind::Conv3x3:
             case LayerKind::Conv1x1:
+            case LayerKind::Conv7x7:
             case LayerKind::DepthwiseConv3x3:
             case LayerKind::PointwiseConv:
                 l.wn = static_cast<long long>(lp.weight.data.size());
@@ -588,7 +593,7 @@ void NetExec::prepare(DevBlock& b) {
     if (b.derived_ok) return;
     for (DevBlock::Layer& l : b.layers) {
         const bool conv = l.kind == LayerKind::Conv3x3 || l.kind == LayerKind::Conv1x1 ||
-                          (l.kind == LayerKind::Add && l.w >= 0);
+                          l.kind == LayerKind::Conv7x7 || (l.kind == LayerKind::Add && l.w >= 0);
         if (conv) {
             const int kk = l.k * l.k;
             if (!l.wk) {
@@ -740,6 +745,7 @@ DTensor NetExec::forward(DevBlock& b, const DTensor& x, bool train, BlockCacheDe
         switch (l.kind) {
             case LayerKind::Conv3x3:
             case LayerKind::Conv1x1:
+            case LayerKind::Conv7x7:
                 if (cur.c != l.cin) throw pbkd::ShapeError("conv: input channels do not match the layer");
                 next = conv_fwd(l, cur);
                 break;
@@ -812,6 +818,10 @@ DTensor NetExec::forward(DevBlock& b, const DTensor& x, bool train, BlockCacheDe
                 k_relu<<<grid_for(cur.size()), 256, 0, st_>>>(cur.p, next.p, cur.size());
                 PBKD_LAUNCH_CHECK();
                 break;
+            case LayerKind::MaxPool3x3:
+                next = alloc(cur.n, cur.c, (cur.h - 1) / 2 + 1, (cur.w - 1) / 2 + 1);
+                launch_maxpool3x3(cur.p, next.p, nullptr, nullptr, cur.n, cur.h, cur.w, cur.c, st_);
+                break;
             case LayerKind::GlobalAvgPool:
                 next = alloc(cur.n, cur.c, 1, 1);
                 k_gap<<<grid_for(static_cast<long long>(cur.n) * cur.c), 256, 0, st_>>>(cur.p, next.p, cur.n,
@@ -858,6 +868,7 @@ DTensor NetExec::backward(DevBlock& b, const BlockCacheDev& cache, const DTensor
         switch (l.kind) {
             case LayerKind::Conv3x3:
             case LayerKind::Conv1x1:
+            case LayerKind::Conv7x7:
                 conv_bwd(b, l, x, g, want_gx ? &gx : nullptr, param_grads);
                 break;
             case LayerKind::DepthwiseConv3x3: {
@@ -923,6 +934,12 @@ DTensor NetExec::backward(DevBlock& b, const BlockCacheDev& cache, const DTensor
                     gx = alloc(x.n, x.c, x.h, x.w);
                     k_relu_bwd<<<grid_for(x.size()), 256, 0, st_>>>(x.p, g.p, gx.p, x.size());
                     PBKD_LAUNCH_CHECK();
+                }
+                break;
+            case LayerKind::MaxPool3x3:
+                if (want_gx) {
+                    gx = alloc(x.n, x.c, x.h, x.w, true);
+                    launch_maxpool3x3_bwd(x.p, g.p, gx.p, x.n, x.h, x.w, x.c, st_);
                 }
                 break;
             case LayerKind::GlobalAvgPool:

@@ -844,44 +844,52 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
     int local;
     const LossOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
-    const Geo g = geo_of(o.c);
-    const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
-    const bool lane_ok = rr < g.RP;
+    // channel passes of kThreads*V channels (one pass unless c > 1024, e.g.
+    // the 2048-channel ResNet-50 stage): thread (rr, gg) of a pass owns V
+    // channels and rows rr, rr+RP, ... of the CTA's row range
+    const int V = (o.c % 4 == 0) ? 4 : 1;
     const long long r0 = static_cast<long long>(local) * o.rows_per;
     const long long r1 = min(static_cast<long long>(o.rows), r0 + o.rows_per);
-    const int c0 = gg * g.V;
-    float sg[4] = {0, 0, 0, 0}, sgx[4] = {0, 0, 0, 0};
     float lsum = 0.0f;
-    if (lane_ok) {
-        float mean[4], inv[4], gam[4], bet[4];
-        load_v(o.mean + c0, g.V, mean);
-        load_v(o.inv + c0, g.V, inv);
-        load_v(o.gamma + c0, g.V, gam);
-        load_v(o.beta + c0, g.V, bet);
-        auto body = [&](long long r, const float* tp) {
-            float pv[4], tv[4];
-            load_v(o.p + r * o.c + c0, g.V, pv);
-            load_v(tp, g.V, tv);
-            for (int q = 0; q < g.V; ++q) {
-                const float xh = mul(sub(pv[q], mean[q]), inv[q]);
-                const float y = add(mul(gam[q], xh), bet[q]);
-                const float d = sub(relu(y), tv[q]);
-                lsum += d * d;
-                const float gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
-                sg[q] += gy;
-                sgx[q] += gy * xh;
+    for (int cb = 0; cb < o.c; cb += kThreads * V) {
+        const int cw = min(kThreads * V, o.c - cb);
+        Geo g;
+        g.V = V, g.G = cw / V, g.RP = max(1, kThreads / g.G);
+        const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
+        const bool lane_ok = rr < g.RP;
+        const int c0 = cb + gg * g.V;
+        float sg[4] = {0, 0, 0, 0}, sgx[4] = {0, 0, 0, 0};
+        if (lane_ok) {
+            float mean[4], inv[4], gam[4], bet[4];
+            load_v(o.mean + c0, g.V, mean);
+            load_v(o.inv + c0, g.V, inv);
+            load_v(o.gamma + c0, g.V, gam);
+            load_v(o.beta + c0, g.V, bet);
+            auto body = [&](long long r, const float* tp) {
+                float pv[4], tv[4];
+                load_v(o.p + r * o.c + c0, g.V, pv);
+                load_v(tp, g.V, tv);
+                for (int q = 0; q < g.V; ++q) {
+                    const float xh = mul(sub(pv[q], mean[q]), inv[q]);
+                    const float y = add(mul(gam[q], xh), bet[q]);
+                    const float d = sub(relu(y), tv[q]);
+                    lsum += d * d;
+                    const float gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
+                    sg[q] += gy;
+                    sgx[q] += gy * xh;
+                }
+            };
+            if (o.trows == nullptr) {
+#pragma unroll 4
+                for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + r * o.c + c0);
+            } else {  // targets gathered through the epoch order
+#pragma unroll 4
+                for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + row_remap(o.trows, o.srow, r * o.c + c0));
             }
-        };
-        if (o.trows == nullptr) {
-#pragma unroll 4
-            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + r * o.c + c0);
-        } else {  // targets gathered through the epoch order
-#pragma unroll 4
-            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + row_remap(o.trows, o.srow, r * o.c + c0));
         }
+        cta_reduce_rows(red, sg, g, rr, gg, lane_ok, cw, o.part_sg + static_cast<long long>(local) * o.c + cb);
+        cta_reduce_rows(red, sgx, g, rr, gg, lane_ok, cw, o.part_sgx + static_cast<long long>(local) * o.c + cb);
     }
-    cta_reduce_rows(red, sg, g, rr, gg, lane_ok, o.c, o.part_sg + static_cast<long long>(local) * o.c);
-    cta_reduce_rows(red, sgx, g, rr, gg, lane_ok, o.c, o.part_sgx + static_cast<long long>(local) * o.c);
     lred[threadIdx.x] = lsum;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1227,6 +1235,88 @@ void launch_bn_infer_relu(const float* x, float* y, long long total, int c, cons
                           const float* shift, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>(4096, (total + 255) / 256));
     launch_k(bn_infer_relu_kernel, dim3(std::max(1, blocks)), dim3(256), 0, st, x, y, total, c, scale, shift);
+    PBKD_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------- max pool
+__global__ void maxpool3x3_kernel(const float* __restrict__ x, float* __restrict__ y, float* y_hi, float* y_lo,
+                                  int n, int h, int w, int c, int ho, int wo) {
+    pdl_enter();
+    const long long total = static_cast<long long>(n) * ho * wo * c;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int ch = static_cast<int>(i % c);
+        long long r = i / c;
+        const int ox = static_cast<int>(r % wo);
+        r /= wo;
+        const int oy = static_cast<int>(r % ho);
+        const long long b = r / ho;
+        float m = -INFINITY;
+        for (int ky = 0; ky < 3; ++ky) {
+            const int iy = oy * 2 - 1 + ky;
+            if (iy < 0 || iy >= h) continue;
+            for (int kx = 0; kx < 3; ++kx) {
+                const int ix = ox * 2 - 1 + kx;
+                if (ix < 0 || ix >= w) continue;
+                m = fmaxf(m, x[((b * h + iy) * w + ix) * c + ch]);
+            }
+        }
+        y[i] = m;
+        if (y_hi) {
+            const float hv = __uint_as_float(tc_split_hi(m));
+            y_hi[i] = hv;
+            y_lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(m, hv)));
+        }
+    }
+}
+
+void launch_maxpool3x3(const float* x, float* y, float* y_hi, float* y_lo, int n, int h, int w, int c,
+                       cudaStream_t st) {
+    const int ho = (h + 2 - 3) / 2 + 1, wo = (w + 2 - 3) / 2 + 1;
+    const long long total = static_cast<long long>(n) * ho * wo * c;
+    const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(148LL * 16, (total + 255) / 256)));
+    launch_k(maxpool3x3_kernel, dim3(blocks), dim3(256), 0, st, x, y, y_hi, y_lo, n, h, w, c, ho, wo);
+    PBKD_LAUNCH_CHECK();
+}
+
+__global__ void maxpool3x3_bwd_kernel(const float* __restrict__ x, const float* __restrict__ gy, float* gx, int n,
+                                      int h, int w, int c, int ho, int wo) {
+    pdl_enter();
+    const long long total = static_cast<long long>(n) * h * w * c;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int ch = static_cast<int>(i % c);
+        long long r = i / c;
+        const int ix = static_cast<int>(r % w);
+        r /= w;
+        const int iy = static_cast<int>(r % h);
+        const long long b = r / h;
+        float acc = 0.0f;
+        for (int oy = max(0, iy / 2 - 1); oy <= min(ho - 1, (iy + 1) / 2); ++oy)
+            for (int ox = max(0, ix / 2 - 1); ox <= min(wo - 1, (ix + 1) / 2); ++ox) {
+                int by = -1, bx = -1;  // the window's first maximum
+                float m = -INFINITY;
+                for (int ky = 0; ky < 3; ++ky) {
+                    const int yy = oy * 2 - 1 + ky;
+                    if (yy < 0 || yy >= h) continue;
+                    for (int kx = 0; kx < 3; ++kx) {
+                        const int xx = ox * 2 - 1 + kx;
+                        if (xx < 0 || xx >= w) continue;
+                        const float v = x[((b * h + yy) * w + xx) * c + ch];
+                        if (v > m || by < 0) m = v, by = yy, bx = xx;
+                    }
+                }
+                if (by == iy && bx == ix) acc = __fadd_rn(acc, gy[((b * ho + oy) * wo + ox) * c + ch]);
+            }
+        gx[i] = __fadd_rn(gx[i], acc);
+    }
+}
+
+void launch_maxpool3x3_bwd(const float* x, const float* gy, float* gx, int n, int h, int w, int c, cudaStream_t st) {
+    const int ho = (h + 2 - 3) / 2 + 1, wo = (w + 2 - 3) / 2 + 1;
+    const long long total = static_cast<long long>(n) * h * w * c;
+    const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(148LL * 16, (total + 255) / 256)));
+    launch_k(maxpool3x3_bwd_kernel, dim3(blocks), dim3(256), 0, st, x, gy, gx, n, h, w, c, ho, wo);
     PBKD_LAUNCH_CHECK();
 }
 

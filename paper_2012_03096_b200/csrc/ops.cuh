@@ -299,6 +299,14 @@ void launch_bn_infer_relu(const float* x, float* y, long long total, int c, cons
 // teacher conv weights [cout][cin][kk] -> [cout][kk][cin] + tf32 planes
 void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, float* w, float* hi, float* lo,
                              cudaStream_t st);
+// 3x3 / stride 2 / pad 1 max pooling over NHWC (the ResNet-50 stem, SURVEY
+// 8f-4): out-of-image taps are skipped; optional tf32 planes of the output
+void launch_maxpool3x3(const float* x, float* y, float* y_hi, float* y_lo, int n, int h, int w, int c,
+                       cudaStream_t st);
+// its backward: each input pixel gathers gy of the outputs whose first
+// maximum (ky, kx order) it is, in ascending output order (deterministic)
+void launch_maxpool3x3_bwd(const float* x, const float* gy, float* gx, int n, int h, int w, int c,
+                           cudaStream_t st);
 // tf32 hi / lo planes of n floats (the 3xTF32 operand split)
 void launch_tf32_split(const float* x, long long n, float* hi, float* lo, cudaStream_t st);
 // per-segment MSE sums (segment = one batch of the epoch-0 baseline)

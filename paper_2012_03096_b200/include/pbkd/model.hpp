@@ -33,6 +33,9 @@ enum class LayerKind {
     GlobalAvgPool,
     Dense,
     Add,
+    // beyond the reference vocabulary (ResNet-50 / ImageNet):
+    Conv7x7,     // the 7x7 stride-2 stem convolution
+    MaxPool3x3,  // 3x3 stride-2 pad-1 max pooling after the stem
 };
 
 const char* layer_kind_name(LayerKind k);
@@ -75,6 +78,7 @@ LayerParams make_relu_layer(int channels);
 LayerParams make_gap_layer(int channels);
 LayerParams make_dense_layer(int in_features, int out_features);
 LayerParams make_add_layer(int in_c, int out_c, int stride);
+LayerParams make_maxpool_layer(int channels);
 
 Network parse_model_spec(const std::string& text, const std::string& origin = "<memory>");
 Network load_model_spec_file(const std::string& path);

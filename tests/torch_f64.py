@@ -45,7 +45,15 @@ def _teacher(spec, tw, dev):
         co, s = b["out_channels"], b.get("stride", 1)
         ks = 1 if b["kind"] == "conv1x1" else 3
         pad = b.get("padding", 0 if ks == 1 else 1)  # model.cpp:281
-        if b["kind"] == "residual3x3":
+        if b["kind"] == "bottleneck":  # model.cpp build_bottleneck
+            mid = max(1, co // 4)
+            blk = {"kind": "bottleneck", "s": s, "w1": take(mid, c, 1, 1), "bn1": [take(mid) for _ in range(4)],
+                   "w2": take(mid, mid, 3, 3), "bn2": [take(mid) for _ in range(4)],
+                   "w3": take(co, mid, 1, 1), "bn3": [take(co) for _ in range(4)]}
+            blk["proj"] = take(co, c, 1, 1) if (s != 1 or c != co) else None
+        elif b["kind"] == "stem7x7":
+            blk = {"kind": "stem", "s": s, "w1": take(co, c, 7, 7), "bn1": [take(co) for _ in range(4)]}
+        elif b["kind"] == "residual3x3":
             blk = {"kind": "res", "s": s, "p": pad, "w1": take(co, c, 3, 3), "bn1": [take(co) for _ in range(4)],
                    "w2": take(co, co, 3, 3), "bn2": [take(co) for _ in range(4)]}
             blk["proj"] = take(co, c, 1, 1) if (s != 1 or c != co) else None  # model.cpp:211-219
@@ -63,6 +71,15 @@ def _bn_infer(x, bn):
 
 
 def _teacher_block(blk, x):
+    if blk["kind"] == "bottleneck":
+        y = F.relu(_bn_infer(F.conv2d(x, blk["w1"]), blk["bn1"]))
+        y = F.relu(_bn_infer(F.conv2d(y, blk["w2"], stride=blk["s"], padding=1), blk["bn2"]))
+        y = _bn_infer(F.conv2d(y, blk["w3"]), blk["bn3"])
+        skip = x if blk["proj"] is None else F.conv2d(x, blk["proj"], stride=blk["s"])
+        return F.relu(y + skip)
+    if blk["kind"] == "stem":
+        y = F.relu(_bn_infer(F.conv2d(x, blk["w1"], stride=blk["s"], padding=3), blk["bn1"]))
+        return F.max_pool2d(y, 3, stride=2, padding=1)
     y = F.relu(_bn_infer(F.conv2d(x, blk["w1"], stride=blk["s"], padding=blk["p"]), blk["bn1"]))
     if blk["kind"] == "conv":
         return y
