@@ -31,7 +31,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {"vgg16": "vgg16_cifar", "resnet18": "resnet18_cifar", "resnet34": "resnet34_cifar100",
-           "c1": "c1_small_vgg"}
+           "c1": "c1_small_vgg", "resnet50": "resnet50_imagenet"}
+DEFAULT_BATCH = {"resnet50": 256}  # BASELINE.json configs[4]; the CIFAR configs use 32
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -43,7 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="vgg16", choices=sorted(CONFIGS))
     ap.add_argument("--dataset-size", type=int, default=1000)
-    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -54,13 +55,17 @@ def workload(cfg, n, P):
     front end -- both expose mix_seed / stratified_split with the reference's
     bit-exact semantics."""
     spec = open(os.path.join(ROOT, "configs", CONFIGS[cfg] + ".json")).read()
-    classes = 100 if cfg == "resnet34" else 10
-    images = np.random.default_rng(2012).random((n, 3, 32, 32), dtype=np.float32)
+    d = json.loads(spec)
+    classes = d["classifier"][-1]["out_features"]
+    c, h, w = d["input_shape"]
+    images = np.random.default_rng(2012).random((n, c, h, w), dtype=np.float32)
     labels = (np.arange(n) % classes).astype(np.int32)
-    tr, ev = P.stratified_split(labels, 0.1, P.mix_seed(42, 0x5711))
-    nb = P.spec_num_blocks(spec) if hasattr(P, "spec_num_blocks") else P.teacher_num_blocks(spec)
-    # every conv block of these configs is replaceable (identify_replaceable)
-    blocks = list(range(1, nb + 1))
+    if n // classes >= 2:  # stratified_split needs two samples per class
+        tr, ev = P.stratified_split(labels, 0.1, P.mix_seed(42, 0x5711))
+    else:  # ImageNet-shape runs with fewer samples than 2 x 1000 classes: a fixed 90/10 cut
+        tr, ev = np.arange(n - n // 10, dtype=np.int32), np.arange(n - n // 10, n, dtype=np.int32)
+    # the replaceable blocks (identify_replaceable): every conv block, not the stems
+    blocks = [i + 1 for i, b in enumerate(d["blocks"]) if b["kind"] in ("conv3x3", "residual3x3", "bottleneck")]
     return spec, classes, images, labels, tr, ev, blocks
 
 
@@ -159,6 +164,10 @@ def run_reference(args):
     reference sources; the restatement if that build is absent).  The product
     package is NOT imported here: split and seeds come from the reference's
     own library through the oracle front end."""
+    if CONFIGS[args.config] == "resnet50_imagenet":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference's model vocabulary has no bottleneck "
+                          "block, 7x7 stem or max pooling (SURVEY 8f-4): ResNet-50 cannot be expressed in it"}))
+        return
     from oracle import oracle as OR
     kind = "reference" if OR.available("ref") else "port"
     O = OR.Oracle("ref" if kind == "reference" else "orc")
@@ -178,7 +187,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": "distillation samples/sec (all blocks)", "value": v,
             "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform [0,1), CIFAR-10 shape)",
+            "vs_baseline": None, "dtype": "f32", "data": f"synthetic (seeded uniform [0,1), {CONFIGS[args.config]} input shape)",
             "config": {"workload": f"{CONFIGS[args.config]}: {len(blocks)} blocks, batch {bsz}, "
                                    f"dataset {args.dataset_size}, CPU reference step-only"},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": kind,
@@ -201,6 +210,8 @@ def launch_ranks(args):
 
 def main():
     args = parse()
+    if args.batch is None:
+        args.batch = DEFAULT_BATCH.get(args.config, 32)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         launch_ranks(args)
     rank = int(os.environ.get("RANK", "0"))
@@ -392,7 +403,7 @@ def main():
             "metric": "distillation samples/sec (all blocks)", "value": value, "unit": "samples/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": t_ms / K,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded uniform [0,1) images, CIFAR-10 shape; random-init teacher "
+            "data": f"synthetic (seeded uniform [0,1) images, {CONFIGS[args.config]} input shape; random-init teacher "
                     "init_weights(mix_seed(42,0x7e11)))",
             "config": {"workload": f"{CONFIGS[args.config]}: all {len(blocks)} blocks distilled, "
                                    f"TwoLayer students, batch {B}, dataset {args.dataset_size} "

@@ -1171,7 +1171,10 @@ struct Engine::Impl {
                 f.failed = s.failed.i();
                 fs.push_back(f);
             }
-            P.grouped<LossOp>(launch_loss, ls, [](const LossOp& o) { return o.ctas; });
+            std::vector<LossOp> narrow, wide;  // one CTA thread per 4 channels up to 1024 channels
+            for (const LossOp& o : ls) (o.c <= (o.c % 4 == 0 ? 4 : 1) * kThreads ? narrow : wide).push_back(o);
+            P.grouped<LossOp>(launch_loss, narrow, [](const LossOp& o) { return o.ctas; });
+            P.grouped<LossOp>(launch_loss_wide, wide, [](const LossOp& o) { return o.ctas; });
             P.grouped<BnBwdFinOp>(launch_bn_bwd_fin, fs, [](const BnBwdFinOp& o) { return ctas_cols(o.c); });
         }
         // ---- backward

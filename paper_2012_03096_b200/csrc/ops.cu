@@ -837,6 +837,49 @@ void launch_bn_stat(const BnStatOp* d, int nd, int ctas, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------- loss + BN
+// One channel pass of the loss kernel: thread (rr, gg) owns V channels of
+// [cb, cb+cw) and rows rr, rr+RP, ... of the CTA's row range.
+__device__ __forceinline__ void loss_pass(const LossOp& o, int local, int cb, int cw, int V, float* red, float& lsum) {
+    Geo g;
+    g.V = V, g.G = cw / V, g.RP = max(1, kThreads / g.G);
+    const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
+    const bool lane_ok = rr < g.RP;
+    const long long r0 = static_cast<long long>(local) * o.rows_per;
+    const long long r1 = min(static_cast<long long>(o.rows), r0 + o.rows_per);
+    const int c0 = cb + gg * g.V;
+    float sg[4] = {0, 0, 0, 0}, sgx[4] = {0, 0, 0, 0};
+    if (lane_ok) {
+        float mean[4], inv[4], gam[4], bet[4];
+        load_v(o.mean + c0, g.V, mean);
+        load_v(o.inv + c0, g.V, inv);
+        load_v(o.gamma + c0, g.V, gam);
+        load_v(o.beta + c0, g.V, bet);
+        auto body = [&](long long r, const float* tp) {
+            float pv[4], tv[4];
+            load_v(o.p + r * o.c + c0, g.V, pv);
+            load_v(tp, g.V, tv);
+            for (int q = 0; q < g.V; ++q) {
+                const float xh = mul(sub(pv[q], mean[q]), inv[q]);
+                const float y = add(mul(gam[q], xh), bet[q]);
+                const float d = sub(relu(y), tv[q]);
+                lsum += d * d;
+                const float gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
+                sg[q] += gy;
+                sgx[q] += gy * xh;
+            }
+        };
+        if (o.trows == nullptr) {
+#pragma unroll 4
+            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + r * o.c + c0);
+        } else {  // targets gathered through the epoch order
+#pragma unroll 4
+            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + row_remap(o.trows, o.srow, r * o.c + c0));
+        }
+    }
+    cta_reduce_rows(red, sg, g, rr, gg, lane_ok, cw, o.part_sg + static_cast<long long>(local) * o.c + cb);
+    cta_reduce_rows(red, sgx, g, rr, gg, lane_ok, cw, o.part_sgx + static_cast<long long>(local) * o.c + cb);
+}
+
 __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict__ ops, int nd) {
     pdl_enter();
     extern __shared__ float red[];
@@ -844,52 +887,65 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
     int local;
     const LossOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     if (is_failed(o.failed)) return;
-    // channel passes of kThreads*V channels (one pass unless c > 1024, e.g.
-    // the 2048-channel ResNet-50 stage): thread (rr, gg) of a pass owns V
-    // channels and rows rr, rr+RP, ... of the CTA's row range
-    const int V = (o.c % 4 == 0) ? 4 : 1;
+    const Geo g = geo_of(o.c);
+    const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
+    const bool lane_ok = rr < g.RP;
     const long long r0 = static_cast<long long>(local) * o.rows_per;
     const long long r1 = min(static_cast<long long>(o.rows), r0 + o.rows_per);
+    const int c0 = gg * g.V;
+    float sg[4] = {0, 0, 0, 0}, sgx[4] = {0, 0, 0, 0};
     float lsum = 0.0f;
-    for (int cb = 0; cb < o.c; cb += kThreads * V) {
-        const int cw = min(kThreads * V, o.c - cb);
-        Geo g;
-        g.V = V, g.G = cw / V, g.RP = max(1, kThreads / g.G);
-        const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
-        const bool lane_ok = rr < g.RP;
-        const int c0 = cb + gg * g.V;
-        float sg[4] = {0, 0, 0, 0}, sgx[4] = {0, 0, 0, 0};
-        if (lane_ok) {
-            float mean[4], inv[4], gam[4], bet[4];
-            load_v(o.mean + c0, g.V, mean);
-            load_v(o.inv + c0, g.V, inv);
-            load_v(o.gamma + c0, g.V, gam);
-            load_v(o.beta + c0, g.V, bet);
-            auto body = [&](long long r, const float* tp) {
-                float pv[4], tv[4];
-                load_v(o.p + r * o.c + c0, g.V, pv);
-                load_v(tp, g.V, tv);
-                for (int q = 0; q < g.V; ++q) {
-                    const float xh = mul(sub(pv[q], mean[q]), inv[q]);
-                    const float y = add(mul(gam[q], xh), bet[q]);
-                    const float d = sub(relu(y), tv[q]);
-                    lsum += d * d;
-                    const float gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
-                    sg[q] += gy;
-                    sgx[q] += gy * xh;
-                }
-            };
-            if (o.trows == nullptr) {
-#pragma unroll 4
-                for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + r * o.c + c0);
-            } else {  // targets gathered through the epoch order
-#pragma unroll 4
-                for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + row_remap(o.trows, o.srow, r * o.c + c0));
+    if (lane_ok) {
+        float mean[4], inv[4], gam[4], bet[4];
+        load_v(o.mean + c0, g.V, mean);
+        load_v(o.inv + c0, g.V, inv);
+        load_v(o.gamma + c0, g.V, gam);
+        load_v(o.beta + c0, g.V, bet);
+        auto body = [&](long long r, const float* tp) {
+            float pv[4], tv[4];
+            load_v(o.p + r * o.c + c0, g.V, pv);
+            load_v(tp, g.V, tv);
+            for (int q = 0; q < g.V; ++q) {
+                const float xh = mul(sub(pv[q], mean[q]), inv[q]);
+                const float y = add(mul(gam[q], xh), bet[q]);
+                const float d = sub(relu(y), tv[q]);
+                lsum += d * d;
+                const float gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
+                sg[q] += gy;
+                sgx[q] += gy * xh;
             }
+        };
+        if (o.trows == nullptr) {
+#pragma unroll 4
+            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + r * o.c + c0);
+        } else {  // targets gathered through the epoch order
+#pragma unroll 4
+            for (long long r = r0 + rr; r < r1; r += g.RP) body(r, o.t + row_remap(o.trows, o.srow, r * o.c + c0));
         }
-        cta_reduce_rows(red, sg, g, rr, gg, lane_ok, cw, o.part_sg + static_cast<long long>(local) * o.c + cb);
-        cta_reduce_rows(red, sgx, g, rr, gg, lane_ok, cw, o.part_sgx + static_cast<long long>(local) * o.c + cb);
     }
+    cta_reduce_rows(red, sg, g, rr, gg, lane_ok, o.c, o.part_sg + static_cast<long long>(local) * o.c);
+    cta_reduce_rows(red, sgx, g, rr, gg, lane_ok, o.c, o.part_sgx + static_cast<long long>(local) * o.c);
+    lred[threadIdx.x] = lsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.0f;
+        for (int i = 0; i < kThreads; ++i) s += lred[i];
+        o.part_loss[local] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) loss_wide_kernel(const LossOp* __restrict__ ops, int nd) {
+    pdl_enter();
+    extern __shared__ float red[];
+    __shared__ float lred[kThreads];
+    int local;
+    const LossOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    if (is_failed(o.failed)) return;
+    const int V = (o.c % 4 == 0) ? 4 : 1;
+    float lsum = 0.0f;
+    // channel passes of kThreads*V (the 2048-channel ResNet-50 stage); same
+    // per-thread order as loss_kernel when there is one pass
+    for (int cb = 0; cb < o.c; cb += kThreads * V) loss_pass(o, local, cb, min(kThreads * V, o.c - cb), V, red, lsum);
     lred[threadIdx.x] = lsum;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -901,6 +957,11 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
 
 void launch_loss(const LossOp* d, int nd, int ctas, cudaStream_t st) {
     launch_k(loss_kernel, dim3(ctas), dim3(kThreads), red_smem(0), st, d, nd);
+    PBKD_LAUNCH_CHECK();
+}
+
+void launch_loss_wide(const LossOp* d, int nd, int ctas, cudaStream_t st) {
+    launch_k(loss_wide_kernel, dim3(ctas), dim3(kThreads), red_smem(0), st, d, nd);
     PBKD_LAUNCH_CHECK();
 }
 

@@ -265,7 +265,8 @@ void launch_reduce(const ReduceOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_gemm_bn(const GemmOp* d_ops, int nd, int ctas, int cls, cudaStream_t st);
 void launch_gemm_tma(const GemmOp* d_ops, int nd, int tiles, int cls, cudaStream_t st);  // cls: gemm_bn_class
 void launch_bn_stat(const BnStatOp* d_ops, int nd, int ctas, cudaStream_t st);
-void launch_loss(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);
+void launch_loss(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);       // c <= 1024
+void launch_loss_wide(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);  // any c (channel passes)
 void launch_bn_bwd_fin(const BnBwdFinOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_bn_bwd_apply(const BnBwdApplyOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_sgd(const SgdOp* d_ops, int nd, int ctas, cudaStream_t st);
