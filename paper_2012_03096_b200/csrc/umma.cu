@@ -265,9 +265,6 @@ int bn_for(int n) {
 }  // namespace
 
 void gemm_finalize(GemmOp& o) {
-    o.bn = bn_for(o.N);
-    o.tiles_m = ceil_div(o.M, kBM);
-    o.tiles_n = ceil_div(o.N, o.bn);
     if (o.ksplit < 1) o.ksplit = 1;
     if (o.ksplit == 1) {
         o.kchunk = ((o.K + kBK - 1) / kBK) * kBK;
@@ -275,6 +272,18 @@ void gemm_finalize(GemmOp& o) {
         o.kchunk = ((ceil_div(o.K, o.ksplit) + kBK - 1) / kBK) * kBK;
         o.ksplit = ceil_div(o.K, o.kchunk);
     }
+    // PBKD_BN64_K=<k>: run tiles whose K range is >= k on 64-wide N tiles (4
+    // operand stages instead of 3, twice the tiles).  Measured on the VGG-16
+    // epoch (tools/gpu_ab_env.sh, k = 64..512): neutral for the student GEMMs
+    // and 22% slower teacher convs, so off by default.  Same bits either way.
+    static const int longk = [] {
+        const char* e = std::getenv("PBKD_BN64_K");
+        return e ? std::atoi(e) : 0;
+    }();
+    o.bn = bn_for(o.N);
+    if (o.bn == 128 && longk > 0 && o.kchunk >= longk) o.bn = 64;
+    o.tiles_m = ceil_div(o.M, kBM);
+    o.tiles_n = ceil_div(o.N, o.bn);
     if (o.tf32x3 == 0) {  // parity mode: split fp32 into tf32 hi+lo
         static const int terms = [] {
             const char* e = std::getenv("PBKD_TF32_TERMS");
@@ -295,9 +304,9 @@ void gemm_finalize(GemmOp& o) {
 int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
 // + kGemmClassTma: TMA kernel; + 2 kGemmClassTma: TMA kernel, both operands pre-split
 int gemm_bn_class(const GemmOp& o) {
-    if (!o.tma) return bn_for(o.N);
+    if (!o.tma) return o.bn;
     const int kind = o.conv ? kGemmKindConv : o.epi;
-    return bn_for(o.N) + kGemmClassTma + (o.a_presplit && o.b_presplit ? kGemmClassTma : 0) + kind * kGemmClassKind;
+    return o.bn + kGemmClassTma + (o.a_presplit && o.b_presplit ? kGemmClassTma : 0) + kind * kGemmClassKind;
 }
 
 template <int BN>
