@@ -327,14 +327,16 @@ def main():
     # launch list (profiles/r1_traffic.json, tools/traffic_summary.py), next to
     # its algorithmic bytes per launch
     traffic, traffic_note = None, None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
     if os.path.exists(tpath):
         tr_all = json.load(open(tpath))
         if dom in tr_all:
             traffic = tr_all[dom]["dram_bytes_per_launch"]
             c = kclasses[dom]
             traffic_note = {"unit": "bytes per launch", "algorithmic_bytes_per_launch": c["bytes"] / c["launches"],
-                            "source": "profiles/r1_traffic.json: " + tr_all[dom]["source"]}
+                            "source": "profiles/" + os.path.basename(tpath) + ": " + tr_all[dom]["source"]}
     roofline = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
                 "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic, "traffic_detail": traffic_note,
                 "peak_source": ("MEASURED_PEAKS.json " + ("bf16_tflops/2/3 (3xTF32 fp32-equivalent roof)"
