@@ -87,6 +87,12 @@ __device__ __forceinline__ uint32_t tc_split_hi(float x) {
     asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return r & 0xFFFFE000u;
 }
+// lo = hi(x - hi); for x = +-inf the remainder inf - inf would be NaN, but
+// the fp32 product the split stands for is (+-inf) * b: lo is 0 so that
+// hi*b_hi + hi*b_lo + lo*b_hi keeps the infinity (NaN x stays NaN)
+__device__ __forceinline__ uint32_t tc_split_lo(float x, float hv) {
+    return isinf(x) ? 0u : tc_split_hi(__fsub_rn(x, hv));
+}
 
 // Packed fp32x2 arithmetic (FFMA2: two lanes per instruction, each rounded
 // exactly like the scalar _rn op).  mul / add / sub are spelled as single

@@ -173,8 +173,9 @@ __device__ __forceinline__ void dw_fwd_tile(const DwFwdOp& o, const DwPos& q, fl
                     const float2 hv = make_float2(__uint_as_float(tc_split_hi(acc.x)), __uint_as_float(tc_split_hi(acc.y)));
                     const float2 d = sub2(K, acc, hv);
                     *reinterpret_cast<float2*>(yh + off) = hv;
-                    *reinterpret_cast<float2*>(yl + off) =
-                        make_float2(__uint_as_float(tc_split_hi(d.x)), __uint_as_float(tc_split_hi(d.y)));
+                    *reinterpret_cast<float2*>(yl + off) =  // infinities: lo = 0 (tc_split_lo)
+                        make_float2(isinf(acc.x) ? 0.0f : __uint_as_float(tc_split_hi(d.x)),
+                                    isinf(acc.y) ? 0.0f : __uint_as_float(tc_split_hi(d.y)));
                 } else {
                     *reinterpret_cast<float2*>(yf + off) = acc;
                 }

@@ -75,7 +75,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmOp& op, float* acc, int 
                     if (ncol + j < N) {
                         const float hv = __uint_as_float(tc_split_hi(val[j]));
                         Ch[off + j] = hv;
-                        Cl[off + j] = __uint_as_float(tc_split_hi(__fsub_rn(val[j], hv)));
+                        Cl[off + j] = __uint_as_float(tc_split_lo(val[j], hv));
                     }
             }
         }

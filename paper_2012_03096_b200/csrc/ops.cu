@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
                 if (yh) {  // tf32 planes for the pointwise GEMMs (3xTF32 operand split)
                     const float hv = __uint_as_float(tc_split_hi(acc));
                     yh[off] = hv;
-                    yl[off] = __uint_as_float(tc_split_hi(__fsub_rn(acc, hv)));
+                    yl[off] = __uint_as_float(tc_split_lo(acc, hv));
                 } else {
                     yf[off] = acc;
                 }
@@ -1035,10 +1035,10 @@ __device__ __forceinline__ float4 bn_bwd_quad(const BnBwdApplyOp& o, int ch, flo
 }
 __device__ __forceinline__ void split_store4(float* hi, float* lo, long long i, float4 r) {
     float4 h, l;
-    h.x = __uint_as_float(tc_split_hi(r.x)), l.x = __uint_as_float(tc_split_hi(__fsub_rn(r.x, h.x)));
-    h.y = __uint_as_float(tc_split_hi(r.y)), l.y = __uint_as_float(tc_split_hi(__fsub_rn(r.y, h.y)));
-    h.z = __uint_as_float(tc_split_hi(r.z)), l.z = __uint_as_float(tc_split_hi(__fsub_rn(r.z, h.z)));
-    h.w = __uint_as_float(tc_split_hi(r.w)), l.w = __uint_as_float(tc_split_hi(__fsub_rn(r.w, h.w)));
+    h.x = __uint_as_float(tc_split_hi(r.x)), l.x = __uint_as_float(tc_split_lo(r.x, h.x));
+    h.y = __uint_as_float(tc_split_hi(r.y)), l.y = __uint_as_float(tc_split_lo(r.y, h.y));
+    h.z = __uint_as_float(tc_split_hi(r.z)), l.z = __uint_as_float(tc_split_lo(r.z, h.z));
+    h.w = __uint_as_float(tc_split_hi(r.w)), l.w = __uint_as_float(tc_split_lo(r.w, h.w));
     *reinterpret_cast<float4*>(hi + i) = h;
     *reinterpret_cast<float4*>(lo + i) = l;
 }
@@ -1085,7 +1085,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApply
             if (o.gout_hi) {
                 const float hv = __uint_as_float(tc_split_hi(rv[q]));
                 o.gout_hi[base + q] = hv;
-                o.gout_lo[base + q] = __uint_as_float(tc_split_hi(__fsub_rn(rv[q], hv)));
+                o.gout_lo[base + q] = __uint_as_float(tc_split_lo(rv[q], hv));
             } else {
                 o.gout[base + q] = rv[q];
             }
@@ -1141,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__
             if (o.w_hi) {
                 const float hv = __uint_as_float(tc_split_hi(ww));
                 o.w_hi[i] = hv;
-                o.w_lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(ww, hv)));
+                o.w_lo[i] = __uint_as_float(tc_split_lo(ww, hv));
             }
         }
     }
@@ -1203,7 +1203,7 @@ __global__ void tf32_split_kernel(const float* __restrict__ x, long long n, floa
         const float v = x[i];
         const float h = __uint_as_float(tc_split_hi(v));
         hi[i] = h;
-        lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(v, h)));
+        lo[i] = __uint_as_float(tc_split_lo(v, h));
     }
 }
 
@@ -1223,7 +1223,7 @@ __global__ void conv_weight_prep_kernel(const float* __restrict__ raw, int cout,
         const float h = __uint_as_float(tc_split_hi(v));
         w[i] = v;
         hi[i] = h;
-        lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(v, h)));
+        lo[i] = __uint_as_float(tc_split_lo(v, h));
     }
 }
 
@@ -1326,7 +1326,7 @@ __global__ void maxpool3x3_kernel(const float* __restrict__ x, float* __restrict
         if (y_hi) {
             const float hv = __uint_as_float(tc_split_hi(m));
             y_hi[i] = hv;
-            y_lo[i] = __uint_as_float(tc_split_hi(__fsub_rn(m, hv)));
+            y_lo[i] = __uint_as_float(tc_split_lo(m, hv));
         }
     }
 }

@@ -52,7 +52,7 @@ __device__ __forceinline__ void put_half(uint8_t* hi, uint8_t* lo, int r, int h,
         for (int q = 0; q < 4; ++q) {
             const float x = v[cc * 4 + q];
             hv[q] = to_tf32(x);
-            lv[q] = split ? to_tf32(__fsub_rn(x, __uint_as_float(hv[q]))) : 0u;
+            lv[q] = split && !isinf(x) ? to_tf32(__fsub_rn(x, __uint_as_float(hv[q]))) : 0u;
         }
         const int off = sw128(r, c);
         *reinterpret_cast<uint4*>(hi + off) = make_uint4(hv[0], hv[1], hv[2], hv[3]);

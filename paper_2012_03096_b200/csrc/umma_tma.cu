@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -114,7 +115,7 @@ __device__ __forceinline__ void split4(const float* x, uint32_t* hv, uint32_t* l
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         hv[q] = to_tf32(x[q]);
-        lv[q] = split ? to_tf32(__fsub_rn(x[q], __uint_as_float(hv[q]))) : 0u;
+        lv[q] = split && !isinf(x[q]) ? to_tf32(__fsub_rn(x[q], __uint_as_float(hv[q]))) : 0u;
     }
 }
 __device__ __forceinline__ void convert_tile(uint32_t raw, uint32_t hi, uint32_t lo, int rows, bool kmajor,
@@ -225,7 +226,7 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
                 if (c_hi) {
                     const float hv = __uint_as_float(tc_split_hi(x));
                     c_hi[static_cast<long long>(row) * ldc + n] = hv;
-                    c_lo[static_cast<long long>(row) * ldc + n] = __uint_as_float(tc_split_hi(__fsub_rn(x, hv)));
+                    c_lo[static_cast<long long>(row) * ldc + n] = __uint_as_float(tc_split_lo(x, hv));
                 }
             }
         }
@@ -881,7 +882,7 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
     };
     for (size_t i = 0; i < n; ++i) {
         const float h = rne(x[i]);
-        volatile float d = x[i] - h;  // exact (Sterbenz), no contraction
+        volatile float d = std::isinf(x[i]) ? 0.0f : x[i] - h;  // exact (Sterbenz), no contraction; inf: lo 0
         hi[i] = h;
         lo[i] = rne(d);
     }

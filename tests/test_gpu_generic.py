@@ -101,3 +101,41 @@ def test_combined_objective_is_linear_in_lambda(ctx):
         return ctx.run([t], G["train_idx"], G["eval_idx"])["results"][0]["loss_history"]
     ce_only, both, local = run(1, 0.0), run(1, 2.0), run(0, 0.0)
     assert both[1] == pytest.approx(2.0 * local[1] + ce_only[1], rel=1e-9)
+
+
+def test_mixed_paths_in_one_run_match_single_runs(ctx):
+    """Grouped (LocalOnly two-layer) and layer-by-layer (Combined, skip)
+    tasks in one run / one run_parallel give each task's single-run bits."""
+    def tasks():
+        return [P.make_task(1, epochs=2, eval_every=1, seed=11, batch_size=16, lr=0.02),
+                P.make_task(2, epochs=2, eval_every=1, seed=12, batch_size=16, lr=0.02, loss_mode=1,
+                            lambda_local=0.5),
+                P.make_task(3, kind=2, epochs=2, eval_every=1, seed=13, batch_size=16, lr=0.02)]
+    alone = [ctx.run([t], G["train_idx"], G["eval_idx"])["results"][0] for t in tasks()]
+    grouped = ctx.run(tasks(), G["train_idx"], G["eval_idx"])["results"]
+    par = ctx.run(tasks(), G["train_idx"], G["eval_idx"], plan=[[1, 3], [2]], workers=2, policy="wfd")["results"]
+    for a, b, c in zip(alone, grouped, par):
+        for x in (b, c):
+            assert x["block_index"] == a["block_index"] and not x["failed"]
+            assert np.array_equal(x["block"], a["block"]) and x["loss_history"] == a["loss_history"]
+
+
+def test_divergence_is_reported_like_the_reference(ctx, orc):
+    """distill.cpp:236-244 on the grouped engine: a non-finite local loss
+    (targets from a teacher block holding +inf) marks the task failed with
+    the reference's message instead of throwing; the CPU restatement fails
+    the same task at the same epoch and batch."""
+    tw = np.array(G["teacher_w"], np.float32)
+    tw[16 * 3 * 9 + 4 * 16 + 5] = np.inf  # block 2's first conv weight: boundary 2 non-finite
+    ctx.teacher_load(SPEC, tw)
+    try:
+        t = P.make_task(2, epochs=2, eval_every=1, seed=1234, batch_size=16, lr=0.02)
+        r = ctx.run([t], G["train_idx"], G["eval_idx"])["results"][0]
+        from oracle.oracle import make_task as orc_task
+        want = orc.train_block(SPEC, tw, G["images"], G["labels"], G["train_idx"], G["eval_idx"],
+                               orc_task(2, epochs=2, eval_every=1, seed=1234, batch_size=16, lr=0.02), 1 << 16)
+        assert want["failed"] and r["failed"], (want["failure"], r["failure"])
+        prefix = want["failure"].split(" (loss")[0]
+        assert r["failure"].startswith(prefix), (r["failure"], want["failure"])
+    finally:
+        ctx.teacher_load(SPEC, G["teacher_w"])
