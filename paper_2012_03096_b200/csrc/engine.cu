@@ -206,8 +206,13 @@ public:
         // landing last behind the short tiles (the launch's critical path).
         // Tile results do not depend on which CTA computes them.
         std::stable_sort(ops.begin(), ops.end(), [](const GemmOp& a, const GemmOp& b) { return a.kchunk > b.kchunk; });
-        if (knocked_out(std::string("gemm_") + (ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad")))
-            return;
+        const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
+        const std::string cname = std::string("gemm_") + kind +
+                                  (cls % kGemmClassKind >= 2 * kGemmClassTma ? "_pre"
+                                   : cls % kGemmClassKind >= kGemmClassTma   ? "_tma"
+                                                                             : "_reg") +
+                                  std::to_string(cls % kGemmClassTma);
+        if (knocked_out(cname)) return;
         int total = 0;
         for (GemmOp& o : ops) {
             o.cta_begin = total;
@@ -220,12 +225,7 @@ public:
         steps_.push_back([off, nd, total, cls](cudaStream_t st, const uint8_t* slab) {
             launch_gemm_bn(reinterpret_cast<const GemmOp*>(slab + off), nd, total, cls, st);
         });
-        const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
-        names_.push_back(std::string("gemm_") + kind +
-                         (cls % kGemmClassKind >= 2 * kGemmClassTma ? "_pre"
-                          : cls % kGemmClassKind >= kGemmClassTma   ? "_tma"
-                                                                    : "_reg") +
-                         std::to_string(cls % kGemmClassTma));
+        names_.push_back(cname);
         KernelStat w;
         for (const GemmOp& o : ops) {
             const auto bf = op_work(o);
@@ -533,7 +533,12 @@ struct TaskState {
     int units = 2;
     UnitDims u[kMaxUnits];
     int k = 0;  // block index
-    int in_row = 0, out_row = 0;
+    // in_row: one sample of the student's input.  The first unit of a block
+    // whose input has a channel count that is not a multiple of 4 (the
+    // network input, 3 channels) runs on zero-padded channels (u[0].cin, a
+    // multiple of 4: 16-byte rows for the TMA GEMMs and depthwise tiles);
+    // cin_ref is the real count (parameter layout of the results)
+    int in_row = 0, out_row = 0, cin_ref = 0;
     long long total_steps = 0;
     std::vector<int> steps_in_epoch;  // [epochs+1], index 0 unused
     // parameters
@@ -591,7 +596,24 @@ void pad4(std::vector<float>& v) {
     while (v.size() % 4) v.push_back(0.0f);
 }
 
-int split_count(long long kdim) { return std::max(1, std::min(64, ceil_div(kdim, 512))); }
+// channel count a student unit runs its input on (see TaskState::cin_ref)
+int padded_channels(int c) { return c % 4 == 0 ? c : (c + 3) / 4 * 4; }
+
+int split_rows() {  // rows per wgrad K split (diagnosis knob PBKD_SPLIT_ROWS)
+    static const int r = [] {
+        const char* e = std::getenv("PBKD_SPLIT_ROWS");
+        return e ? std::max(32, std::atoi(e)) : 512;
+    }();
+    return r;
+}
+int split_max() {
+    static const int r = [] {
+        const char* e = std::getenv("PBKD_SPLIT_MAX");
+        return e ? std::max(1, std::atoi(e)) : 64;
+    }();
+    return r;
+}
+int split_count(long long kdim) { return std::max(1, std::min<int>(split_max(), ceil_div(kdim, split_rows()))); }
 
 }  // namespace
 
@@ -887,8 +909,10 @@ struct Engine::Impl {
         const TBlockDev& tb = tblocks[static_cast<size_t>(s.k) - 1];
         s.units = (t.kind == pbkd::CandidateKind::ThreeLayer) ? 3 : 2;
         const int ho = (tb.hin - 1) / tb.stride + 1, wo = (tb.win - 1) / tb.stride + 1;
+        s.cin_ref = tb.cin;
+        const int cpad = padded_channels(tb.cin);
         for (int u = 0; u < s.units; ++u)
-            s.u[u] = u == 0 ? UnitDims{tb.cin, tb.hin, tb.win, tb.cout, ho, wo, tb.stride}
+            s.u[u] = u == 0 ? UnitDims{cpad, tb.hin, tb.win, tb.cout, ho, wo, tb.stride}
                             : UnitDims{tb.cout, ho, wo, tb.cout, ho, wo, 1};
     }
 
@@ -897,7 +921,7 @@ struct Engine::Impl {
         const TBlockDev& tb = tblocks[static_cast<size_t>(s.k) - 1];
         const int ho = s.u[0].ho, wo = s.u[0].wo;
         if (ho != tb.hout || wo != tb.wout) throw SpecError("candidate output shape differs from teacher block");
-        s.in_row = tb.cin * tb.hin * tb.win;
+        s.in_row = s.u[0].cin * tb.hin * tb.win;
         s.out_row = tb.cout * ho * wo;
         const int B = t.batch_size;
         const int spe = ceil_div(ntrain, B);
@@ -940,7 +964,7 @@ struct Engine::Impl {
     // parameter layout.
     static void init_task_host(TaskState& s) {
         const DistillTask& t = s.task;
-        pbkd::ReplacementBlock cand = pbkd::build_candidate(t.kind, s.u[0].cin, s.u[0].cout, s.u[0].stride,
+        pbkd::ReplacementBlock cand = pbkd::build_candidate(t.kind, s.cin_ref, s.u[0].cout, s.u[0].stride,
                                                             pbkd::mix_seed(t.seed, 0));
         std::vector<float>& host = s.host_params;
         std::vector<float>& stats = s.host_stats;
@@ -952,14 +976,15 @@ struct Engine::Impl {
             const pbkd::LayerParams& pwl = cand.block.layers[li + 1];
             const pbkd::LayerParams& bnl = cand.block.layers[li + 2];
             li += 4;
-            const int ci = s.u[u].cin, co = s.u[u].cout;
+            const int ci = s.u[u].cin, cr = u == 0 ? s.cin_ref : ci, co = s.u[u].cout;
             pad4(host);
             s.off_dw[u] = host.size();
             for (int tap = 0; tap < 9; ++tap)
-                for (int c = 0; c < ci; ++c) host.push_back(dwl.weight.data[static_cast<size_t>(c) * 9 + tap]);
+                for (int c = 0; c < ci; ++c) host.push_back(c < cr ? dwl.weight.data[static_cast<size_t>(c) * 9 + tap] : 0.0f);
             pad4(host);
             s.off_pw[u] = host.size();
-            host.insert(host.end(), pwl.weight.data.begin(), pwl.weight.data.end());
+            for (int o = 0; o < co; ++o)  // [co][ci], padded input channels 0
+                for (int c = 0; c < ci; ++c) host.push_back(c < cr ? pwl.weight.data[static_cast<size_t>(o) * cr + c] : 0.0f);
             pad4(host);
             s.off_g[u] = host.size();
             host.insert(host.end(), bnl.gamma.data.begin(), bnl.gamma.data.end());
@@ -979,8 +1004,10 @@ struct Engine::Impl {
         // epoch order and workspace
         s.pos.alloc(static_cast<size_t>(ntrain) * sizeof(int));
         s.eval_in.alloc(static_cast<size_t>(std::max(neval, 1)) * s.in_row * sizeof(float));
+        if (s.cin_ref != s.u[0].cin)  // padded channels stay 0 (the sink writes the real ones)
+            PBKD_CUDA(cudaMemsetAsync(s.eval_in.p, 0, static_cast<size_t>(std::max(neval, 1)) * s.in_row * sizeof(float), st));
         const long long M = static_cast<long long>(B) * ho * wo;
-        const int cin = tb.cin, cout = tb.cout, cmax = std::max(cin, cout);
+        const int cin = s.u[0].cin, cout = tb.cout, cmax = std::max(cin, cout);
         for (int u = 0; u < s.units; ++u) {
             s.d[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
             s.planes_d[u] = gemm_presplit_ok(s.u[u].cin) && gemm_presplit_ok(s.u[u].cout) && s.planes_w;
@@ -1374,6 +1401,7 @@ struct Engine::Impl {
         float* dst;
         const int* pos;
         int width;
+        int cs = 0, cd = 0;  // channel padding of the destination rows (ScatterOp)
     };
     // Teacher boundaries: boundary j of training row t lives at bnd[j] + t *
     // bnd_row(j) (bnd[0] = the NHWC images, gathered for every row first).
@@ -1434,7 +1462,7 @@ struct Engine::Impl {
             for (int j = 0; j <= kmax; ++j) {
                 std::vector<ScatterOp> sc;
                 for (const Sink& s : sinks)
-                    if (s.boundary == j) sc.push_back(ScatterOp{cur, s.dst, s.pos + t0, nc, s.width, 0});
+                    if (s.boundary == j) sc.push_back(ScatterOp{cur, s.dst, s.pos + t0, nc, s.width, s.cs, s.cd, 0});
                 auto scatter = [](Program& Q, std::vector<ScatterOp> ops) {
                     Q.grouped<ScatterOp>(launch_scatter, std::move(ops), [](const ScatterOp&) { return kScatterCtas; });
                 };
@@ -1520,6 +1548,14 @@ struct Engine::Impl {
     struct Boundaries {
         std::vector<DevBuf> bufs;
         std::vector<float*> bnd;  // bnd[j], j = 0..kmax, [ntrain][bnd_row(j)]
+        // student inputs on zero-padded channels (TaskState::cin_ref): a copy
+        // of boundary j with cd channels per pixel, made once the rows are in
+        struct Pad {
+            int j, cs, cd;
+            DevBuf buf;
+        };
+        std::vector<Pad> pads;
+        const int* iota = nullptr;  // 0..ntrain-1
         BoundaryPlan plan;
         int kmax = 0, me = 0, world = 1, chunk = 1;
         bool done = false;
@@ -1590,6 +1626,15 @@ struct Engine::Impl {
                 P.run(st);
         }
         if (b.world > 1) comm->exchange(b.plan, b.bnd, st);  // boundary rows to the blocks that read them
+        if (!b.pads.empty()) {
+            Program P;
+            std::vector<ScatterOp> ops;
+            for (auto& p : b.pads)
+                ops.push_back(ScatterOp{b.bnd[static_cast<size_t>(p.j)], p.buf.f(), b.iota, ntrain, bnd_row(p.j), p.cs,
+                                        p.cd, 0});
+            P.grouped<ScatterOp>(launch_scatter, std::move(ops), [](const ScatterOp&) { return kScatterCtas; });
+            P.run(st);
+        }
         PBKD_CUDA(cudaEventRecord(b.t1, st));
         trace.mark("run: teacher boundaries");
     }
@@ -1726,10 +1771,25 @@ std::vector<TaskOutcome> Engine::Impl::run_grouped(const std::vector<DistillTask
         }
         PBKD_CUDA(cudaEventCreate(&bd.t0));
         PBKD_CUDA(cudaEventCreate(&bd.t1));
+        bd.iota = d_iota.i();
         for (auto& sp : states) {
             sp->bx = bd.bnd[static_cast<size_t>(sp->k) - 1];
             sp->bt = bd.bnd[static_cast<size_t>(sp->k)];
             sp->nsrc = ntrain;
+            if (sp->cin_ref != sp->u[0].cin) {
+                const int j = sp->k - 1;
+                auto it = std::find_if(bd.pads.begin(), bd.pads.end(), [&](const Boundaries::Pad& p) { return p.j == j; });
+                if (it == bd.pads.end()) {
+                    Boundaries::Pad p{j, sp->cin_ref, sp->u[0].cin, DevBuf{}};
+                    const UnitDims& d0 = sp->u[0];  // (in_row is set later, by init_task)
+                    const size_t bytes = static_cast<size_t>(ntrain) * d0.cin * d0.hin * d0.win * sizeof(float);
+                    p.buf.alloc(bytes);
+                    PBKD_CUDA(cudaMemsetAsync(p.buf.p, 0, bytes, st));
+                    bd.pads.push_back(std::move(p));
+                    it = bd.pads.end() - 1;
+                }
+                sp->bx = it->buf.f();
+            }
         }
     }
     for (auto& kv : groups) run_group(kv.second, train_idx, eval_idx, opt, d_train, d_eval, d_iota, bd, prepare);
@@ -1816,14 +1876,17 @@ std::vector<TaskOutcome> Engine::Impl::run_grouped(const std::vector<DistillTask
         // reference's for_each_block_array order, written in place
         auto to_ref_order = [&](const float* flat) {
             size_t n = 0;
-            for (int u = 0; u < s.units; ++u) n += static_cast<size_t>(s.u[u].cin) * (9 + s.u[u].cout) + 4 * s.u[u].cout;
+            auto real_c = [&](int u) { return u == 0 ? s.cin_ref : s.u[u].cin; };
+            for (int u = 0; u < s.units; ++u) n += static_cast<size_t>(real_c(u)) * (9 + s.u[u].cout) + 4 * s.u[u].cout;
             std::vector<float> o(n);
             float* w = o.data();
             for (int u = 0; u < s.units; ++u) {
-                const int ci = s.u[u].cin, co = s.u[u].cout;
-                for (int c = 0; c < ci; ++c)
+                const int ci = s.u[u].cin, cr = real_c(u), co = s.u[u].cout;
+                for (int c = 0; c < cr; ++c)
                     for (int tap = 0; tap < 9; ++tap) *w++ = flat[s.off_dw[u] + static_cast<size_t>(tap) * ci + c];
-                w = std::copy(flat + s.off_pw[u], flat + s.off_pw[u] + static_cast<size_t>(co) * ci, w);
+                for (int oc = 0; oc < co; ++oc)
+                    w = std::copy(flat + s.off_pw[u] + static_cast<size_t>(oc) * ci,
+                                  flat + s.off_pw[u] + static_cast<size_t>(oc) * ci + cr, w);
                 w = std::copy(flat + s.off_g[u], flat + s.off_g[u] + co, w);
                 w = std::copy(flat + s.off_b[u], flat + s.off_b[u] + co, w);
                 const size_t st0 = s.nparams + static_cast<size_t>(u) * 2 * co;
@@ -2075,7 +2138,11 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         {  // eval-split prefix activations (once per run)
             Program P;
             std::vector<Sink> sk_eval;
-            for (TaskState* s : ts) sk_eval.push_back({s->k - 1, s->eval_in.f(), d_iota.i(), s->in_row});
+            for (TaskState* s : ts) {
+                const int c0 = s->u[0].cin, cr = s->cin_ref;
+                const int wsrc = s->in_row / c0 * cr;  // the boundary's own row width
+                sk_eval.push_back({s->k - 1, s->eval_in.f(), d_iota.i(), wsrc, cr != c0 ? cr : 0, cr != c0 ? c0 : 0});
+            }
             add_teacher_pass(P, d_eval.i(), neval, sk_eval, chunk, ping.f(), pong.f(), t1.f(), sk.f());
             P.run(st);
         }

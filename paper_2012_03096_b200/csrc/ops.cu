@@ -1158,6 +1158,16 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const ScatterOp* __re
     int local;
     const ScatterOp o = op_of(ops, nd, local);  // copy: no reloads after stores
     const long long step = static_cast<long long>(kThreads) * kScatterCtas;
+    if (o.cd > 0) {  // channel-padded destination rows
+        const long long total = static_cast<long long>(o.rows) * o.width;
+        const long long wd = static_cast<long long>(o.width / o.cs) * o.cd;
+        for (long long i = static_cast<long long>(local) * kThreads + threadIdx.x; i < total; i += step) {
+            const long long r = i / o.width, j = i - r * o.width;
+            const long long px = j / o.cs, ch = j - px * o.cs;
+            o.dst[static_cast<long long>(__ldg(o.pos + r)) * wd + px * o.cd + ch] = __ldg(o.src + i);
+        }
+        return;
+    }
     if ((o.width % 4) == 0) {
         const int wv = o.width / 4;
         const long long total = static_cast<long long>(o.rows) * wv;

@@ -245,11 +245,15 @@ struct SgdOp {
 // dst row pos[i] <- src row i   (activation streaming into a task's epoch order);
 // kScatterCtas CTAs per op
 constexpr int kScatterCtas = 148;
+// dst row pos[r] = src row r.  cd > 0: rows are pixels x cs channels in src
+// and pixels x cd channels in dst (cd > cs; the extra channels are left as
+// they are: zeroed by the owner once)
 struct ScatterOp {
     const float* src;
     float* dst;
     const int* pos;
     int rows, width;
+    int cs, cd;
     int cta_begin;
 };
 

@@ -460,7 +460,11 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                         const uint64_t dbl = bmn ? smem_desc_mn(bl, lbo, sbo) : smem_desc(bl);
                         mma_chunk3d(tmem + a * BN, dah, dal, dbh, dbl, amn ? 64 : 2, bmn ? 64 : 2, idesc);
                     } else {
+#ifdef PBKD_EXP_TERMS1  // diagnosis build only: hi*hi alone (wrong results)
+                        mma_chunk(tmem + a * BN, ah, al, bh, bl, idesc, 1);
+#else
                         mma_chunk(tmem + a * BN, ah, al, bh, bl, idesc, terms);
+#endif
                     }
                     mma_commit(&op_empty[s]);
                     mma_commit(&acc_full[a]);
@@ -493,7 +497,11 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                 for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                     const int s = it % S;
                     mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
+#ifdef PBKD_EXP_NOLO  // diagnosis build only: hi planes alone (wrong results)
+                    const uint32_t bytes = (apre ? C::a_op : 0) + (bpre ? C::b_op : 0);
+#else
                     const uint32_t bytes = (apre ? 2 * C::a_op : 0) + (bpre ? 2 * C::b_op : 0);
+#endif
                     if (bytes == 0) {
                         mbar_arrive(&op_full[s]);
                         continue;
@@ -510,12 +518,16 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                             tma_load_4d(os + C::a_op, &o.map_al, &op_full[s], c0, kx - o.cpad, y0 + ky, img);
                         } else if (akm) {
                             tma_load_2d(os, &o.map_ah, &op_full[s], k, m0);
+                            #ifndef PBKD_EXP_NOLO
                             tma_load_2d(os + C::a_op, &o.map_al, &op_full[s], k, m0);
+#endif
                         } else {
 #pragma unroll
                             for (int at = 0; at < kBM / 32; ++at) {
                                 tma_load_2d(os + at * 4096, &o.map_ah, &op_full[s], m0 + 32 * at, k);
+                                #ifndef PBKD_EXP_NOLO
                                 tma_load_2d(os + C::a_op + at * 4096, &o.map_al, &op_full[s], m0 + 32 * at, k);
+#endif
                             }
                         }
                     }
@@ -523,12 +535,16 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                         uint8_t* ob = os + 2 * C::a_op;
                         if (bkm) {
                             tma_load_2d(ob, &o.map_bh, &op_full[s], k, n0);
+                            #ifndef PBKD_EXP_NOLO
                             tma_load_2d(ob + C::b_op, &o.map_bl, &op_full[s], k, n0);
+#endif
                         } else {
 #pragma unroll
                             for (int at = 0; at < BN / 32; ++at) {
                                 tma_load_2d(ob + at * 4096, &o.map_bh, &op_full[s], n0 + 32 * at, k);
+                                #ifndef PBKD_EXP_NOLO
                                 tma_load_2d(ob + C::b_op + at * 4096, &o.map_bl, &op_full[s], n0 + 32 * at, k);
+#endif
                             }
                         }
                     }
@@ -590,7 +606,11 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                 tc_fence_after();
                 const uint32_t base = tmem + lane_off + a * BN + h * HB;
 #pragma unroll
-                for (int c0 = 0; c0 < HB; c0 += 16) tmem_add16(base + c0, acc + c0);
+                for (int c0 = 0; c0 < HB; c0 += 16) {
+#ifndef PBKD_EXP_NODRAIN  // diagnosis build only: no per-chunk drain (wrong results)
+                    tmem_add16(base + c0, acc + c0);
+#endif
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
