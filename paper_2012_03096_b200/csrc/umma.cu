@@ -306,6 +306,15 @@ int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }
 int gemm_bn_class(const GemmOp& o) {
     if (!o.tma) return o.bn;
     const int kind = o.conv ? kGemmKindConv : o.epi;
+    // pre-split student ops of every N tile share one launch of the 128-wide
+    // kernel (per-op MMA width, B box and epilogue passes): one launch per
+    // phase instead of a parallel section of 1-CTA-per-SM persistent kernels
+    // queueing for the SMs.  PBKD_GEMM_MERGE=0: one launch per N tile.
+    static const bool merge = [] {
+        const char* e = std::getenv("PBKD_GEMM_MERGE");
+        return !(e && e[0] == '0');
+    }();
+    if (merge && !o.conv && o.a_presplit && o.b_presplit) return 128 + 2 * kGemmClassTma + kind * kGemmClassKind;
     return o.bn + kGemmClassTma + (o.a_presplit && o.b_presplit ? kGemmClassTma : 0) + kind * kGemmClassKind;
 }
 

@@ -176,7 +176,7 @@ __device__ __forceinline__ uint32_t cs_addr(uint32_t cs, int r, int col) {  // e
 template <int BN, int KIND>
 __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* acc, int tm, int tn, int split, int q,
                                                 int h, int lane, int et, float (*red)[4][32], uint32_t cs,
-                                                int& stores) {
+                                                int& stores, int bnt) {
     constexpr int HB = BN / 2;
     const int warp8 = et >> 5;
     // every descriptor field in registers up front: the global stores below
@@ -192,11 +192,12 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
     float* __restrict__ part0 = op.part0;
     float* __restrict__ part1 = op.part1;
     const CUtensorMap* map_c = &op.map_c;
-    const int m0 = tm * kBM, n0 = tn * BN;
+    const int m0 = tm * kBM, n0 = tn * bnt;  // bnt: the op's N tile (<= BN)
     const int r = q * 32 + lane;
     const bool xform = KIND == kGemmKindConv && (scale || skip || relu_on || c_hi);
 #pragma unroll
     for (int pass = 0; pass < BN / 32; ++pass) {
+        if (pass * 32 >= bnt) break;  // tile-uniform
         if (et == 0 && stores) tma_store_wait_read();  // staging block free again
         named_bar(1, 256);
 #pragma unroll
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             const int terms = o.tf32x3;
             // pre-split MN-major operands stay MN-major in shared memory
             const bool amn = o.a_presplit && !(CONV && o.conv) && !o.a_kmajor, bmn = o.b_presplit && !o.b_kmajor;
-            const uint32_t idesc = instr_desc(BN, amn, bmn);
+            const uint32_t idesc = instr_desc(PS ? o.bn : BN, amn, bmn);
             for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                 const int s = it % S, a = it % C::A;
                 mbar_wait(&op_full[s], (it / S) & 1);
@@ -484,7 +485,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
-            const int m0 = g.tm * kBM, n0 = g.tn * BN;
+            const int bnt = PS ? o.bn : BN;  // a pre-split launch mixes N tiles (gemm_bn_class)
+            const int m0 = g.tm * kBM, n0 = g.tn * bnt;
             const bool apre = o.a_presplit != 0, bpre = o.b_presplit != 0;
             const bool akm = (CONV && o.conv != 0) || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
             int img = 0, y0 = 0;
@@ -498,9 +500,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     const int s = it % S;
                     mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
 #ifdef PBKD_EXP_NOLO  // diagnosis build only: hi planes alone (wrong results)
-                    const uint32_t bytes = (apre ? C::a_op : 0) + (bpre ? C::b_op : 0);
+                    const uint32_t bytes = (apre ? C::a_op : 0) + (bpre ? bnt * kRowBytes : 0);
 #else
-                    const uint32_t bytes = (apre ? 2 * C::a_op : 0) + (bpre ? 2 * C::b_op : 0);
+                    const uint32_t bytes = (apre ? 2 * C::a_op : 0) + (bpre ? 2 * bnt * kRowBytes : 0);
 #endif
                     if (bytes == 0) {
                         mbar_arrive(&op_full[s]);
@@ -541,6 +543,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                         } else {
 #pragma unroll
                             for (int at = 0; at < BN / 32; ++at) {
+                                if (at * 32 >= bnt) break;
                                 tma_load_2d(ob + at * 4096, &o.map_bh, &op_full[s], n0 + 32 * at, k);
                                 #ifndef PBKD_EXP_NOLO
                                 tma_load_2d(ob + C::b_op + at * 4096, &o.map_bl, &op_full[s], n0 + 32 * at, k);
@@ -597,6 +600,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
+            const int bnt = PS ? o.bn : BN;
+            const int hcols = min(HB, max(0, bnt - h * HB));  // this half's live columns
             float acc[HB];
 #pragma unroll
             for (int j = 0; j < HB; ++j) acc[j] = 0.0f;
@@ -608,7 +613,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
 #pragma unroll
                 for (int c0 = 0; c0 < HB; c0 += 16) {
 #ifndef PBKD_EXP_NODRAIN  // diagnosis build only: no per-chunk drain (wrong results)
-                    tmem_add16(base + c0, acc + c0);
+                    if (c0 < hcols) tmem_add16(base + c0, acc + c0);
 #endif
                 }
                 tc_fence_before();
@@ -618,7 +623,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     if (warp == kEpiWarp0) mark(3, it);
                 }
             }
-            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores);
+            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores, bnt);
             if (warp == kEpiWarp0 && lane == 0) mark(4, j);
         }
     }
