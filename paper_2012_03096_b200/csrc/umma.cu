@@ -314,7 +314,11 @@ int gemm_bn_class(const GemmOp& o) {
         const char* e = std::getenv("PBKD_GEMM_MERGE");
         return !(e && e[0] == '0');
     }();
-    if (merge && !o.conv && o.a_presplit && o.b_presplit) return 128 + 2 * kGemmClassTma + kind * kGemmClassKind;
+    // Plain stores (epi 0) and split-K partial stores (epi 2) share kernel
+    // kind 0 (the store's split coordinate is 0 without split-K), so a
+    // unit's dgrad and wgrad can run as one launch.
+    if (merge && !o.conv && o.a_presplit && o.b_presplit)
+        return 128 + 2 * kGemmClassTma + (kind == 2 ? 0 : kind) * kGemmClassKind;
     return o.bn + kGemmClassTma + (o.a_presplit && o.b_presplit ? kGemmClassTma : 0) + kind * kGemmClassKind;
 }
 

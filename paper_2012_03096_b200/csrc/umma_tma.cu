@@ -234,7 +234,7 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
         fence_async_smem();
         named_bar(1, 256);
         if (et == 0) {
-            tma_store_3d(map_c, cs, n0 + pass * 32, m0, KIND == 2 ? split : 0);
+            tma_store_3d(map_c, cs, n0 + pass * 32, m0, split);  // split 0 unless split-K (epi 2)
             tma_store_commit();
             stores = 1;
         }
