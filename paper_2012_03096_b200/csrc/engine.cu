@@ -703,9 +703,12 @@ struct Engine::Impl {
         } else if (nflat != total) {
             throw std::invalid_argument("teacher weights: flat size does not match the network");
         }
+        trace.st = st;
+        trace.t = std::chrono::steady_clock::now();
         tnet.reset();
         teacher_flat.alloc(std::max<size_t>(total, 1) * sizeof(float));
         PBKD_CUDA(cudaMemcpyAsync(teacher_flat.p, flat, total * sizeof(float), cudaMemcpyHostToDevice, st));
+        trace.mark("teacher: H2D copy");
         const float* dbase = teacher_flat.f();
         auto dev_of = [&](const pbkd::Tensor& t) { return dbase + off.at(&t); };
         tblocks.clear();
@@ -771,6 +774,7 @@ struct Engine::Impl {
             w = d.wout;
             tblocks.push_back(std::move(d));
         }
+        trace.mark("teacher: blocks (prep)");
         cls_in_c = c;
         cls_hw = h * w;
         std::vector<int> kinds;
@@ -2456,6 +2460,11 @@ void Engine::set_teacher(const Network& net) { impl_->load_teacher(net); }
 void Engine::set_teacher(Network&& net) { impl_->load_teacher(std::move(net)); }
 void Engine::set_teacher(Network&& net, const float* flat, size_t n) { impl_->load_teacher(std::move(net), flat, n); }
 const Network& Engine::teacher() const { return impl_->net; }
+Network Engine::take_teacher() {
+    impl_->has_teacher = false;
+    impl_->tnet.reset();
+    return std::move(impl_->net);
+}
 bool Engine::has_teacher() const { return impl_->has_teacher; }
 void Engine::set_dataset(const float* img, const int* lab, int n, int c, int h, int w, int cls, bool on_dev) {
     impl_->load_dataset(img, lab, n, c, h, w, cls, on_dev);

@@ -103,6 +103,10 @@ public:
     void set_teacher(pbkd::Network&& net);
     // flat: the same weights in for_each_array order (one H2D copy from it)
     void set_teacher(pbkd::Network&& net, const float* flat, size_t n);
+    // Moves the loaded teacher network (host tensors) out of the engine, which
+    // then holds no teacher until the next set_teacher: a reload with the same
+    // spec refills these tensors instead of parsing and allocating anew.
+    pbkd::Network take_teacher();
     const pbkd::Network& teacher() const;
     bool has_teacher() const;
     void set_dataset(const float* images, const int* labels, int count, int c, int h, int w,

@@ -206,7 +206,21 @@ int pbkd_spec_num_blocks(const char* spec, int* n) {
 
 int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec, const float* w, size_t n) {
     return guard([&] {
-        pbkd::Network net = spec_net(spec);
+        static const bool tr = std::getenv("PBKD_TRACE") != nullptr;
+        auto t0 = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (!tr) return;
+            const auto now = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[pbkd] teacher_load: %-22s %9.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(now - t0).count());
+            t0 = now;
+        };
+        // same spec as the loaded teacher (single engine): refill its host
+        // tensors in place (no parse, no fresh pages for tens of MB)
+        const bool reuse = ctx->peers.empty() && ctx->eng->has_teacher() && spec != nullptr && ctx->spec == spec &&
+                           net_floats(const_cast<pbkd::Network&>(ctx->eng->teacher())) == n;
+        pbkd::Network net = reuse ? ctx->eng->take_teacher() : spec_net(spec);
+        mark(reuse ? "host tensors (reused)" : "parse + host tensors");
         const size_t need_n = net_floats(net);
         if (n != need_n)
             throw std::invalid_argument("teacher weights: got " + std::to_string(n) + " floats, spec needs " +
@@ -230,8 +244,10 @@ int pbkd_teacher_load(pbkd_ctx* ctx, const char* spec, const float* w, size_t n)
         for (int i = 1; i < nth; ++i) th.emplace_back(copy_range, at * i / nth, at * (i + 1) / nth);
         copy_range(0, at / nth);
         for (std::thread& x : th) x.join();
+        mark("copy into host tensors");
         for (auto& p : ctx->peers) p->set_teacher(pbkd::Network(net), w, n);
         ctx->eng->set_teacher(std::move(net), w, n);  // device copy straight from the caller's buffer
+        mark("engine load (async)");
         ctx->spec = spec;
     });
 }
