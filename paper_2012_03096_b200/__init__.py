@@ -17,7 +17,8 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpbkd_b200.so")
+# PBKD_LIB: another build of the same library (A/B diagnosis runs)
+LIB_PATH = os.environ.get("PBKD_LIB") or os.path.join(HERE, "libpbkd_b200.so")
 
 KINDS = {"two_layer": 0, "three_layer": 1, "two_layer_skip": 2, "three_layer_skip": 3}
 POLICIES = {"round_robin": 0, "wfd": 1, "work_stealing": 2}

@@ -22,7 +22,7 @@ namespace pbkd_gpu {
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("PBKD_PDL");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
     return on;
 }

@@ -55,7 +55,11 @@ constexpr int kEpiWarp0 = 6;
 template <int BN, bool PS>
 struct Cfg {
     static constexpr int R = PS ? 0 : (BN >= 64 ? 2 : 4);  // raw (TMA) stages
+#ifdef PBKD_EXP_STAGES128  // diagnosis build only: operand stages of the 128-wide pre-split kernel
+    static constexpr int S = PS ? (BN >= 128 ? PBKD_EXP_STAGES128 : BN >= 64 ? 4 : 5) : (BN >= 128 ? 2 : 3);
+#else
     static constexpr int S = PS ? (BN >= 128 ? 3 : BN >= 64 ? 4 : 5) : (BN >= 128 ? 2 : 3);  // operand stages
+#endif
     static constexpr int a_raw = kBM * kBK * 4;
     static constexpr int b_raw = BN * kBK * 4;
     static constexpr int raw_stage = a_raw + b_raw;

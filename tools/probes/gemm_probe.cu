@@ -186,6 +186,8 @@ int main(int argc, char** argv) {
             run(("16 tiles K" + std::to_string(k)).c_str(), {{512, k, 512}}, 0, false, iters);
             run(("16 tiles epi1 K" + std::to_string(k)).c_str(), {{512, k, 512}}, 1, false, iters);
             run(("148 tiles K" + std::to_string(k)).c_str(), {{148 * 128, k, 128}}, 0, false, iters);
+            run(("1 tile N64 K" + std::to_string(k)).c_str(), {{128, k, 64}}, 0, false, iters);
+            run(("148 tiles N64 K" + std::to_string(k)).c_str(), {{148 * 128, k, 64}}, 0, false, iters);
         }
         return 0;
     }
