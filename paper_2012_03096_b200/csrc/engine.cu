@@ -208,7 +208,8 @@ public:
         std::stable_sort(ops.begin(), ops.end(), [](const GemmOp& a, const GemmOp& b) { return a.kchunk > b.kchunk; });
         const char* kind = ops[0].conv ? "conv" : ops[0].epi == 2 ? "wgrad" : ops[0].epi == 1 ? "fwd" : "dgrad";
         const std::string cname = std::string("gemm_") + kind +
-                                  (cls % kGemmClassKind >= 2 * kGemmClassTma ? "_pre"
+                                  (cls % kGemmClassKind >= 3 * kGemmClassTma   ? "_ts"
+                                   : cls % kGemmClassKind >= 2 * kGemmClassTma ? "_pre"
                                    : cls % kGemmClassKind >= kGemmClassTma   ? "_tma"
                                                                              : "_reg") +
                                   std::to_string(cls % kGemmClassTma);
@@ -1022,7 +1023,9 @@ struct Engine::Impl {
             s.p[u].alloc(static_cast<size_t>(M) * cout * sizeof(float));
         }
         s.gp.alloc(static_cast<size_t>(M) * cout * sizeof(float));
-        if (s.planes_w && gemm_presplit_ok(cout)) {
+        // BN gradient planes only when the backward GEMMs take A pre-split
+        // (PBKD_GEMM_TS=0); by default they split the raw gradient themselves
+        if (s.planes_w && gemm_presplit_ok(cout) && !gemm_ts_enabled()) {
             s.gp_hi.alloc(static_cast<size_t>(M) * cout * sizeof(float));
             s.gp_lo.alloc(static_cast<size_t>(M) * cout * sizeof(float));
         }
@@ -1223,7 +1226,7 @@ struct Engine::Impl {
                 a.t = u == U - 1 ? c.t : nullptr;
                 a.gin = u == U - 1 ? nullptr : s.gy.f();
                 a.gout = s.gp.f();
-                if (s.planes_d[u]) a.gout_hi = s.gp_hi.f(), a.gout_lo = s.gp_lo.f();
+                if (s.planes_d[u] && s.gp_hi.p) a.gout_hi = s.gp_hi.f(), a.gout_lo = s.gp_lo.f();
                 a.mean = s.mean_u(u);
                 a.inv = s.inv_u(u);
                 a.gamma = s.w_g(u);
@@ -1243,7 +1246,10 @@ struct Engine::Impl {
                 g.N = d.cin;
                 g.K = d.cout;
                 g.A = s.gp.f();
-                if (s.planes_d[u]) g.a_hi = s.gp_hi.f(), g.a_lo = s.gp_lo.f();
+                if (s.planes_d[u]) {
+                    if (s.gp_hi.p) g.a_hi = s.gp_hi.f(), g.a_lo = s.gp_lo.f();
+                    else g.a_ts_req = 1;  // raw gradient split into TMEM by the GEMM
+                }
                 if (s.planes_w) g.b_hi = s.params_hi.f() + s.off_pw[u], g.b_lo = s.params_lo.f() + s.off_pw[u];
                 g.lda = d.cout;
                 g.a_kmajor = 1;
@@ -1255,7 +1261,8 @@ struct Engine::Impl {
                 g.epi = 0;
                 g.ksplit = 1;
                 gemm_finalize(g);
-                if (s.planes_d[u] && !g.a_presplit) throw std::logic_error("pre-split BN gradient not consumed by dgrad");
+                if (s.planes_d[u] && !(g.a_presplit || g.a_tmem))
+                    throw std::logic_error("BN gradient operand not consumed by dgrad");
                 g.failed = c.failed;
                 dg.push_back(g);
                 // wgrad: gW[o][j] = sum_m gp[m][o] d[m][j]  (split-K over rows)
@@ -1264,7 +1271,10 @@ struct Engine::Impl {
                 w.N = d.cin;
                 w.K = static_cast<int>(c.M);
                 w.A = s.gp.f();
-                if (s.planes_d[u]) w.a_hi = s.gp_hi.f(), w.a_lo = s.gp_lo.f();
+                if (s.planes_d[u]) {
+                    if (s.gp_hi.p) w.a_hi = s.gp_hi.f(), w.a_lo = s.gp_lo.f();
+                    else w.a_ts_req = 1;
+                }
                 w.lda = d.cout;
                 w.a_kmajor = 0;
                 w.B = s.d[u].f();
@@ -1278,7 +1288,7 @@ struct Engine::Impl {
                 // before gemm_finalize, which builds the TMA store map from it)
                 w.C = w.ksplit == 1 ? s.g_pw(u) : s.wsplit.f();
                 gemm_finalize(w);
-                if (s.planes_d[u] && !(w.a_presplit && w.b_presplit))
+                if (s.planes_d[u] && !((w.a_presplit || w.a_tmem) && w.b_presplit))
                     throw std::logic_error("pre-split operands not consumed by wgrad");
                 w.failed = c.failed;
                 if (w.ksplit > 1) {

@@ -952,7 +952,7 @@ int pbkd_k_pw_fwd(pbkd_ctx* ctx, const float* x, const float* w, float* y, int r
         g.M = rows, g.N = cout, g.K = cin;
         g.A = x, g.lda = cin, g.a_kmajor = 1;
         g.B = w, g.ldb = cin, g.b_kmajor = 1;
-        g.a_hi = px.h, g.a_lo = px.l, g.b_hi = pw.h, g.b_lo = pw.l;
+        g.a_hi = px.h, g.a_lo = px.l, g.a_ts_req = 1, g.b_hi = pw.h, g.b_lo = pw.l;
         g.C = y, g.ldc = cout;
         g.ksplit = 1;
         gemm_finalize(g);
@@ -987,7 +987,7 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             g.M = rows, g.N = cin, g.K = cout;
             g.A = gy, g.lda = cout, g.a_kmajor = 1;
             g.B = w, g.ldb = cin, g.b_kmajor = 0;
-            g.a_hi = pg.h, g.a_lo = pg.l, g.b_hi = pw.h, g.b_lo = pw.l;
+            g.a_hi = pg.h, g.a_lo = pg.l, g.a_ts_req = 1, g.b_hi = pw.h, g.b_lo = pw.l;
             g.C = gx, g.ldc = cin;
             g.ksplit = 1;
             gemm_finalize(g);
@@ -1000,7 +1000,7 @@ int pbkd_k_pw_bwd(pbkd_ctx* ctx, const float* x, const float* w, const float* gy
             g.M = cout, g.N = cin, g.K = rows;
             g.A = gy, g.lda = cout, g.a_kmajor = 0;
             g.B = x, g.ldb = cin, g.b_kmajor = 0;
-            g.a_hi = pg.h, g.a_lo = pg.l, g.b_hi = px.h, g.b_lo = px.l;
+            g.a_hi = pg.h, g.a_lo = pg.l, g.a_ts_req = 1, g.b_hi = px.h, g.b_lo = px.l;
             g.ldc = cin;
             g.epi = 2;
             g.ksplit = splits;

@@ -195,7 +195,10 @@ static int dw_tile_bytes2() {
 
 DwTile dw_tile(int n, int ho, int wo, int c, int stride, int arrays) {
     DwTile t{};
-    const int target = 256;  // output pixels per CTA
+    static const int target = [] {  // output pixels per CTA (PBKD_DW_TARGET)
+        const char* e = std::getenv("PBKD_DW_TARGET");
+        return e ? std::max(32, std::atoi(e)) : 256;
+    }();
     if (ho * wo >= target) {
         t.ni = 1;
         t.th = std::max(1, std::min(ho, target / wo));

@@ -145,6 +145,9 @@ struct GemmOp {
     CUtensorMap map_a, map_b;     // 2-D fp32 maps of A and B (64-byte aligned)
     CUtensorMap map_ah, map_al;   // SWIZZLE_128B maps of the planes
     CUtensorMap map_bh, map_bl;
+    // a_ts_req (caller): A is valid raw fp32 (not only planes); gemm_finalize
+    // then sets a_tmem when the A-through-TMEM kernel takes the op (B pre-split)
+    int a_ts_req, a_tmem;
     int c_tma;                    // epilogue stores C through shared memory + TMA
     CUtensorMap map_c;            // 3-D {N, M, ksplit} SWIZZLE_128B map of C
 };
@@ -169,6 +172,8 @@ bool gemm_tma_prepare(GemmOp& o);  // umma_tma.cu: tensor maps, false if ineligi
 // as pre-split tf32 planes (TMA kernel on, 3xTF32, 16-byte rows): producers
 // then write planes instead of fp32.
 bool gemm_presplit_ok(long long ld);
+// Whether ops flagged a_ts_req run on the A-through-TMEM kernel (PBKD_GEMM_TS)
+bool gemm_ts_enabled();
 
 // Batch-norm statistics from the GEMM column partials (ops.hpp:273-299):
 // mean, var = E[x^2]-mean^2 clamped, inv_std, moving-stat update.

@@ -204,6 +204,54 @@ __device__ __forceinline__ void mma_chunk3d(uint32_t d, uint64_t dah, uint64_t d
         : "memory");
 }
 
+// One 32-wide K chunk of the 3xTF32 split with A in tensor memory (tcgen05
+// "ts" form): ah / al = TMEM addresses of the chunk's 32 columns of the A hi /
+// lo planes (lane = row, column = k), B from shared-memory descriptors.  Same
+// MMA order as mma_chunk3d (hi*lo, lo*hi, hi*hi per 8-wide k step), so the
+// accumulated bits match the all-shared-memory form.
+__device__ __forceinline__ void mma_chunk3_ts(uint32_t d, uint32_t ah, uint32_t al, uint64_t dbh, uint64_t dbl,
+                                              uint64_t inc_b, uint32_t idesc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred F, T;\n\t"
+        ".reg .b32 ah, al;\n\t"
+        ".reg .b64 bh, bl;\n\t"
+        "setp.ne.b32 F, 0, 0;\n\t"
+        "setp.eq.b32 T, 0, 0;\n\t"
+        "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, F;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, T;\n\t"
+        "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, %6;\n\tadd.s64 bl, bl, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, T;\n\t"
+        "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, %6;\n\tadd.s64 bl, bl, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, T;\n\t"
+        "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, %6;\n\tadd.s64 bl, bl, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, T;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, T;\n\t"
+        "}\n" ::"r"(d),
+        "r"(ah), "r"(al), "l"(dbh), "l"(dbl), "r"(idesc), "l"(inc_b)
+        : "memory");
+}
+
+// 32 consecutive TMEM columns of this thread's lane <- v[0..31]
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+        "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+        "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // K-major SW128 operands: the k-step advances 32 bytes (+2 in the >>4 field).
 __device__ __forceinline__ void mma_chunk3(uint32_t d, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl,
                                            uint32_t idesc) {

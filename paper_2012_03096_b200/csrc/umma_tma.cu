@@ -655,6 +655,246 @@ done:
     }
 }
 
+// ------------------------------------------------------- A through TMEM
+// Variant for ops whose A operand is raw fp32 in global memory (o.a_tmem):
+// the loader warp brings the raw A tile (K-major, 128-byte swizzled, or
+// MN-major [32 k][128 m]) and the pre-split B planes into a kSt-deep ring;
+// converter warps 2-5 (thread = TMEM lane = tile row) split their row into
+// tf32 hi / lo and store them into TMEM (tcgen05.st); the MMA warp issues
+// the chunk's 12 MMAs with A read from TMEM ("ts" form) and only B from
+// shared memory.  Per 32-wide K chunk the SM's shared memory then carries
+// 48 KB of TMA writes + 16 KB of converter reads + 48 KB of MMA reads instead
+// of 64 + 96 KB (hi/lo planes of both operands): the pre-split kernel is
+// shared-memory-bandwidth bound (tools/probes/gemm_probe.cu).  Same MMA
+// sequence and per-chunk drain as umma_tma_kernel: identical bits.
+namespace {
+constexpr int kTsBN = 128;
+constexpr int kTsSt = 4;                                     // smem stages
+constexpr int kTsTm = 3;                                     // TMEM A stages
+constexpr int kTsAcc = 2;                                    // TMEM accumulator slots
+constexpr int kTsARaw = kBM * kBK * 4;                       // 16 KB raw A
+constexpr int kTsBOp = kTsBN * kRowBytes;                    // 16 KB per B plane
+constexpr int kTsStage = kTsARaw + 2 * kTsBOp;               // 48 KB
+constexpr int kTsSmem = 1024 + kTsSt * kTsStage + kBM * 32 * 4;  // + epilogue staging
+constexpr int kTsAcol0 = kTsAcc * kTsBN;                     // first TMEM column of the A stages
+}  // namespace
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __restrict__ ops, int nd, int total) {
+    constexpr int BN = kTsBN, HB = BN / 2, S = kTsSt, T = kTsTm, AC = kTsAcc;
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t op_full[S], op_empty[S], a_full[T], a_empty[T], acc_full[AC], acc_empty[AC];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ float red_buf[256];
+    auto red = reinterpret_cast<float(*)[4][32]>(red_buf);
+    __shared__ int begins[kMaxOps];
+    __shared__ TileInfo tiles_sh[kMaxTiles];
+    const uint32_t sbase = smem_u32(smem_raw);
+    const uint32_t pad = (1024u - (sbase & 1023u)) & 1023u;
+    uint8_t* ring = smem_raw + pad;
+    const uint32_t ring_s = sbase + pad;
+    const uint32_t cs_s = ring_s + S * kTsStage;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&op_full[i], 1);
+            mbar_init(&op_empty[i], 1);
+        }
+        for (int i = 0; i < T; ++i) {
+            mbar_init(&a_full[i], kConvThreads / 32);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < AC; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < nd; i += kThreadsT) begins[i] = ops[i].cta_begin;
+    __syncthreads();
+    const int ntiles = static_cast<int>(blockIdx.x) < total ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+    for (int j = tid; j < ntiles; j += kThreadsT) {
+        const int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+        int lo = 0, hi = nd - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (begins[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const GemmOp& o = ops[lo];
+        TileInfo ti;
+        ti.op = lo;
+        ti.g = tile_geo<BN>(o, t - begins[lo]);
+        tiles_sh[j] = ti;
+        if (j == 0) prefetch_map(&o.map_a), prefetch_map(&o.map_bh), prefetch_map(&o.map_bl);
+    }
+    pdl_enter();
+    for (int j = tid; j < ntiles; j += kThreadsT)
+        if (op_failed(ops[tiles_sh[j].op])) tiles_sh[j].op = -1;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == kBWarp) {
+        // ------------------------------------------------------ loader
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const int bnt = o.bn;
+            const int m0 = g.tm * kBM, n0 = g.tn * bnt;
+            const bool akm = o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            if (lane == 0) {
+                for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                    const int s = it % S;
+                    mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&op_full[s], static_cast<uint32_t>(kTsARaw + 2 * bnt * kRowBytes));
+                    uint8_t* st = ring + s * kTsStage;
+                    const int k = g.k0 + kc * kBK;
+                    if (akm) tma_load_2d(st, &o.map_a, &op_full[s], k, m0);
+                    else tma_load_2d(st, &o.map_a, &op_full[s], m0, k);
+                    uint8_t* ob = st + kTsARaw;
+                    if (bkm) {
+                        tma_load_2d(ob, &o.map_bh, &op_full[s], k, n0);
+                        tma_load_2d(ob + kTsBOp, &o.map_bl, &op_full[s], k, n0);
+                    } else {
+#pragma unroll
+                        for (int at = 0; at < BN / 32; ++at) {
+                            if (at * 32 >= bnt) break;
+                            tma_load_2d(ob + at * 4096, &o.map_bh, &op_full[s], n0 + 32 * at, k);
+                            tma_load_2d(ob + kTsBOp + at * 4096, &o.map_bl, &op_full[s], n0 + 32 * at, k);
+                        }
+                    }
+                }
+            } else {
+                it += g.nchunks;
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 2 && warp < kEpiWarp0) {
+        // ------------------------------------------------------ converters
+        const int row = (warp & 3) * 32 + lane;  // this warp's TMEM lane quarter
+        const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const bool akm = o.a_kmajor != 0;
+            for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                const int s = it % S, t = it % T;
+                mbar_wait(&op_full[s], (it / S) & 1);
+                mbar_wait(&a_empty[t], ((it / T) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t raw = ring_s + s * kTsStage;
+                uint32_t hv[32], lv[32];
+                if (akm) {  // [128 rows][32 k], 128-byte swizzled rows
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float4 x = lds128(raw + sw128(row, c));
+                        const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            hv[4 * c + q] = tc_split_hi(xs[q]);
+                            lv[4 * c + q] = tc_split_lo(xs[q], __uint_as_float(hv[4 * c + q]));
+                        }
+                    }
+                } else {  // [32 k][128 m]
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        const float x = lds32(raw + (k * kBM + row) * 4);
+                        hv[k] = tc_split_hi(x);
+                        lv[k] = tc_split_lo(x, __uint_as_float(hv[k]));
+                    }
+                }
+                const uint32_t acol = tmem + lane_off + kTsAcol0 + t * 64;
+                tmem_st32(acol, hv);
+                tmem_st32(acol + 32, lv);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_full[t]);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const bool bmn = !o.b_kmajor;
+            const uint32_t idesc = instr_desc(o.bn, false, bmn);
+            for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                const int s = it % S, t = it % T, a = it % AC;
+                mbar_wait(&op_full[s], (it / S) & 1);
+                mbar_wait(&a_full[t], (it / T) & 1);
+                mbar_wait(&acc_empty[a], ((it / AC) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t bh = ring_s + s * kTsStage + kTsARaw, bl = bh + kTsBOp;
+                const uint32_t ah = tmem + kTsAcol0 + t * 64, al = ah + 32;
+                if (elect_one()) {
+                    if (bmn) {
+                        constexpr uint32_t lbo = 4096, sbo = 512;
+                        mma_chunk3_ts(tmem + a * BN, ah, al, smem_desc_mn(bh, lbo, sbo), smem_desc_mn(bl, lbo, sbo), 64,
+                                      idesc);
+                    } else {
+                        mma_chunk3_ts(tmem + a * BN, ah, al, smem_desc(bh), smem_desc(bl), 2, idesc);
+                    }
+                    mma_commit(&op_empty[s]);
+                    mma_commit(&a_empty[t]);
+                    mma_commit(&acc_full[a]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 8) {
+        // ------------------------------------------------------ drain + epilogue
+        const int q = warp & 3, h = (warp - kEpiWarp0) >> 2, et = tid - kEpiWarp0 * 32;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        int stores = 0;
+        uint32_t it = 0;
+        for (int j = 0; j < ntiles; ++j) {
+            if (tiles_sh[j].op < 0) continue;
+            const GemmOp& o = ops[tiles_sh[j].op];
+            const TileGeo g = tiles_sh[j].g;
+            const int bnt = o.bn;
+            const int hcols = min(HB, max(0, bnt - h * HB));
+            float acc[HB];
+#pragma unroll
+            for (int i = 0; i < HB; ++i) acc[i] = 0.0f;
+            for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
+                const int a = it % AC;
+                mbar_wait(&acc_full[a], (it / AC) & 1);
+                tc_fence_after();
+                const uint32_t base = tmem + lane_off + a * BN + h * HB;
+#pragma unroll
+                for (int c0 = 0; c0 < HB; c0 += 16)
+                    if (c0 < hcols) tmem_add16(base + c0, acc + c0);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[a]);
+            }
+            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores, bnt);
+        }
+        if (tid == kEpiWarp0 * 32) tma_store_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
 // ------------------------------------------------------------------- host
 namespace {
 
@@ -766,6 +1006,19 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     }
 }
 
+template <int KIND>
+void launch_ts_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        PBKD_CUDA(cudaFuncSetAttribute(umma_ts_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmem));
+        attr = true;
+    }
+    if (nd > kMaxOps) throw CudaError("umma_ts: too many ops in one launch");
+    const int grid = std::max({1, std::min(total, num_sms()), (total + kMaxTiles - 1) / kMaxTiles});
+    launch_k(umma_ts_kernel<KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(kTsSmem), st, d, nd, total);
+    PBKD_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 bool encode_nhwc_box(CUtensorMap* m, const float* base, int n, int h, int w, int c, int bc, int bw, int bh, int bn) {
@@ -819,6 +1072,14 @@ bool encode_conv(CUtensorMap* m, const GemmOp& o, CUtensorMapSwizzle sw = CU_TEN
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+bool gemm_ts_enabled() {  // PBKD_GEMM_TS=0: pre-split planes for A as well
+    static const bool on = [] {
+        const char* e = std::getenv("PBKD_GEMM_TS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 bool gemm_presplit_ok(long long ld) {
@@ -897,6 +1158,19 @@ bool gemm_tma_prepare(GemmOp& o) {
         presplit_maps(o);
         o.c_tma = encode_c(o) ? 1 : 0;
     }
+    o.a_tmem = 0;
+    if (ok && gemm_ts_enabled() && o.a_ts_req && o.b_presplit && o.tf32x3 == 3 && bn <= kTsBN) {
+        // raw A for the converter warps: K-major 128-byte swizzled {32 k, 128 rows},
+        // MN-major plain {128 m, 32 k}
+        CUtensorMap m;
+        const bool enc = o.a_kmajor ? encode(&m, o.A, o.K, o.M, o.lda, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B)
+                                    : encode(&m, o.A, o.M, o.K, o.lda, kBM, kBK);
+        if (enc) {
+            o.map_a = m;
+            o.a_tmem = 1;
+            o.a_presplit = 0;
+        }
+    }
     return ok && o.c_tma != 0;  // the TMA kernel's epilogue stores through the C map
 }
 
@@ -920,6 +1194,11 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
 
 template <int KIND>
 void launch_tma_kind(const GemmOp* d, int nd, int total, int cls, cudaStream_t st) {
+    if (cls >= 3 * kGemmClassTma) {  // A through TMEM (kinds 0 / 1)
+        if constexpr (KIND == 0 || KIND == 1) launch_ts_t<KIND>(d, nd, total, st);
+        else throw CudaError("umma_ts: unsupported epilogue kind");
+        return;
+    }
     switch (cls) {
         case kGemmClassTma + 32: launch_tma_t<32, false, KIND>(d, nd, total, st); break;
         case kGemmClassTma + 64: launch_tma_t<64, false, KIND>(d, nd, total, st); break;

@@ -345,19 +345,21 @@ def test_gemm_kernels_agree_bitwise(ctx, tmp_path):
     (incl. ragged M/N/K, MN-major operands, split-K) and every teacher conv
     (implicit im2col, stride 1/2, 1x1 projections) must agree bit for bit,
     also when the operands arrive as pre-split tf32 planes (no conversion,
-    K-major and MN-major shared-memory descriptors);
+    K-major and MN-major shared-memory descriptors) and when A is split by
+    converter warps into tensor memory (umma_ts_kernel);
     both are also checked against fp64 (rel 1e-5) inside gemm_dump.py."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    # register-staged | TMA with converter warps | TMA on pre-split tf32 planes
-    for name, tma, pre in (("reg", "0", "0"), ("tma", "1", "0"), ("pre", "1", "1")):
+    # register-staged | TMA on pre-split tf32 planes of both operands | A
+    # through TMEM (raw fp32 A split by converter warps, B planes)
+    for name, tma, ts in (("reg", "0", "0"), ("pre", "1", "0"), ("ts", "1", "1")):
         path = str(tmp_path / f"g{name}.npz")
-        env = dict(os.environ, PBKD_GEMM_TMA=tma, PBKD_CONV_TMA=tma, PBKD_GEMM_PRESPLIT=pre, PYTHONPATH=root)
+        env = dict(os.environ, PBKD_GEMM_TMA=tma, PBKD_CONV_TMA=tma, PBKD_GEMM_TS=ts, PYTHONPATH=root)
         subprocess.run([sys.executable, os.path.join(root, "tests", "gemm_dump.py"), path], env=env, check=True,
                        timeout=300)
         outs[name] = np.load(path)
     for k in outs["reg"].files:
-        assert np.array_equal(outs["reg"][k], outs["tma"][k]), k
         assert np.array_equal(outs["reg"][k], outs["pre"][k]), k
+        assert np.array_equal(outs["reg"][k], outs["ts"][k]), k

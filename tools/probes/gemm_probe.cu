@@ -60,6 +60,7 @@ static void run(const char* name, std::vector<Shape> shapes, int epi, bool wgrad
             else g.B = b, g.ldb = s.K, g.b_kmajor = 1;
             g.a_hi = dalloc(static_cast<size_t>(s.M) * s.K), g.a_lo = dalloc(static_cast<size_t>(s.M) * s.K);
             g.b_hi = dalloc(static_cast<size_t>(s.N) * s.K), g.b_lo = dalloc(static_cast<size_t>(s.N) * s.K);
+            g.a_ts_req = std::getenv("PROBE_TS") ? 1 : 0;
             g.C = dalloc(static_cast<size_t>(s.M) * s.N), g.ldc = s.N;
             g.ksplit = 1;
         } else {  // dW[N=cin? ] : C[cout][cin] = sum_rows dY[row][cout] X[row][cin]
@@ -70,6 +71,7 @@ static void run(const char* name, std::vector<Shape> shapes, int epi, bool wgrad
             g.B = x, g.ldb = s.K, g.b_kmajor = 0;
             g.a_hi = dalloc(static_cast<size_t>(s.M) * s.N), g.a_lo = dalloc(static_cast<size_t>(s.M) * s.N);
             g.b_hi = dalloc(static_cast<size_t>(s.M) * s.K), g.b_lo = dalloc(static_cast<size_t>(s.M) * s.K);
+            g.a_ts_req = std::getenv("PROBE_TS") ? 1 : 0;
             g.ksplit = std::max(1, std::min(64, (s.M + 511) / 512));
             g.epi = 2;
         }
