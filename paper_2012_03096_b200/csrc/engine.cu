@@ -1388,19 +1388,27 @@ struct Engine::Impl {
                 both.insert(both.end(), wg.begin(), wg.end());
                 P.gemm(both);
             }
+            // PBKD_RED_MERGE=1: the two branches' partial-sum reductions as one
+            // launch after the branches join
+            static const bool red_merge = [] {
+                const char* e = std::getenv("PBKD_RED_MERGE");
+                return e && e[0] == '1';
+            }();
             std::vector<Program*> br = P.par(2);
             Program& bx = *br[0];
             Program& bw = *br[1];
             if (!bwd_merge) bx.gemm(dg);
-            if (u > 0) {
-                bx.grouped<DwBwdOp>(launch_dw_bwd, dbs, ctas_dw_bwd);
-                bx.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
-            } else {
-                bx.grouped<DwGkOp>(launch_dw_gk, gks, ctas_dw_gk);
-                bx.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
-            }
+            if (u > 0) bx.grouped<DwBwdOp>(launch_dw_bwd, dbs, ctas_dw_bwd);
+            else bx.grouped<DwGkOp>(launch_dw_gk, gks, ctas_dw_gk);
+            if (!red_merge) bx.grouped<ReduceOp>(launch_reduce, kr, red_ctas);
             if (!bwd_merge) bw.gemm(wg);
-            bw.grouped<ReduceOp>(launch_reduce, wr, red_ctas);
+            if (!red_merge) {
+                bw.grouped<ReduceOp>(launch_reduce, wr, red_ctas);
+            } else {
+                std::vector<ReduceOp> all = kr;
+                all.insert(all.end(), wr.begin(), wr.end());
+                P.grouped<ReduceOp>(launch_reduce, all, red_ctas);
+            }
         }
         // ---- optimizer
         std::vector<SgdOp> sg;
