@@ -271,8 +271,13 @@ void launch_dw_bwd(const DwBwdOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_dw_gk(const DwGkOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_reduce(const ReduceOp* d_ops, int nd, int ctas, cudaStream_t st);
 // ctas: the ops' total tile count (sum of ctas_gemm); cls: gemm_bn_class
-void launch_gemm_bn(const GemmOp* d_ops, int nd, int ctas, int cls, cudaStream_t st);
-void launch_gemm_tma(const GemmOp* d_ops, int nd, int tiles, int cls, cudaStream_t st);  // cls: gemm_bn_class
+// perm (optional, TMA classes): tile slots of the persistent grid -- CTA b
+// takes slots b, b + G, b + 2G, ... (G = gemm_tma_grid(tiles)), slot -> tile id
+// or -1; tiles = G * slots per CTA.  Null: slot = tile (round robin).
+void launch_gemm_bn(const GemmOp* d_ops, int nd, int ctas, int cls, cudaStream_t st, const int* perm = nullptr);
+void launch_gemm_tma(const GemmOp* d_ops, int nd, int tiles, int cls, cudaStream_t st,
+                     const int* perm = nullptr);  // cls: gemm_bn_class
+int gemm_tma_grid(int tiles);  // persistent grid of a TMA GEMM launch over `tiles` tile slots
 void launch_bn_stat(const BnStatOp* d_ops, int nd, int ctas, cudaStream_t st);
 void launch_loss(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);       // c <= 1024
 void launch_loss_wide(const LossOp* d_ops, int nd, int ctas, cudaStream_t st);  // any c (channel passes)

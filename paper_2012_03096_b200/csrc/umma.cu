@@ -339,9 +339,9 @@ static void launch_bn_t(const GemmOp* d, int nd, int ctas, cudaStream_t st) {
 
 // All ops of one launch share the N tile and the kernel (the caller groups
 // ops by gemm_bn_class; narrower ops would pad their B rows with zeros).
-void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int cls, cudaStream_t st) {
+void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int cls, cudaStream_t st, const int* perm) {
     if (cls % kGemmClassKind >= kGemmClassTma) {
-        launch_gemm_tma(d, nd, ctas, cls, st);
+        launch_gemm_tma(d, nd, ctas, cls, st, perm);
         return;
     }
     switch (bn_for(cls)) {

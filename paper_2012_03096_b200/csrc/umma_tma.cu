@@ -282,7 +282,8 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
 
 template <int BN, bool PS, int KIND>
 __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __restrict__ ops, int nd, int total,
-                                                                 unsigned long long* __restrict__ trace) {
+                                                                 unsigned long long* __restrict__ trace,
+                                                                 const int* __restrict__ perm) {
     using C = Cfg<BN, PS>;
     constexpr bool CONV = KIND == kGemmKindConv;
     constexpr int R = C::R, S = C::S, HB = BN / 2;
@@ -354,7 +355,14 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     __syncthreads();
     const int ntiles = static_cast<int>(blockIdx.x) < total ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
     for (int j = tid; j < ntiles; j += kThreadsT) {
-        const int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+        int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+        if (perm) {  // balanced slot -> tile map (host LPT schedule)
+            t = perm[t];
+            if (t < 0) {
+                tiles_sh[j].op = -1;
+                continue;
+            }
+        }
         int lo = 0, hi = nd - 1;  // last op with begins[op] <= t
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -376,7 +384,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
     // predecessor results (failure flags, operands) only after this point
     pdl_enter();
     for (int j = tid; j < ntiles; j += kThreadsT)
-        if (op_failed(ops[tiles_sh[j].op])) tiles_sh[j].op = -1;  // task predicated off (diverged)
+        if (tiles_sh[j].op >= 0 && op_failed(ops[tiles_sh[j].op])) tiles_sh[j].op = -1;  // task predicated off (diverged)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -680,7 +688,8 @@ constexpr int kTsAcol0 = kTsAcc * kTsBN;                     // first TMEM colum
 }  // namespace
 
 template <int KIND>
-__global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __restrict__ ops, int nd, int total) {
+__global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __restrict__ ops, int nd, int total,
+                                                                const int* __restrict__ perm) {
     constexpr int BN = kTsBN, HB = BN / 2, S = kTsSt, T = kTsTm, AC = kTsAcc;
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t op_full[S], op_empty[S], a_full[T], a_empty[T], acc_full[AC], acc_empty[AC];
@@ -720,7 +729,14 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
     __syncthreads();
     const int ntiles = static_cast<int>(blockIdx.x) < total ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
     for (int j = tid; j < ntiles; j += kThreadsT) {
-        const int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+        int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+        if (perm) {  // balanced slot -> tile map (host LPT schedule)
+            t = perm[t];
+            if (t < 0) {
+                tiles_sh[j].op = -1;
+                continue;
+            }
+        }
         int lo = 0, hi = nd - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -736,7 +752,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
     }
     pdl_enter();
     for (int j = tid; j < ntiles; j += kThreadsT)
-        if (op_failed(ops[tiles_sh[j].op])) tiles_sh[j].op = -1;
+        if (tiles_sh[j].op >= 0 && op_failed(ops[tiles_sh[j].op])) tiles_sh[j].op = -1;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -935,7 +951,7 @@ int num_sms() {
 }
 
 template <int BN, bool PS, int KIND>
-void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
+void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st, const int* perm) {
     static bool attr = false;
     if (!attr) {
         PBKD_CUDA(cudaFuncSetAttribute(umma_tma_kernel<BN, PS, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -947,7 +963,8 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
         const char* e = std::getenv("PBKD_GEMM_GRID_MAX");
         return e ? std::max(1, std::atoi(e)) : 1 << 30;
     }();
-    const int grid = std::max({1, std::min({total, num_sms(), grid_cap}), (total + kMaxTiles - 1) / kMaxTiles});
+    const int grid = perm ? gemm_tma_grid(total)
+                          : std::max({1, std::min({total, num_sms(), grid_cap}), (total + kMaxTiles - 1) / kMaxTiles});
     static const bool trace_on = std::getenv("PBKD_GEMM_TRACE") != nullptr;
     static unsigned long long* trace = nullptr;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -957,7 +974,7 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
     unsigned long long* tr = cap == cudaStreamCaptureStatusNone ? trace : nullptr;
     if (tr) PBKD_CUDA(cudaMemsetAsync(tr, 0, (10 * 512 + 3 * 1024) * sizeof(unsigned long long), st));
     launch_k(umma_tma_kernel<BN, PS, KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(Cfg<BN, PS>::smem), st, d, nd,
-             total, tr);
+             total, tr, perm);
     PBKD_LAUNCH_CHECK();
     static const int trace_from = [] {
         const char* e = std::getenv("PBKD_GEMM_TRACE");
@@ -1007,19 +1024,27 @@ void launch_tma_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
 }
 
 template <int KIND>
-void launch_ts_t(const GemmOp* d, int nd, int total, cudaStream_t st) {
+void launch_ts_t(const GemmOp* d, int nd, int total, cudaStream_t st, const int* perm) {
     static bool attr = false;
     if (!attr) {
         PBKD_CUDA(cudaFuncSetAttribute(umma_ts_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmem));
         attr = true;
     }
     if (nd > kMaxOps) throw CudaError("umma_ts: too many ops in one launch");
-    const int grid = std::max({1, std::min(total, num_sms()), (total + kMaxTiles - 1) / kMaxTiles});
-    launch_k(umma_ts_kernel<KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(kTsSmem), st, d, nd, total);
+    const int grid = gemm_tma_grid(total);
+    launch_k(umma_ts_kernel<KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(kTsSmem), st, d, nd, total, perm);
     PBKD_LAUNCH_CHECK();
 }
 
 }  // namespace
+
+int gemm_tma_grid(int total) {
+    static const int grid_cap = [] {  // diagnosis (tools/gpu_gridcap.sh): cap the persistent grid
+        const char* e = std::getenv("PBKD_GEMM_GRID_MAX");
+        return e ? std::max(1, std::atoi(e)) : 1 << 30;
+    }();
+    return std::max({1, std::min({total, num_sms(), grid_cap}), (total + kMaxTiles - 1) / kMaxTiles});
+}
 
 bool encode_nhwc_box(CUtensorMap* m, const float* base, int n, int h, int w, int c, int bc, int bw, int bh, int bn) {
     static const bool on = [] {
@@ -1193,30 +1218,30 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
 
 
 template <int KIND>
-void launch_tma_kind(const GemmOp* d, int nd, int total, int cls, cudaStream_t st) {
+void launch_tma_kind(const GemmOp* d, int nd, int total, int cls, cudaStream_t st, const int* perm) {
     if (cls >= 3 * kGemmClassTma) {  // A through TMEM (kinds 0 / 1)
-        if constexpr (KIND == 0 || KIND == 1) launch_ts_t<KIND>(d, nd, total, st);
+        if constexpr (KIND == 0 || KIND == 1) launch_ts_t<KIND>(d, nd, total, st, perm);
         else throw CudaError("umma_ts: unsupported epilogue kind");
         return;
     }
     switch (cls) {
-        case kGemmClassTma + 32: launch_tma_t<32, false, KIND>(d, nd, total, st); break;
-        case kGemmClassTma + 64: launch_tma_t<64, false, KIND>(d, nd, total, st); break;
-        case kGemmClassTma + 128: launch_tma_t<128, false, KIND>(d, nd, total, st); break;
-        case 2 * kGemmClassTma + 32: launch_tma_t<32, true, KIND>(d, nd, total, st); break;
-        case 2 * kGemmClassTma + 64: launch_tma_t<64, true, KIND>(d, nd, total, st); break;
-        default: launch_tma_t<128, true, KIND>(d, nd, total, st); break;
+        case kGemmClassTma + 32: launch_tma_t<32, false, KIND>(d, nd, total, st, perm); break;
+        case kGemmClassTma + 64: launch_tma_t<64, false, KIND>(d, nd, total, st, perm); break;
+        case kGemmClassTma + 128: launch_tma_t<128, false, KIND>(d, nd, total, st, perm); break;
+        case 2 * kGemmClassTma + 32: launch_tma_t<32, true, KIND>(d, nd, total, st, perm); break;
+        case 2 * kGemmClassTma + 64: launch_tma_t<64, true, KIND>(d, nd, total, st, perm); break;
+        default: launch_tma_t<128, true, KIND>(d, nd, total, st, perm); break;
     }
 }
 
 // cls: gemm_bn_class of every op of the launch (kind, pre-split, N tile)
-void launch_gemm_tma(const GemmOp* d, int nd, int total, int cls, cudaStream_t st) {
+void launch_gemm_tma(const GemmOp* d, int nd, int total, int cls, cudaStream_t st, const int* perm) {
     const int kind = cls / kGemmClassKind, rest = cls % kGemmClassKind;
     switch (kind) {
-        case 0: launch_tma_kind<0>(d, nd, total, rest, st); break;
-        case 1: launch_tma_kind<1>(d, nd, total, rest, st); break;
-        case 2: launch_tma_kind<2>(d, nd, total, rest, st); break;
-        default: launch_tma_kind<kGemmKindConv>(d, nd, total, rest, st); break;
+        case 0: launch_tma_kind<0>(d, nd, total, rest, st, perm); break;
+        case 1: launch_tma_kind<1>(d, nd, total, rest, st, perm); break;
+        case 2: launch_tma_kind<2>(d, nd, total, rest, st, perm); break;
+        default: launch_tma_kind<kGemmKindConv>(d, nd, total, rest, st, perm); break;
     }
 }
 
