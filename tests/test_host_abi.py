@@ -45,7 +45,8 @@ def test_mix_seed_and_shuffle_match_oracle(orc):
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
 def test_candidate_init_bit_exact(orc, kind):
-    for (cin, cout, s) in [(3, 64, 1), (64, 128, 2), (16, 16, 1)]:
+    # (256, 512, 2) / (512, 512, 1): tensors above he_fill's two-pass threshold
+    for (cin, cout, s) in [(3, 64, 1), (64, 128, 2), (16, 16, 1), (256, 512, 2), (512, 512, 1)]:
         assert np.array_equal(P.build_candidate(kind, cin, cout, s, 99),
                               orc.build_candidate(kind, cin, cout, s, 99))
 

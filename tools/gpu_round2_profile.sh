@@ -18,8 +18,8 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 echo "ref rc=$?" >> gpurun_out/bench_ref.log
 NCCL_DEBUG=INFO timeout 300 python -m pytest tests/test_multigpu.py -m gpu -q -s -p no:cacheprovider -k gpu_list > gpurun_out/nccl_clique.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_bench.log 2>&1
-timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:umma_tma_kernel -c 480 --csv --log-file gpurun_out/traffic.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_traffic.log 2>&1
-for k in umma_tma_kernel dw_bwd_kernel dw_fwd_kernel dw_gk_kernel bn_bwd_apply_kernel loss_kernel sgd_kernel reduce_kernel bn_stat_kernel; do
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:umma_t -c 480 --csv --log-file gpurun_out/traffic.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_traffic.log 2>&1
+for k in umma_ts_kernel umma_tma_kernel dw_bwd_kernel dw_fwd_kernel dw_gk_kernel bn_bwd_apply_kernel loss_kernel sgd_kernel reduce_kernel bn_stat_kernel; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 60 -c 1 -o gpurun_out/full_$k python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_$k.log 2>&1
 done
 bash tools/gpu_knockout.sh > /dev/null 2>&1

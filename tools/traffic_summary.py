@@ -1,6 +1,6 @@
 """DRAM traffic per launch of the TMA GEMM kernel classes from an ncu launch
 list (tools/gpu_full.sh: --metrics dram__bytes_read.sum,dram__bytes_write.sum,
-gpu__time_duration.sum -k regex:umma_tma_kernel).  Teacher convs are the
+gpu__time_duration.sum -k regex:umma_t: both TMA GEMM kernels).  Teacher convs are the
 launches of the epoch's teacher pass (the first 13 per epoch for VGG-16:
 identified by duration > 150 us); the rest are student pointwise GEMMs.
 Writes profiles/r1_traffic.json, which bench.py reports as roofline.traffic."""
