@@ -354,13 +354,14 @@ __device__ __forceinline__ int op_to_shared(const Op* __restrict__ ops, int nd, 
 // (image i, row oy) of the tile, lane = channel; stride 1 slides a 3x3
 // register window along x (3 shared loads per output).
 __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     cta_mark(0);
     extern __shared__ __align__(128) float xs[];
     __shared__ DwFwdOp osh;
     __shared__ uint64_t bar;
     int local;
     const int oi = op_to_shared(ops, nd, &osh, &bar, local);
+    pdl_wait();  // descriptor copy above overlaps the predecessor's tail
     cta_mark(1);
     const DwFwdOp& o = osh;
     if (is_failed(o.failed)) return;
@@ -493,13 +494,14 @@ __device__ __forceinline__ void dw_lane_sum(float* red, const float* v, float* o
 // (oy, ox) order with zero terms skipped (ops.hpp:156-174), the weight-
 // gradient terms, the previous ReLU mask and batch-norm partial sums.
 __global__ void __launch_bounds__(kThreads) dw_bwd_kernel(const DwBwdOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     cta_mark(0);
     extern __shared__ __align__(128) float sm[];
     __shared__ DwBwdOp osh;
     __shared__ uint64_t bar;
     int local;
     const int oi = op_to_shared(ops, nd, &osh, &bar, local);
+    pdl_wait();  // descriptor copy above overlaps the predecessor's tail
     cta_mark(1);
     const DwBwdOp& o = osh;
     if (is_failed(o.failed)) return;
@@ -627,13 +629,14 @@ void launch_dw_bwd(const DwBwdOp* d, int nd, int ctas, cudaStream_t st) {
 // model.cpp:570 skips the input gradient of the block's first layer.  With
 // TMA both the input tile (halo) and the output-gradient tile are staged.
 __global__ void __launch_bounds__(kThreads) dw_gk_kernel(const DwGkOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     cta_mark(0);
     extern __shared__ __align__(128) float sm[];
     __shared__ DwGkOp osh;
     __shared__ uint64_t bar;
     int local;
     const int oi = op_to_shared(ops, nd, &osh, &bar, local);
+    pdl_wait();  // descriptor copy above overlaps the predecessor's tail
     cta_mark(1);
     const DwGkOp& o = osh;
     if (is_failed(o.failed)) return;
@@ -767,10 +770,11 @@ __device__ __forceinline__ void col_sum2(const float* __restrict__ pa, const flo
 }
 
 __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     __shared__ float red[kColLanes][2][32];
     int local;
     const BnStatOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     if (is_failed(o.failed)) return;
     const int ch = local * 32 + threadIdx.x % 32;
     float sum, sq;
@@ -798,10 +802,11 @@ __global__ void __launch_bounds__(kThreads) bn_stat_kernel(const BnStatOp* __res
 int ctas_reduce(const ReduceOp& o) { return std::max(1, ceil_div(o.width, 32)); }
 
 __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     __shared__ float red[kThreads / 32][32];
     int local;
     const ReduceOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     if (is_failed(o.failed)) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int col = local * 32 + lane;
@@ -884,11 +889,12 @@ __device__ __forceinline__ void loss_pass(const LossOp& o, int local, int cb, in
 }
 
 __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ float red[];
     __shared__ float lred[kThreads];
     int local;
     const LossOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     if (is_failed(o.failed)) return;
     const Geo g = geo_of(o.c);
     const int rr = threadIdx.x / g.G, gg = threadIdx.x % g.G;
@@ -938,11 +944,12 @@ __global__ void __launch_bounds__(kThreads) loss_kernel(const LossOp* __restrict
 }
 
 __global__ void __launch_bounds__(kThreads) loss_wide_kernel(const LossOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ float red[];
     __shared__ float lred[kThreads];
     int local;
     const LossOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     if (is_failed(o.failed)) return;
     const int V = (o.c % 4 == 0) ? 4 : 1;
     float lsum = 0.0f;
@@ -969,10 +976,11 @@ void launch_loss_wide(const LossOp* d, int nd, int ctas, cudaStream_t st) {
 }
 
 __global__ void __launch_bounds__(kThreads) bn_bwd_fin_kernel(const BnBwdFinOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     __shared__ float red[kColLanes][2][32];
     int local;
     const BnBwdFinOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     if (is_failed(o.failed)) return;
     if (o.loss_out && local == 0 && threadIdx.x < 32) {  // one warp, fixed-order tree
         double s = 0.0;
@@ -1054,9 +1062,10 @@ constexpr int kSgdQuads = 1;  // SGD: more CTAs beat deeper per-thread batches (
 int ctas_sgd(long long n) { return std::max(1, ceil_div(n, 4LL * kThreads * kSgdQuads)); }
 
 __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApplyOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     int local;
     const BnBwdApplyOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     if (is_failed(o.failed)) return;
     const float* tg = o.t ? o.t : o.gin;
     const long long cta0 = static_cast<long long>(local) * kThreads * kElemQuads * 4;
@@ -1115,9 +1124,10 @@ __device__ __forceinline__ void sgd_quad(const SgdOp& o, long long i, float4 v, 
 }
 
 __global__ void __launch_bounds__(kThreads) sgd_kernel(const SgdOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     int local;
     const SgdOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     if (is_failed(o.failed)) return;
     const long long cta0 = static_cast<long long>(local) * kThreads * kSgdQuads * 4;
     if (cta0 + 4LL * kThreads * kSgdQuads <= o.n) {  // flat buffers: 16-byte aligned, n % 4 == 0
@@ -1157,9 +1167,10 @@ void launch_sgd(const SgdOp* d, int nd, int ctas, cudaStream_t st) {
 
 // ---------------------------------------------------------------- scatter
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const ScatterOp* __restrict__ ops, int nd) {
-    pdl_enter();
+    pdl_trigger();
     int local;
     const ScatterOp o = op_of(ops, nd, local);  // copy: no reloads after stores
+    pdl_wait();  // the static descriptor read above overlaps the predecessor's tail
     const long long step = static_cast<long long>(kThreads) * kScatterCtas;
     if (o.cd > 0) {  // channel-padded destination rows
         const long long total = static_cast<long long>(o.rows) * o.width;
