@@ -348,42 +348,12 @@ __device__ __forceinline__ int op_to_shared(const Op* __restrict__ ops, int nd, 
     return t;
 }
 
-// ---------------------------------------------------------- depthwise fwd
-// The x tile arrives by one 4-D TMA box (zero-filled halo / channel tail) or,
-// for channel counts TMA cannot address, by cp.async.  Warp = output row
-// (image i, row oy) of the tile, lane = channel; stride 1 slides a 3x3
-// register window along x (3 shared loads per output).
-__global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restrict__ ops, int nd) {
-    pdl_trigger();
-    cta_mark(0);
-    extern __shared__ __align__(128) float xs[];
-    __shared__ DwFwdOp osh;
-    __shared__ uint64_t bar;
-    int local;
-    const int oi = op_to_shared(ops, nd, &osh, &bar, local);
-    pdl_wait();  // descriptor copy above overlaps the predecessor's tail
-    cta_mark(1);
-    const DwFwdOp& o = osh;
-    if (is_failed(o.failed)) return;
+// Depthwise forward of one tile staged by cp.async (channel counts TMA cannot
+// address): warp = output row, lane = channel.  Called by the whole CTA.
+__device__ __forceinline__ void dw_fwd_plain(const DwFwdOp& o, const DwPos& q, float* xs) {
     const DwTile t = o.tile;
-    const DwPos q = dw_pos(t, local);
     const int n = o.n, h = o.h, w = o.wd, C = o.c, ho = o.ho, wo = o.wo, s = o.stride, pad = o.pad, pro = o.pro;
     const int iy0 = q.y0 * s - pad;
-    const bool tma = o.tma != 0;
-    if (tma && threadIdx.x < 32) {
-        if (o.rows == nullptr) {
-            if (threadIdx.x == 0) {
-                tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(t.ni * t.tr * t.tw * kDwC * 4));
-                tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, iy0, q.n0);
-            }
-        } else {  // gather: one single-image box per batch image, lanes in parallel
-            const int cnt = min(t.ni, n - q.n0), img_f = t.tr * t.tw * kDwC;
-            if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(cnt * img_f * 4));
-            __syncwarp();
-            for (int i = threadIdx.x; i < cnt; i += 32)
-                tc::tma_load_4d(xs + i * img_f, &ops[oi].map_x, &bar, q.c0, -pad, iy0, __ldg(o.rows + q.n0 + i));
-        }
-    }
     const int ch = threadIdx.x & 31, warp = threadIdx.x >> 5, c = q.c0 + ch;
     const bool cok = c < C;
     float wk[9];
@@ -392,11 +362,7 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
     float* const yh = o.y_hi;
     float* const yl = o.y_lo;
     float* const yf = o.y;
-    if (tma) {
-        dw_fwd_tile(o, q, xs, [&] { tc::mbar_wait(&bar, 0); cta_mark(2); });
-        cta_mark(3);
-        return;
-    } else {
+    {
         float pa = 0, pb = 0, pc = 0, pd = 0;
         if (pro != 0 && cok) {
             pa = o.pa[c], pb = o.pb[c];
@@ -456,10 +422,175 @@ __global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restr
         oy += kThreads / 32;
         while (oy >= t.th) oy -= t.th, ++i;
     }
+}
+
+
+// ---------------------------------------------------------- depthwise fwd
+// The x tile arrives by one 4-D TMA box (zero-filled halo / channel tail) or,
+// for channel counts TMA cannot address, by cp.async.  Warp = output row
+// (image i, row oy) of the tile, lane = channel; stride 1 slides a 3x3
+// register window along x (3 shared loads per output).
+__global__ void __launch_bounds__(kThreads) dw_fwd_kernel(const DwFwdOp* __restrict__ ops, int nd) {
+    pdl_trigger();
+    cta_mark(0);
+    extern __shared__ __align__(128) float xs[];
+    __shared__ DwFwdOp osh;
+    __shared__ uint64_t bar;
+    int local;
+    const int oi = op_to_shared(ops, nd, &osh, &bar, local);
+    pdl_wait();  // descriptor copy above overlaps the predecessor's tail
+    cta_mark(1);
+    const DwFwdOp& o = osh;
+    if (is_failed(o.failed)) return;
+    const DwTile t = o.tile;
+    const DwPos q = dw_pos(t, local);
+    const int n = o.n, h = o.h, w = o.wd, C = o.c, ho = o.ho, wo = o.wo, s = o.stride, pad = o.pad, pro = o.pro;
+    const int iy0 = q.y0 * s - pad;
+    const bool tma = o.tma != 0;
+    if (tma && threadIdx.x < 32) {
+        if (o.rows == nullptr) {
+            if (threadIdx.x == 0) {
+                tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(t.ni * t.tr * t.tw * kDwC * 4));
+                tc::tma_load_4d(xs, &ops[oi].map_x, &bar, q.c0, -pad, iy0, q.n0);
+            }
+        } else {  // gather: one single-image box per batch image, lanes in parallel
+            const int cnt = min(t.ni, n - q.n0), img_f = t.tr * t.tw * kDwC;
+            if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(&bar, static_cast<uint32_t>(cnt * img_f * 4));
+            __syncwarp();
+            for (int i = threadIdx.x; i < cnt; i += 32)
+                tc::tma_load_4d(xs + i * img_f, &ops[oi].map_x, &bar, q.c0, -pad, iy0, __ldg(o.rows + q.n0 + i));
+        }
+    }
+    if (tma) {
+        dw_fwd_tile(o, q, xs, [&] { tc::mbar_wait(&bar, 0); cta_mark(2); });
+    } else {
+        dw_fwd_plain(o, q, xs);
+    }
     cta_mark(3);
 }
 
+// Persistent variant: 2 CTAs per SM, each walks tiles b, b + G, ... with two
+// staging buffers, so tile j+1's TMA box (and its descriptor copy) is in
+// flight while tile j is mapped and computed.  Same per-tile code as
+// dw_fwd_kernel: identical bits.
+constexpr int kDwPersistPerSm = 2;
+constexpr int kDwMaxOps = 64;
+
+// warp 0: stage tile q of op o (TMA path) into xs, completion on bar
+__device__ __forceinline__ void dw_fwd_issue(const DwFwdOp& o, const CUtensorMap* map, const DwPos& q, float* xs,
+                                             uint64_t* bar) {
+    const DwTile& t = o.tile;
+    const int iy0 = q.y0 * o.stride - o.pad;
+    if (o.rows == nullptr) {
+        if (threadIdx.x == 0) {
+            tc::mbar_arrive_expect_tx(bar, static_cast<uint32_t>(t.ni * t.tr * t.tw * kDwC * 4));
+            tc::tma_load_4d(xs, map, bar, q.c0, -o.pad, iy0, q.n0);
+        }
+    } else {
+        const int cnt = min(t.ni, o.n - q.n0), img_f = t.tr * t.tw * kDwC;
+        if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(bar, static_cast<uint32_t>(cnt * img_f * 4));
+        __syncwarp();
+        for (int i = threadIdx.x; i < cnt; i += 32) tc::tma_load_4d(xs + i * img_f, map, bar, q.c0, -o.pad, iy0, __ldg(o.rows + q.n0 + i));
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, kDwPersistPerSm) dw_fwd_persist_kernel(const DwFwdOp* __restrict__ ops,
+                                                                                 int nd, int total, int buf_floats) {
+    pdl_trigger();
+    extern __shared__ __align__(128) float xbuf[];
+    __shared__ __align__(16) DwFwdOp osh[2];
+    __shared__ uint64_t bar[2];
+    __shared__ int begins[kDwMaxOps];
+    __shared__ int opi[2];
+    const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+    for (int i = threadIdx.x; i < nd; i += blockDim.x) begins[i] = ops[i].cta_begin;
+    if (threadIdx.x == 0) {
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int nt = b < total ? (total - 1 - b) / G + 1 : 0;
+    // descriptor of tile j into slot j & 1 (all threads); returns the tile's local index
+    auto load_desc = [&](int j) {
+        const int t = b + j * G;
+        int lo = 0, hi = nd - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (begins[mid] <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const uint4* src = reinterpret_cast<const uint4*>(ops + lo);
+        uint4* dst = reinterpret_cast<uint4*>(&osh[j & 1]);
+        for (int i = threadIdx.x; i < static_cast<int>(sizeof(DwFwdOp) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+        if (threadIdx.x == 0) opi[j & 1] = lo;
+        return t - begins[lo];
+    };
+    auto stage = [&](int j, int local) {  // warp 0, after the descriptor is visible
+        const DwFwdOp& o = osh[j & 1];
+        if (threadIdx.x < 32 && o.tma && !is_failed(o.failed)) {
+            tc::fence_async_smem();  // generic writes of this buffer's previous tile precede the TMA
+            dw_fwd_issue(o, &ops[opi[j & 1]].map_x, dw_pos(o.tile, local), xbuf + (j & 1) * buf_floats, &bar[j & 1]);
+        }
+    };
+    if (nt == 0) return;
+    int local = load_desc(0);
+    __syncthreads();
+    pdl_wait();  // descriptors above overlap the predecessor's tail
+    stage(0, local);
+    uint32_t phase[2] = {0u, 0u};
+    for (int j = 0; j < nt; ++j) {
+        const int slot = j & 1;
+        int next = 0;
+        if (j + 1 < nt) next = load_desc(j + 1);
+        __syncthreads();
+        if (j + 1 < nt) stage(j + 1, next);
+        const DwFwdOp& o = osh[slot];
+        if (!is_failed(o.failed)) {
+            const DwPos q = dw_pos(o.tile, local);
+            float* xs = xbuf + slot * buf_floats;
+            if (o.tma) {
+                const uint32_t ph = phase[slot];
+                dw_fwd_tile(o, q, xs, [&] { tc::mbar_wait(&bar[slot], ph); });
+                phase[slot] ^= 1u;
+            } else {
+                dw_fwd_plain(o, q, xs);
+            }
+        }
+        __syncthreads();  // buffer and descriptor slot free for tile j + 2
+        local = next;
+    }
+}
+
 void launch_dw_fwd(const DwFwdOp* d, int nd, int ctas, cudaStream_t st) {
+    // PBKD_DW_PERSIST=1: the persistent double-buffered variant -- measured
+    // 6% slower per launch (2 CTAs / 16 warps per SM hide the window's FFMA2
+    // and shared-memory latencies worse than 3 one-tile CTAs), so off
+    static const bool persist = [] {
+        const char* e = std::getenv("PBKD_DW_PERSIST");
+        return e && e[0] == '1';
+    }();
+    if (persist && nd <= kDwMaxOps) {
+        static bool pattr = false;
+        const int bytes = 2 * dw_tile_bytes();
+        if (!pattr) {
+            PBKD_CUDA(cudaFuncSetAttribute(dw_fwd_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            pattr = true;
+        }
+        static int sms = [] {
+            int dev = 0, v = 0;
+            PBKD_CUDA(cudaGetDevice(&dev));
+            PBKD_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+            return std::max(1, v);
+        }();
+        const int grid = std::max(1, std::min(ctas, kDwPersistPerSm * sms));
+        traced("dw_fwd", grid, st, [&] {
+            launch_k(dw_fwd_persist_kernel, dim3(grid), dim3(kThreads), static_cast<size_t>(bytes), st, d, nd, ctas,
+                     dw_tile_bytes() / 4);
+        });
+        PBKD_LAUNCH_CHECK();
+        return;
+    }
     static bool attr = false;
     if (!attr) {  // 48 KB dynamic + the static descriptor copy exceed the default
         PBKD_CUDA(cudaFuncSetAttribute(dw_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_tile_bytes()));
