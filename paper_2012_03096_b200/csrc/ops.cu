@@ -1200,6 +1200,56 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(const BnBwdApply
     if (is_failed(o.failed)) return;
     const float* tg = o.t ? o.t : o.gin;
     const long long cta0 = static_cast<long long>(local) * kThreads * kElemQuads * 4;
+    if ((o.c & 3) == 0 && (4 * kThreads * kElemQuads) % o.c == 0 && cta0 + 4LL * kThreads * kElemQuads <= o.total) {
+        // c divides the CTA's element span: all of this thread's quads are the
+        // same four channels, so the per-channel parameters and the products
+        // gamma*inv, inv_m*sg (bn_bwd_one) are loaded / formed once
+        const int ch = (threadIdx.x * 4) % o.c;
+        const float4 mn = __ldg(reinterpret_cast<const float4*>(o.mean + ch));
+        const float4 iv = __ldg(reinterpret_cast<const float4*>(o.inv + ch));
+        const float4 gm = __ldg(reinterpret_cast<const float4*>(o.gamma + ch));
+        const float4 bt = __ldg(reinterpret_cast<const float4*>(o.beta + ch));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(o.sg + ch));
+        const float4 s2 = __ldg(reinterpret_cast<const float4*>(o.sgx + ch));
+        const float mnv[4] = {mn.x, mn.y, mn.z, mn.w}, ivv[4] = {iv.x, iv.y, iv.z, iv.w};
+        const float gmv[4] = {gm.x, gm.y, gm.z, gm.w}, btv[4] = {bt.x, bt.y, bt.z, bt.w};
+        const float s2v[4] = {s2.x, s2.y, s2.z, s2.w};
+        float kk[4], a1[4];
+        const float s1v[4] = {s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kk[q] = mul(gmv[q], ivv[q]), a1[q] = mul(o.inv_m, s1v[q]);
+        float4 p[kElemQuads], g[kElemQuads];
+#pragma unroll
+        for (int j = 0; j < kElemQuads; ++j) {
+            const long long i = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
+            p[j] = __ldg(reinterpret_cast<const float4*>(o.p + i));
+            g[j] = __ldg(reinterpret_cast<const float4*>(tg + (o.trows ? row_remap(o.trows, o.srow, i) : i)));
+        }
+#pragma unroll
+        for (int j = 0; j < kElemQuads; ++j) {
+            const long long i = cta0 + (static_cast<long long>(j) * kThreads + threadIdx.x) * 4;
+            const float pv[4] = {p[j].x, p[j].y, p[j].z, p[j].w}, gv[4] = {g[j].x, g[j].y, g[j].z, g[j].w};
+            float rv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // bn_bwd_one with the hoisted products
+                const float xh = mul(sub(pv[q], mnv[q]), ivv[q]);
+                float gy;
+                if (o.t) {
+                    const float y = add(mul(gmv[q], xh), btv[q]);
+                    const float d = sub(relu(y), gv[q]);
+                    gy = y > 0.0f ? add(0.0f, mul(o.kmse, d)) : 0.0f;
+                } else {
+                    gy = gv[q];
+                }
+                const float inner = sub(sub(gy, a1[q]), mul(mul(xh, o.inv_m), s2v[q]));
+                rv[q] = add(0.0f, mul(kk[q], inner));
+            }
+            const float4 r = make_float4(rv[0], rv[1], rv[2], rv[3]);
+            if (o.gout_hi) split_store4(o.gout_hi, o.gout_lo, i, r);
+            else *reinterpret_cast<float4*>(o.gout + i) = r;
+        }
+        return;
+    }
     if ((o.c & 3) == 0 && cta0 + 4LL * kThreads * kElemQuads <= o.total) {
         float4 p[kElemQuads], g[kElemQuads];
 #pragma unroll
