@@ -132,6 +132,8 @@ struct GemmOp {
     const float *scale, *shift, *skip;
     int relu;
     int bn;              // N tile (multiple of 16, <= 256), set by gemm_finalize
+    int bm;              // M rows per tile: 128, or fewer for an implicit-GEMM conv whose
+                         // tiles are whole output rows / images (gemm_tma_prepare)
     int tf32x3, tf32x1;  // 3xTF32 split (fp32 parity, default) or plain TF32
     const int* failed;
     int cta_begin;

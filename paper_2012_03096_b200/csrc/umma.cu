@@ -282,6 +282,7 @@ void gemm_finalize(GemmOp& o) {
     }();
     o.bn = bn_for(o.N);
     if (o.bn == 128 && longk > 0 && o.kchunk >= longk) o.bn = 64;
+    o.bm = kBM;
     o.tiles_m = ceil_div(o.M, kBM);
     o.tiles_n = ceil_div(o.N, o.bn);
     if (o.tf32x3 == 0) {  // parity mode: split fp32 into tf32 hi+lo
@@ -299,6 +300,8 @@ void gemm_finalize(GemmOp& o) {
         return !(e && e[0] == '0');
     }();
     o.tma = (tma_on && gemm_tma_prepare(o)) ? 1 : 0;
+    if (!o.tma) o.bm = kBM;  // the register-staged kernel tiles by 128 rows
+    o.tiles_m = ceil_div(o.M, o.bm);
 }
 
 int ctas_gemm(const GemmOp& o) { return o.tiles_m * o.tiles_n * o.ksplit; }

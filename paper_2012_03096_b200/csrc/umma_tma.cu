@@ -196,7 +196,8 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
     float* __restrict__ part0 = op.part0;
     float* __restrict__ part1 = op.part1;
     const CUtensorMap* map_c = &op.map_c;
-    const int m0 = tm * kBM, n0 = tn * bnt;  // bnt: the op's N tile (<= BN)
+    const int bm = (KIND == kGemmKindConv && op.conv) ? op.bm : kBM;  // rows of this tile
+    const int m0 = tm * bm, n0 = tn * bnt;  // bnt: the op's N tile (<= BN)
     const int r = q * 32 + lane;
     const bool xform = KIND == kGemmKindConv && (scale || skip || relu_on || c_hi);
 #pragma unroll
@@ -219,7 +220,7 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
             const int n = n0 + pass * 32 + lane;
             float sc = 1.0f, sh = 0.0f;
             if (scale && n < N) sc = __ldg(scale + n), sh = __ldg(shift + n);
-            for (int rr = warp8; rr < kBM; rr += 8) {
+            for (int rr = warp8; rr < bm; rr += 8) {
                 const int row = m0 + rr;
                 if (row >= M || n >= N) continue;
                 const uint32_t a = cs_addr(cs, rr, lane);
@@ -399,8 +400,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             if (tiles_sh[j].op < 0) continue;  // task predicated off (diverged)
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
-            const int m0 = g.tm * kBM, n0 = g.tn * BN;
             const bool conv = CONV && o.conv != 0, akm = o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            const int bm = conv ? o.bm : kBM;
+            const int m0 = g.tm * bm, n0 = g.tn * BN;
             int img = 0, y0 = 0;
             if (conv) {  // tiles cover whole output rows / images (gemm_tma_prepare)
                 const int hw = o.oh * o.ow;
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     const int r = it % R;
                     mbar_wait(&raw_empty[r], ((it / R) & 1) ^ 1);
                     uint8_t* st = raw_ring + r * C::raw_stage;
-                    const uint32_t bytes = (o.a_presplit ? 0 : C::a_raw) + (o.b_presplit ? 0 : C::b_raw);
+                    const uint32_t bytes = (o.a_presplit ? 0 : bm * kBK * 4) + (o.b_presplit ? 0 : C::b_raw);
                     if (bytes == 0) {  // both operands go straight to the operand ring
                         mbar_arrive(&raw_full[r]);
                         continue;
@@ -498,7 +500,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
             const int bnt = PS ? o.bn : BN;  // a pre-split launch mixes N tiles (gemm_bn_class)
-            const int m0 = g.tm * kBM, n0 = g.tn * bnt;
+            const int bm = (CONV && o.conv) ? o.bm : kBM;
+            const int m0 = g.tm * bm, n0 = g.tn * bnt;
             const bool apre = o.a_presplit != 0, bpre = o.b_presplit != 0;
             const bool akm = (CONV && o.conv != 0) || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
             int img = 0, y0 = 0;
@@ -512,9 +515,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     const int s = it % S;
                     mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
 #ifdef PBKD_EXP_NOLO  // diagnosis build only: hi planes alone (wrong results)
-                    const uint32_t bytes = (apre ? C::a_op : 0) + (bpre ? bnt * kRowBytes : 0);
+                    const uint32_t bytes = (apre ? bm * kRowBytes : 0) + (bpre ? bnt * kRowBytes : 0);
 #else
-                    const uint32_t bytes = (apre ? 2 * C::a_op : 0) + (bpre ? 2 * bnt * kRowBytes : 0);
+                    const uint32_t bytes = (apre ? 2 * bm * kRowBytes : 0) + (bpre ? 2 * bnt * kRowBytes : 0);
 #endif
                     if (bytes == 0) {
                         mbar_arrive(&op_full[s]);
@@ -1072,17 +1075,26 @@ bool encode_nhwc_box(CUtensorMap* m, const float* base, int n, int h, int w, int
 // of a tile, traversal stride = conv stride, out-of-image taps zero filled.
 // Needs C % 32 == 0 and tiles made of whole output rows (ow | 128 and
 // (128/ow) | oh) or whole images (oh*ow | 128).
+// M tile of an implicit-GEMM conv: whole output rows of one image (bh rows,
+// bh | oh, bh * ow <= 128) or whole images; 0 when no such tile exists.
+int conv_tile_rows(const GemmOp& o, int* bh_out, int* bimg_out) {
+    const int hw = o.oh * o.ow;
+    if (hw > kBM) {
+        if (o.ow > kBM) return 0;
+        int bh = kBM / o.ow;
+        while (bh > 1 && o.oh % bh != 0) --bh;
+        *bh_out = bh, *bimg_out = 1;
+        return bh * o.ow;
+    }
+    *bh_out = o.oh, *bimg_out = kBM / hw;
+    return *bimg_out * hw;
+}
+
 bool encode_conv(CUtensorMap* m, const GemmOp& o, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE) {
     if (o.ic % kBK != 0 || (reinterpret_cast<uintptr_t>(o.A) & 15) != 0) return false;
     const int hw = o.oh * o.ow;
-    int bw = o.ow, bh, bimg;
-    if (hw >= kBM) {
-        if (kBM % o.ow != 0 || o.oh % (kBM / o.ow) != 0) return false;
-        bh = kBM / o.ow, bimg = 1;
-    } else {
-        if (kBM % hw != 0) return false;
-        bh = o.oh, bimg = kBM / hw;
-    }
+    int bw = o.ow, bh = 0, bimg = 0;
+    if (conv_tile_rows(o, &bh, &bimg) == 0) return false;
     const int s = o.cstride;
     const long long nimg = o.M / hw;
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(o.ic), static_cast<cuuint64_t>(o.iw),
@@ -1156,7 +1168,7 @@ bool encode_c(GemmOp& o) {
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(o.N), static_cast<cuuint64_t>(o.M),
                                 static_cast<cuuint64_t>(splits)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(o.ldc) * 4, static_cast<cuuint64_t>(o.ldc) * o.M * 4};
-    const cuuint32_t box[3] = {32, static_cast<cuuint32_t>(kBM), 1};
+    const cuuint32_t box[3] = {32, static_cast<cuuint32_t>(o.bm > 0 ? o.bm : kBM), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return encode_fn()(&o.map_c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, o.C, dims, strides, box, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1172,6 +1184,12 @@ bool gemm_tma_prepare(GemmOp& o) {
             return !(e && e[0] == '0');
         }();
         if (!conv_on || o.ksplit != 1 || !o.b_kmajor) return false;
+        int bh = 0, bimg = 0;
+        o.bm = conv_tile_rows(o, &bh, &bimg);
+        if (o.bm == 0) {
+            o.bm = kBM;
+            return false;
+        }
         if (!(encode_conv(&o.map_a, o) && encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn))) return false;
         presplit_maps(o);
         o.c_tma = encode_c(o) ? 1 : 0;

@@ -52,6 +52,13 @@ def main(out):
         nb = P.spec_num_blocks(spec)
         for k in range(1, nb + 1):
             res[f"{name}_{k}"] = ctx.prefix_infer(x, k, True, 5 * 64 * 32 * 32)
+    # ResNet-50 / 224x224: 56/28/14/7-pixel outputs, whose TMA conv tiles are
+    # 112 or 98 rows (whole output rows / images), every bottleneck block
+    spec = open(os.path.join(root, "configs", "resnet50_imagenet.json")).read()
+    ctx.teacher_init(spec, 78)
+    x = np.random.default_rng(6).random((2, 3, 224, 224), dtype=np.float32)
+    for k in range(1, P.spec_num_blocks(spec) + 1):
+        res[f"resnet50_{k}"] = ctx.prefix_infer(x, k, True, 2 * 256 * 56 * 56)
     np.savez(out, **res)
 
 
