@@ -885,20 +885,20 @@ struct Engine::Impl {
 
     void teacher_block(Program& P, int j, const float* x, float* y, int n, float* t1, float* sk) {
         const TBlockDev& b = tblocks[static_cast<size_t>(j)];
-        const Planes2 xp = planes_for(x), yp = planes_for(y), tp = planes_for(t1);
+        const Planes2 xp = planes_for(x), yp = planes_for(y), tp = planes_for(t1), sp = planes_for(sk);
         if (b.kind == 0) {
             P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, y, true, nullptr, true, xp, yp)});
             return;
         }
         if (b.kind == 2) {  // bottleneck: t1 = reduce(x), sk = 3x3(t1), y = expand(sk) + skip
             P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true, xp, tp)});
-            P.gemm({conv_gemm(b.c2, t1, n, b.hin, b.win, sk, true, nullptr, true, tp)});
+            P.gemm({conv_gemm(b.c2, t1, n, b.hin, b.win, sk, true, nullptr, true, tp, sp)});
             const float* skip = x;
             if (b.has_proj) {  // the projection lands in y; the expand conv adds it element-wise in place
                 P.gemm({conv_gemm(b.proj, x, n, b.hin, b.win, y, false, nullptr, false, xp)});
                 skip = y;
             }
-            P.gemm({conv_gemm(b.c3, sk, n, b.hout, b.wout, y, true, skip, true, {}, yp)});
+            P.gemm({conv_gemm(b.c3, sk, n, b.hout, b.wout, y, true, skip, true, sp, yp)});
             return;
         }
         if (b.kind == 3) {  // stem: conv7x7 + BN + ReLU into t1, 3x3/2 max pool into y
@@ -1671,20 +1671,20 @@ struct Engine::Impl {
     // its registered tf32 planes (unregistered on destruction).
     struct TeacherWs {
         Impl& m;
-        std::vector<std::array<DevBuf, 10>> bufs;
+        std::vector<std::array<DevBuf, 12>> bufs;
         std::vector<TLane> lanes;
         TeacherWs(Impl& im, size_t bytes, int nlanes) : m(im), bufs(static_cast<size_t>(nlanes)) {
             const bool tplanes = gemm_presplit_ok(32);
             for (auto& lb : bufs) {
-                for (DevBuf& d : lb) d.alloc(bytes);  // ping, pong, t1, sk + planes of ping / pong / t1
+                for (DevBuf& d : lb) d.alloc(bytes);  // ping, pong, t1, sk + planes of each
                 if (tplanes)
-                    for (int i = 0; i < 3; ++i) m.act_planes[lb[static_cast<size_t>(i)].f()] = Planes2{lb[4 + 2 * i].f(), lb[5 + 2 * i].f()};
+                    for (int i = 0; i < 4; ++i) m.act_planes[lb[static_cast<size_t>(i)].f()] = Planes2{lb[4 + 2 * i].f(), lb[5 + 2 * i].f()};
                 lanes.push_back(TLane{lb[0].f(), lb[1].f(), lb[2].f(), lb[3].f()});
             }
         }
         ~TeacherWs() {
             for (auto& lb : bufs)
-                for (int i = 0; i < 3; ++i) m.act_planes.erase(lb[static_cast<size_t>(i)].f());
+                for (int i = 0; i < 4; ++i) m.act_planes.erase(lb[static_cast<size_t>(i)].f());
         }
     };
     // The boundary pass of this rank (images of every training row into
@@ -2104,11 +2104,11 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     const size_t wsz = static_cast<size_t>(std::max(chunk, ichunk)) * mrow * sizeof(float);
     DevBuf ping(wsz), pong(wsz), t1(wsz), sk(wsz), ia(wsz), ib(wsz), io(wsz);
     // tf32 planes of the teacher's working buffers (pre-split conv operands)
-    DevBuf plane_bufs[6];
+    DevBuf plane_bufs[8];
     const bool tplanes = gemm_presplit_ok(32);
     if (tplanes) {
-        float* bufs[3] = {ping.f(), pong.f(), t1.f()};
-        for (int i = 0; i < 3; ++i) {
+        float* bufs[4] = {ping.f(), pong.f(), t1.f(), sk.f()};
+        for (int i = 0; i < 4; ++i) {
             plane_bufs[2 * i].alloc(wsz);
             plane_bufs[2 * i + 1].alloc(wsz);
             act_planes[bufs[i]] = Planes2{plane_bufs[2 * i].f(), plane_bufs[2 * i + 1].f()};
@@ -2125,7 +2125,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     const int nbr = std::max(1, std::min(static_cast<int>(ts.size()), 1 + static_cast<int>(side_streams.size())));
     const size_t esz = static_cast<size_t>(std::max(1, std::min(neval, ichunk))) * mrow * sizeof(float);
     struct BranchWs {
-        DevBuf ia, ib, io, ping, pong, t1, sk, pl[6];
+        DevBuf ia, ib, io, ping, pong, t1, sk, pl[8];
     };
     std::vector<BranchWs> bws(static_cast<size_t>(nbr));
     for (size_t b = 0; b < bws.size(); ++b) {
@@ -2134,8 +2134,8 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
         for (DevBuf* d : {&w.ia, &w.ib, &w.io}) d->alloc(wsz);
         for (DevBuf* d : {&w.ping, &w.pong, &w.t1, &w.sk}) d->alloc(esz);
         if (tplanes) {
-            float* bufs[3] = {w.ping.f(), w.pong.f(), w.t1.f()};
-            for (int i = 0; i < 3; ++i) {
+            float* bufs[4] = {w.ping.f(), w.pong.f(), w.t1.f(), w.sk.f()};
+            for (int i = 0; i < 4; ++i) {
                 w.pl[2 * i].alloc(esz);
                 w.pl[2 * i + 1].alloc(esz);
                 act_planes[bufs[i]] = Planes2{w.pl[2 * i].f(), w.pl[2 * i + 1].f()};
