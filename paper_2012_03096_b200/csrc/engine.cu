@@ -556,6 +556,12 @@ struct Planes2 {
 GemmOp conv_gemm(const ConvDev& c, const float* x, int n, int ih, int iw, float* y, bool affine,
                  const float* skip, bool relu_out, Planes2 xp = {}, Planes2 yp = {}) {
     GemmOp o{};
+    if (gemm_ts_enabled()) {
+        // A through tensor memory: the conv splits its raw fp32 input itself,
+        // so neither input nor output planes are needed (PBKD_GEMM_TS=0: planes)
+        o.a_ts_req = 1;
+        xp = Planes2{}, yp = Planes2{};
+    }
     o.a_hi = xp.hi, o.a_lo = xp.lo;  // input planes: the conv runs on pre-split A
     o.c_hi = yp.hi, o.c_lo = yp.lo;  // output planes for the next conv
     o.conv = 1;
@@ -904,7 +910,9 @@ struct Engine::Impl {
         if (b.kind == 3) {  // stem: conv7x7 + BN + ReLU into t1, 3x3/2 max pool into y
             P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true, xp)});
             const int c = b.cout, mh = b.mid_h, mw = b.mid_w;
-            P.raw([=](cudaStream_t s2) { launch_maxpool3x3(t1, y, yp.hi, yp.lo, n, mh, mw, c, s2); }, "MaxPoolOp");
+            float* ph = gemm_ts_enabled() ? nullptr : yp.hi;  // planes only for pre-split consumers
+            float* pl = gemm_ts_enabled() ? nullptr : yp.lo;
+            P.raw([=](cudaStream_t s2) { launch_maxpool3x3(t1, y, ph, pl, n, mh, mw, c, s2); }, "MaxPoolOp");
             return;
         }
         P.gemm({conv_gemm(b.c1, x, n, b.hin, b.win, t1, true, nullptr, true, xp, tp)});

@@ -320,7 +320,7 @@ int gemm_bn_class(const GemmOp& o) {
     // Plain stores (epi 0) and split-K partial stores (epi 2) share kernel
     // kind 0 (the store's split coordinate is 0 without split-K), so a
     // unit's dgrad and wgrad can run as one launch.
-    if (!o.conv && o.a_tmem)  // A through TMEM (umma_ts_kernel), one launch per phase
+    if (o.a_tmem)  // A through TMEM (umma_ts_kernel), one launch per phase
         return 128 + 3 * kGemmClassTma + (kind == 2 ? 0 : kind) * kGemmClassKind;
     if (merge && !o.conv && o.a_presplit && o.b_presplit)
         return 128 + 2 * kGemmClassTma + (kind == 2 ? 0 : kind) * kGemmClassKind;

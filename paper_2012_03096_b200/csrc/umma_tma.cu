@@ -769,17 +769,32 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
             const int bnt = o.bn;
-            const int m0 = g.tm * kBM, n0 = g.tn * bnt;
-            const bool akm = o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            const bool conv = KIND == kGemmKindConv && o.conv != 0;
+            const int bm = conv ? o.bm : kBM;
+            const int m0 = g.tm * bm, n0 = g.tn * bnt;
+            const bool akm = conv || o.a_kmajor != 0, bkm = o.b_kmajor != 0;
+            int img = 0, y0 = 0;
+            if (conv) {  // tiles of whole output rows / images (gemm_tma_prepare)
+                const int hw = o.oh * o.ow;
+                img = m0 / hw;
+                y0 = (m0 - img * hw) / o.ow * o.cstride - o.cpad;
+            }
             if (lane == 0) {
                 for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                     const int s = it % S;
                     mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&op_full[s], static_cast<uint32_t>(kTsARaw + 2 * bnt * kRowBytes));
+                    mbar_arrive_expect_tx(&op_full[s], static_cast<uint32_t>(bm * kBK * 4 + 2 * bnt * kRowBytes));
                     uint8_t* st = ring + s * kTsStage;
                     const int k = g.k0 + kc * kBK;
-                    if (akm) tma_load_2d(st, &o.map_a, &op_full[s], k, m0);
-                    else tma_load_2d(st, &o.map_a, &op_full[s], m0, k);
+                    if (conv) {  // implicit im2col: tap (ky, kx), channels c0..c0+31 of the raw input
+                        const int tap = k / o.ic, c0 = k - tap * o.ic;
+                        const int ky = tap / o.ksz, kx = tap - ky * o.ksz;
+                        tma_load_4d(st, &o.map_a, &op_full[s], c0, kx - o.cpad, y0 + ky, img);
+                    } else if (akm) {
+                        tma_load_2d(st, &o.map_a, &op_full[s], k, m0);
+                    } else {
+                        tma_load_2d(st, &o.map_a, &op_full[s], m0, k);
+                    }
                     uint8_t* ob = st + kTsARaw;
                     if (bkm) {
                         tma_load_2d(ob, &o.map_bh, &op_full[s], k, n0);
@@ -807,7 +822,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
             if (tiles_sh[j].op < 0) continue;
             const GemmOp& o = ops[tiles_sh[j].op];
             const TileGeo g = tiles_sh[j].g;
-            const bool akm = o.a_kmajor != 0;
+            const bool akm = (KIND == kGemmKindConv && o.conv != 0) || o.a_kmajor != 0;
             for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                 const int s = it % S, t = it % T;
                 mbar_wait(&op_full[s], (it / S) & 1);
@@ -1193,6 +1208,15 @@ bool gemm_tma_prepare(GemmOp& o) {
         if (!(encode_conv(&o.map_a, o) && encode(&o.map_b, o.B, o.K, o.N, o.ldb, kBK, bn))) return false;
         presplit_maps(o);
         o.c_tma = encode_c(o) ? 1 : 0;
+        o.a_tmem = 0;
+        if (o.c_tma && gemm_ts_enabled() && o.a_ts_req && o.b_presplit && o.tf32x3 == 3 && bn <= kTsBN) {
+            CUtensorMap m;  // raw input, 128-byte swizzled im2col boxes for the converter warps
+            if (encode_conv(&m, o, CU_TENSOR_MAP_SWIZZLE_128B)) {
+                o.map_a = m;
+                o.a_tmem = 1;
+                o.a_presplit = 0;
+            }
+        }
         return o.c_tma != 0;
     }
     bool ok = o.a_kmajor ? encode(&o.map_a, o.A, o.K, o.M, o.lda, kBK, kBM) : encode(&o.map_a, o.A, o.M, o.K, o.lda, kBM, kBK);
@@ -1238,7 +1262,7 @@ void tf32_split_host(const float* x, size_t n, float* hi, float* lo) {
 template <int KIND>
 void launch_tma_kind(const GemmOp* d, int nd, int total, int cls, cudaStream_t st, const int* perm) {
     if (cls >= 3 * kGemmClassTma) {  // A through TMEM (kinds 0 / 1)
-        if constexpr (KIND == 0 || KIND == 1) launch_ts_t<KIND>(d, nd, total, st, perm);
+        if constexpr (KIND == 0 || KIND == 1 || KIND == kGemmKindConv) launch_ts_t<KIND>(d, nd, total, st, perm);
         else throw CudaError("umma_ts: unsupported epilogue kind");
         return;
     }
