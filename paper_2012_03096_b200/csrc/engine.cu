@@ -1682,9 +1682,10 @@ struct Engine::Impl {
         std::vector<std::array<DevBuf, 12>> bufs;
         std::vector<TLane> lanes;
         TeacherWs(Impl& im, size_t bytes, int nlanes) : m(im), bufs(static_cast<size_t>(nlanes)) {
-            const bool tplanes = gemm_presplit_ok(32);
+            const bool tplanes = gemm_presplit_ok(32) && !gemm_ts_enabled();  // convs split raw inputs themselves otherwise
             for (auto& lb : bufs) {
-                for (DevBuf& d : lb) d.alloc(bytes);  // ping, pong, t1, sk + planes of each
+                for (size_t i = 0; i < lb.size(); ++i)  // ping, pong, t1, sk (+ planes of each)
+                    if (i < 4 || tplanes) lb[i].alloc(bytes);
                 if (tplanes)
                     for (int i = 0; i < 4; ++i) m.act_planes[lb[static_cast<size_t>(i)].f()] = Planes2{lb[4 + 2 * i].f(), lb[5 + 2 * i].f()};
                 lanes.push_back(TLane{lb[0].f(), lb[1].f(), lb[2].f(), lb[3].f()});
@@ -2113,7 +2114,7 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
     DevBuf ping(wsz), pong(wsz), t1(wsz), sk(wsz), ia(wsz), ib(wsz), io(wsz);
     // tf32 planes of the teacher's working buffers (pre-split conv operands)
     DevBuf plane_bufs[8];
-    const bool tplanes = gemm_presplit_ok(32);
+    const bool tplanes = gemm_presplit_ok(32) && !gemm_ts_enabled();  // convs split raw inputs themselves otherwise
     if (tplanes) {
         float* bufs[4] = {ping.f(), pong.f(), t1.f(), sk.f()};
         for (int i = 0; i < 4; ++i) {
