@@ -498,6 +498,7 @@ void print_profile(const char* what, const std::map<std::string, KernelStat>& pr
 // ------------------------------------------------------------- teacher dev
 struct ConvDev {
     int cin = 0, cout = 0, k = 0, stride = 1, pad = 0;
+    int kp = 0;          // weight row pitch: k*k*cin rounded up to 4 floats (16-byte TMA rows)
     DevBuf w;            // [cout][k*k][cin]
     DevBuf w_hi, w_lo;   // the same, pre-split into tf32 hi / lo (3xTF32 operands)
     DevBuf scale, shift; // inference batch-norm affine (ops.hpp:304-321)
@@ -524,12 +525,15 @@ ConvDev conv_upload(const pbkd::LayerParams& conv, const pbkd::LayerParams* bn, 
     d.stride = conv.stride;
     d.pad = conv.padding;
     const int kk = d.k * d.k;
-    const size_t nw = static_cast<size_t>(d.cout) * kk * d.cin;
-    {  // relayout [cout][cin][kk] -> [cout][kk][cin] and tf32 split on the device
+    d.kp = (kk * d.cin + 3) / 4 * 4;
+    const size_t nw = static_cast<size_t>(d.cout) * d.kp;
+    {  // relayout [cout][cin][kk] -> [cout][kk][cin] (rows of pitch kp) and tf32 split on the device
         d.w.alloc(nw * sizeof(float));
         d.w_hi.alloc(nw * sizeof(float));
         d.w_lo.alloc(nw * sizeof(float));
-        launch_conv_weight_prep(dev_w, d.cout, d.cin, kk, d.w.f(), d.w_hi.f(), d.w_lo.f(), st);
+        if (d.kp != kk * d.cin)
+            for (DevBuf* b : {&d.w, &d.w_hi, &d.w_lo}) PBKD_CUDA(cudaMemsetAsync(b->p, 0, nw * sizeof(float), st));
+        launch_conv_weight_prep(dev_w, d.cout, d.cin, kk, d.kp, d.w.f(), d.w_hi.f(), d.w_lo.f(), st);
     }
     if (bn) {
         std::vector<float> sc(d.cout), sh(d.cout);
@@ -580,7 +584,7 @@ GemmOp conv_gemm(const ConvDev& c, const float* x, int n, int ih, int iw, float*
     o.B = c.w.f();
     o.b_hi = c.w_hi.f();
     o.b_lo = c.w_lo.f();
-    o.ldb = o.K;
+    o.ldb = c.kp;
     o.b_kmajor = 1;
     o.C = y;
     o.ldc = c.cout;

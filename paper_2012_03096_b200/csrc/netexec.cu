@@ -601,12 +601,12 @@ void NetExec::prepare(DevBlock& b) {
                 l.whi = alloc(1, 1, 1, static_cast<int>(l.wn));
                 l.wlo = alloc(1, 1, 1, static_cast<int>(l.wn));
             }
-            launch_conv_weight_prep(b.at(l.w), l.cout, l.cin, kk, l.wk.p, l.whi.p, l.wlo.p, st_);
+            launch_conv_weight_prep(b.at(l.w), l.cout, l.cin, kk, kk * l.cin, l.wk.p, l.whi.p, l.wlo.p, st_);
         } else if (l.kind == LayerKind::PointwiseConv) {
             if (!l.wk) l.wk = alloc(1, 1, 1, static_cast<int>(l.wn));
             if (l.stride != 1) {  // strided 1x1: the implicit-im2col conv ([cout][1][cin] = [cout][cin])
                 if (!l.whi) l.whi = alloc(1, 1, 1, static_cast<int>(l.wn)), l.wlo = alloc(1, 1, 1, static_cast<int>(l.wn));
-                launch_conv_weight_prep(b.at(l.w), l.cout, l.cin, 1, l.wk.p, l.whi.p, l.wlo.p, st_);
+                launch_conv_weight_prep(b.at(l.w), l.cout, l.cin, 1, l.cin, l.wk.p, l.whi.p, l.wlo.p, st_);
             } else {
                 PBKD_CUDA(cudaMemcpyAsync(l.wk.p, b.at(l.w), l.wn * sizeof(float), cudaMemcpyDeviceToDevice, st_));
             }

@@ -1414,7 +1414,9 @@ __global__ void tf32_split_kernel(const float* __restrict__ x, long long n, floa
 
 // Teacher conv weights [cout][cin][kk] (model.cpp layout) -> implicit-GEMM
 // layout [cout][kk][cin] (K index = tap * cin + j) plus its tf32 planes.
-__global__ void conv_weight_prep_kernel(const float* __restrict__ raw, int cout, int cin, int kk,
+// [cout][cin][kk] -> [cout][kk][cin] rows of pitch kp >= kk * cin (the pad
+// stays as the caller zeroed it), with the tf32 planes
+__global__ void conv_weight_prep_kernel(const float* __restrict__ raw, int cout, int cin, int kk, int kp,
                                         float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo) {
     pdl_enter();
     const long long n = static_cast<long long>(cout) * cin * kk;
@@ -1426,17 +1428,18 @@ __global__ void conv_weight_prep_kernel(const float* __restrict__ raw, int cout,
         const long long o = r / kk;
         const float v = raw[(o * cin + j) * kk + t];
         const float h = __uint_as_float(tc_split_hi(v));
-        w[i] = v;
-        hi[i] = h;
-        lo[i] = __uint_as_float(tc_split_lo(v, h));
+        const long long d = o * kp + static_cast<long long>(t) * cin + j;
+        w[d] = v;
+        hi[d] = h;
+        lo[d] = __uint_as_float(tc_split_lo(v, h));
     }
 }
 
-void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, float* w, float* hi, float* lo,
+void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, int kp, float* w, float* hi, float* lo,
                              cudaStream_t st) {
     const long long n = static_cast<long long>(cout) * cin * kk;
     const int blocks = static_cast<int>(std::min<long long>(4096, (n + 255) / 256));
-    launch_k(conv_weight_prep_kernel, dim3(std::max(1, blocks)), dim3(256), 0, st, raw, cout, cin, kk, w, hi, lo);
+    launch_k(conv_weight_prep_kernel, dim3(std::max(1, blocks)), dim3(256), 0, st, raw, cout, cin, kk, kp, w, hi, lo);
     PBKD_LAUNCH_CHECK();
 }
 

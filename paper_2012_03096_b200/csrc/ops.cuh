@@ -150,6 +150,7 @@ struct GemmOp {
     // a_ts_req (caller): A is valid raw fp32 (not only planes); gemm_finalize
     // then sets a_tmem when the A-through-TMEM kernel takes the op (B pre-split)
     int a_ts_req, a_tmem;
+    int a_gather;  // a_tmem conv with ic % 32 != 0: converter warps gather the im2col rows from global
     int c_tma;                    // epilogue stores C through shared memory + TMA
     CUtensorMap map_c;            // 3-D {N, M, ksplit} SWIZZLE_128B map of C
 };
@@ -314,7 +315,7 @@ void launch_bn_infer_prep(const float* gamma, const float* beta, const float* mm
 void launch_bn_infer_relu(const float* x, float* y, long long total, int c, const float* scale,
                           const float* shift, cudaStream_t st);
 // teacher conv weights [cout][cin][kk] -> [cout][kk][cin] + tf32 planes
-void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, float* w, float* hi, float* lo,
+void launch_conv_weight_prep(const float* raw, int cout, int cin, int kk, int kp, float* w, float* hi, float* lo,
                              cudaStream_t st);
 // 3x3 / stride 2 / pad 1 max pooling over NHWC (the ResNet-50 stem, SURVEY
 // 8f-4): out-of-image taps are skipped; optional tf32 planes of the output
