@@ -1643,6 +1643,8 @@ struct Engine::Impl {
             gm.C = bufb;
             gm.ldc = cout;
             gm.ksplit = 1;
+            gm.a_ts_req = 1;  // raw dw output split into TMEM by the GEMM
+            if (s.planes_w && s.params_hi.p) gm.b_hi = s.params_hi.f() + s.off_pw[u], gm.b_lo = s.params_lo.f() + s.off_pw[u];
             gemm_finalize(gm);
             P.gemm({gm});
             if (u == U - 1) {
