@@ -2332,7 +2332,11 @@ void Engine::Impl::run_group(std::vector<TaskState*>& ts, const std::vector<int>
                 }
             add_step(*prog, act, step, 0, ntrain, gs);
         }
-        if (opt.use_graphs && key_uses[key] > 1) prog->build_graph(st, &side_streams);
+        static const bool graph_single = [] {  // diagnosis: PBKD_GRAPH_SINGLE=1 captures single-use epochs too
+            const char* e = std::getenv("PBKD_GRAPH_SINGLE");
+            return e && e[0] == '1';
+        }();
+        if (opt.use_graphs && (key_uses[key] > 1 || graph_single)) prog->build_graph(st, &side_streams);
         progs.emplace(key, std::move(prog));
     }
     trace.mark("epoch: record programs / graphs");
