@@ -23,5 +23,6 @@ for k in umma_ts_kernel umma_tma_kernel dw_bwd_kernel dw_fwd_kernel dw_gk_kernel
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 60 -c 1 -o gpurun_out/full_$k python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_$k.log 2>&1
 done
 bash tools/gpu_knockout.sh > /dev/null 2>&1
+bash tools/gpu_cta_trace2.sh > /dev/null 2>&1
 PBKD_TRACE=1 timeout 300 python tools/e2e_probe.py > gpurun_out/e2e_probe.log 2>&1
 ls -la gpurun_out > gpurun_out/ls.txt
