@@ -13,7 +13,7 @@ done
 for tool in memcheck racecheck synccheck; do
   timeout 1500 $CS --tool $tool --target-processes all --print-limit 50 \
       python -m pytest -q -p no:cacheprovider -m gpu tests/test_gpu_parity.py \
-      -k "dw_fwd_bit_exact or dw_bwd_fused or dw_gk or pointwise_fwd_bwd or sgd_bit_exact or toy_step_replay or prefix_infer" \
+      -k "dw_fwd_bit_exact or dw_bwd_fused or dw_gk or pointwise_fwd_bwd or sgd_bit_exact or toy_step_replay or prefix_infer or three_layer" \
       > gpurun_out/sanitize_${tool}_kernels.log 2>&1
   echo "rc=$?" >> gpurun_out/sanitize_${tool}_kernels.log
 done
