@@ -16,10 +16,6 @@
 
 using namespace pbkd_gpu;
 
-namespace pbkd_gpu {
-void launch_gemm_bn(const GemmOp* d, int nd, int ctas, int cls, cudaStream_t st);
-int ctas_gemm(const GemmOp& o);
-}
 
 #define CK(x)                                                                      \
     do {                                                                           \
