@@ -934,8 +934,9 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
                 tc_fence_after();
                 const uint32_t base = tmem + lane_off + a * BN + h * HB;
 #pragma unroll
-                for (int c0 = 0; c0 < HB; c0 += 16)
-                    if (c0 < hcols) tmem_add16(base + c0, acc + c0);
+                for (int c0 = 0; c0 < HB; c0 += 32) {  // hcols is a multiple of 32: one load + wait per 32 columns
+                    if (c0 < hcols) tmem_add32(base + c0, acc + c0);
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[a]);
