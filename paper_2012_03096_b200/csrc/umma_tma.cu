@@ -681,8 +681,11 @@ done:
 namespace {
 constexpr int kTsBN = 128;
 constexpr int kTsSt = 4;                                     // smem stages
-constexpr int kTsTm = 3;                                     // TMEM A stages
-constexpr int kTsAcc = 2;                                    // TMEM accumulator slots
+// TMEM: 3 accumulator slots x 128 + 2 A stages x 64 = all 512 columns (the
+// third accumulator slot lets the MMA run further ahead of a tile epilogue;
+// 3 A stages / 2 slots measured 0.3% slower on the epoch)
+constexpr int kTsTm = 2;                                     // TMEM A stages
+constexpr int kTsAcc = 3;                                    // TMEM accumulator slots
 constexpr int kTsARaw = kBM * kBK * 4;                       // 16 KB raw A
 constexpr int kTsBOp = kTsBN * kRowBytes;                    // 16 KB per B plane
 constexpr int kTsStage = kTsARaw + 2 * kTsBOp;               // 48 KB
