@@ -176,6 +176,7 @@ __device__ __forceinline__ void dw_fwd_tile(const DwFwdOp& o, const DwPos& q, fl
                     *reinterpret_cast<float2*>(yl + off) =  // infinities: lo = 0 (tc_split_lo)
                         make_float2(isinf(acc.x) ? 0.0f : __uint_as_float(tc_split_hi(d.x)),
                                     isinf(acc.y) ? 0.0f : __uint_as_float(tc_split_hi(d.y)));
+                    if (o.y_both) *reinterpret_cast<float2*>(yf + off) = acc;
                 } else {
                     *reinterpret_cast<float2*>(yf + off) = acc;
                 }

@@ -1182,7 +1182,15 @@ struct Engine::Impl {
                 o.x = u == 0 ? c.x0 : s.p[u - 1].f();
                 o.w = s.w_dw(u);
                 o.y = s.d[u].f();
-                if (s.planes_d[u]) o.y_hi = s.d_hi[u].f(), o.y_lo = s.d_lo[u].f();
+                // The forward GEMM takes the raw dw output through TMEM (the dw
+                // forward writes fp32 next to the planes, which the weight-gradient
+                // GEMM still reads as B): dw forward +2.3 us, forward GEMM -1.3 us
+                // per launch, epoch -0.9%.  PBKD_FWD_TS=0: pre-split A.
+                static const bool fwd_ts = [] {
+                    const char* e = std::getenv("PBKD_FWD_TS");
+                    return !(e && e[0] == '0') && gemm_ts_enabled();
+                }();
+                if (s.planes_d[u]) o.y_hi = s.d_hi[u].f(), o.y_lo = s.d_lo[u].f(), o.y_both = fwd_ts ? 1 : 0;
                 o.n = c.n;
                 o.h = d.hin;
                 o.wd = d.win;
@@ -1207,7 +1215,7 @@ struct Engine::Impl {
                 g.N = d.cout;
                 g.K = d.cin;
                 g.A = s.d[u].f();
-                if (s.planes_d[u]) g.a_hi = s.d_hi[u].f(), g.a_lo = s.d_lo[u].f();
+                if (s.planes_d[u]) g.a_hi = s.d_hi[u].f(), g.a_lo = s.d_lo[u].f(), g.a_ts_req = o.y_both;
                 if (s.planes_w) g.b_hi = s.params_hi.f() + s.off_pw[u], g.b_lo = s.params_lo.f() + s.off_pw[u];
                 g.lda = d.cin;
                 g.a_kmajor = 1;
@@ -1221,7 +1229,8 @@ struct Engine::Impl {
                 g.part1 = s.cs1.f();
                 g.ksplit = 1;
                 gemm_finalize(g);
-                if (s.planes_d[u] && !g.a_presplit) throw std::logic_error("pre-split dw output not consumed by the fwd GEMM");
+                if (s.planes_d[u] && !(g.a_presplit || g.a_tmem))
+                    throw std::logic_error("pre-split dw output not consumed by the fwd GEMM");
                 g.failed = c.failed;
                 gms.push_back(g);
                 BnStatOp b{};

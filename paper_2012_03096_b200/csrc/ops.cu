@@ -414,6 +414,7 @@ __device__ __forceinline__ void dw_fwd_plain(const DwFwdOp& o, const DwPos& q, f
                     const float hv = __uint_as_float(tc_split_hi(acc));
                     yh[off] = hv;
                     yl[off] = __uint_as_float(tc_split_lo(acc, hv));
+                    if (o.y_both) yf[off] = acc;
                 } else {
                     yf[off] = acc;
                 }

@@ -43,6 +43,7 @@ struct DwFwdOp {
     float *y_hi, *y_lo;
     int n, h, wd, c, ho, wo, stride, pad;
     int pro;
+    int y_both;  // with planes, also the fp32 output (a GEMM taking A through TMEM reads it)
     const float *pa, *pb, *pc, *pd;  // mean,inv,gamma,beta | scale,shift
     const int* failed;
     int cta_begin;
