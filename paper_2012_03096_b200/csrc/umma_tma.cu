@@ -693,11 +693,23 @@ constexpr int kTsSmem = 1024 + kTsSt * kTsStage + kBM * 32 * 4;  // + epilogue s
 constexpr int kTsAcol0 = kTsAcc * kTsBN;                     // first TMEM column of the A stages
 }  // namespace
 
+#ifdef PBKD_GEMM_TRACE_BUILD
+__device__ unsigned long long* g_ts_trace = nullptr;  // per-CTA [start | end | chunks, tiles] (tracer build)
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <int KIND>
 __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __restrict__ ops, int nd, int total,
                                                                 const int* __restrict__ perm) {
     constexpr int BN = kTsBN, HB = BN / 2, S = kTsSt, T = kTsTm, AC = kTsAcc;
     extern __shared__ uint8_t smem_raw[];
+#ifdef PBKD_GEMM_TRACE_BUILD
+    if (threadIdx.x == 0 && g_ts_trace && blockIdx.x < 1024) g_ts_trace[blockIdx.x] = gtimer();
+#endif
     __shared__ uint64_t op_full[S], op_empty[S], a_full[T], a_empty[T], acc_full[AC], acc_empty[AC];
     __shared__ uint32_t tmem_base_sh;
     __shared__ float red_buf[256];
@@ -950,6 +962,15 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
     }
     tc_fence_before();
     __syncthreads();
+#ifdef PBKD_GEMM_TRACE_BUILD
+    if (threadIdx.x == 0 && g_ts_trace && blockIdx.x < 1024) {
+        g_ts_trace[1024 + blockIdx.x] = gtimer();
+        unsigned long long nc = 0, nt = 0;
+        for (int j = 0; j < ntiles; ++j)
+            if (tiles_sh[j].op >= 0) nc += tiles_sh[j].g.nchunks, ++nt;
+        g_ts_trace[2048 + blockIdx.x] = nc | (nt << 32);
+    }
+#endif
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -1077,8 +1098,46 @@ void launch_ts_t(const GemmOp* d, int nd, int total, cudaStream_t st, const int*
     }
     if (nd > kMaxOps) throw CudaError("umma_ts: too many ops in one launch");
     const int grid = gemm_tma_grid(total);
+#ifdef PBKD_GEMM_TRACE_BUILD
+    // diagnosis (PBKD_GEMM_TRACE set, uncaptured launches): per-CTA lines in
+    // launch_tma_t's [gemm-cta] format (tools/cta_trace_summary.py), launch
+    // ids 1000 * kind + n
+    static const bool trace_on = std::getenv("PBKD_GEMM_TRACE") != nullptr;
+    static unsigned long long* buf = nullptr;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (trace_on) PBKD_CUDA(cudaStreamIsCapturing(st, &cap));
+    const bool tr = trace_on && cap == cudaStreamCaptureStatusNone;
+    if (tr) {
+        if (!buf) PBKD_CUDA(cudaMalloc(&buf, 3 * 1024 * sizeof(unsigned long long)));
+        PBKD_CUDA(cudaMemsetAsync(buf, 0, 3 * 1024 * sizeof(unsigned long long), st));
+        PBKD_CUDA(cudaMemcpyToSymbolAsync(g_ts_trace, &buf, sizeof(buf), 0, cudaMemcpyHostToDevice, st));
+    }
+#endif
     launch_k(umma_ts_kernel<KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(kTsSmem), st, d, nd, total, perm);
     PBKD_LAUNCH_CHECK();
+#ifdef PBKD_GEMM_TRACE_BUILD
+    if (tr) {
+        static int launch_no = 0;
+        ++launch_no;
+        std::vector<unsigned long long> h(3 * 1024);
+        PBKD_CUDA(cudaMemcpyAsync(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        unsigned long long* none = nullptr;
+        PBKD_CUDA(cudaMemcpyToSymbolAsync(g_ts_trace, &none, sizeof(none), 0, cudaMemcpyHostToDevice, st));
+        PBKD_CUDA(cudaStreamSynchronize(st));
+        unsigned long long s0 = ~0ull, e1 = 0;
+        for (int b = 0; b < grid && b < 1024; ++b) s0 = std::min(s0, h[b]), e1 = std::max(e1, h[1024 + b]);
+        std::fprintf(stderr, "[gemm-cta] launch %d BN=%d PS=2 grid=%d span %.2f us\n", launch_no + 1000 * KIND, kTsBN, grid,
+                     (e1 - s0) * 1e-3);
+        std::vector<GemmOp> hop(static_cast<size_t>(nd));
+        PBKD_CUDA(cudaMemcpy(hop.data(), d, hop.size() * sizeof(GemmOp), cudaMemcpyDeviceToHost));
+        for (const GemmOp& o : hop)
+            std::fprintf(stderr, "[gemm-cta]   op M=%d N=%d K=%d ksplit=%d tiles=%dx%d epi=%d conv=%d\n", o.M, o.N, o.K,
+                         o.ksplit, o.tiles_m, o.tiles_n, o.epi, o.conv);
+        for (int b = 0; b < grid && b < 1024; ++b)
+            std::fprintf(stderr, "[gemm-cta]   cta %3d start %7.2f end %7.2f chunks %4llu tiles %llu\n", b, (h[b] - s0) * 1e-3,
+                         (h[1024 + b] - s0) * 1e-3, h[2048 + b] & 0xffffffffull, h[2048 + b] >> 32);
+    }
+#endif
 }
 
 }  // namespace
