@@ -161,6 +161,7 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
 }
 __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Epilogue through shared memory, in 32-column passes: the pass's block of
@@ -179,8 +180,8 @@ __device__ __forceinline__ uint32_t cs_addr(uint32_t cs, int r, int col) {  // e
 
 template <int BN, int KIND>
 __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* acc, int tm, int tn, int split, int q,
-                                                int h, int lane, int et, float (*red)[4][32], uint32_t cs,
-                                                int& stores, int bnt) {
+                                                int h, int lane, int et, float (*red)[4][32], uint32_t cs0,
+                                                uint32_t cs1, int& stores, int bnt) {
     constexpr int HB = BN / 2;
     const int warp8 = et >> 5;
     // every descriptor field in registers up front: the global stores below
@@ -203,7 +204,14 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
 #pragma unroll
     for (int pass = 0; pass < BN / 32; ++pass) {
         if (pass * 32 >= bnt) break;  // tile-uniform
-        if (et == 0 && stores) tma_store_wait_read();  // staging block free again
+        // staging block of this pass: with a second block (cs1) the passes
+        // alternate, so only the store issued two passes ago must have read
+        // its block; otherwise the previous pass's store
+        const uint32_t cs = (cs1 && (stores & 1)) ? cs1 : cs0;
+        if (et == 0 && stores) {
+            if (cs1) tma_store_wait_read1();
+            else tma_store_wait_read();
+        }
         named_bar(1, 256);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -241,8 +249,8 @@ __device__ __forceinline__ void staged_epilogue(const GemmOp& op, const float* a
         if (et == 0) {
             tma_store_3d(map_c, cs, n0 + pass * 32, m0, split);  // split 0 unless split-K (epi 2)
             tma_store_commit();
-            stores = 1;
         }
+        ++stores;  // every thread: the pass parity picks the staging block
         if (KIND == 1) {
             // thread = (column, row quarter, sum | sum of squares), warp-uniform
             // quarter and kind: the quarter's 32 rows summed serially in the
@@ -638,7 +646,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_tma_kernel(const GemmOp* __
                     if (warp == kEpiWarp0) mark(3, it);
                 }
             }
-            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores, bnt);
+            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, 0u, stores, bnt);
             if (warp == kEpiWarp0 && lane == 0) mark(4, j);
         }
     }
@@ -689,7 +697,12 @@ constexpr int kTsAcc = 3;                                    // TMEM accumulator
 constexpr int kTsARaw = kBM * kBK * 4;                       // 16 KB raw A
 constexpr int kTsBOp = kTsBN * kRowBytes;                    // 16 KB per B plane
 constexpr int kTsStage = kTsARaw + 2 * kTsBOp;               // 48 KB
-constexpr int kTsSmem = 1024 + kTsSt * kTsStage + kBM * 32 * 4;  // + epilogue staging
+// + epilogue staging: two alternating 16 KB blocks (one for the forward kind,
+// whose batch-norm partial buffer leaves no room for a second next to the ring)
+template <int KIND>
+constexpr int ts_staging_blocks() { return KIND == 1 ? 1 : 2; }
+template <int KIND>
+constexpr int ts_smem() { return 1024 + kTsSt * kTsStage + ts_staging_blocks<KIND>() * kBM * 32 * 4; }
 constexpr int kTsAcol0 = kTsAcc * kTsBN;                     // first TMEM column of the A stages
 }  // namespace
 
@@ -956,7 +969,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[a]);
             }
-            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s, stores, bnt);
+            staged_epilogue<BN, KIND>(o, acc, g.tm, g.tn, g.split, q, h, lane, et, red, cs_s,
+                                      ts_staging_blocks<KIND>() > 1 ? cs_s + kBM * 32 * 4 : 0u, stores, bnt);
         }
         if (tid == kEpiWarp0 * 32) tma_store_wait_all();
     }
@@ -1093,7 +1107,7 @@ template <int KIND>
 void launch_ts_t(const GemmOp* d, int nd, int total, cudaStream_t st, const int* perm) {
     static bool attr = false;
     if (!attr) {
-        PBKD_CUDA(cudaFuncSetAttribute(umma_ts_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmem));
+        PBKD_CUDA(cudaFuncSetAttribute(umma_ts_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts_smem<KIND>()));
         attr = true;
     }
     if (nd > kMaxOps) throw CudaError("umma_ts: too many ops in one launch");
@@ -1113,7 +1127,8 @@ void launch_ts_t(const GemmOp* d, int nd, int total, cudaStream_t st, const int*
         PBKD_CUDA(cudaMemcpyToSymbolAsync(g_ts_trace, &buf, sizeof(buf), 0, cudaMemcpyHostToDevice, st));
     }
 #endif
-    launch_k(umma_ts_kernel<KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(kTsSmem), st, d, nd, total, perm);
+    launch_k(umma_ts_kernel<KIND>, dim3(grid), dim3(kThreadsT), static_cast<size_t>(ts_smem<KIND>()), st, d, nd, total,
+             perm);
     PBKD_LAUNCH_CHECK();
 #ifdef PBKD_GEMM_TRACE_BUILD
     if (tr) {
