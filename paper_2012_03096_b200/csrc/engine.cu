@@ -97,6 +97,16 @@ DevBuf upload(const std::vector<T>& v, cudaStream_t st) {
     return b;
 }
 
+// The forward GEMM takes the raw dw output through TMEM (PBKD_FWD_TS=0:
+// pre-split planes written by the dw forward).
+bool fwd_ts_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("PBKD_FWD_TS");
+        return !(e && e[0] == '0') && gemm_ts_enabled();
+    }();
+    return on;
+}
+
 // ------------------------------------------------------- algorithmic work
 // Compulsory fp32 bytes and flops of one op: what the kernel must
 // move / compute at minimum, not what it does move (pre-split operand planes,
@@ -1095,7 +1105,7 @@ struct Engine::Impl {
         for (int u = 0; u < s.units; ++u) {
             s.d[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
             s.planes_d[u] = gemm_presplit_ok(s.u[u].cin) && gemm_presplit_ok(s.u[u].cout) && s.planes_w;
-            if (s.planes_d[u]) {
+            if (s.planes_d[u] && !(fwd_ts_on() && gemm_bsplit_enabled())) {
                 s.d_hi[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
                 s.d_lo[u].alloc(static_cast<size_t>(M) * s.u[u].cin * sizeof(float));
             }
@@ -1182,15 +1192,11 @@ struct Engine::Impl {
                 o.x = u == 0 ? c.x0 : s.p[u - 1].f();
                 o.w = s.w_dw(u);
                 o.y = s.d[u].f();
-                // The forward GEMM takes the raw dw output through TMEM (the dw
-                // forward writes fp32 next to the planes, which the weight-gradient
-                // GEMM still reads as B): dw forward +2.3 us, forward GEMM -1.3 us
-                // per launch, epoch -0.9%.  PBKD_FWD_TS=0: pre-split A.
-                static const bool fwd_ts = [] {
-                    const char* e = std::getenv("PBKD_FWD_TS");
-                    return !(e && e[0] == '0') && gemm_ts_enabled();
-                }();
-                if (s.planes_d[u]) o.y_hi = s.d_hi[u].f(), o.y_lo = s.d_lo[u].f(), o.y_both = fwd_ts ? 1 : 0;
+                // The forward GEMM takes the raw dw output through TMEM, and the
+                // weight-gradient GEMM splits it as B in shared memory, so the dw
+                // forward writes fp32 only.  With planes (PBKD_GEMM_BSPLIT=0) it
+                // writes both; PBKD_FWD_TS=0: planes only, pre-split A.
+                if (s.d_hi[u].p) o.y_hi = s.d_hi[u].f(), o.y_lo = s.d_lo[u].f(), o.y_both = fwd_ts_on() ? 1 : 0;
                 o.n = c.n;
                 o.h = d.hin;
                 o.wd = d.win;
@@ -1215,7 +1221,8 @@ struct Engine::Impl {
                 g.N = d.cout;
                 g.K = d.cin;
                 g.A = s.d[u].f();
-                if (s.planes_d[u]) g.a_hi = s.d_hi[u].f(), g.a_lo = s.d_lo[u].f(), g.a_ts_req = o.y_both;
+                if (s.d_hi[u].p) g.a_hi = s.d_hi[u].f(), g.a_lo = s.d_lo[u].f(), g.a_ts_req = o.y_both;
+                else if (s.planes_d[u]) g.a_ts_req = 1;
                 if (s.planes_w) g.b_hi = s.params_hi.f() + s.off_pw[u], g.b_lo = s.params_lo.f() + s.off_pw[u];
                 g.lda = d.cin;
                 g.a_kmajor = 1;
@@ -1229,7 +1236,7 @@ struct Engine::Impl {
                 g.part1 = s.cs1.f();
                 g.ksplit = 1;
                 gemm_finalize(g);
-                if (s.planes_d[u] && !(g.a_presplit || g.a_tmem))
+                if (s.d_hi[u].p && !(g.a_presplit || g.a_tmem))
                     throw std::logic_error("pre-split dw output not consumed by the fwd GEMM");
                 g.failed = c.failed;
                 gms.push_back(g);
@@ -1366,7 +1373,8 @@ struct Engine::Impl {
                 w.lda = d.cout;
                 w.a_kmajor = 0;
                 w.B = s.d[u].f();
-                if (s.planes_d[u]) w.b_hi = s.d_hi[u].f(), w.b_lo = s.d_lo[u].f();
+                if (s.d_hi[u].p) w.b_hi = s.d_hi[u].f(), w.b_lo = s.d_lo[u].f();
+                else if (s.planes_d[u]) w.b_split_req = 1;  // raw dw output split by the GEMM
                 w.ldb = d.cin;
                 w.b_kmajor = 0;
                 w.ldc = d.cin;
@@ -1376,7 +1384,7 @@ struct Engine::Impl {
                 // before gemm_finalize, which builds the TMA store map from it)
                 w.C = w.ksplit == 1 ? s.g_pw(u) : s.wsplit.f();
                 gemm_finalize(w);
-                if (s.planes_d[u] && !((w.a_presplit || w.a_tmem) && w.b_presplit))
+                if (s.planes_d[u] && !((w.a_presplit || w.a_tmem) && (w.b_presplit || w.b_split)))
                     throw std::logic_error("pre-split operands not consumed by wgrad");
                 w.failed = c.failed;
                 if (w.ksplit > 1) {

@@ -151,6 +151,10 @@ struct GemmOp {
     // a_ts_req (caller): A is valid raw fp32 (not only planes); gemm_finalize
     // then sets a_tmem when the A-through-TMEM kernel takes the op (B pre-split)
     int a_ts_req, a_tmem;
+    // b_split_req (caller): B has no planes, only raw fp32; when the
+    // A-through-TMEM kernel takes the op, its converter warps split the raw B
+    // box in shared memory (b_split set; map_bh then addresses raw B)
+    int b_split_req, b_split;
     int a_gather;  // a_tmem conv with ic % 32 != 0: converter warps gather the im2col rows from global
     int c_tma;                    // epilogue stores C through shared memory + TMA
     CUtensorMap map_c;            // 3-D {N, M, ksplit} SWIZZLE_128B map of C
@@ -178,6 +182,10 @@ bool gemm_tma_prepare(GemmOp& o);  // umma_tma.cu: tensor maps, false if ineligi
 bool gemm_presplit_ok(long long ld);
 // Whether ops flagged a_ts_req run on the A-through-TMEM kernel (PBKD_GEMM_TS)
 bool gemm_ts_enabled();
+// Whether raw-B ops (b_split_req) are split in the A-through-TMEM kernel
+// (PBKD_GEMM_BSPLIT, default on with PBKD_GEMM_TS): producers then skip the
+// B operand's planes
+bool gemm_bsplit_enabled();
 
 // Batch-norm statistics from the GEMM column partials (ops.hpp:273-299):
 // mean, var = E[x^2]-mean^2 clamped, inv_std, moving-stat update.

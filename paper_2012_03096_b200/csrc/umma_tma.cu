@@ -811,8 +811,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
                 for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                     const int s = it % S;
                     mbar_wait(&op_empty[s], ((it / S) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&op_full[s],
-                                          static_cast<uint32_t>((o.a_gather ? 0 : bm * kBK * 4) + 2 * bnt * kRowBytes));
+                    mbar_arrive_expect_tx(&op_full[s], static_cast<uint32_t>((o.a_gather ? 0 : bm * kBK * 4) +
+                                                                             (o.b_split ? 1 : 2) * bnt * kRowBytes));
                     uint8_t* st = ring + s * kTsStage;
                     const int k = g.k0 + kc * kBK;
                     if (o.a_gather) {
@@ -829,13 +829,13 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
                     uint8_t* ob = st + kTsARaw;
                     if (bkm) {
                         tma_load_2d(ob, &o.map_bh, &op_full[s], k, n0);
-                        tma_load_2d(ob + kTsBOp, &o.map_bl, &op_full[s], k, n0);
+                        if (!o.b_split) tma_load_2d(ob + kTsBOp, &o.map_bl, &op_full[s], k, n0);
                     } else {
 #pragma unroll
                         for (int at = 0; at < BN / 32; ++at) {
                             if (at * 32 >= bnt) break;
                             tma_load_2d(ob + at * 4096, &o.map_bh, &op_full[s], n0 + 32 * at, k);
-                            tma_load_2d(ob + kTsBOp + at * 4096, &o.map_bl, &op_full[s], n0 + 32 * at, k);
+                            if (!o.b_split) tma_load_2d(ob + kTsBOp + at * 4096, &o.map_bl, &op_full[s], n0 + 32 * at, k);
                         }
                     }
                 }
@@ -903,6 +903,34 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
                 const uint32_t acol = tmem + lane_off + kTsAcol0 + t * 64;
                 tmem_st32(acol, hv);
                 tmem_st32(acol + 32, lv);
+                if (KIND == 0 && o.b_split) {
+                    // raw B box -> hi in place, lo into the lo plane's slot: an
+                    // elementwise pass, so the planes keep the box's swizzled layout
+                    const uint32_t bh = raw + kTsARaw, bl = bh + kTsBOp;
+                    const int n16 = o.bn * (kRowBytes / 16);  // 16-byte items: bn 32 / 64 / 128 -> 2 / 4 / 8 per thread
+                    for (int i0 = row; i0 < n16; i0 += 4 * kConvThreads) {
+                        const int nj = min(4, (n16 - i0 + kConvThreads - 1) / kConvThreads);
+                        float4 x[4];  // loads in flight before the splits
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (j < nj) x[j] = lds128(bh + 16 * (i0 + j * kConvThreads));
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (j >= nj) break;
+                            const float xs[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+                            uint32_t h4[4], l4[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                h4[q] = tc_split_hi(xs[q]);
+                                l4[q] = tc_split_lo(xs[q], __uint_as_float(h4[q]));
+                            }
+                            const uint32_t off = 16 * (i0 + j * kConvThreads);
+                            sts128(bh + off, h4[0], h4[1], h4[2], h4[3]);
+                            sts128(bl + off, l4[0], l4[1], l4[2], l4[3]);
+                        }
+                    }
+                    fence_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
@@ -1235,6 +1263,14 @@ bool gemm_ts_enabled() {  // PBKD_GEMM_TS=0: pre-split planes for A as well
     return on;
 }
 
+bool gemm_bsplit_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PBKD_GEMM_BSPLIT");
+        return !(e && e[0] == '0');
+    }();
+    return on && gemm_ts_enabled();
+}
+
 bool gemm_presplit_ok(long long ld) {
     static const bool on = [] {
         const char* t = std::getenv("PBKD_GEMM_TMA");
@@ -1346,7 +1382,13 @@ bool gemm_tma_prepare(GemmOp& o) {
         o.c_tma = encode_c(o) ? 1 : 0;
     }
     o.a_tmem = 0;
-    if (ok && gemm_ts_enabled() && o.a_ts_req && o.b_presplit && o.tf32x3 == 3 && bn <= kTsBN) {
+    o.b_split = 0;
+    // raw B without planes: boxes of the planes' geometry and swizzle, split in
+    // place (hi) and into the lo plane's slot by the converter warps
+    CUtensorMap mb_raw, mb_unused;
+    const bool bsplit = ok && !o.b_presplit && o.b_split_req && o.epi != 1 && gemm_bsplit_enabled() &&
+                        presplit_pair(&mb_raw, &mb_unused, o.B, o.B, o.b_kmajor != 0, o.N, o.K, o.ldb, o.bn);
+    if (ok && gemm_ts_enabled() && o.a_ts_req && (o.b_presplit || bsplit) && o.tf32x3 == 3 && bn <= kTsBN) {
         // raw A for the converter warps: K-major 128-byte swizzled {32 k, 128 rows},
         // MN-major plain {128 m, 32 k}
         CUtensorMap m;
@@ -1356,6 +1398,7 @@ bool gemm_tma_prepare(GemmOp& o) {
             o.map_a = m;
             o.a_tmem = 1;
             o.a_presplit = 0;
+            if (!o.b_presplit) o.map_bh = mb_raw, o.b_split = 1;
         }
     }
     return ok && o.c_tma != 0;  // the TMA kernel's epilogue stores through the C map
