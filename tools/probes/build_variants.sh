@@ -1,7 +1,8 @@
-# Diagnosis builds of the GEMM kernel (umma_tma.cu) with experiment macros,
+# Diagnosis builds of one kernel source (SRC=umma_tma default, or ops, ...) with experiment macros,
 # each linked into tools/probes/_build/<name>/libpbkd_b200.so (product objects
 # otherwise).  Usage: tools/probes/build_variants.sh name=-DMACRO ...
 set -e
+SRC=${SRC:-umma_tma}
 R=$(cd "$(dirname "$0")/../.." && pwd)
 P=$R/paper_2012_03096_b200
 make -s -C $P -j16
@@ -11,9 +12,9 @@ for spec in "$@"; do
   out=$R/tools/probes/_build/$name; mkdir -p $out
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++20 -Xcompiler -fPIC \
     -Xcompiler -ffp-contract=off -I$P/include -I$R/include -I$JSON_INC --expt-relaxed-constexpr $flags \
-    -c $P/csrc/umma_tma.cu -o $out/umma_tma.o
-  objs=$(ls $P/build/obj/*.o | grep -v '/umma_tma.o$')
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libpbkd_b200.so $objs $out/umma_tma.o -lcudart
-  rm -f $out/umma_tma.o
+    -c $P/csrc/$SRC.cu -o $out/$SRC.o
+  objs=$(ls $P/build/obj/*.o | grep -v "/$SRC.o\$")
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libpbkd_b200.so $objs $out/$SRC.o -lcudart
+  rm -f $out/$SRC.o
   echo "built $name ($flags)"
 done
