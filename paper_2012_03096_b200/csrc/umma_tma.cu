@@ -699,10 +699,19 @@ constexpr int kTsBOp = kTsBN * kRowBytes;                    // 16 KB per B plan
 constexpr int kTsStage = kTsARaw + 2 * kTsBOp;               // 48 KB
 // + epilogue staging: two alternating 16 KB blocks (one for the forward kind,
 // whose batch-norm partial buffer leaves no room for a second next to the ring)
+#ifdef PBKD_EXP_TS1_ST3  // diagnosis build: forward kind with 3 operand stages and two staging blocks
+template <int KIND>
+constexpr int ts_stages() { return KIND == 1 ? 3 : kTsSt; }
+template <int KIND>
+constexpr int ts_staging_blocks() { return 2; }
+#else
+template <int KIND>
+constexpr int ts_stages() { return kTsSt; }
 template <int KIND>
 constexpr int ts_staging_blocks() { return KIND == 1 ? 1 : 2; }
+#endif
 template <int KIND>
-constexpr int ts_smem() { return 1024 + kTsSt * kTsStage + ts_staging_blocks<KIND>() * kBM * 32 * 4; }
+constexpr int ts_smem() { return 1024 + ts_stages<KIND>() * kTsStage + ts_staging_blocks<KIND>() * kBM * 32 * 4; }
 constexpr int kTsAcol0 = kTsAcc * kTsBN;                     // first TMEM column of the A stages
 }  // namespace
 
@@ -718,7 +727,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <int KIND>
 __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __restrict__ ops, int nd, int total,
                                                                 const int* __restrict__ perm) {
-    constexpr int BN = kTsBN, HB = BN / 2, S = kTsSt, T = kTsTm, AC = kTsAcc;
+    constexpr int BN = kTsBN, HB = BN / 2, S = ts_stages<KIND>(), T = kTsTm, AC = kTsAcc;
     extern __shared__ uint8_t smem_raw[];
 #ifdef PBKD_GEMM_TRACE_BUILD
     if (threadIdx.x == 0 && g_ts_trace && blockIdx.x < 1024) g_ts_trace[blockIdx.x] = gtimer();
