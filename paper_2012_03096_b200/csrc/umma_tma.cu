@@ -724,6 +724,29 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+// Raw B box of one operand stage -> tf32 hi in place, lo into the lo plane's
+// slot (an elementwise pass: the planes keep the box's swizzled layout), by
+// the 256 epilogue threads; generic-proxy stores, then the proxy fence the
+// MMA's async-proxy reads need.
+__device__ __forceinline__ void split_b_stage(uint32_t bh, uint32_t bl, int bn, int et) {
+    const int n16 = bn * (kRowBytes / 16);  // 16-byte items: bn 32 / 64 / 128 -> 1 / 2 / 4 per thread
+    // one item at a time: the drain's accumulator registers are live here
+#pragma unroll 1
+    for (int i = et; i < n16; i += 256) {
+        const float4 x = lds128(bh + 16 * i);
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+        uint32_t h4[4], l4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            h4[q] = tc_split_hi(xs[q]);
+            l4[q] = tc_split_lo(xs[q], __uint_as_float(h4[q]));
+        }
+        sts128(bh + 16 * i, h4[0], h4[1], h4[2], h4[3]);
+        sts128(bl + 16 * i, l4[0], l4[1], l4[2], l4[3]);
+    }
+    fence_async_smem();
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __restrict__ ops, int nd, int total,
                                                                 const int* __restrict__ perm) {
@@ -733,6 +756,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
     if (threadIdx.x == 0 && g_ts_trace && blockIdx.x < 1024) g_ts_trace[blockIdx.x] = gtimer();
 #endif
     __shared__ uint64_t op_full[S], op_empty[S], a_full[T], a_empty[T], acc_full[AC], acc_empty[AC];
+    __shared__ uint64_t b_full[S];  // raw B split by the epilogue warps (launches with b_split ops)
     __shared__ uint32_t tmem_base_sh;
     __shared__ float red_buf[256];
     auto red = reinterpret_cast<float(*)[4][32]>(red_buf);
@@ -763,10 +787,17 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], 8);
         }
+        for (int i = 0; i < S; ++i) mbar_init(&b_full[i], 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < nd; i += kThreadsT) begins[i] = ops[i].cta_begin;
-    __syncthreads();
+    int any_bsplit = 0;
+    for (int i = tid; i < nd; i += kThreadsT) {
+        begins[i] = ops[i].cta_begin;
+        any_bsplit |= ops[i].b_split;
+    }
+    // a launch with raw-B ops: the epilogue warps split every stage's B (an
+    // op with planes only passes), the MMA waits for that on every chunk
+    const bool bsp = KIND == 0 && __syncthreads_or(any_bsplit) != 0;
     const int ntiles = static_cast<int>(blockIdx.x) < total ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
     for (int j = tid; j < ntiles; j += kThreadsT) {
         int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
@@ -912,34 +943,6 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
                 const uint32_t acol = tmem + lane_off + kTsAcol0 + t * 64;
                 tmem_st32(acol, hv);
                 tmem_st32(acol + 32, lv);
-                if (KIND == 0 && o.b_split) {
-                    // raw B box -> hi in place, lo into the lo plane's slot: an
-                    // elementwise pass, so the planes keep the box's swizzled layout
-                    const uint32_t bh = raw + kTsARaw, bl = bh + kTsBOp;
-                    const int n16 = o.bn * (kRowBytes / 16);  // 16-byte items: bn 32 / 64 / 128 -> 2 / 4 / 8 per thread
-                    for (int i0 = row; i0 < n16; i0 += 4 * kConvThreads) {
-                        const int nj = min(4, (n16 - i0 + kConvThreads - 1) / kConvThreads);
-                        float4 x[4];  // loads in flight before the splits
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            if (j < nj) x[j] = lds128(bh + 16 * (i0 + j * kConvThreads));
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            if (j >= nj) break;
-                            const float xs[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
-                            uint32_t h4[4], l4[4];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                h4[q] = tc_split_hi(xs[q]);
-                                l4[q] = tc_split_lo(xs[q], __uint_as_float(h4[q]));
-                            }
-                            const uint32_t off = 16 * (i0 + j * kConvThreads);
-                            sts128(bh + off, h4[0], h4[1], h4[2], h4[3]);
-                            sts128(bl + off, l4[0], l4[1], l4[2], l4[3]);
-                        }
-                    }
-                    fence_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
-                }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
@@ -959,6 +962,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
                 const int s = it % S, t = it % T, a = it % AC;
                 mbar_wait(&op_full[s], (it / S) & 1);
                 mbar_wait(&a_full[t], (it / T) & 1);
+                if (bsp) mbar_wait(&b_full[s], (it / S) & 1);
                 mbar_wait(&acc_empty[a], ((it / AC) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t bh = ring_s + s * kTsStage + kTsARaw, bl = bh + kTsBOp;
@@ -984,6 +988,30 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         int stores = 0;
         uint32_t it = 0;
+        // split cursor (bsp launches): the B box of chunk `sit` (tile sj, chunk
+        // skc) is split while the drain waits for chunk it; kept kBLead
+        // chunks ahead of the drain, so the MMA can run that far ahead
+        constexpr uint32_t kBLead = 2;
+        int sj = 0, skc = 0;
+        uint32_t sit = 0;
+        auto split_ahead = [&](uint32_t upto) {  // split chunks sit .. upto-1
+            while (sit < upto && sj < ntiles) {
+                if (tiles_sh[sj].op < 0 || skc >= tiles_sh[sj].g.nchunks) {
+                    ++sj, skc = 0;
+                    continue;
+                }
+                const GemmOp& so = ops[tiles_sh[sj].op];
+                const int s = sit % S;
+                mbar_wait(&op_full[s], (sit / S) & 1);
+                if (so.b_split) {
+                    const uint32_t bh = ring_s + s * kTsStage + kTsARaw;
+                    split_b_stage(bh, bh + kTsBOp, so.bn, et);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&b_full[s]);
+                ++skc, ++sit;
+            }
+        };
         for (int j = 0; j < ntiles; ++j) {
             if (tiles_sh[j].op < 0) continue;
             const GemmOp& o = ops[tiles_sh[j].op];
@@ -995,6 +1023,7 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
             for (int i = 0; i < HB; ++i) acc[i] = 0.0f;
             for (int kc = 0; kc < g.nchunks; ++kc, ++it) {
                 const int a = it % AC;
+                if (bsp) split_ahead(it + 1 + kBLead);
                 mbar_wait(&acc_full[a], (it / AC) & 1);
                 tc_fence_after();
                 const uint32_t base = tmem + lane_off + a * BN + h * HB;
