@@ -991,7 +991,11 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
         // split cursor (bsp launches): the B box of chunk `sit` (tile sj, chunk
         // skc) is split while the drain waits for chunk it; kept kBLead
         // chunks ahead of the drain, so the MMA can run that far ahead
+#ifndef PBKD_EXP_BLEAD
         constexpr uint32_t kBLead = 2;
+#else
+        constexpr uint32_t kBLead = PBKD_EXP_BLEAD;  // diagnosis build
+#endif
         int sj = 0, skc = 0;
         uint32_t sit = 0;
         auto split_ahead = [&](uint32_t upto) {  // split chunks sit .. upto-1
