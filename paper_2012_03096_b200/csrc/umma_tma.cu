@@ -797,7 +797,8 @@ __global__ void __launch_bounds__(kThreadsT, 1) umma_ts_kernel(const GemmOp* __r
     }
     // a launch with raw-B ops: the epilogue warps split every stage's B (an
     // op with planes only passes), the MMA waits for that on every chunk
-    const bool bsp = KIND == 0 && __syncthreads_or(any_bsplit) != 0;
+    const int any_b = __syncthreads_or(any_bsplit);  // also the barrier after the setup above (every kind)
+    const bool bsp = KIND == 0 && any_b != 0;
     const int ntiles = static_cast<int>(blockIdx.x) < total ? (total - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
     for (int j = tid; j < ntiles; j += kThreadsT) {
         int t = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
